@@ -1,0 +1,176 @@
+/*
+ * rii.h -- C ABI of the B200-native Rii hot path (Reconfigurable Inverted Index,
+ * Matsui, Hinami, Satoh, ACM MM 2018, arXiv 1808.03969).
+ *
+ * Citation keys: "P:n" = PAPER.md line n (section / equation / algorithm named),
+ * "S:n" = SPEC.md line n, "R#" = a reading of the paper listed in DESIGN.md.
+ *
+ * General conventions (every entry point):
+ *  - Every call returns rii_status; RII_OK == 0.  On failure nothing the call was
+ *    asked to produce is valid, and rii_last_error() returns a message for the
+ *    calling thread.  The index stays usable after RII_ERR_ARG / RII_ERR_STATE.
+ *  - Ids are 0-based and dense (the paper's 1..N is 0..N-1, R4), int64 at the
+ *    boundary.  A vector added as the n-th row overall has id n.
+ *  - Distances are squared L2 ADC values in fp32 (Eq. 3; R17), computed
+ *    in the canonical order of DESIGN.md (CA1 / CA2), so they equal the oracle's.
+ *  - Code books have Ks = 256 code words per subspace ("we set Z to 256");
+ *    codes are M bytes per vector.
+ *  - `where` says where the caller's arrays of that call live: RII_MEM_HOST
+ *    (pageable or pinned host memory; copied in/out inside the call, the call
+ *    returns after results are on the host) or RII_MEM_DEVICE (device pointers
+ *    on the index's device; results are complete when the call returns).
+ *  - `stream` is a cudaStream_t (NULL = the legacy default stream); all device
+ *    work of a call is ordered on it.  Caller arrays are borrowed for the call.
+ *  - Ownership: the index owns every device buffer it allocates (code book,
+ *    codes, centres, posting lists, scratch) and frees them in rii_destroy.
+ *  - Concurrency: one writer (train / add / reconfigure / set_*) or many readers
+ *    (query / get_*) at a time per index.
+ *  - Multi-GPU (world > 1): one process per GPU, every rank calls every function
+ *    collectively with identical arguments (full x, q, S).  The database is
+ *    sharded by id range; each rank scans its shard and the per-rank top-k lists
+ *    are merged after an NCCL all-gather, so every rank receives the full result.
+ *  - The library never falls back to the CPU: without a usable CUDA device every
+ *    call that needs one returns RII_ERR_CUDA.
+ */
+#ifndef RII_H_
+#define RII_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rii_index rii_index; /* opaque */
+
+typedef enum {
+    RII_OK = 0,
+    RII_ERR_ARG = 1,   /* invalid argument (shape, range, unsorted target ids, ...) */
+    RII_ERR_STATE = 2, /* call not valid in the current state (e.g. untrained)    */
+    RII_ERR_OOM = 3,   /* device or host allocation failed                         */
+    RII_ERR_CUDA = 4,  /* CUDA runtime error, or no usable device                  */
+    RII_ERR_NCCL = 5,  /* NCCL error (world > 1)                                   */
+    RII_ERR_TRAIN = 6  /* code-book training impossible (n < Ks, < Ks distinct rows) */
+} rii_status;
+
+typedef enum { RII_PATH_AUTO = 0, RII_PATH_LINEAR = 1, RII_PATH_IVF = 2 } rii_path;
+typedef enum { RII_MEM_HOST = 0, RII_MEM_DEVICE = 1 } rii_mem;
+
+/* Size of the opaque NCCL unique id accepted by rii_create. */
+#define RII_NCCL_ID_BYTES 128
+
+/* Message of the last failed call on this thread ("" if none).  Never NULL. */
+const char *rii_last_error(void);
+
+/* Number of CUDA kernels this library has launched in this process (all
+ * indexes).  Used by bench.py to report "gpu_launches". */
+uint64_t rii_launch_count(void);
+
+/* Rank 0 calls this to obtain the NCCL unique id that every rank then passes to
+ * rii_create (distributed by the caller, e.g. through torch.distributed).
+ * out: RII_NCCL_ID_BYTES host bytes.  RII_ERR_NCCL if NCCL cannot be loaded. */
+rii_status rii_nccl_unique_id(void *out);
+
+/* Create an empty index (Sec. 4.1) of D-dim vectors with M subspaces.
+ *  D % M == 0, 1 <= M <= 64, Ks == 256, D/M <= 64 (else RII_ERR_ARG).
+ *  device: CUDA ordinal this index lives on.  rank/world: this process's place
+ *  in a one-process-per-GPU job (world == 1: single GPU).  nccl_id: the 128-byte
+ *  id from rii_nccl_unique_id (all ranks identical) or NULL; with world > 1 and
+ *  nccl_id == NULL the index is a *detached shard*: rii_query returns
+ *  RII_ERR_STATE and the caller combines shards with rii_query_partial +
+ *  rii_merge_partials (used for single-GPU logical-shard tests).
+ *  *out receives the index (NULL on failure). */
+rii_status rii_create(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t rank, int32_t world,
+                      const void *nccl_id, rii_index **out);
+
+/* Frees every device buffer and the NCCL communicator.  NULL is a no-op. */
+void rii_destroy(rii_index *idx);
+
+/* Code-book training (R8; the paper: "preliminarily trained"): per
+ * subspace, n_iter Lloyd iterations, seeded distinct-row init, fixed-point
+ * mean update (DESIGN.md O-TRAIN).  x: n x D fp32 row-major.  Requires n >= 256
+ * and >= 256 distinct sub-vectors per subspace (else RII_ERR_TRAIN) and
+ * n * max|x| < 2^31 (else RII_ERR_ARG).  Replaces any code book; only allowed
+ * while the index is empty (N == 0), else RII_ERR_STATE.  Every rank trains
+ * identically (no communication). */
+rii_status rii_train(rii_index *idx, const float *x, int64_t n, int32_t n_iter, uint64_t seed, rii_mem where,
+                     void *stream);
+
+/* Data addition (Sec. 4.3 "Data addition"): encodes x (n x D fp32,
+ * Eq. 1) and appends the codes to the linear array (PushBack(Xbar, y));
+ * if the index has coarse centres (K > 0) each new id is appended to the posting
+ * list of its SDC-nearest centre (PushBack(W_a(n), n); lists stay ascending).
+ * Ids first_id .. first_id+n-1 (first_id may be NULL).  Requires a code book
+ * (RII_ERR_STATE).  With world > 1 the batch is split into `world` contiguous
+ * chunks and rank r stores chunk r. */
+rii_status rii_add(rii_index *idx, const float *x, int64_t n, rii_mem where, void *stream, int64_t *first_id);
+
+/* Reconfigure (Alg. 4): PQk-means (reading R9) over the sample of
+ * min(N, 100*nlist) ids with the smallest splitmix64(seed ^ id) keys (R10), init
+ * = the first nlist distinct sample codes, n_iter iterations; then every code is
+ * assigned to its SDC-nearest centre (ties to the lowest k) and the posting lists
+ * are rebuilt with ascending ids.  1 <= nlist <= N (RII_ERR_ARG), fewer than nlist
+ * distinct sample codes -> RII_ERR_ARG.  Deterministic for (nlist, n_iter, seed)
+ * (P:682).  Resets theta to the default (R3). */
+rii_status rii_reconfigure(rii_index *idx, int32_t nlist, int32_t n_iter, uint64_t seed, void *stream);
+
+/* Query (Alg. 3), nq queries q (nq x D fp32) sharing one target set:
+ *  target_ids: strictly ascending ids in [0, N) (the paper's sorted S, P:366-374;
+ *     R6), n_target of them; NULL = the whole database (S = {0..N-1}).
+ *     Violations -> RII_ERR_ARG (checked on the device before any result).
+ *  topk: R, 1 <= topk <= 1024.
+ *  L: the number of nearest coarse lists to probe (reading R1); the inverted
+ *     index traverses P = min(L, K) lists for S = ALL and
+ *     P = min(K, ceil(L * N / |S|)) lists otherwise, evaluating every
+ *     member of S in them (R2 mode A).  L >= 1.
+ *  path: RII_PATH_AUTO applies Alg. 3 with the index's theta (|S| < theta ->
+ *     PQ linear scan (Alg. 1), else inverted index (Alg. 2)); LINEAR / IVF force
+ *     a path.  K == 0 forces LINEAR; IVF with K == 0 -> RII_ERR_STATE.
+ *  out_ids / out_dist: nq x topk, each row sorted by (dist asc, id asc); rows
+ *     with fewer than topk candidates are padded with id -1 and dist +inf (R18).
+ *  path_used (may be NULL): the path taken. */
+rii_status rii_query(const rii_index *idx, const float *q, int64_t nq, int32_t topk, const int64_t *target_ids,
+                     int64_t n_target, int32_t L, rii_path path, rii_mem where, void *stream, int64_t *out_ids,
+                     float *out_dist, int32_t *path_used);
+
+/* Split-phase query for detached shards (world > 1 with nccl_id == NULL) and for
+ * custom transports: the same arguments as rii_query, but instead of the final
+ * result it writes this rank's top candidates as packed uint64 keys
+ * ((fp32 dist bits) << 32 | global id), nq x kk, each row ascending, unused
+ * slots = UINT64_MAX.  kk = rii_partial_width(topk).  Arrays in device memory.
+ * The path is decided from the global |S| exactly as in rii_query. */
+int32_t rii_partial_width(int32_t topk);
+rii_status rii_query_partial(const rii_index *idx, const float *q, int64_t nq, int32_t topk,
+                             const int64_t *target_ids, int64_t n_target, int32_t L, rii_path path, void *stream,
+                             uint64_t *out_keys, int32_t *path_used);
+
+/* Merge `parts` partial key arrays laid out [parts][nq][kk] (device memory) into
+ * the final nq x topk result (device memory).  The global top-k is contained in
+ * the union of the per-shard top-k, so the result equals the single-index one. */
+rii_status rii_merge_partials(const uint64_t *keys, int32_t parts, int64_t nq, int32_t topk, void *stream,
+                              int64_t *out_ids, float *out_dist);
+
+/* State hand-off (host memory): code book M x 256 x (D/M) fp32; codes of global
+ * ids [first, first+n) (must be stored on this rank, else RII_ERR_ARG); centres
+ * K x M; posting lists of this rank as CSR offsets[K+1] + global ids[N_local]
+ * ascending within each list; assignment a(id) for this rank's ids [N_local]. */
+rii_status rii_get_codebook(const rii_index *idx, float *out);
+rii_status rii_set_codebook(rii_index *idx, const float *cb); /* only while N == 0 */
+rii_status rii_get_codes(const rii_index *idx, int64_t first, int64_t n, uint8_t *out);
+rii_status rii_get_centers(const rii_index *idx, uint8_t *out);
+rii_status rii_get_postings(const rii_index *idx, int64_t *offsets, int64_t *ids);
+
+/* theta of Alg. 3 (reading R3).  theta < 0 restores the default
+ * theta(L) = ceil(L*N/K) + K evaluated at each call's L. */
+rii_status rii_set_theta(rii_index *idx, int64_t theta);
+
+/* N = total ids (all ranks), K = coarse centres, theta = the set value or -1,
+ * n_local = ids stored on this rank, bytes = device bytes of codes + centres +
+ * posting ids on this rank ((N+K) M + 4N for world == 1).  Any may be NULL. */
+rii_status rii_get_info(const rii_index *idx, int64_t *N, int32_t *K, int64_t *theta, int64_t *n_local,
+                        int64_t *bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RII_H_ */

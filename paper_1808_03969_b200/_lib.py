@@ -1,0 +1,71 @@
+"""ctypes declarations of include/rii.h (argument marshalling only).
+
+The shared library is built in-tree by ``paper_1808_03969_b200.build``.  There is
+no CPU fallback: if the library cannot be loaded, or no CUDA device is usable,
+every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librii_b200.so")
+
+RII_OK, RII_ERR_ARG, RII_ERR_STATE, RII_ERR_OOM, RII_ERR_CUDA, RII_ERR_NCCL, RII_ERR_TRAIN = range(7)
+PATH_AUTO, PATH_LINEAR, PATH_IVF = 0, 1, 2
+MEM_HOST, MEM_DEVICE = 0, 1
+NCCL_ID_BYTES = 128
+
+# name -> (restype, argtypes); every symbol include/rii.h declares.
+_p, _i32, _i64, _u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64
+SIGNATURES = {
+    "rii_last_error": (C.c_char_p, []),
+    "rii_launch_count": (_u64, []),
+    "rii_nccl_unique_id": (C.c_int, [_p]),
+    "rii_create": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _i32, _p, C.POINTER(_p)]),
+    "rii_destroy": (None, [_p]),
+    "rii_train": (C.c_int, [_p, _p, _i64, _i32, _u64, C.c_int, _p]),
+    "rii_add": (C.c_int, [_p, _p, _i64, C.c_int, _p, C.POINTER(_i64)]),
+    "rii_reconfigure": (C.c_int, [_p, _i32, _i32, _u64, _p]),
+    "rii_query": (C.c_int, [_p, _p, _i64, _i32, _p, _i64, _i32, C.c_int, C.c_int, _p, _p, _p, C.POINTER(_i32)]),
+    "rii_partial_width": (_i32, [_i32]),
+    "rii_query_partial": (C.c_int, [_p, _p, _i64, _i32, _p, _i64, _i32, C.c_int, _p, _p, C.POINTER(_i32)]),
+    "rii_merge_partials": (C.c_int, [_p, _i32, _i64, _i32, _p, _p, _p]),
+    "rii_get_codebook": (C.c_int, [_p, _p]),
+    "rii_set_codebook": (C.c_int, [_p, _p]),
+    "rii_get_codes": (C.c_int, [_p, _i64, _i64, _p]),
+    "rii_get_centers": (C.c_int, [_p, _p]),
+    "rii_get_postings": (C.c_int, [_p, _p, _p]),
+    "rii_set_theta": (C.c_int, [_p, _i64]),
+    "rii_get_info": (C.c_int, [_p, C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_i64),
+                               C.POINTER(_i64)]),
+}
+
+_lib = None
+
+
+class RiiError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"rii status {status}: {msg}")
+        self.status = status
+
+
+def load(path: str = LIB_PATH):
+    """Load librii_b200.so (raises if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} not built; run `python -m paper_1808_03969_b200.build`")
+        lib = C.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def check(status: int):
+    if status != RII_OK:
+        raise RiiError(status, load().rii_last_error().decode())

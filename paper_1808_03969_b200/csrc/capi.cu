@@ -1,0 +1,698 @@
+// capi.cu -- the C ABI of include/rii.h: argument checks, the index state held in
+// HBM (Sec. 4.1), and the orchestration of the kernels of
+// k_scan.cu / k_ivf.cu / k_build.cu for train, add, reconfigure and query.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/rii.h"
+#include "comm.hpp"
+#include "kernels.cuh"
+
+namespace rii {
+std::atomic<uint64_t> g_launches{0};
+
+// Grow-only device buffer (scratch and index arrays).
+struct Buf {
+    void *p = nullptr;
+    size_t cap = 0;
+    Buf() = default;
+    Buf(const Buf &) = delete;
+    Buf &operator=(const Buf &) = delete;
+    ~Buf() { if (p) cudaFree(p); }
+    template <class T>
+    T *get(size_t count) {
+        const size_t b = std::max<size_t>(count * sizeof(T), 16);
+        if (b > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            RII_CUDA(cudaMalloc(&p, b));
+            cap = b;
+        }
+        return reinterpret_cast<T *>(p);
+    }
+    template <class T>
+    T *as() const { return reinterpret_cast<T *>(p); }
+    // keep the first `keep` bytes when growing
+    template <class T>
+    T *grow(size_t count, size_t keep, cudaStream_t st) {
+        const size_t b = std::max<size_t>(count * sizeof(T), 16);
+        if (b <= cap) return reinterpret_cast<T *>(p);
+        size_t nb = std::max(b, cap + cap / 2);
+        void *np = nullptr;
+        RII_CUDA(cudaMalloc(&np, nb));
+        if (keep) RII_CUDA(cudaMemcpyAsync(np, p, keep, cudaMemcpyDeviceToDevice, st));
+        RII_CUDA(cudaStreamSynchronize(st));
+        if (p) cudaFree(p);
+        p = np;
+        cap = nb;
+        return reinterpret_cast<T *>(p);
+    }
+};
+
+struct Seg {
+    int64_t local_off, global_first, count;
+};
+
+}  // namespace rii
+
+using namespace rii;
+
+struct rii_index {
+    int D = 0, M = 0, ds = 0, device = 0, rank = 0, world = 1, num_sms = 148;
+    void *comm = nullptr;
+    bool trained = false, T_valid = false;
+    Buf cb, T;
+    int64_t N = 0, n_local = 0;
+    Buf codes, assign;
+    std::vector<Seg> segs;
+    Buf seg_local, seg_global;
+    int64_t K = 0;
+    Buf centers, offsets, ids;
+    int64_t theta = -1;
+    // scratch (query side is const-callable: mutable)
+    mutable Buf s_q, s_S, s_pos, s_sub, s_part, s_keys, s_gather, s_d0, s_probe, s_roff, s_rids, s_rkey, s_rval,
+        s_out_ids, s_out_dist, s_flag, s_x;
+};
+
+namespace {
+thread_local std::string t_err;
+
+rii_status fail(int st, const std::string &msg) {
+    t_err = msg;
+    return (rii_status)st;
+}
+
+template <class F>
+rii_status guarded(F &&f) {
+    try {
+        t_err.clear();
+        f();
+        return RII_OK;
+    } catch (const rii::Error &e) {
+        return fail(e.status, e.what());
+    } catch (const std::bad_alloc &) {
+        return fail(RII_ERR_OOM, "host allocation failed");
+    } catch (const std::exception &e) {
+        return fail(RII_ERR_CUDA, e.what());
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        RII_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) RII_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+void arg_check(bool ok, const char *msg) {
+    if (!ok) throw Error(RII_ERR_ARG, msg);
+}
+void state_check(bool ok, const char *msg) {
+    if (!ok) throw Error(RII_ERR_STATE, msg);
+}
+
+IdMap local_map(const rii_index *x) {
+    IdMap m;
+    if (x->world == 1) return m;  // local position == global id
+    m.kind = 2;
+    m.seg_local = x->seg_local.as<int64_t>();
+    m.seg_global = x->seg_global.as<int64_t>();
+    m.nseg = (int)x->segs.size();
+    return m;
+}
+
+void upload_segs(rii_index *x, cudaStream_t st) {
+    std::vector<int64_t> lo, gl;
+    for (auto &s : x->segs) { lo.push_back(s.local_off); gl.push_back(s.global_first); }
+    int64_t *dl = x->seg_local.get<int64_t>(lo.size() + 1), *dg = x->seg_global.get<int64_t>(gl.size() + 1);
+    if (!lo.empty()) {
+        RII_CUDA(cudaMemcpyAsync(dl, lo.data(), lo.size() * 8, cudaMemcpyHostToDevice, st));
+        RII_CUDA(cudaMemcpyAsync(dg, gl.data(), gl.size() * 8, cudaMemcpyHostToDevice, st));
+    }
+    RII_CUDA(cudaStreamSynchronize(st));
+}
+
+void ensure_T(rii_index *x, cudaStream_t st) {
+    if (x->T_valid) return;
+    float *T = x->T.get<float>((size_t)x->M * KS * KS);
+    launch_sdc_tables(x->cb.as<float>(), x->D, x->M, T, st);
+    x->T_valid = true;
+}
+
+__global__ void iota_u32_kernel(uint32_t *v, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = (uint32_t)i;
+}
+
+__global__ void gather_i32_kernel(const int32_t *src, const int64_t *pos, int64_t n, int32_t *dst, uint32_t *val) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) { dst[i] = src[pos[i]]; val[i] = (uint32_t)pos[i]; }
+}
+
+__global__ void widen_ids_kernel(const uint32_t *src, int64_t n, IdMap map, int64_t *dst) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = map_id(map, src[i]);
+}
+
+__global__ void gather_u32pos_codes_kernel(const uint8_t *codes, int M, const uint32_t *pos, int64_t n, uint8_t *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int m = 0; m < M; ++m) out[i * M + m] = codes[(int64_t)pos[i] * M + m];
+}
+
+void rebuild_csr(rii_index *x, cudaStream_t st) {
+    uint32_t *vals = x->s_rval.get<uint32_t>(x->n_local + 1);
+    if (x->n_local > 0) {
+        iota_u32_kernel<<<(unsigned)ceil_div(x->n_local, 256), 256, 0, st>>>(vals, x->n_local);
+        RII_LAUNCHED();
+    }
+    int64_t *off = x->offsets.get<int64_t>(x->K + 1);
+    uint32_t *ids = x->ids.get<uint32_t>(x->n_local + 1);
+    build_csr(x->assign.as<int32_t>(), vals, x->n_local, x->K, off, ids, st);
+}
+
+// Rows [lo, hi) of this rank in a batch of n rows split into `world` chunks.
+void rank_rows(int64_t n, int rank, int world, int64_t &lo, int64_t &hi) {
+    const int64_t per = ceil_div(n, world);
+    lo = std::min<int64_t>(n, per * rank);
+    hi = std::min<int64_t>(n, lo + per);
+}
+
+// Target ids of this rank: global ids (device) and local positions (device).
+// world == 1: positions == ids (no copy).  Returns the local count.
+int64_t route_targets(const rii_index *x, const int64_t *S, int64_t nS, cudaStream_t st, const int64_t **S_local,
+                      const int64_t **pos_local) {
+    if (x->world == 1) {
+        *S_local = S;
+        *pos_local = S;
+        return nS;
+    }
+    std::vector<int64_t> hs((size_t)nS);
+    if (nS) RII_CUDA(cudaMemcpyAsync(hs.data(), S, (size_t)nS * 8, cudaMemcpyDeviceToHost, st));
+    RII_CUDA(cudaStreamSynchronize(st));
+    std::vector<int64_t> gl, lp;
+    for (auto &s : x->segs) {
+        auto b = std::lower_bound(hs.begin(), hs.end(), s.global_first);
+        auto e = std::lower_bound(hs.begin(), hs.end(), s.global_first + s.count);
+        for (auto it = b; it != e; ++it) { gl.push_back(*it); lp.push_back(*it - s.global_first + s.local_off); }
+    }
+    int64_t *dS = x->s_S.get<int64_t>(gl.size() + 1), *dP = x->s_pos.get<int64_t>(lp.size() + 1);
+    if (!gl.empty()) {
+        RII_CUDA(cudaMemcpyAsync(dS, gl.data(), gl.size() * 8, cudaMemcpyHostToDevice, st));
+        RII_CUDA(cudaMemcpyAsync(dP, lp.data(), lp.size() * 8, cudaMemcpyHostToDevice, st));
+    }
+    RII_CUDA(cudaStreamSynchronize(st));
+    *S_local = dS;
+    *pos_local = dP;
+    return (int64_t)gl.size();
+}
+
+struct QueryArgs {
+    const float *q;          // device
+    int64_t nq;
+    int topk, kk;
+    const int64_t *S;        // device global ids or nullptr
+    int64_t nS;
+    int L;
+    int path;                // resolved LINEAR / IVF
+};
+
+int resolve_path(const rii_index *x, int64_t nS_global, bool has_S, int L, rii_path path) {
+    if (x->K == 0) {
+        state_check(path != RII_PATH_IVF, "inverted-index path requested but the index has no coarse centres (K == 0)");
+        return RII_PATH_LINEAR;
+    }
+    if (path != RII_PATH_AUTO) return path;
+    const int64_t ns = has_S ? nS_global : x->N;
+    const int64_t th = x->theta >= 0 ? x->theta : ceil_div((int64_t)L * x->N, x->K) + x->K;  // R3
+    return ns < th ? RII_PATH_LINEAR : RII_PATH_IVF;  // Alg. 3 L1
+}
+
+// Local search; writes either the final result (world == 1, out_keys == nullptr)
+// or this rank's top-kk keys with global ids (out_keys, device [nq][kk]).
+void search_local(const rii_index *x, const QueryArgs &a, cudaStream_t st, int64_t *out_ids, float *out_dist,
+                  uint64_t *out_keys) {
+    const int kk = a.kk;
+    const float *cb = x->cb.as<float>();
+    const uint8_t *codes = x->codes.as<uint8_t>();
+    IdMap map = local_map(x);
+    const uint64_t *parts = nullptr;
+    int64_t q_stride = kk, p_stride = kk;
+    int nparts = 1;
+    if (a.path == RII_PATH_LINEAR) {
+        const uint8_t *scan_codes = codes;
+        int64_t n_codes = x->n_local;
+        if (a.S) {
+            const int64_t *S_loc = nullptr, *pos = nullptr;
+            n_codes = route_targets(x, a.S, a.nS, st, &S_loc, &pos);
+            uint8_t *sub = x->s_sub.get<uint8_t>((size_t)std::max<int64_t>(n_codes, 1) * x->M + 64);
+            launch_gather_codes(codes, x->M, pos, n_codes, sub, st);
+            scan_codes = sub;
+            map = IdMap();
+            map.kind = 1;
+            map.table = S_loc;
+        }
+        if (n_codes == 0) {
+            uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
+            RII_CUDA(cudaMemsetAsync(pp, 0xff, (size_t)a.nq * kk * 8, st));
+            parts = pp;
+        } else {
+            ScanPlan pl = plan_linear(x->M, kk, a.nq, n_codes, x->num_sms);
+            uint64_t *pp = x->s_part.get<uint64_t>((size_t)pl.nb * pl.B * pl.nc * kk);
+            launch_linear_scan(pl, scan_codes, n_codes, x->M, a.q, a.nq, cb, x->D, kk, pp, st);
+            parts = pp;
+            q_stride = (int64_t)pl.nc * kk;
+            p_stride = kk;
+            nparts = pl.nc;
+        }
+    } else {
+        const int64_t P = a.S ? std::min<int64_t>(x->K, ceil_div((int64_t)a.L * x->N, std::max<int64_t>(a.nS, 1)))
+                              : std::min<int64_t>(a.L, x->K);  // P:492-502, R1
+        float *d0 = x->s_d0.get<float>((size_t)a.nq * x->K);
+        launch_coarse_dist(x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, d0, st);
+        int32_t *probes = x->s_probe.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
+        launch_select_probes(d0, a.nq, x->K, P, probes, st);
+        const int64_t *off = x->offsets.as<int64_t>();
+        const uint32_t *ids = x->ids.as<uint32_t>();
+        if (a.S) {  // restrict the posting lists to S once per call (R7)
+            const int64_t *S_loc = nullptr, *pos = nullptr;
+            const int64_t n_loc = route_targets(x, a.S, a.nS, st, &S_loc, &pos);
+            int32_t *rk = x->s_rkey.get<int32_t>(n_loc + 1);
+            uint32_t *rv = x->s_rval.get<uint32_t>(n_loc + 1);
+            if (n_loc > 0) {
+                gather_i32_kernel<<<(unsigned)ceil_div(n_loc, 256), 256, 0, st>>>(x->assign.as<int32_t>(), pos, n_loc,
+                                                                                 rk, rv);
+                RII_LAUNCHED();
+            }
+            int64_t *roff = x->s_roff.get<int64_t>(x->K + 1);
+            uint32_t *rids = x->s_rids.get<uint32_t>(n_loc + 1);
+            build_csr(rk, rv, n_loc, x->K, roff, rids, st);
+            off = roff;
+            ids = rids;
+        }
+        uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
+        launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st);
+        parts = pp;
+    }
+    launch_merge(parts, q_stride, p_stride, nparts, a.nq, kk, a.topk, map, out_ids, out_dist, out_keys, st);
+}
+
+void check_targets(const rii_index *x, const int64_t *S, int64_t nS, cudaStream_t st) {
+    if (!S || nS == 0) return;
+    int *flag = x->s_flag.get<int>(1);
+    RII_CUDA(cudaMemsetAsync(flag, 0, 4, st));
+    launch_validate_targets(S, nS, x->N, flag, st);
+    int h = 0;
+    RII_CUDA(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, st));
+    RII_CUDA(cudaStreamSynchronize(st));
+    arg_check(h == 0, "target_ids must be strictly ascending and inside [0, N)");
+}
+
+void common_query_checks(const rii_index *x, int64_t nq, int topk, const int64_t *S, int64_t nS, int L,
+                         rii_path path) {
+    arg_check(x != nullptr, "index is NULL");
+    state_check(x->trained, "index has no code book (call rii_train or rii_set_codebook)");
+    arg_check(nq >= 0, "nq must be >= 0");
+    arg_check(topk >= 1 && topk <= 1024, "topk must be in [1, 1024]");
+    arg_check(!S || nS >= 0, "n_target must be >= 0");
+    arg_check(!S || nS <= x->N, "n_target larger than N");
+    arg_check(L >= 1, "L must be >= 1");
+    arg_check(path == RII_PATH_AUTO || path == RII_PATH_LINEAR || path == RII_PATH_IVF, "unknown path");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *rii_last_error(void) { return t_err.c_str(); }
+
+uint64_t rii_launch_count(void) { return g_launches.load(); }
+
+int32_t rii_partial_width(int32_t topk) { return partial_width(topk); }
+
+rii_status rii_nccl_unique_id(void *out) {
+    return guarded([&] {
+        arg_check(out != nullptr, "out is NULL");
+        nccl_unique_id(out);
+    });
+}
+
+rii_status rii_create(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t rank, int32_t world,
+                      const void *nccl_id, rii_index **out) {
+    if (out) *out = nullptr;
+    return guarded([&] {
+        arg_check(out != nullptr, "out is NULL");
+        arg_check(M >= 1 && M <= 64, "M must be in [1, 64]");
+        arg_check(D >= M && D % M == 0, "D must be a positive multiple of M");
+        arg_check(D / M <= 64, "D / M must be <= 64");
+        arg_check(Ks == 256, "Ks must be 256 (one byte per subspace, P:287)");
+        arg_check(world >= 1 && rank >= 0 && rank < world, "need 0 <= rank < world");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw Error(RII_ERR_CUDA, "no CUDA device");
+        arg_check(device >= 0 && device < ndev, "device ordinal out of range");
+        DeviceGuard g(device);
+        auto *x = new rii_index();
+        x->D = D;
+        x->M = M;
+        x->ds = D / M;
+        x->device = device;
+        x->rank = rank;
+        x->world = world;
+        RII_CUDA(cudaDeviceGetAttribute(&x->num_sms, cudaDevAttrMultiProcessorCount, device));
+        try {
+            x->cb.get<float>((size_t)M * KS * x->ds);
+            if (world > 1 && nccl_id) x->comm = nccl_init(nccl_id, rank, world);
+        } catch (...) {
+            delete x;
+            throw;
+        }
+        *out = x;
+    });
+}
+
+void rii_destroy(rii_index *x) {
+    if (!x) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(x->device);
+    nccl_destroy(x->comm);
+    delete x;
+    if (prev >= 0) cudaSetDevice(prev);
+}
+
+rii_status rii_train(rii_index *x, const float *xs, int64_t n, int32_t n_iter, uint64_t seed, rii_mem where,
+                     void *stream) {
+    return guarded([&] {
+        arg_check(x && xs, "NULL argument");
+        arg_check(n_iter >= 0, "n_iter must be >= 0");
+        state_check(x->N == 0, "the code book can only be (re)trained while the index is empty");
+        if (n < KS) throw Error(RII_ERR_TRAIN, "training needs n >= 256 rows");
+        DeviceGuard g(x->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        const float *dx = xs;
+        if (where == RII_MEM_HOST) {
+            float *b = x->s_x.get<float>((size_t)n * x->D);
+            RII_CUDA(cudaMemcpyAsync(b, xs, (size_t)n * x->D * 4, cudaMemcpyHostToDevice, st));
+            dx = b;
+        }
+        int *err = x->s_flag.get<int>(1);
+        RII_CUDA(cudaMemsetAsync(err, 0, 4, st));
+        Buf tmp;
+        float *cb = tmp.get<float>((size_t)x->M * KS * x->ds);
+        run_train(dx, n, x->D, x->M, n_iter, seed, cb, err, st);
+        int h = 0;
+        RII_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, st));
+        RII_CUDA(cudaStreamSynchronize(st));
+        if (h) throw Error(RII_ERR_TRAIN, "fewer than 256 distinct sub-vectors in some subspace");
+        RII_CUDA(cudaMemcpyAsync(x->cb.as<float>(), cb, (size_t)x->M * KS * x->ds * 4, cudaMemcpyDeviceToDevice, st));
+        RII_CUDA(cudaStreamSynchronize(st));
+        x->trained = true;
+        x->T_valid = false;
+    });
+}
+
+rii_status rii_set_codebook(rii_index *x, const float *cb) {
+    return guarded([&] {
+        arg_check(x && cb, "NULL argument");
+        state_check(x->N == 0, "the code book can only be set while the index is empty");
+        DeviceGuard g(x->device);
+        RII_CUDA(cudaMemcpy(x->cb.as<float>(), cb, (size_t)x->M * KS * x->ds * 4, cudaMemcpyHostToDevice));
+        x->trained = true;
+        x->T_valid = false;
+    });
+}
+
+rii_status rii_get_codebook(const rii_index *x, float *out) {
+    return guarded([&] {
+        arg_check(x && out, "NULL argument");
+        state_check(x->trained, "no code book");
+        DeviceGuard g(x->device);
+        RII_CUDA(cudaMemcpy(out, x->cb.as<float>(), (size_t)x->M * KS * x->ds * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+rii_status rii_add(rii_index *x, const float *xs, int64_t n, rii_mem where, void *stream, int64_t *first_id) {
+    return guarded([&] {
+        arg_check(x != nullptr, "index is NULL");
+        arg_check(n >= 0 && (n == 0 || xs), "bad x / n");
+        state_check(x->trained, "index has no code book");
+        arg_check(x->N + n < (1ll << 32), "at most 2^32 ids");
+        DeviceGuard g(x->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        const int64_t first = x->N;
+        if (first_id) *first_id = first;
+        int64_t lo, hi;
+        rank_rows(n, x->rank, x->world, lo, hi);
+        const int64_t cnt = hi - lo;
+        if (cnt > 0) {
+            uint8_t *codes = x->codes.grow<uint8_t>((size_t)(x->n_local + cnt) * x->M, (size_t)x->n_local * x->M, st);
+            const int64_t chunk = (int64_t)1 << 22;  // bound the staging buffer for host input
+            for (int64_t s = lo; s < hi; s += chunk) {
+                const int64_t e = std::min(hi, s + chunk);
+                const float *dx = xs + s * x->D;
+                if (where == RII_MEM_HOST) {
+                    float *b = x->s_x.get<float>((size_t)(e - s) * x->D);
+                    RII_CUDA(cudaMemcpyAsync(b, dx, (size_t)(e - s) * x->D * 4, cudaMemcpyHostToDevice, st));
+                    dx = b;
+                }
+                launch_encode(dx, e - s, x->D, x->M, x->cb.as<float>(), codes + (x->n_local + (s - lo)) * x->M, st);
+            }
+            if (x->K > 0) {
+                ensure_T(x, st);
+                int32_t *as = x->assign.grow<int32_t>((size_t)(x->n_local + cnt), (size_t)x->n_local * 4, st);
+                launch_assign(codes + x->n_local * x->M, cnt, x->centers.as<uint8_t>(), x->K, x->M, x->T.as<float>(),
+                              as + x->n_local, nullptr, st);
+            }
+            x->segs.push_back({x->n_local, first + lo, cnt});
+            x->n_local += cnt;
+            upload_segs(x, st);
+            if (x->K > 0) rebuild_csr(x, st);  // PushBack(W_a(n), n): lists stay ascending
+        }
+        x->N += n;
+        RII_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+rii_status rii_reconfigure(rii_index *x, int32_t nlist, int32_t n_iter, uint64_t seed, void *stream) {
+    return guarded([&] {
+        arg_check(x != nullptr, "index is NULL");
+        state_check(x->trained, "index has no code book");
+        arg_check(nlist >= 1 && nlist <= x->N, "nlist must be in [1, N]");
+        arg_check(n_iter >= 0, "n_iter must be >= 0");
+        DeviceGuard g(x->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        ensure_T(x, st);
+        const int M = x->M;
+        const int64_t ns = std::min<int64_t>(x->N, (int64_t)100 * nlist);
+        Buf pos_b, X_b;
+        uint8_t *X = X_b.get<uint8_t>((size_t)ns * M);
+        if (x->world == 1) {
+            uint32_t *pos = pos_b.get<uint32_t>(ns);
+            select_sample(x->n_local, IdMap(), ns, seed, pos, st);
+            gather_u32pos_codes_kernel<<<(unsigned)ceil_div(ns, 256), 256, 0, st>>>(x->codes.as<uint8_t>(), M, pos, ns,
+                                                                                   X);
+            RII_LAUNCHED();
+        } else {
+            state_check(x->comm != nullptr, "multi-rank reconfigure needs an NCCL communicator");
+            // each rank contributes its ns smallest keys; the global ns smallest are
+            // selected identically on every rank after an all-gather.
+            const int64_t nl = std::min<int64_t>(x->n_local, ns);
+            Buf lk, lc, gk, gc, sk, sv, iv;
+            uint32_t *pos = pos_b.get<uint32_t>(std::max<int64_t>(nl, 1));
+            uint64_t *keys = lk.get<uint64_t>(ns);
+            uint8_t *lcodes = lc.get<uint8_t>((size_t)ns * M);
+            RII_CUDA(cudaMemsetAsync(keys, 0xff, (size_t)ns * 8, st));
+            RII_CUDA(cudaMemsetAsync(lcodes, 0, (size_t)ns * M, st));
+            if (nl > 0) {
+                select_sample(x->n_local, local_map(x), nl, seed, pos, st);
+                gather_u32pos_codes_kernel<<<(unsigned)ceil_div(nl, 256), 256, 0, st>>>(x->codes.as<uint8_t>(), M,
+                                                                                        pos, nl, lcodes);
+                RII_LAUNCHED();
+                sample_keys_for_positions(x->n_local, local_map(x), pos, nl, seed, keys, st);
+            }
+            uint64_t *gkeys = gk.get<uint64_t>((size_t)ns * x->world);
+            uint8_t *gcodes = gc.get<uint8_t>((size_t)ns * x->world * M);
+            nccl_allgather_u64(x->comm, keys, gkeys, (size_t)ns, st);
+            nccl_allgather_u8(x->comm, lcodes, gcodes, (size_t)ns * M, st);
+            const int64_t tot = ns * x->world;
+            uint32_t *order = sv.get<uint32_t>(tot);
+            sort_keys_with_index(gkeys, tot, order, st);
+            gather_u32pos_codes_kernel<<<(unsigned)ceil_div(ns, 256), 256, 0, st>>>(gcodes, M, order, ns, X);
+            RII_LAUNCHED();
+        }
+        Buf newc;
+        uint8_t *C = newc.get<uint8_t>((size_t)nlist * M);
+        int *err = x->s_flag.get<int>(1);
+        RII_CUDA(cudaMemsetAsync(err, 0, 4, st));
+        run_pqkmeans(X, ns, nlist, M, x->T.as<float>(), n_iter, C, err, st);
+        int h = 0;
+        RII_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, st));
+        RII_CUDA(cudaStreamSynchronize(st));
+        arg_check(h == 0, "fewer than nlist distinct codes in the reconfigure sample");
+        uint8_t *cent = x->centers.get<uint8_t>((size_t)nlist * M);
+        RII_CUDA(cudaMemcpyAsync(cent, C, (size_t)nlist * M, cudaMemcpyDeviceToDevice, st));
+        x->K = nlist;
+        int32_t *as = x->assign.get<int32_t>(x->n_local + 1);
+        launch_assign(x->codes.as<uint8_t>(), x->n_local, cent, x->K, M, x->T.as<float>(), as, nullptr, st);
+        rebuild_csr(x, st);
+        x->theta = -1;
+        RII_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+static rii_status query_impl(const rii_index *x, const float *q, int64_t nq, int32_t topk, const int64_t *S,
+                             int64_t nS, int32_t L, rii_path path, rii_mem where, void *stream, int64_t *out_ids,
+                             float *out_dist, int32_t *path_used, uint64_t *out_keys) {
+    return guarded([&] {
+        common_query_checks(x, nq, topk, S, nS, L, path);
+        DeviceGuard g(x->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        const int used = resolve_path(x, nS, S != nullptr, L, path);
+        if (path_used) *path_used = used;
+        if (nq == 0) return;
+        arg_check(q && (out_keys || (out_ids && out_dist)), "NULL argument");
+        const bool host = where == RII_MEM_HOST && !out_keys;
+        const float *dq = q;
+        const int64_t *dS = S;
+        if (host) {
+            float *b = x->s_q.get<float>((size_t)nq * x->D);
+            RII_CUDA(cudaMemcpyAsync(b, q, (size_t)nq * x->D * 4, cudaMemcpyHostToDevice, st));
+            dq = b;
+            if (S && nS > 0) {
+                int64_t *sb = x->s_gather.get<int64_t>(nS);
+                RII_CUDA(cudaMemcpyAsync(sb, S, (size_t)nS * 8, cudaMemcpyHostToDevice, st));
+                dS = sb;
+            }
+        }
+        check_targets(x, dS, S ? nS : 0, st);
+        QueryArgs a{dq, nq, topk, partial_width(topk), S ? dS : nullptr, S ? nS : 0, L, used};
+        if (S && nS == 0) {  // empty subset: nothing to return but padding
+            a.S = dS;
+        }
+        int64_t *oid = out_ids;
+        float *od = out_dist;
+        if (host) {
+            oid = x->s_out_ids.get<int64_t>((size_t)nq * topk);
+            od = x->s_out_dist.get<float>((size_t)nq * topk);
+        }
+        if (out_keys) {
+            search_local(x, a, st, nullptr, nullptr, out_keys);
+        } else if (x->world == 1) {
+            search_local(x, a, st, oid, od, nullptr);
+        } else {
+            state_check(x->comm != nullptr,
+                        "detached shard (world > 1, no NCCL id): use rii_query_partial + rii_merge_partials");
+            const int kk = a.kk;
+            uint64_t *lk = x->s_keys.get<uint64_t>((size_t)nq * kk * (x->world + 1));
+            uint64_t *gk = lk + (size_t)nq * kk;
+            search_local(x, a, st, nullptr, nullptr, lk);
+            nccl_allgather_u64(x->comm, lk, gk, (size_t)nq * kk, st);
+            launch_merge(gk, kk, (int64_t)nq * kk, x->world, nq, kk, topk, IdMap(), oid, od, nullptr, st);
+        }
+        if (host) {
+            RII_CUDA(cudaMemcpyAsync(out_ids, oid, (size_t)nq * topk * 8, cudaMemcpyDeviceToHost, st));
+            RII_CUDA(cudaMemcpyAsync(out_dist, od, (size_t)nq * topk * 4, cudaMemcpyDeviceToHost, st));
+        }
+        RII_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+rii_status rii_query(const rii_index *x, const float *q, int64_t nq, int32_t topk, const int64_t *target_ids,
+                     int64_t n_target, int32_t L, rii_path path, rii_mem where, void *stream, int64_t *out_ids,
+                     float *out_dist, int32_t *path_used) {
+    return query_impl(x, q, nq, topk, target_ids, n_target, L, path, where, stream, out_ids, out_dist, path_used,
+                      nullptr);
+}
+
+rii_status rii_query_partial(const rii_index *x, const float *q, int64_t nq, int32_t topk, const int64_t *target_ids,
+                             int64_t n_target, int32_t L, rii_path path, void *stream, uint64_t *out_keys,
+                             int32_t *path_used) {
+    return query_impl(x, q, nq, topk, target_ids, n_target, L, path, RII_MEM_DEVICE, stream, nullptr, nullptr,
+                      path_used, out_keys);
+}
+
+rii_status rii_merge_partials(const uint64_t *keys, int32_t parts, int64_t nq, int32_t topk, void *stream,
+                              int64_t *out_ids, float *out_dist) {
+    return guarded([&] {
+        arg_check(keys && out_ids && out_dist, "NULL argument");
+        arg_check(parts >= 1 && nq >= 0 && topk >= 1 && topk <= 1024, "bad parts / nq / topk");
+        const int kk = partial_width(topk);
+        cudaStream_t st = (cudaStream_t)stream;
+        launch_merge(keys, kk, (int64_t)nq * kk, parts, nq, kk, topk, IdMap(), out_ids, out_dist, nullptr, st);
+        RII_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+rii_status rii_get_codes(const rii_index *x, int64_t first, int64_t n, uint8_t *out) {
+    return guarded([&] {
+        arg_check(x && (n == 0 || out), "NULL argument");
+        arg_check(first >= 0 && n >= 0 && first + n <= x->N, "range outside [0, N)");
+        DeviceGuard g(x->device);
+        int64_t done = 0;
+        for (auto &s : x->segs) {  // copy the parts of [first, first+n) stored here
+            const int64_t a = std::max(first, s.global_first), b = std::min(first + n, s.global_first + s.count);
+            if (a >= b) continue;
+            RII_CUDA(cudaMemcpy(out + (a - first) * x->M, x->codes.as<uint8_t>() + (a - s.global_first + s.local_off) * x->M,
+                                (size_t)(b - a) * x->M, cudaMemcpyDeviceToHost));
+            done += b - a;
+        }
+        arg_check(done == n, "part of the requested range is stored on another rank");
+    });
+}
+
+rii_status rii_get_centers(const rii_index *x, uint8_t *out) {
+    return guarded([&] {
+        arg_check(x && out, "NULL argument");
+        DeviceGuard g(x->device);
+        if (x->K) RII_CUDA(cudaMemcpy(out, x->centers.as<uint8_t>(), (size_t)x->K * x->M, cudaMemcpyDeviceToHost));
+    });
+}
+
+rii_status rii_get_postings(const rii_index *x, int64_t *offsets, int64_t *ids) {
+    return guarded([&] {
+        arg_check(x && offsets && ids, "NULL argument");
+        state_check(x->K > 0, "no posting lists (K == 0)");
+        DeviceGuard g(x->device);
+        RII_CUDA(cudaMemcpy(offsets, x->offsets.as<int64_t>(), (size_t)(x->K + 1) * 8, cudaMemcpyDeviceToHost));
+        if (x->n_local) {
+            Buf w;
+            int64_t *d = w.get<int64_t>(x->n_local);
+            widen_ids_kernel<<<(unsigned)ceil_div(x->n_local, 256), 256>>>(x->ids.as<uint32_t>(), x->n_local,
+                                                                           local_map(x), d);
+            RII_LAUNCHED();
+            RII_CUDA(cudaMemcpy(ids, d, (size_t)x->n_local * 8, cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
+rii_status rii_set_theta(rii_index *x, int64_t theta) {
+    return guarded([&] {
+        arg_check(x != nullptr, "index is NULL");
+        x->theta = theta < 0 ? -1 : theta;
+    });
+}
+
+rii_status rii_get_info(const rii_index *x, int64_t *N, int32_t *K, int64_t *theta, int64_t *n_local,
+                        int64_t *bytes) {
+    return guarded([&] {
+        arg_check(x != nullptr, "index is NULL");
+        if (N) *N = x->N;
+        if (K) *K = (int32_t)x->K;
+        if (theta) *theta = x->theta;
+        if (n_local) *n_local = x->n_local;
+        if (bytes) *bytes = x->n_local * x->M + x->K * x->M + (x->K ? 4 * x->n_local : 0);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// common.cuh -- shared device helpers of the B200 Rii library (sm_100a only).
+// Canonical arithmetic CA1/CA2 and the (dist, id) key order follow DESIGN.md
+// "Readings" (CA1: P:292-294; CA2: Eq. 2; CA4: ties to the lowest id).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "error.hpp"
+
+namespace rii {
+
+constexpr int KS = 256;                      // code words per subspace
+constexpr uint64_t KEY_MAX = ~0ull;          // empty candidate slot
+constexpr int NT = 256;                      // threads per CTA of the scan kernels
+
+// ---------------------------------------------------------------- errors ---
+#define RII_CUDA(call)                                                                            \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            throw ::rii::Error(e_ == cudaErrorMemoryAllocation ? 3 : 4,                           \
+                               std::string(#call) + ": " + cudaGetErrorString(e_));               \
+    } while (0)
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(int n = 1) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+#define RII_LAUNCHED()                                                                            \
+    do {                                                                                          \
+        ::rii::count_launch();                                                                    \
+        RII_CUDA(cudaGetLastError());                                                             \
+    } while (0)
+
+// -------------------------------------------------------- arithmetic ------
+// CA1: t = u - c; acc = acc + t*t; fp32 round-to-nearest, no contraction.
+__device__ __forceinline__ float ca1_step(float acc, float u, float c) {
+    float t = __fsub_rn(u, c);
+    return __fadd_rn(acc, __fmul_rn(t, t));
+}
+
+// (dist, id) packed so that unsigned order == (dist asc, id asc) for dist >= +0.
+__device__ __forceinline__ uint64_t make_key(float d, uint32_t id) {
+    return ((uint64_t)__float_as_uint(d) << 32) | (uint64_t)id;
+}
+__device__ __forceinline__ float key_dist(uint64_t k) { return __uint_as_float((uint32_t)(k >> 32)); }
+__device__ __forceinline__ uint32_t key_id(uint64_t k) { return (uint32_t)(k & 0xffffffffu); }
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// splitmix64 finaliser (counter-based hash for every seeded choice, R8 / R10).
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+inline int next_pow2(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+// Width of the per-query candidate lists kept by every kernel: a power of two
+// with at least 16 slots of slack above topk.
+inline int partial_width(int topk) { return next_pow2(topk + 16 < 32 ? 32 : topk + 16); }
+
+// Mapping of the 32-bit candidate index stored in a key to a global id.
+struct IdMap {
+    int kind = 0;                 // 0 identity, 1 table (int64 global ids), 2 ranges
+    const int64_t *table = nullptr;
+    const int64_t *seg_local = nullptr;  // ranges: local offset of each segment (ascending)
+    const int64_t *seg_global = nullptr; // ranges: global id of the segment's first code
+    int nseg = 0;
+};
+
+__device__ __forceinline__ int64_t map_id(const IdMap &m, uint32_t i) {
+    if (m.kind == 0) return (int64_t)i;
+    if (m.kind == 1) return m.table[i];
+    int lo = 0, hi = m.nseg - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (m.seg_local[mid] <= (int64_t)i) lo = mid; else hi = mid - 1;
+    }
+    return m.seg_global[lo] + ((int64_t)i - m.seg_local[lo]);
+}
+
+}  // namespace rii

@@ -1,0 +1,338 @@
+// k_ivf.cu -- inverted-index search (Alg. 2 InvertedIndex) on sm_100a.
+//
+//  coarse_dist   : d0[q][k] = CA2 ADC of q to every centre code cbar_k (L2-L5).
+//  select_probes : per query, radix-select the P smallest (d0, k)   (L6, reading R1).
+//  ivf_scan      : one CTA per query pair; warps pull (query, list) work items
+//                  from a shared counter and stream the list's ids (coalesced)
+//                  and codes (16-byte gathers from the linear array),
+//                  evaluate ADC with the lane-rotated table of k_scan.cu and keep
+//                  the top-kk in shared memory (L7-L16, mode A of reading R2).
+#include "kernels.cuh"
+#include "topk.cuh"
+
+namespace rii {
+
+constexpr int CQ = 4;  // queries per CTA in coarse_dist
+
+__global__ void __launch_bounds__(NT) coarse_dist_kernel(const uint8_t *__restrict__ centers, int64_t K, int M,
+                                                         const float *__restrict__ q, int64_t nq,
+                                                         const float *__restrict__ cb, int ds,
+                                                         float *__restrict__ d0) {
+    extern __shared__ __align__(16) float clut[];  // [CQ][M][256]
+    const int64_t q0 = (int64_t)blockIdx.y * CQ;
+    const int D = M * ds;
+    for (int e = threadIdx.x; e < CQ * M * KS; e += blockDim.x) {
+        const int qq = e / (M * KS), m = (e / KS) % M, z = e % KS;
+        const int64_t qi = min(q0 + qq, nq - 1);
+        const float *qv = q + qi * D + m * ds, *cv = cb + ((size_t)m * KS + z) * ds;
+        float a = 0.f;
+        for (int j = 0; j < ds; ++j) a = ca1_step(a, qv[j], cv[j]);
+        clut[e] = a;
+    }
+    __syncthreads();
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t *cp = centers + k * M;
+        float acc[CQ];
+#pragma unroll
+        for (int qq = 0; qq < CQ; ++qq) acc[qq] = 0.f;
+        for (int m = 0; m < M; ++m) {
+            const int z = cp[m];
+#pragma unroll
+            for (int qq = 0; qq < CQ; ++qq) acc[qq] = __fadd_rn(acc[qq], clut[(qq * M + m) * KS + z]);
+        }
+#pragma unroll
+        for (int qq = 0; qq < CQ; ++qq)
+            if (q0 + qq < nq) d0[(q0 + qq) * K + k] = acc[qq];
+    }
+}
+
+void launch_coarse_dist(const uint8_t *centers, int64_t K, int M, const float *q, int64_t nq, const float *cb, int D,
+                        float *d0, cudaStream_t st) {
+    if (nq <= 0 || K <= 0) return;
+    const size_t smem = (size_t)CQ * M * KS * 4;
+    RII_CUDA(cudaFuncSetAttribute(coarse_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((unsigned)std::min<int64_t>(ceil_div(K, NT), 16), (unsigned)ceil_div(nq, CQ));
+    coarse_dist_kernel<<<grid, NT, smem, st>>>(centers, K, M, q, nq, cb, D / M, d0);
+    RII_LAUNCHED();
+}
+
+// Block-wide exclusive prefix over a 0/1 flag per thread (NT threads).
+__device__ __forceinline__ int block_excl_scan(int flag, int *wsum, int &total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < NT / 32; ++w) {
+        if (w < warp) off += wsum[w];
+        tot += wsum[w];
+    }
+    __syncthreads();
+    total = tot;
+    return off + __popc(bal & ((1u << lane) - 1u));
+}
+
+// Radix select of the P smallest (d0 bits, k) per query; output in ascending k.
+__global__ void __launch_bounds__(NT) select_probes_kernel(const float *__restrict__ d0, int64_t K, int64_t P,
+                                                           int32_t *__restrict__ probes) {
+    __shared__ int hist[256];
+    __shared__ uint32_t s_prefix, s_mask;
+    __shared__ int64_t s_rem;
+    __shared__ int wsum[NT / 32];
+    const int64_t qi = blockIdx.x;
+    const uint32_t *u = reinterpret_cast<const uint32_t *>(d0 + qi * K);
+    int32_t *outp = probes + qi * P;
+    if (P >= K) {  // every list: order does not matter under mode A
+        for (int64_t k = threadIdx.x; k < K; k += NT) outp[k] = (int32_t)k;
+        return;
+    }
+    if (threadIdx.x == 0) { s_prefix = 0; s_mask = 0; s_rem = P; }
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0;
+        __syncthreads();
+        const uint32_t pre = s_prefix, msk = s_mask;
+        for (int64_t k = threadIdx.x; k < K; k += NT) {
+            const uint32_t v = u[k];
+            if ((v & msk) == pre) atomicAdd(&hist[(v >> shift) & 255], 1);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t rem = s_rem, acc = 0;
+            int d = 0;
+            for (; d < 256; ++d) {
+                if (acc + hist[d] >= rem) break;
+                acc += hist[d];
+            }
+            s_rem = rem - acc;
+            s_prefix = pre | ((uint32_t)d << shift);
+            s_mask = msk | (255u << shift);
+        }
+        __syncthreads();
+    }
+    const uint32_t t = s_prefix;
+    const int64_t ties = s_rem;  // how many keys equal to t are taken (lowest k first)
+    int64_t tie_base = 0, out_base = 0;
+    for (int64_t k0 = 0; k0 < K; k0 += NT) {
+        const int64_t k = k0 + threadIdx.x;
+        const uint32_t v = k < K ? u[k] : 0xffffffffu;
+        const int is_tie = (k < K && v == t) ? 1 : 0;
+        int ntie;
+        const int tie_rank = block_excl_scan(is_tie, wsum, ntie);
+        const int take = (k < K && (v < t || (is_tie && tie_base + tie_rank < ties))) ? 1 : 0;
+        int ntake;
+        const int pos = block_excl_scan(take, wsum, ntake);
+        if (take) outp[out_base + pos] = (int32_t)k;
+        tie_base += ntie;
+        out_base += ntake;
+    }
+}
+
+void launch_select_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int32_t *probes, cudaStream_t st) {
+    if (nq <= 0) return;
+    select_probes_kernel<<<(unsigned)nq, NT, 0, st>>>(d0, K, P, probes);
+    RII_LAUNCHED();
+}
+
+// ----------------------------------------------------------- list scan -----
+template <int W>
+__device__ __forceinline__ void load_code_ivf(const uint8_t *p, uint32_t (&w)[W]) {
+    if constexpr (W == 8) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
+        const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    } else if constexpr (W == 4) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+    } else if constexpr (W == 2) {
+        const uint2 a = __ldg(reinterpret_cast<const uint2 *>(p));
+        w[0] = a.x; w[1] = a.y;
+    } else {
+        w[0] = __ldg(reinterpret_cast<const uint32_t *>(p));
+    }
+}
+
+constexpr int PAIR_BYTES = 256 * 256;
+
+// Per-warp work pulling: (qq, r) items = query half qq, probe rank r.
+struct ListCursor {
+    int64_t beg, end;
+    int qq;
+    bool done;
+};
+
+__device__ __forceinline__ void next_list(ListCursor &c, int *s_next, int64_t P, int64_t q0, int64_t nq,
+                                          const int32_t *probes, const int64_t *offsets, int lane) {
+    while (!c.done && c.beg >= c.end) {
+        int it = 0;
+        if (lane == 0) it = atomicAdd(s_next, 1);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if ((int64_t)it >= 2 * P) { c.done = true; break; }
+        const int qq = it & 1;
+        const int64_t r = it >> 1, qi = q0 + qq;
+        if (qi >= nq) continue;
+        const int32_t k = probes[qi * P + r];
+        c.qq = qq;
+        c.beg = offsets[k];
+        c.end = offsets[k + 1];
+    }
+}
+
+template <int M, bool FAST>
+__global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict__ codes, const float *__restrict__ q,
+                                                      int64_t nq, const float *__restrict__ cb, int Mrt, int ds,
+                                                      int kk, const int32_t *__restrict__ probes, int64_t P,
+                                                      const int64_t *__restrict__ offsets,
+                                                      const uint32_t *__restrict__ ids, uint64_t *__restrict__ out) {
+    constexpr int W = FAST ? M / 4 : 1;
+    const int MM = FAST ? M : Mrt;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const size_t lut_bytes = FAST ? (size_t)PAIR_BYTES : (size_t)2 * MM * KS * 4;
+    uint8_t *lut = smem;
+    uint64_t *top = reinterpret_cast<uint64_t *>(smem + lut_bytes);
+    uint64_t *fresh = top + 2 * kk;
+    int *cnt = reinterpret_cast<int *>(fresh + 2 * NEWCAP);
+    float *thr = reinterpret_cast<float *>(cnt + 2);
+    int *scratch = reinterpret_cast<int *>(thr + 2);
+    int *s_next = scratch + 2;
+
+    const int64_t q0 = (int64_t)blockIdx.x * 2;
+    const int D = MM * ds, tid = threadIdx.x, lane = tid & 31;
+    const float *qa = q + min(q0, nq - 1) * D, *qb = q + min(q0 + 1, nq - 1) * D;
+    if constexpr (FAST) {
+        const int m = lane & (M - 1);
+        float *lp = reinterpret_cast<float *>(lut);
+        for (int z = tid >> 5; z < KS; z += NT / 32) {
+            const float *cv = cb + ((size_t)m * KS + z) * ds;
+            float a0 = 0.f, a1 = 0.f;
+            for (int j = 0; j < ds; ++j) {
+                a0 = ca1_step(a0, qa[m * ds + j], cv[j]);
+                a1 = ca1_step(a1, qb[m * ds + j], cv[j]);
+            }
+            lp[z * 64 + lane] = a0;
+            lp[z * 64 + 32 + lane] = a1;
+        }
+    } else {
+        float *lp = reinterpret_cast<float *>(lut);
+        for (int e = tid; e < 2 * MM * KS; e += NT) {
+            const int qq = e / (MM * KS), m = (e / KS) % MM, z = e % KS;
+            const float *qv = (qq ? qb : qa) + m * ds, *cv = cb + ((size_t)m * KS + z) * ds;
+            float a = 0.f;
+            for (int j = 0; j < ds; ++j) a = ca1_step(a, qv[j], cv[j]);
+            lp[e] = a;
+        }
+    }
+    for (int e = tid; e < 2 * kk; e += NT) top[e] = KEY_MAX;
+    if (tid < 2) { cnt[tid] = 0; thr[tid] = __int_as_float(0x7f800000); }
+    if (tid == 0) *s_next = 0;
+    __syncthreads();
+
+    uint32_t sel[4];
+    const uint32_t r = (uint32_t)lane & (FAST ? (M - 1) : 0), rw = r >> 2;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) sel[t] = 0x5504u | ((((uint32_t)t ^ r) & 3u) << 4);
+    float th0 = thr[0], th1 = thr[1];
+    bool need = false;
+    ListCursor cur{0, 0, 0, false};
+    while (true) {
+        next_list(cur, s_next, P, q0, nq, probes, offsets, lane);
+        if (!__syncthreads_or(!cur.done)) break;
+        if (!cur.done) {
+            const int64_t p = cur.beg + lane;
+            const bool valid = p < cur.end;
+            const uint32_t pos = valid ? __ldg(ids + p) : 0u;
+            float acc = 0.f;
+            if constexpr (FAST) {
+                uint32_t w[W];
+#pragma unroll
+                for (int i = 0; i < W; ++i) w[i] = 0;
+                if (valid) load_code_ivf<W>(codes + (size_t)pos * M, w);
+#pragma unroll
+                for (int b = 1; b < W; b <<= 1) {
+                    const bool c = (rw & b) != 0;
+#pragma unroll
+                    for (int i = 0; i < W; ++i) {
+                        if (i & b) continue;
+                        const uint32_t x = w[i], y = w[i | b];
+                        w[i] = c ? y : x;
+                        w[i | b] = c ? x : y;
+                    }
+                }
+                const uint32_t l4 = ((uint32_t)cur.qq << 7) | ((uint32_t)lane << 2);
+#pragma unroll
+                for (int j = 0; j < (FAST ? M : 1); ++j) {
+                    const uint32_t off = __byte_perm(w[j >> 2], l4 ^ (uint32_t)(j << 2), sel[j & 3]);
+                    acc += *reinterpret_cast<const float *>(lut + off);
+                }
+            } else if (valid) {
+                const float *lq = reinterpret_cast<const float *>(lut) + (size_t)cur.qq * MM * KS;
+                const uint8_t *cp = codes + (size_t)pos * MM;
+                for (int m = 0; m < MM; ++m) acc = __fadd_rn(acc, lq[m * KS + cp[m]]);
+            }
+            const float th = cur.qq ? th1 : th0;
+            push_candidate(valid && acc <= th, make_key(acc, pos), fresh + cur.qq * NEWCAP, cnt + cur.qq, lane,
+                           need);
+            cur.beg += 32;
+        }
+        if (__syncthreads_or(need)) {
+            compact_topk(top, fresh, cnt, thr, 2, kk, scratch);
+            th0 = thr[0];
+            th1 = thr[1];
+            need = false;
+        }
+    }
+    compact_topk(top, fresh, cnt, thr, 2, kk, scratch);
+    if constexpr (FAST) {  // canonical rescore (CA2) of the kept candidates, replica 0
+        for (int e = tid; e < 2 * kk; e += NT) {
+            const uint64_t k = top[e];
+            if (k == KEY_MAX) continue;
+            const int qq = e / kk;
+            const uint32_t id = key_id(k);
+            const uint8_t *cp = codes + (size_t)id * M;
+            const float *lq = reinterpret_cast<const float *>(lut) + qq * 32;
+            float d = 0.f;
+            for (int m = 0; m < M; ++m) d = __fadd_rn(d, lq[(int)cp[m] * 64 + m]);
+            top[e] = make_key(d, id);
+        }
+        __syncthreads();
+        bitonic_sort_rows(top, 2, kk, kk);
+    }
+    for (int e = tid; e < 2 * kk; e += NT) {
+        const int qq = e / kk, i = e - qq * kk;
+        if (q0 + qq < nq) out[(q0 + qq) * kk + i] = top[e];
+    }
+}
+
+size_t ivf_smem(int M, int kk) {
+    const bool fast = (M == 4 || M == 8 || M == 16 || M == 32);
+    const size_t lut = fast ? (size_t)PAIR_BYTES : (size_t)2 * M * KS * 4;
+    return lut + (size_t)2 * (kk + NEWCAP) * 8 + 64;
+}
+
+template <int M, bool FAST>
+static void ivf_launch_t(const uint8_t *codes, int Mrt, const float *q, int64_t nq, const float *cb, int ds, int kk,
+                         const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
+                         cudaStream_t st) {
+    const size_t smem = ivf_smem(Mrt, kk);
+    auto kern = ivf_scan_kernel<M, FAST>;
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)ceil_div(nq, 2), NT, smem, st>>>(codes, q, nq, cb, Mrt, ds, kk, probes, P, offsets, ids, out);
+    RII_LAUNCHED();
+}
+
+void launch_ivf_scan(const uint8_t *codes, int M, const float *q, int64_t nq, const float *cb, int D, int kk,
+                     const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
+                     cudaStream_t st) {
+    if (nq <= 0) return;
+    if (ivf_smem(M, kk) > 227 * 1024) throw Error(1, "topk too large for the inverted-index kernel");
+    const int ds = D / M;
+    switch (M) {
+        case 4: ivf_launch_t<4, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st); break;
+        case 8: ivf_launch_t<8, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st); break;
+        case 16: ivf_launch_t<16, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st); break;
+        case 32: ivf_launch_t<32, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st); break;
+        default: ivf_launch_t<1, false>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st); break;
+    }
+}
+
+}  // namespace rii

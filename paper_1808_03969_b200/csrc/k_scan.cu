@@ -1,0 +1,403 @@
+// k_scan.cu -- PQ linear scan (Alg. 1 PQLinearScan) on sm_100a.
+//
+// One CTA = (a batch of B queries) x (a chunk of the linear code array).  The
+// ADC table A of every query of the batch is built once in shared
+// memory; each thread then streams one uint8 code per step from HBM (coalesced
+// 16-byte loads, prefetched one step ahead) and evaluates Eq. 2 for
+// all B queries, so every code byte fetched is reused B times from registers.
+//
+// Bank-conflict-free lookups ("fast" layout, M in {4,8,16,32}): lane l walks the
+// subspaces of its code in the order m = j XOR (l mod M) and reads replica
+// g = l / M of the table, whose word for (z, m) sits at column g*M + m of row z.
+// For a fixed step j the 32 lanes then hit 32 distinct banks whatever their
+// code bytes are.  Two queries share each 256-byte row, so one PRMT builds the
+// byte offset (z << 8) | 4*(l ^ j) from the code word and the LDS immediate
+// selects the query.  The lane-dependent summation order is undone by a
+// canonical (CA2, m ascending) rescore of the kept candidates, so the returned
+// distances equal the oracle's bit for bit.
+#include "kernels.cuh"
+#include "topk.cuh"
+
+namespace rii {
+
+constexpr int LUT_PAIR_BYTES = 256 * 256;  // 256 rows x 64 fp32 words (two queries)
+
+template <int W>
+__device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
+    if constexpr (W == 8) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
+        const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    } else if constexpr (W == 4) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+    } else if constexpr (W == 2) {
+        const uint2 a = __ldg(reinterpret_cast<const uint2 *>(p));
+        w[0] = a.x; w[1] = a.y;
+    } else {
+        w[0] = __ldg(reinterpret_cast<const uint32_t *>(p));
+    }
+}
+
+// Replica layout of a query pair: word z*64 + half*32 + c = A_half(c mod M, z).
+template <int M>
+__device__ void build_lut_pair(float *lutp, const float *q0, const float *q1, const float *__restrict__ cb, int ds) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int m = lane & (M - 1);
+    for (int z = warp; z < KS; z += NT / 32) {
+        const float *cv = cb + ((size_t)m * KS + z) * ds;
+        float a0 = 0.f, a1 = 0.f;
+        for (int j = 0; j < ds; ++j) {
+            const float c = cv[j];
+            a0 = ca1_step(a0, q0[m * ds + j], c);
+            a1 = ca1_step(a1, q1[m * ds + j], c);
+        }
+        lutp[z * 64 + lane] = a0;
+        lutp[z * 64 + 32 + lane] = a1;
+    }
+}
+
+// Lane-rotated ADC of one code (M bytes in w) against the B tables of the CTA.
+template <int M, int B>
+__device__ __forceinline__ void adc_rotated(const uint8_t *lut, const uint32_t (&w)[M / 4], uint32_t rw,
+                                            const uint32_t (&sel)[4], uint32_t l4, float (&acc)[B]) {
+    constexpr int W = M / 4;
+    uint32_t wp[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) wp[i] = w[i];
+#pragma unroll
+    for (int b = 1; b < W; b <<= 1) {
+        const bool c = (rw & b) != 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            if (i & b) continue;
+            const uint32_t x = wp[i], y = wp[i | b];
+            wp[i] = c ? y : x;
+            wp[i | b] = c ? x : y;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        const uint32_t off = __byte_perm(wp[j >> 2], l4 ^ (uint32_t)(j << 2), sel[j & 3]);
+#pragma unroll
+        for (int qq = 0; qq < B; ++qq) {
+            const float v = *reinterpret_cast<const float *>(lut + (qq >> 1) * LUT_PAIR_BYTES + (qq & 1) * 128 + off);
+            acc[qq] = j == 0 ? v : acc[qq] + v;  // 0 + v == v for v >= +0
+        }
+    }
+}
+
+template <int M, int B>
+__global__ void __launch_bounds__(NT, 1)
+    scan_fast_kernel(const uint8_t *__restrict__ codes, int64_t n_codes, const float *__restrict__ q, int64_t nq,
+                     const float *__restrict__ cb, int ds, int kk, int nb, int64_t chunk, int nc,
+                     uint64_t *__restrict__ out) {
+    constexpr int W = M / 4, NP = B / 2;
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint8_t *lut = smem;
+    uint64_t *top = reinterpret_cast<uint64_t *>(smem + NP * LUT_PAIR_BYTES);
+    uint64_t *fresh = top + B * kk;
+    int *cnt = reinterpret_cast<int *>(fresh + B * NEWCAP);
+    float *thr = reinterpret_cast<float *>(cnt + B);
+    int *scratch = reinterpret_cast<int *>(thr + B);
+
+    const int item = blockIdx.x, ci = item / nb, qb = item - ci * nb;
+    const int64_t c0 = (int64_t)ci * chunk, c1 = min(n_codes, c0 + chunk);
+    const int D = M * ds, tid = threadIdx.x, lane = tid & 31;
+
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const int64_t qa = min((int64_t)qb * B + 2 * p, nq - 1), qc = min((int64_t)qb * B + 2 * p + 1, nq - 1);
+        build_lut_pair<M>(reinterpret_cast<float *>(lut + p * LUT_PAIR_BYTES), q + qa * D, q + qc * D, cb, ds);
+    }
+    for (int e = tid; e < B * kk; e += NT) top[e] = KEY_MAX;
+    if (tid < B) { cnt[tid] = 0; thr[tid] = __int_as_float(0x7f800000); }
+    __syncthreads();
+
+    const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l4 = (uint32_t)lane << 2;
+    uint32_t sel[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) sel[t] = 0x5504u | ((((uint32_t)t ^ r) & 3u) << 4);
+    float th[B];
+#pragma unroll
+    for (int qq = 0; qq < B; ++qq) th[qq] = thr[qq];
+    bool need = false;
+
+    uint32_t w[W];
+    int64_t pos = c0 + tid;
+#pragma unroll
+    for (int i = 0; i < W; ++i) w[i] = 0;
+    if (pos < c1) load_code<W>(codes + pos * M, w);
+    for (int64_t base = c0; base < c1; base += NT) {
+        const bool valid = pos < c1;
+        const int64_t npos = pos + NT;
+        uint32_t wn[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) wn[i] = 0;
+        if (npos < c1) load_code<W>(codes + npos * M, wn);
+        float acc[B];
+        adc_rotated<M, B>(lut, w, rw, sel, l4, acc);
+#pragma unroll
+        for (int qq = 0; qq < B; ++qq)
+            push_candidate(valid && acc[qq] <= th[qq], make_key(acc[qq], (uint32_t)pos), fresh + qq * NEWCAP,
+                           cnt + qq, lane, need);
+        if (__syncthreads_or(need)) {
+            compact_topk(top, fresh, cnt, thr, B, kk, scratch);
+#pragma unroll
+            for (int qq = 0; qq < B; ++qq) th[qq] = thr[qq];
+            need = false;
+        }
+#pragma unroll
+        for (int i = 0; i < W; ++i) w[i] = wn[i];
+        pos = npos;
+    }
+    compact_topk(top, fresh, cnt, thr, B, kk, scratch);
+
+    // Canonical rescore (CA2: m ascending, replica 0) of the kept candidates.
+    for (int e = tid; e < B * kk; e += NT) {
+        const uint64_t k = top[e];
+        if (k == KEY_MAX) continue;
+        const int qq = e / kk;
+        const uint32_t id = key_id(k);
+        const uint8_t *cp = codes + (size_t)id * M;
+        const float *lq = reinterpret_cast<const float *>(lut + (qq >> 1) * LUT_PAIR_BYTES) + (qq & 1) * 32;
+        float d = 0.f;
+#pragma unroll
+        for (int m = 0; m < M; ++m) d = __fadd_rn(d, lq[(int)cp[m] * 64 + m]);
+        top[e] = make_key(d, id);
+    }
+    __syncthreads();
+    bitonic_sort_rows(top, B, kk, kk);
+    for (int e = tid; e < B * kk; e += NT) {
+        const int qq = e / kk, i = e - qq * kk;
+        const int64_t qi = (int64_t)qb * B + qq;
+        if (qi < nq) out[(qi * nc + ci) * kk + i] = top[e];
+    }
+}
+
+// Generic layout (any M <= 64): table A[q][m][z], canonical m-ascending sums.
+template <int B>
+__global__ void __launch_bounds__(NT, 1)
+    scan_generic_kernel(const uint8_t *__restrict__ codes, int64_t n_codes, const float *__restrict__ q, int64_t nq,
+                        const float *__restrict__ cb, int M, int ds, int kk, int nb, int64_t chunk, int nc,
+                        uint64_t *__restrict__ out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    float *lut = reinterpret_cast<float *>(smem);
+    uint64_t *top = reinterpret_cast<uint64_t *>(smem + (size_t)B * M * KS * 4);
+    uint64_t *fresh = top + B * kk;
+    int *cnt = reinterpret_cast<int *>(fresh + B * NEWCAP);
+    float *thr = reinterpret_cast<float *>(cnt + B);
+    int *scratch = reinterpret_cast<int *>(thr + B);
+
+    const int item = blockIdx.x, ci = item / nb, qb = item - ci * nb;
+    const int64_t c0 = (int64_t)ci * chunk, c1 = min(n_codes, c0 + chunk);
+    const int D = M * ds, tid = threadIdx.x, lane = tid & 31;
+
+    for (int e = tid; e < B * M * KS; e += NT) {
+        const int qq = e / (M * KS), m = (e / KS) % M, z = e % KS;
+        const int64_t qi = min((int64_t)qb * B + qq, nq - 1);
+        const float *qv = q + qi * D + m * ds, *cv = cb + ((size_t)m * KS + z) * ds;
+        float a = 0.f;
+        for (int j = 0; j < ds; ++j) a = ca1_step(a, qv[j], cv[j]);
+        lut[e] = a;
+    }
+    for (int e = tid; e < B * kk; e += NT) top[e] = KEY_MAX;
+    if (tid < B) { cnt[tid] = 0; thr[tid] = __int_as_float(0x7f800000); }
+    __syncthreads();
+    float th[B];
+#pragma unroll
+    for (int qq = 0; qq < B; ++qq) th[qq] = thr[qq];
+    bool need = false;
+    for (int64_t base = c0; base < c1; base += NT) {
+        const int64_t pos = base + tid;
+        const bool valid = pos < c1;
+        float acc[B];
+#pragma unroll
+        for (int qq = 0; qq < B; ++qq) acc[qq] = 0.f;
+        if (valid) {
+            const uint8_t *cp = codes + pos * M;
+            for (int m = 0; m < M; ++m) {
+                const int z = cp[m];
+#pragma unroll
+                for (int qq = 0; qq < B; ++qq) acc[qq] = __fadd_rn(acc[qq], lut[(qq * M + m) * KS + z]);
+            }
+        }
+#pragma unroll
+        for (int qq = 0; qq < B; ++qq)
+            push_candidate(valid && acc[qq] <= th[qq], make_key(acc[qq], (uint32_t)pos), fresh + qq * NEWCAP,
+                           cnt + qq, lane, need);
+        if (__syncthreads_or(need)) {
+            compact_topk(top, fresh, cnt, thr, B, kk, scratch);
+#pragma unroll
+            for (int qq = 0; qq < B; ++qq) th[qq] = thr[qq];
+            need = false;
+        }
+    }
+    compact_topk(top, fresh, cnt, thr, B, kk, scratch);
+    for (int e = tid; e < B * kk; e += NT) {
+        const int qq = e / kk, i = e - qq * kk;
+        const int64_t qi = (int64_t)qb * B + qq;
+        if (qi < nq) out[(qi * nc + ci) * kk + i] = top[e];
+    }
+}
+
+static size_t smem_fast(int B, int kk) { return (size_t)(B / 2) * LUT_PAIR_BYTES + (size_t)B * (kk + NEWCAP) * 8 + 64; }
+static size_t smem_generic(int B, int M, int kk) {
+    return (size_t)B * M * KS * 4 + (size_t)B * (kk + NEWCAP) * 8 + 64;
+}
+static constexpr size_t SMEM_CAP = 227 * 1024;
+
+ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms) {
+    ScanPlan p{};
+    p.fast = (M == 4 || M == 8 || M == 16 || M == 32);
+    p.B = 0;
+    if (p.fast) {
+        for (int B : {6, 4, 2})
+            if (smem_fast(B, kk) <= SMEM_CAP) { p.B = B; p.smem = smem_fast(B, kk); break; }
+    } else {
+        for (int B : {4, 2, 1})
+            if (smem_generic(B, M, kk) <= SMEM_CAP) { p.B = B; p.smem = smem_generic(B, M, kk); break; }
+    }
+    if (p.B == 0) throw Error(1, "topk too large for the scan kernel's shared-memory budget");
+    p.nb = (int)ceil_div(nq, p.B);
+    // Code chunks: minimise waves(nc) / nc (per-CTA work ~ n_codes / nc), >= 8192 codes per chunk.
+    int64_t nc_max = n_codes / 8192;
+    if (nc_max < 1) nc_max = 1;
+    if (nc_max > 64) nc_max = 64;
+    double best = 1e300;
+    int bnc = 1;
+    for (int nc = 1; nc <= nc_max; ++nc) {
+        const double waves = (double)ceil_div((int64_t)p.nb * nc, num_sms);
+        const double t = waves / nc * (1.0 + 0.002 * nc);
+        if (t < best * 0.999) { best = t; bnc = nc; }
+    }
+    p.nc = bnc;
+    p.chunk = ceil_div(n_codes, bnc);
+    if (p.chunk < 1) p.chunk = 1;
+    return p;
+}
+
+template <int M, int B>
+static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
+                          const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st) {
+    auto kern = scan_fast_kernel<M, B>;
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    kern<<<pl.nb * pl.nc, NT, pl.smem, st>>>(codes, n, q, nq, cb, ds, kk, pl.nb, pl.chunk, pl.nc, out);
+    RII_LAUNCHED();
+}
+
+template <int M>
+static void launch_fast_m(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
+                          const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st) {
+    if (pl.B == 6) launch_fast_t<M, 6>(pl, codes, n, q, nq, cb, ds, kk, out, st);
+    else if (pl.B == 4) launch_fast_t<M, 4>(pl, codes, n, q, nq, cb, ds, kk, out, st);
+    else launch_fast_t<M, 2>(pl, codes, n, q, nq, cb, ds, kk, out, st);
+}
+
+template <int B>
+static void launch_generic_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, int M, const float *q, int64_t nq,
+                             const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st) {
+    auto kern = scan_generic_kernel<B>;
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    kern<<<pl.nb * pl.nc, NT, pl.smem, st>>>(codes, n, q, nq, cb, M, ds, kk, pl.nb, pl.chunk, pl.nc, out);
+    RII_LAUNCHED();
+}
+
+void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_codes, int M, const float *q, int64_t nq,
+                        const float *cb, int D, int kk, uint64_t *out, cudaStream_t st) {
+    const int ds = D / M;
+    if (pl.fast) {
+        switch (M) {
+            case 4: launch_fast_m<4>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st); break;
+            case 8: launch_fast_m<8>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st); break;
+            case 16: launch_fast_m<16>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st); break;
+            default: launch_fast_m<32>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st); break;
+        }
+    } else if (pl.B == 4) {
+        launch_generic_t<4>(pl, codes, n_codes, M, q, nq, cb, ds, kk, out, st);
+    } else if (pl.B == 2) {
+        launch_generic_t<2>(pl, codes, n_codes, M, q, nq, cb, ds, kk, out, st);
+    } else {
+        launch_generic_t<1>(pl, codes, n_codes, M, q, nq, cb, ds, kk, out, st);
+    }
+}
+
+// ---------------------------------------------------------------- gather ---
+__global__ void gather_codes_kernel(const uint8_t *__restrict__ codes, int M, const int64_t *__restrict__ pos,
+                                    int64_t n, uint8_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint8_t *src = codes + pos[i] * M;
+    uint8_t *dst = out + i * M;
+    if ((M & 3) == 0) {
+        for (int b = 0; b < M; b += 4)
+            *reinterpret_cast<uint32_t *>(dst + b) = __ldg(reinterpret_cast<const uint32_t *>(src + b));
+    } else {
+        for (int b = 0; b < M; ++b) dst[b] = src[b];
+    }
+}
+
+void launch_gather_codes(const uint8_t *codes, int M, const int64_t *pos, int64_t n, uint8_t *out, cudaStream_t st) {
+    if (n <= 0) return;
+    gather_codes_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(codes, M, pos, n, out);
+    RII_LAUNCHED();
+}
+
+__global__ void validate_targets_kernel(const int64_t *__restrict__ ids, int64_t n, int64_t N, int *flag) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t v = ids[i];
+    if (v < 0 || v >= N || (i > 0 && v <= ids[i - 1])) atomicOr(flag, 1);
+}
+
+void launch_validate_targets(const int64_t *ids, int64_t n, int64_t N, int *flag, cudaStream_t st) {
+    if (n <= 0) return;
+    validate_targets_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(ids, n, N, flag);
+    RII_LAUNCHED();
+}
+
+// ----------------------------------------------------------------- merge ---
+__global__ void __launch_bounds__(NT) merge_kernel(const uint64_t *__restrict__ keys, int64_t q_stride,
+                                                   int64_t p_stride, int parts, int kk, int topk, IdMap map,
+                                                   int64_t *__restrict__ out_ids, float *__restrict__ out_dist,
+                                                   uint64_t *__restrict__ out_keys) {
+    extern __shared__ __align__(16) uint64_t msm[];
+    uint64_t *top = msm, *prt = msm + kk;
+    const int64_t q = blockIdx.x;
+    const uint64_t *base = keys + q * q_stride;
+    for (int i = threadIdx.x; i < kk; i += blockDim.x) top[i] = base[i];
+    __syncthreads();
+    for (int p = 1; p < parts; ++p) {
+        for (int i = threadIdx.x; i < kk; i += blockDim.x) prt[i] = base[(int64_t)p * p_stride + i];
+        __syncthreads();
+        for (int i = threadIdx.x; i < kk; i += blockDim.x) {
+            const uint64_t v = prt[kk - 1 - i];
+            if (v < top[i]) top[i] = v;
+        }
+        __syncthreads();
+        bitonic_merge_rows(top, 1, kk, kk);
+    }
+    if (out_keys) {
+        for (int i = threadIdx.x; i < kk; i += blockDim.x) {
+            const uint64_t k = top[i];
+            out_keys[q * kk + i] = k == KEY_MAX ? KEY_MAX : make_key(key_dist(k), (uint32_t)map_id(map, key_id(k)));
+        }
+    } else {
+        for (int i = threadIdx.x; i < topk; i += blockDim.x) {
+            const uint64_t k = top[i];
+            out_ids[q * topk + i] = k == KEY_MAX ? -1 : map_id(map, key_id(k));
+            out_dist[q * topk + i] = k == KEY_MAX ? __int_as_float(0x7f800000) : key_dist(k);
+        }
+    }
+}
+
+void launch_merge(const uint64_t *keys, int64_t q_stride, int64_t p_stride, int parts, int64_t nq, int kk, int topk,
+                  const IdMap &map, int64_t *out_ids, float *out_dist, uint64_t *out_keys, cudaStream_t st) {
+    if (nq <= 0) return;
+    merge_kernel<<<(unsigned)nq, NT, (size_t)2 * kk * 8, st>>>(keys, q_stride, p_stride, parts, kk, topk, map,
+                                                               out_ids, out_dist, out_keys);
+    RII_LAUNCHED();
+}
+
+}  // namespace rii

@@ -1,0 +1,73 @@
+// kernels.cuh -- host-side launchers of the sm_100a kernels (internal interface).
+#pragma once
+#include "common.cuh"
+
+namespace rii {
+
+// ---- search (k_scan.cu) ------------------------------------------------------
+// Linear ADC scan (Alg. 1) of n_codes codes (M bytes each) for nq queries.
+// Writes out[nq_pad][nc][kk] sorted keys with canonical (CA2) distances and
+// key ids = position in `codes`.  Returns nc (number of code chunks).
+struct ScanPlan {
+    int B;        // queries per CTA
+    int nb;       // query batches
+    int nc;       // code chunks
+    int64_t chunk;
+    bool fast;    // lane-rotated conflict-free LUT layout
+    size_t smem;
+};
+ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms);
+void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_codes, int M, const float *q, int64_t nq,
+                        const float *cb, int D, int kk, uint64_t *out, cudaStream_t st);
+
+// out[i] = codes[pos[i]] for i < n (subset gather, Alg. 1 "pick up target PQ-codes").
+void launch_gather_codes(const uint8_t *codes, int M, const int64_t *pos, int64_t n, uint8_t *out, cudaStream_t st);
+
+// Checks that ids are strictly ascending and inside [0, N); sets *flag != 0 otherwise.
+void launch_validate_targets(const int64_t *ids, int64_t n, int64_t N, int *flag, cudaStream_t st);
+
+// Merge `parts` ascending kk-key lists per query into the final result.
+// keys addressed as base[q * q_stride + p * p_stride + i].  Either writes
+// (out_ids, out_dist) [nq][topk] or, if out_keys != nullptr, [nq][kk] keys with
+// ids mapped to global ids.
+void launch_merge(const uint64_t *keys, int64_t q_stride, int64_t p_stride, int parts, int64_t nq, int kk, int topk,
+                  const IdMap &map, int64_t *out_ids, float *out_dist, uint64_t *out_keys, cudaStream_t st);
+
+// ---- inverted index (k_ivf.cu) -----------------------------------------------
+// d0[q][k] = CA2 ADC of query q to centre code k (Alg. 2 L2-L5).
+void launch_coarse_dist(const uint8_t *centers, int64_t K, int M, const float *q, int64_t nq, const float *cb, int D,
+                        float *d0, cudaStream_t st);
+// probes[q][0..P) = the P centres with the smallest (d0, k) (Alg. 2 L6), ascending k.
+void launch_select_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int32_t *probes, cudaStream_t st);
+// Posting-list traversal (Alg. 2 L7-L16, mode A): out[nq][kk] keys, ids = local positions.
+size_t ivf_smem(int M, int kk);
+void launch_ivf_scan(const uint8_t *codes, int M, const float *q, int64_t nq, const float *cb, int D, int kk,
+                     const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
+                     cudaStream_t st);
+
+// ---- build side (k_build.cu) -------------------------------------------------
+void launch_encode(const float *x, int64_t n, int D, int M, const float *cb, uint8_t *codes, cudaStream_t st);
+void launch_sdc_tables(const float *cb, int D, int M, float *T, cudaStream_t st);
+// a[i] = argmin_k d_S(codes[i], centers[k]) (CA2, ties lowest k); dist optional.
+void launch_assign(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, int M, const float *T,
+                   int32_t *assign, float *dist, cudaStream_t st);
+// k-means code-book training (O-TRAIN), all subspaces; returns status via *err (device int).
+struct TrainScratch;
+void run_train(const float *x, int64_t n, int D, int M, int n_iter, uint64_t seed, float *cb, int *err,
+               cudaStream_t st);
+// CSR of `vals` (local positions) grouped by `keys` (list ids in [0,K)), stable.
+void build_csr(const int32_t *keys, const uint32_t *vals, int64_t n, int64_t K, int64_t *offsets, uint32_t *ids,
+               cudaStream_t st);
+// PQk-means over a sample (R9); centers out [K][M]; *err set if < K distinct codes.
+void run_pqkmeans(const uint8_t *X, int64_t ns, int64_t K, int M, const float *T, int n_iter, uint8_t *centers,
+                  int *err, cudaStream_t st);
+// The ns smallest splitmix64(seed ^ gid) keys among n codes with global ids gid(i);
+// writes their local positions in ascending key order.
+void select_sample(int64_t n, const IdMap &gid, int64_t ns, uint64_t seed, uint32_t *out_pos, cudaStream_t st);
+// keys[i] = splitmix64(seed ^ gid(pos[i])) for i < n.
+void sample_keys_for_positions(int64_t n_local, const IdMap &gid, const uint32_t *pos, int64_t n, uint64_t seed,
+                               uint64_t *keys, cudaStream_t st);
+// order[0..n) = indices of keys in ascending key order (stable).
+void sort_keys_with_index(const uint64_t *keys, int64_t n, uint32_t *order, cudaStream_t st);
+
+}  // namespace rii

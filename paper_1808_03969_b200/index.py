@@ -1,0 +1,226 @@
+"""Python binding of the C ABI (include/rii.h): argument marshalling only.
+
+Every step of the method runs in the CUDA kernels of librii_b200.so; this module
+only converts numpy arrays / torch tensors into pointers.  Torch CUDA tensors
+are passed as device memory (RII_MEM_DEVICE) on torch's current stream; numpy
+arrays and CPU tensors as host memory (RII_MEM_HOST).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as _rl
+
+_PATHS = {"auto": _rl.PATH_AUTO, "linear": _rl.PATH_LINEAR, "ivf": _rl.PATH_IVF,
+          _rl.PATH_AUTO: _rl.PATH_AUTO, _rl.PATH_LINEAR: _rl.PATH_LINEAR, _rl.PATH_IVF: _rl.PATH_IVF}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _is_cuda_tensor(a) -> bool:
+    try:
+        torch = _torch()
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(a, torch.Tensor) and a.is_cuda
+
+
+def _stream_ptr(stream):
+    if stream is not None:
+        return C.c_void_p(int(getattr(stream, "cuda_stream", stream)))
+    torch = _torch()
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _host(a, dtype):
+    """Contiguous host array of `dtype` (numpy or CPU tensor in)."""
+    try:
+        torch = _torch()
+        if isinstance(a, torch.Tensor):
+            a = a.detach().cpu().numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _dev(a, dtype):
+    torch = _torch()
+    tdt = {np.float32: torch.float32, np.int64: torch.int64, np.uint64: torch.uint64}[dtype]
+    if a.dtype != tdt or not a.is_contiguous():
+        a = a.to(tdt).contiguous()
+    return a
+
+
+def _ptr(a):
+    if _is_cuda_tensor(a) or (hasattr(a, "data_ptr") and not isinstance(a, np.ndarray)):
+        return C.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * _rl.NCCL_ID_BYTES)()
+    _rl.check(_rl.load().rii_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+def launch_count() -> int:
+    return int(_rl.load().rii_launch_count())
+
+
+def partial_width(topk: int) -> int:
+    return int(_rl.load().rii_partial_width(topk))
+
+
+class Index:
+    """Rii index (Sec. 4.1) on one GPU, or one shard of a multi-GPU job."""
+
+    def __init__(self, D: int, M: int, Ks: int = 256, device: int | None = None, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None):
+        self._lib = _rl.load()
+        if device is None:
+            try:
+                device = _torch().cuda.current_device()
+            except Exception:
+                device = 0
+        self.D, self.M, self.Ks, self.device, self.rank, self.world = D, M, Ks, device, rank, world
+        h = C.c_void_p()
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = (C.c_uint8 * _rl.NCCL_ID_BYTES).from_buffer_copy(nccl_id)
+        _rl.check(self._lib.rii_create(D, M, Ks, device, rank, world,
+                                     C.cast(idbuf, C.c_void_p) if idbuf is not None else None, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.rii_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------- build ---
+    def _rows(self, x):
+        if _is_cuda_tensor(x):
+            x = _dev(x, np.float32)
+            return x, x.shape[0], _rl.MEM_DEVICE, _stream_ptr(None)
+        x = _host(x, np.float32)
+        return x, x.shape[0], _rl.MEM_HOST, None
+
+    def train(self, x, n_iter: int = 20, seed: int = 0):
+        x, n, where, st = self._rows(x)
+        _rl.check(self._lib.rii_train(self._h, _ptr(x), n, n_iter, seed, where, st))
+
+    def add(self, x) -> int:
+        x, n, where, st = self._rows(x)
+        first = C.c_int64(0)
+        _rl.check(self._lib.rii_add(self._h, _ptr(x), n, where, st, C.byref(first)))
+        return first.value
+
+    def reconfigure(self, nlist: int, n_iter: int = 10, seed: int = 0, stream=None):
+        st = _stream_ptr(stream) if stream is not None else None
+        _rl.check(self._lib.rii_reconfigure(self._h, nlist, n_iter, seed, st))
+
+    # ------------------------------------------------------------- query ---
+    def query(self, q, topk: int, target_ids=None, L: int = 1, path="auto", out=None, stream=None):
+        """Alg. 3 Query.  Returns (ids [nq, topk] int64, dist [nq, topk] fp32, path_used)."""
+        Lp = L
+        used = C.c_int32(0)
+        if _is_cuda_tensor(q):
+            torch = _torch()
+            q = _dev(q, np.float32)
+            nq = q.shape[0]
+            S = None if target_ids is None else _dev(torch.as_tensor(target_ids, device=q.device), np.int64)
+            if out is None:
+                ids = torch.empty((nq, topk), dtype=torch.int64, device=q.device)
+                dist = torch.empty((nq, topk), dtype=torch.float32, device=q.device)
+            else:
+                ids, dist = out
+            _rl.check(self._lib.rii_query(self._h, _ptr(q), nq, topk, _ptr(S) if S is not None else None,
+                                        0 if S is None else S.numel(), Lp, _PATHS[path], _rl.MEM_DEVICE,
+                                        _stream_ptr(stream), _ptr(ids), _ptr(dist), C.byref(used)))
+            return ids, dist, used.value
+        q = _host(q, np.float32)
+        nq = q.shape[0]
+        S = None if target_ids is None else _host(target_ids, np.int64)
+        if out is None:
+            ids = np.empty((nq, topk), np.int64)
+            dist = np.empty((nq, topk), np.float32)
+        else:
+            ids, dist = out
+        _rl.check(self._lib.rii_query(self._h, _ptr(q), nq, topk, _ptr(S) if S is not None else None,
+                                    0 if S is None else S.shape[0], Lp, _PATHS[path], _rl.MEM_HOST,
+                                    _stream_ptr(stream) if stream is not None else None, _ptr(ids), _ptr(dist),
+                                    C.byref(used)))
+        return ids, dist, used.value
+
+    def query_partial(self, q, topk: int, target_ids=None, L: int = 1, path="auto", stream=None):
+        """This shard's top candidates as packed uint64 keys [nq, partial_width(topk)] (device)."""
+        torch = _torch()
+        q = _dev(q, np.float32)
+        nq = q.shape[0]
+        S = None if target_ids is None else _dev(torch.as_tensor(target_ids, device=q.device), np.int64)
+        keys = torch.empty((nq, partial_width(topk)), dtype=torch.uint64, device=q.device)
+        used = C.c_int32(0)
+        _rl.check(self._lib.rii_query_partial(self._h, _ptr(q), nq, topk, _ptr(S) if S is not None else None,
+                                            0 if S is None else S.numel(), L, _PATHS[path], _stream_ptr(stream),
+                                            _ptr(keys), C.byref(used)))
+        return keys, used.value
+
+    # ------------------------------------------------------------- state ---
+    def get_codebook(self) -> np.ndarray:
+        out = np.empty((self.M, self.Ks, self.D // self.M), np.float32)
+        _rl.check(self._lib.rii_get_codebook(self._h, _ptr(out)))
+        return out
+
+    def set_codebook(self, cb):
+        cb = _host(cb, np.float32)
+        assert cb.size == self.M * self.Ks * (self.D // self.M)
+        _rl.check(self._lib.rii_set_codebook(self._h, _ptr(cb)))
+
+    def get_codes(self, first: int = 0, n: int | None = None) -> np.ndarray:
+        if n is None:
+            n = self.info()["N"] - first
+        out = np.empty((n, self.M), np.uint8)
+        _rl.check(self._lib.rii_get_codes(self._h, first, n, _ptr(out)))
+        return out
+
+    def get_centers(self) -> np.ndarray:
+        out = np.empty((self.info()["K"], self.M), np.uint8)
+        _rl.check(self._lib.rii_get_centers(self._h, _ptr(out)))
+        return out
+
+    def get_postings(self):
+        inf = self.info()
+        off = np.empty(inf["K"] + 1, np.int64)
+        ids = np.empty(inf["n_local"], np.int64)
+        _rl.check(self._lib.rii_get_postings(self._h, _ptr(off), _ptr(ids)))
+        return off, ids
+
+    def set_theta(self, theta: int):
+        _rl.check(self._lib.rii_set_theta(self._h, theta))
+
+    def info(self) -> dict:
+        N, K, th, nl, b = C.c_int64(), C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
+        _rl.check(self._lib.rii_get_info(self._h, C.byref(N), C.byref(K), C.byref(th), C.byref(nl), C.byref(b)))
+        return {"N": N.value, "K": K.value, "theta": th.value, "n_local": nl.value, "bytes": b.value}
+
+
+def merge_partials(keys, topk: int, stream=None):
+    """Merge [parts, nq, kk] device keys from rii_query_partial into the final top-k."""
+    torch = _torch()
+    keys = keys.contiguous()
+    parts, nq = keys.shape[0], keys.shape[1]
+    ids = torch.empty((nq, topk), dtype=torch.int64, device=keys.device)
+    dist = torch.empty((nq, topk), dtype=torch.float32, device=keys.device)
+    _rl.check(_rl.load().rii_merge_partials(C.c_void_p(keys.data_ptr()), parts, nq, topk, _stream_ptr(stream),
+                                        C.c_void_p(ids.data_ptr()), C.c_void_p(dist.data_ptr())))
+    return ids, dist

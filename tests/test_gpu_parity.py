@@ -1,0 +1,236 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by
+element on the same seeded inputs (BASELINE.json north_star tolerances; see
+tests/parity.py).  Sizes span several CTAs/tiles and a ragged tail while the
+oracle still finishes in seconds."""
+import numpy as np
+import pytest
+
+from synth import generators as gen
+from tests.parity import assert_topk_parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rii():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1808_03969_b200 as r
+    r.load()
+    return r
+
+
+def _build_pair(rii, ref, x, M, K, n_iter=5, seed=0, train_rows=None, train_iter=5):
+    """GPU index and oracle index built the same way: train on the same rows,
+    add, reconfigure.  Returns (gpu, oracle)."""
+    D = x.shape[1]
+    tr = x if train_rows is None else train_rows
+    g = rii.Index(D, M)
+    g.train(tr, n_iter=train_iter, seed=seed)
+    o = ref.OracleIndex(D, M)
+    o.train(tr, n_iter=train_iter, seed=seed)
+    g.add(x)
+    o.add(x)
+    if K:
+        g.reconfigure(K, n_iter=n_iter, seed=seed)
+        o.reconfigure(K, n_iter=n_iter, seed=seed)
+    return g, o
+
+
+def _check_state(g, o):
+    assert np.array_equal(g.get_codebook(), o.cb), "code book differs (O-TRAIN)"
+    assert np.array_equal(g.get_codes(), o.codes), "codes differ (Eq. 1)"
+    if o.K:
+        assert np.array_equal(g.get_centers(), o.centers), "PQk-means centres differ (R9)"
+        off, ids = g.get_postings()
+        assert np.array_equal(off, o.offsets) and np.array_equal(ids, o.ids), "posting lists differ"
+
+
+# ------------------------------------------------------------------ tiny ----
+def test_tiny_config_end_to_end(rii, ref):
+    """BASELINE.json configs[0]: N=10k N(0,1) D=32, M=4, 20 k-means iters on the data,
+    nlist=100, 100 queries, topk=10, whole search at L=8 and a 1000-id subset."""
+    c = gen.CONFIGS["tiny"]
+    x = gen.gaussian(c["N"], c["D"], seed=0)
+    q = gen.gaussian(c["nq"], c["D"], seed=0, stream=gen.STREAM_QUERY)
+    S = gen.subset(c["N"], 1000, seed=0)
+    g, o = _build_pair(rii, ref, x, c["M"], c["nlist"], n_iter=10, train_iter=20)
+    _check_state(g, o)
+    for path in ("linear", "ivf", "auto"):
+        for sub in (None, S):
+            for L in (1, 8, 100):
+                gr = g.query(q, 10, target_ids=sub, L=L, path=path)
+                orr = o.query(q, 10, S=sub, L=L, path={"linear": 1, "ivf": 2, "auto": 0}[path])
+                assert gr[2] == orr[2], f"path_used {gr[2]} != {orr[2]}"
+                assert_topk_parity(ref, o.cb, o.codes, q, gr, orr, S=sub, what=f"tiny {path} L={L} S={sub is not None}")
+
+
+# ------------------------------------------------------- shapes / kernels ---
+CASES = [
+    # (kind, N, D, M, K, nq, topk)       -- M in {4,8,16,32}: lane-rotated kernel; 12, 6: generic kernel
+    ("sift", 23_457, 128, 16, 50, 37, 100),
+    ("deep", 19_999, 96, 32, 40, 25, 100),
+    ("deep", 17_001, 96, 8, 30, 29, 50),
+    ("deep", 9_001, 96, 12, 20, 13, 20),
+    ("gaussian", 5_003, 30, 6, 10, 7, 5),
+]
+
+
+@pytest.mark.parametrize("kind,N,D,M,K,nq,topk", CASES)
+def test_paths_match_oracle(rii, ref, kind, N, D, M, K, nq, topk):
+    x = gen.base(kind, N, D, seed=N)
+    q = gen.base(kind, nq, D, seed=N, stream=gen.STREAM_QUERY)
+    g, o = _build_pair(rii, ref, x, M, K, n_iter=4, train_rows=x[:4000], train_iter=4)
+    _check_state(g, o)
+    S_small = gen.subset(N, 777, seed=1)
+    S_big = gen.subset(N, N // 2 + 3, seed=2)
+    for path in ("linear", "ivf"):
+        for sub in (None, S_small, S_big):
+            for L in (1, 4):
+                gr = g.query(q, topk, target_ids=sub, L=L, path=path)
+                orr = o.query(q, topk, S=sub, L=L, path=1 if path == "linear" else 2)
+                assert_topk_parity(ref, o.cb, o.codes, q, gr, orr, S=sub, what=f"{kind} M={M} {path} L={L}")
+
+
+def test_device_memory_path_matches_host_path(rii, ref):
+    import torch
+    x = gen.deep_like(12_345, 96, seed=3)
+    q = gen.deep_like(40, 96, seed=3, stream=gen.STREAM_QUERY)
+    g, o = _build_pair(rii, ref, x, 32, 0, train_rows=x[:3000], train_iter=3)
+    hi, hd, _ = g.query(q, 64, path="linear")
+    di, dd, _ = g.query(torch.from_numpy(q).cuda(), 64, path="linear")
+    torch.cuda.synchronize()
+    assert np.array_equal(hi, di.cpu().numpy()) and np.array_equal(hd, dd.cpu().numpy())
+    gx = rii.Index(96, 32)
+    gx.set_codebook(g.get_codebook())
+    gx.add(torch.from_numpy(x).cuda())
+    assert np.array_equal(gx.get_codes(), o.codes)
+
+
+# ------------------------------------------------------------- edge cases ---
+def test_edge_cases(rii, ref):
+    x = gen.sift_like(3_001, 128, seed=7)
+    q = gen.sift_like(9, 128, seed=7, stream=gen.STREAM_QUERY)
+    g, o = _build_pair(rii, ref, x, 16, 10, n_iter=3, train_rows=x, train_iter=3)
+    # topk > |S| and > N: padding with (-1, +inf) (R18)
+    for topk, sub in ((1024, None), (50, np.array([5, 17, 3000], np.int64)), (7, np.array([42], np.int64))):
+        for path in ("linear", "ivf"):
+            gr = g.query(q, topk, target_ids=sub, L=3, path=path)
+            orr = o.query(q, topk, S=sub, L=3, path=1 if path == "linear" else 2)
+            assert_topk_parity(ref, o.cb, o.codes, q, gr, orr, S=sub, what=f"edge topk={topk}")
+    # empty subset -> all padding
+    ids, dist, _ = g.query(q, 5, target_ids=np.zeros(0, np.int64), path="linear")
+    assert (ids == -1).all() and np.isinf(dist).all()
+    # invalid subsets (R6): unsorted, duplicate, out of range
+    for bad in ([3, 2], [4, 4], [0, 3001]):
+        with pytest.raises(rii.RiiError) as e:
+            g.query(q, 5, target_ids=np.array(bad, np.int64))
+        assert e.value.status == 1
+    # topk bounds
+    with pytest.raises(rii.RiiError):
+        g.query(q, 0)
+    with pytest.raises(rii.RiiError):
+        g.query(q, 1025)
+    # nq = 0
+    ids, dist, _ = g.query(q[:0], 5)
+    assert ids.shape == (0, 5)
+    # K = 0 (never reconfigured): LINEAR forced, IVF refused
+    g0 = rii.Index(128, 16)
+    g0.set_codebook(o.cb)
+    g0.add(x)
+    assert g0.query(q, 5)[2] == rii.PATH_LINEAR
+    with pytest.raises(rii.RiiError) as e:
+        g0.query(q, 5, path="ivf")
+    assert e.value.status == 2
+    # untrained index
+    with pytest.raises(rii.RiiError) as e:
+        rii.Index(128, 16).add(x)
+    assert e.value.status == 2
+
+
+def test_duplicate_codes_tie_break(rii, ref):
+    """Identical codes give identical distances; ties must resolve to the lowest id
+    (CA4) even across CTAs and chunks."""
+    base = gen.deep_like(300, 96, seed=9)
+    x = np.concatenate([base] * 40)  # 12,000 rows, each code repeated 40 times
+    q = gen.deep_like(11, 96, seed=9, stream=gen.STREAM_QUERY)
+    g, o = _build_pair(rii, ref, x, 32, 0, train_rows=x[:3000], train_iter=2)
+    gr = g.query(q, 100, path="linear")
+    orr = o.query(q, 100, path=1)
+    assert np.array_equal(gr[0], orr[0]) and np.array_equal(gr[1], orr[1])
+
+
+def test_lossless_case_is_exact_knn(rii, ref):
+    """C-PIN7 on the GPU: D = M, code book {0..255}, integer data -> exact kNN."""
+    x = gen.lossless(6_000, 16, seed=5)
+    q = np.random.default_rng(5).integers(0, 256, size=(20, 16)).astype(np.float32)
+    cb = np.tile(np.arange(256, dtype=np.float32)[None, :, None], (16, 1, 1))
+    g = rii.Index(16, 16)
+    g.set_codebook(cb)
+    g.add(x)
+    ids, dist, _ = g.query(q, 30, path="linear")
+    for i in range(len(q)):
+        d = ((x.astype(np.int64) - q[i].astype(np.int64)) ** 2).sum(1)
+        order = np.lexsort((np.arange(len(x)), d))[:30]
+        assert np.array_equal(ids[i], order) and np.array_equal(dist[i], d[order].astype(np.float32))
+
+
+def test_theta_rule_and_ivf_all_lists(rii, ref):
+    x = gen.sift_like(8_000, 128, seed=11)
+    q = gen.sift_like(16, 128, seed=11, stream=gen.STREAM_QUERY)
+    g, o = _build_pair(rii, ref, x, 16, 40, n_iter=3, train_rows=x[:3000], train_iter=3)
+    th = ref.default_theta(g.info()["N"], 40, 2)
+    for size, want in ((th - 1, rii.PATH_LINEAR), (th, rii.PATH_IVF)):
+        S = gen.subset(8_000, size, seed=size)
+        assert g.query(q, 5, target_ids=S, L=2)[2] == want
+    g.set_theta(10**9)
+    assert g.query(q, 5, L=2)[2] == rii.PATH_LINEAR
+    g.set_theta(-1)
+    lin = g.query(q, 40, path="linear")
+    ivf = g.query(q, 40, L=40, path="ivf")     # L = nlist -> linear (BASELINE.json invariant 2)
+    assert np.array_equal(lin[0], ivf[0]) and np.array_equal(lin[1], ivf[1])
+
+
+def test_add_after_reconfigure_and_growth(rii, ref):
+    """Data addition with K > 0 then reconfigure again (config 4 in small)."""
+    x = gen.sift_like(12_000, 128, seed=13)
+    q = gen.sift_like(12, 128, seed=13, stream=gen.STREAM_QUERY)
+    g, o = _build_pair(rii, ref, x[:2_000], 16, 20, n_iter=3, train_rows=x[:2_000], train_iter=3)
+    for s in range(2_000, 12_000, 3_333):
+        g.add(x[s:s + 3_333])
+        o.add(x[s:s + 3_333])
+    _check_state(g, o)
+    for L in (1, 5):
+        assert_topk_parity(ref, o.cb, o.codes, q, g.query(q, 20, L=L, path="ivf"), o.query(q, 20, L=L, path=2))
+    g.reconfigure(110, n_iter=3, seed=4)
+    o.reconfigure(110, n_iter=3, seed=4)
+    _check_state(g, o)
+    assert_topk_parity(ref, o.cb, o.codes, q, g.query(q, 20, L=2, path="ivf"), o.query(q, 20, L=2, path=2))
+
+
+def test_logical_shards_equal_single_index(rii, ref):
+    """Id-range sharding on one GPU: two detached shards, per-shard
+    partial top-k, merge -> identical to the single index (C-PIN10)."""
+    import torch
+    x = gen.deep_like(20_001, 96, seed=17)
+    q = gen.deep_like(33, 96, seed=17, stream=gen.STREAM_QUERY)
+    single, o = _build_pair(rii, ref, x, 32, 0, train_rows=x[:3000], train_iter=2)
+    cb = single.get_codebook()
+    shards = []
+    for r in range(2):
+        s = rii.Index(96, 32, rank=r, world=2)
+        s.set_codebook(cb)
+        for a in range(0, 20_001, 7_000):      # several add batches -> several id ranges per shard
+            s.add(x[a:a + 7_000])
+        shards.append(s)
+    qt = torch.from_numpy(q).cuda()
+    S = gen.subset(20_001, 5_000, seed=3)
+    for sub in (None, S):
+        parts = torch.stack([s.query_partial(qt, 50, target_ids=sub, path="linear")[0] for s in shards])
+        ids, dist = rii.merge_partials(parts, 50)
+        ref_ids, ref_d, _ = single.query(q, 50, target_ids=sub, path="linear")
+        assert np.array_equal(ids.cpu().numpy(), ref_ids) and np.array_equal(dist.cpu().numpy(), ref_d)
+    with pytest.raises(rii.RiiError) as e:
+        shards[0].query(q, 5)
+    assert e.value.status == 2

@@ -66,6 +66,15 @@ const char *rii_last_error(void);
  * indexes).  Used by bench.py to report "gpu_launches". */
 uint64_t rii_launch_count(void);
 
+/* Optional CUDA-event timing of the dominant kernels, recorded on the stream each
+ * kernel is launched on (used by bench.py for the roofline's "achieved").
+ * rii_kernel_timing(1) clears the totals and starts recording; (0) stops.
+ * which: 0 = linear ADC scan kernel, 1 = inverted-index list-scan kernel,
+ * 2 = top-k merge kernel.  total_ms / launches cover every launch since the
+ * last clear (read synchronises with the recorded events). */
+void rii_kernel_timing(int32_t enable);
+rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *launches);
+
 /* Rank 0 calls this to obtain the NCCL unique id that every rank then passes to
  * rii_create (distributed by the caller, e.g. through torch.distributed).
  * out: RII_NCCL_ID_BYTES host bytes.  RII_ERR_NCCL if NCCL cannot be loaded. */

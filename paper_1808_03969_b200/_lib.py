@@ -22,6 +22,8 @@ _p, _i32, _i64, _u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64
 SIGNATURES = {
     "rii_last_error": (C.c_char_p, []),
     "rii_launch_count": (_u64, []),
+    "rii_kernel_timing": (None, [_i32]),
+    "rii_kernel_timing_read": (C.c_int, [_i32, C.POINTER(C.c_double), C.POINTER(_i64)]),
     "rii_nccl_unique_id": (C.c_int, [_p]),
     "rii_create": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _i32, _p, C.POINTER(_p)]),
     "rii_destroy": (None, [_p]),

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstring>
 #include <new>
 #include <string>
@@ -15,6 +16,43 @@
 
 namespace rii {
 std::atomic<uint64_t> g_launches{0};
+
+namespace timing {
+std::mutex g_tmu;
+bool g_timing = false;
+struct TimedPair { int which; cudaEvent_t a, b; };
+std::vector<TimedPair> g_pairs;
+double g_total_ms[TK_COUNT] = {0, 0, 0};
+int64_t g_count[TK_COUNT] = {0, 0, 0};
+
+void drain_pairs() {  // caller holds g_tmu
+    for (auto &p : g_pairs) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            g_total_ms[p.which] += ms;
+            g_count[p.which] += 1;
+        }
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    g_pairs.clear();
+}
+}  // namespace timing
+using namespace timing;
+
+KernelTimer::KernelTimer(int w, cudaStream_t s) : st(s), which(w) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    if (!g_timing) return;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) { a = b = nullptr; return; }
+    cudaEventRecord(a, st);
+}
+
+KernelTimer::~KernelTimer() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    std::lock_guard<std::mutex> lk(g_tmu);
+    g_pairs.push_back({which, a, b});
+}
 
 // Grow-only device buffer (scratch and index arrays).
 struct Buf {
@@ -338,6 +376,23 @@ extern "C" {
 const char *rii_last_error(void) { return t_err.c_str(); }
 
 uint64_t rii_launch_count(void) { return g_launches.load(); }
+
+void rii_kernel_timing(int32_t enable) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    drain_pairs();
+    for (int i = 0; i < TK_COUNT; ++i) { g_total_ms[i] = 0; g_count[i] = 0; }
+    g_timing = enable != 0;
+}
+
+rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *launches) {
+    return guarded([&] {
+        arg_check(which >= 0 && which < TK_COUNT, "which must be 0, 1 or 2");
+        std::lock_guard<std::mutex> lk(g_tmu);
+        drain_pairs();
+        if (total_ms) *total_ms = g_total_ms[which];
+        if (launches) *launches = g_count[which];
+    });
+}
 
 int32_t rii_partial_width(int32_t topk) { return partial_width(topk); }
 

@@ -34,6 +34,16 @@ inline void count_launch(int n = 1) { g_launches.fetch_add((uint64_t)n, std::mem
         RII_CUDA(cudaGetLastError());                                                             \
     } while (0)
 
+// Optional per-kernel event timing (rii_kernel_timing).
+enum TimedKernel { TK_LINEAR = 0, TK_IVF = 1, TK_MERGE = 2, TK_COUNT = 3 };
+struct KernelTimer {
+    cudaStream_t st;
+    int which;
+    cudaEvent_t a = nullptr, b = nullptr;
+    KernelTimer(int w, cudaStream_t s);   // records the start event if timing is on
+    ~KernelTimer();                       // records the stop event
+};
+
 // -------------------------------------------------------- arithmetic ------
 // CA1: t = u - c; acc = acc + t*t; fp32 round-to-nearest, no contraction.
 __device__ __forceinline__ float ca1_step(float acc, float u, float c) {

@@ -316,6 +316,7 @@ static void ivf_launch_t(const uint8_t *codes, int Mrt, const float *q, int64_t 
     const size_t smem = ivf_smem(Mrt, kk);
     auto kern = ivf_scan_kernel<M, FAST>;
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    KernelTimer t(TK_IVF, st);
     kern<<<(unsigned)ceil_div(nq, 2), NT, smem, st>>>(codes, q, nq, cb, Mrt, ds, kk, probes, P, offsets, ids, out);
     RII_LAUNCHED();
 }

@@ -283,6 +283,7 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
                           const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st) {
     auto kern = scan_fast_kernel<M, B>;
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    KernelTimer t(TK_LINEAR, st);
     kern<<<pl.nb * pl.nc, NT, pl.smem, st>>>(codes, n, q, nq, cb, ds, kk, pl.nb, pl.chunk, pl.nc, out);
     RII_LAUNCHED();
 }
@@ -300,6 +301,7 @@ static void launch_generic_t(const ScanPlan &pl, const uint8_t *codes, int64_t n
                              const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st) {
     auto kern = scan_generic_kernel<B>;
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    KernelTimer t(TK_LINEAR, st);
     kern<<<pl.nb * pl.nc, NT, pl.smem, st>>>(codes, n, q, nq, cb, M, ds, kk, pl.nb, pl.chunk, pl.nc, out);
     RII_LAUNCHED();
 }
@@ -395,6 +397,7 @@ __global__ void __launch_bounds__(NT) merge_kernel(const uint64_t *__restrict__ 
 void launch_merge(const uint64_t *keys, int64_t q_stride, int64_t p_stride, int parts, int64_t nq, int kk, int topk,
                   const IdMap &map, int64_t *out_ids, float *out_dist, uint64_t *out_keys, cudaStream_t st) {
     if (nq <= 0) return;
+    KernelTimer t(TK_MERGE, st);
     merge_kernel<<<(unsigned)nq, NT, (size_t)2 * kk * 8, st>>>(keys, q_stride, p_stride, parts, kk, topk, map,
                                                                out_ids, out_dist, out_keys);
     RII_LAUNCHED();

@@ -75,6 +75,10 @@ uint64_t rii_launch_count(void);
 void rii_kernel_timing(int32_t enable);
 rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *launches);
 
+/* The rows [*lo, *hi) of an n-row rii_add batch that rank `rank` of `world` stores
+ * (contiguous chunks of ceil(n / world) rows; host-only, no device needed). */
+rii_status rii_shard_range(int64_t n, int32_t rank, int32_t world, int64_t *lo, int64_t *hi);
+
 /* Rank 0 calls this to obtain the NCCL unique id that every rank then passes to
  * rii_create (distributed by the caller, e.g. through torch.distributed).
  * out: RII_NCCL_ID_BYTES host bytes.  RII_ERR_NCCL if NCCL cannot be loaded. */

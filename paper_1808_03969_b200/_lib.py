@@ -24,6 +24,7 @@ SIGNATURES = {
     "rii_launch_count": (_u64, []),
     "rii_kernel_timing": (None, [_i32]),
     "rii_kernel_timing_read": (C.c_int, [_i32, C.POINTER(C.c_double), C.POINTER(_i64)]),
+    "rii_shard_range": (C.c_int, [_i64, _i32, _i32, C.POINTER(_i64), C.POINTER(_i64)]),
     "rii_nccl_unique_id": (C.c_int, [_p]),
     "rii_create": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _i32, _p, C.POINTER(_p)]),
     "rii_destroy": (None, [_p]),

@@ -396,6 +396,14 @@ rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *laun
 
 int32_t rii_partial_width(int32_t topk) { return partial_width(topk); }
 
+rii_status rii_shard_range(int64_t n, int32_t rank, int32_t world, int64_t *lo, int64_t *hi) {
+    return guarded([&] {
+        arg_check(lo && hi, "NULL argument");
+        arg_check(n >= 0 && world >= 1 && rank >= 0 && rank < world, "need n >= 0 and 0 <= rank < world");
+        rank_rows(n, rank, world, *lo, *hi);
+    });
+}
+
 rii_status rii_nccl_unique_id(void *out) {
     return guarded([&] {
         arg_check(out != nullptr, "out is NULL");

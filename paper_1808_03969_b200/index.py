@@ -68,6 +68,13 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows [lo, hi) of an n-row add batch stored by `rank` of `world` (host-only)."""
+    lo, hi = C.c_int64(), C.c_int64()
+    _rl.check(_rl.load().rii_shard_range(n, rank, world, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
 def launch_count() -> int:
     return int(_rl.load().rii_launch_count())
 

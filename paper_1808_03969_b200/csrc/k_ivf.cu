@@ -8,6 +8,7 @@
 //                  evaluate ADC with the lane-rotated table of k_scan.cu and keep
 //                  the top-kk in shared memory (L7-L16, mode A of reading R2).
 #include "kernels.cuh"
+#include "lut.cuh"
 #include "topk.cuh"
 
 namespace rii {
@@ -152,7 +153,7 @@ __device__ __forceinline__ void load_code_ivf(const uint8_t *p, uint32_t (&w)[W]
     }
 }
 
-constexpr int PAIR_BYTES = 256 * 256;
+constexpr int PAIR_BYTES = LUT_PAIR_BYTES;
 
 // Per-warp work pulling: (qq, r) items = query half qq, probe rank r.
 struct ListCursor {
@@ -200,18 +201,7 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
     const int D = MM * ds, tid = threadIdx.x, lane = tid & 31;
     const float *qa = q + min(q0, nq - 1) * D, *qb = q + min(q0 + 1, nq - 1) * D;
     if constexpr (FAST) {
-        const int m = lane & (M - 1);
-        float *lp = reinterpret_cast<float *>(lut);
-        for (int z = tid >> 5; z < KS; z += NT / 32) {
-            const float *cv = cb + ((size_t)m * KS + z) * ds;
-            float a0 = 0.f, a1 = 0.f;
-            for (int j = 0; j < ds; ++j) {
-                a0 = ca1_step(a0, qa[m * ds + j], cv[j]);
-                a1 = ca1_step(a1, qb[m * ds + j], cv[j]);
-            }
-            lp[z * 64 + lane] = a0;
-            lp[z * 64 + 32 + lane] = a1;
-        }
+        build_lut_pair<M>(reinterpret_cast<float *>(lut), qa, qb, cb, ds);
     } else {
         float *lp = reinterpret_cast<float *>(lut);
         for (int e = tid; e < 2 * MM * KS; e += NT) {
@@ -229,8 +219,7 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
 
     uint32_t sel[4];
     const uint32_t r = (uint32_t)lane & (FAST ? (M - 1) : 0), rw = r >> 2;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) sel[t] = 0x5504u | ((((uint32_t)t ^ r) & 3u) << 4);
+    make_selectors(r, sel);
     float th0 = thr[0], th1 = thr[1];
     bool need = false;
     ListCursor cur{0, 0, 0, false};
@@ -247,21 +236,11 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
 #pragma unroll
                 for (int i = 0; i < W; ++i) w[i] = 0;
                 if (valid) load_code_ivf<W>(codes + (size_t)pos * M, w);
-#pragma unroll
-                for (int b = 1; b < W; b <<= 1) {
-                    const bool c = (rw & b) != 0;
-#pragma unroll
-                    for (int i = 0; i < W; ++i) {
-                        if (i & b) continue;
-                        const uint32_t x = w[i], y = w[i | b];
-                        w[i] = c ? y : x;
-                        w[i | b] = c ? x : y;
-                    }
-                }
-                const uint32_t l4 = ((uint32_t)cur.qq << 7) | ((uint32_t)lane << 2);
+                permute_words<W>(w, rw);
+                const uint32_t l8 = ((uint32_t)lane << 3) | ((uint32_t)cur.qq << 2);
 #pragma unroll
                 for (int j = 0; j < (FAST ? M : 1); ++j) {
-                    const uint32_t off = __byte_perm(w[j >> 2], l4 ^ (uint32_t)(j << 2), sel[j & 3]);
+                    const uint32_t off = __byte_perm(w[j >> 2], l8 ^ (uint32_t)(j << 3), sel[j & 3]);
                     acc += *reinterpret_cast<const float *>(lut + off);
                 }
             } else if (valid) {
@@ -289,9 +268,9 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
             const int qq = e / kk;
             const uint32_t id = key_id(k);
             const uint8_t *cp = codes + (size_t)id * M;
-            const float *lq = reinterpret_cast<const float *>(lut) + qq * 32;
+            const float *lq = reinterpret_cast<const float *>(lut);
             float d = 0.f;
-            for (int m = 0; m < M; ++m) d = __fadd_rn(d, lq[(int)cp[m] * 64 + m]);
+            for (int m = 0; m < M; ++m) d = __fadd_rn(d, lut_pair_entry(lq, qq, m, cp[m]));
             top[e] = make_key(d, id);
         }
         __syncthreads();

@@ -16,11 +16,11 @@
 // canonical (CA2, m ascending) rescore of the kept candidates, so the returned
 // distances equal the oracle's bit for bit.
 #include "kernels.cuh"
+#include "lut.cuh"
 #include "topk.cuh"
 
 namespace rii {
 
-constexpr int LUT_PAIR_BYTES = 256 * 256;  // 256 rows x 64 fp32 words (two queries)
 
 template <int W>
 __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
@@ -40,50 +40,24 @@ __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
     }
 }
 
-// Replica layout of a query pair: word z*64 + half*32 + c = A_half(c mod M, z).
-template <int M>
-__device__ void build_lut_pair(float *lutp, const float *q0, const float *q1, const float *__restrict__ cb, int ds) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int m = lane & (M - 1);
-    for (int z = warp; z < KS; z += NT / 32) {
-        const float *cv = cb + ((size_t)m * KS + z) * ds;
-        float a0 = 0.f, a1 = 0.f;
-        for (int j = 0; j < ds; ++j) {
-            const float c = cv[j];
-            a0 = ca1_step(a0, q0[m * ds + j], c);
-            a1 = ca1_step(a1, q1[m * ds + j], c);
-        }
-        lutp[z * 64 + lane] = a0;
-        lutp[z * 64 + 32 + lane] = a1;
-    }
-}
-
-// Lane-rotated ADC of one code (M bytes in w) against the B tables of the CTA.
+// Lane-rotated ADC of one code (M bytes in w) against the B tables of the CTA:
+// per step j one PRMT builds (z << 8) | 8*(l ^ j); per query pair one LDS.64 +
+// one FADD2.
 template <int M, int B>
 __device__ __forceinline__ void adc_rotated(const uint8_t *lut, const uint32_t (&w)[M / 4], uint32_t rw,
-                                            const uint32_t (&sel)[4], uint32_t l4, float (&acc)[B]) {
-    constexpr int W = M / 4;
+                                            const uint32_t (&sel)[4], uint32_t l8, float2 (&acc)[B / 2]) {
+    constexpr int W = M / 4, NP = B / 2;
     uint32_t wp[W];
 #pragma unroll
     for (int i = 0; i < W; ++i) wp[i] = w[i];
-#pragma unroll
-    for (int b = 1; b < W; b <<= 1) {
-        const bool c = (rw & b) != 0;
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-            if (i & b) continue;
-            const uint32_t x = wp[i], y = wp[i | b];
-            wp[i] = c ? y : x;
-            wp[i | b] = c ? x : y;
-        }
-    }
+    permute_words<W>(wp, rw);
 #pragma unroll
     for (int j = 0; j < M; ++j) {
-        const uint32_t off = __byte_perm(wp[j >> 2], l4 ^ (uint32_t)(j << 2), sel[j & 3]);
+        const uint32_t off = __byte_perm(wp[j >> 2], l8 ^ (uint32_t)(j << 3), sel[j & 3]);
 #pragma unroll
-        for (int qq = 0; qq < B; ++qq) {
-            const float v = *reinterpret_cast<const float *>(lut + (qq >> 1) * LUT_PAIR_BYTES + (qq & 1) * 128 + off);
-            acc[qq] = j == 0 ? v : acc[qq] + v;  // 0 + v == v for v >= +0
+        for (int p = 0; p < NP; ++p) {
+            const float2 v = *reinterpret_cast<const float2 *>(lut + p * LUT_PAIR_BYTES + off);
+            acc[p] = j == 0 ? v : fadd2(acc[p], v);  // 0 + v == v for v >= +0
         }
     }
 }
@@ -115,10 +89,9 @@ __global__ void __launch_bounds__(NT, 1)
     if (tid < B) { cnt[tid] = 0; thr[tid] = __int_as_float(0x7f800000); }
     __syncthreads();
 
-    const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l4 = (uint32_t)lane << 2;
+    const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
     uint32_t sel[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) sel[t] = 0x5504u | ((((uint32_t)t ^ r) & 3u) << 4);
+    make_selectors(r, sel);
     float th[B];
 #pragma unroll
     for (int qq = 0; qq < B; ++qq) th[qq] = thr[qq];
@@ -136,8 +109,11 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int i = 0; i < W; ++i) wn[i] = 0;
         if (npos < c1) load_code<W>(codes + npos * M, wn);
+        float2 acc2[NP];
+        adc_rotated<M, B>(lut, w, rw, sel, l8, acc2);
         float acc[B];
-        adc_rotated<M, B>(lut, w, rw, sel, l4, acc);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) { acc[2 * p] = acc2[p].x; acc[2 * p + 1] = acc2[p].y; }
 #pragma unroll
         for (int qq = 0; qq < B; ++qq)
             push_candidate(valid && acc[qq] <= th[qq], make_key(acc[qq], (uint32_t)pos), fresh + qq * NEWCAP,
@@ -161,10 +137,10 @@ __global__ void __launch_bounds__(NT, 1)
         const int qq = e / kk;
         const uint32_t id = key_id(k);
         const uint8_t *cp = codes + (size_t)id * M;
-        const float *lq = reinterpret_cast<const float *>(lut + (qq >> 1) * LUT_PAIR_BYTES) + (qq & 1) * 32;
+        const float *lq = reinterpret_cast<const float *>(lut + (qq >> 1) * LUT_PAIR_BYTES);
         float d = 0.f;
 #pragma unroll
-        for (int m = 0; m < M; ++m) d = __fadd_rn(d, lq[(int)cp[m] * 64 + m]);
+        for (int m = 0; m < M; ++m) d = __fadd_rn(d, lut_pair_entry(lq, qq & 1, m, cp[m]));
         top[e] = make_key(d, id);
     }
     __syncthreads();

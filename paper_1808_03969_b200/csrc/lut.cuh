@@ -1,0 +1,73 @@
+// lut.cuh -- the lane-rotated, bank-conflict-free ADC table of a query pair
+// (DESIGN.md §6 "Linear scan").  256 rows (code word z) x 32 columns x 2 queries:
+// fp32 word z*64 + 2*c + h holds A_h(c mod M, z) for query h of the pair, so one
+// LDS.64 returns the entries of both queries and one packed FADD2 adds them.
+// Lane l reads column c = l ^ j at step j: 32 distinct columns -> every 16-lane
+// half-warp covers 32 distinct banks whatever the code bytes are.
+#pragma once
+#include "common.cuh"
+
+namespace rii {
+
+constexpr int LUT_PAIR_BYTES = 256 * 256;
+
+// Build the table of queries q0, q1 (global memory) from the code book (CA1).
+template <int M>
+__device__ __forceinline__ void build_lut_pair(float *lutp, const float *q0, const float *q1,
+                                               const float *__restrict__ cb, int ds) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int m = lane & (M - 1);
+    for (int z = warp; z < KS; z += nwarps) {
+        const float *cv = cb + ((size_t)m * KS + z) * ds;
+        float a0 = 0.f, a1 = 0.f;
+        for (int j = 0; j < ds; ++j) {
+            const float c = cv[j];
+            a0 = ca1_step(a0, q0[m * ds + j], c);
+            a1 = ca1_step(a1, q1[m * ds + j], c);
+        }
+        reinterpret_cast<float2 *>(lutp)[z * 32 + lane] = make_float2(a0, a1);
+    }
+}
+
+// Canonical (replica 0) entry A_h(m, z) of the pair table.
+__device__ __forceinline__ float lut_pair_entry(const float *lutp, int h, int m, int z) {
+    return lutp[z * 64 + 2 * m + h];
+}
+
+// Packed fp32x2 add (sm_100 FADD2): two IEEE round-to-nearest fp32 adds.
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    float2 r;
+    asm("{\n\t.reg .b64 ra, rb, rc;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rc, ra, rb;\n\t"
+        "mov.b64 {%0, %1}, rc;\n\t}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
+
+// XOR-permute the code words by the lane's rotation: wp[i] = w[i ^ rw].
+template <int W>
+__device__ __forceinline__ void permute_words(uint32_t (&w)[W], uint32_t rw) {
+#pragma unroll
+    for (int b = 1; b < W; b <<= 1) {
+        const bool c = (rw & b) != 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            if (i & b) continue;
+            const uint32_t x = w[i], y = w[i | b];
+            w[i] = c ? y : x;
+            w[i | b] = c ? x : y;
+        }
+    }
+}
+
+// PRMT selectors: byte0 <- b-operand byte 0 (the column offset), byte1 <- code byte
+// ((t ^ r) & 3) of the word, bytes 2-3 <- 0.  Result = (z << 8) | col_offset.
+__device__ __forceinline__ void make_selectors(uint32_t r, uint32_t (&sel)[4]) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) sel[t] = 0x5504u | ((((uint32_t)t ^ r) & 3u) << 4);
+}
+
+}  // namespace rii

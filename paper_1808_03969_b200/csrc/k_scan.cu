@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(NT, 1)
         build_lut_pair<M>(reinterpret_cast<float *>(lut + p * LUT_PAIR_BYTES), q + qa * D, q + qc * D, cb, ds);
     }
     for (int e = tid; e < B * kk; e += NT) top[e] = KEY_MAX;
-    if (tid < B) { cnt[tid] = 0; thr[tid] = __int_as_float(0x7f800000); }
+    if (tid < B) { cnt[tid] = 0; thr[tid] = __int_as_float(0x7f800000); scratch[2 + tid] = 0; }
+    if (tid == 0) scratch[1] = 0;
     __syncthreads();
 
     const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
@@ -95,38 +96,74 @@ __global__ void __launch_bounds__(NT, 1)
     float th[B];
 #pragma unroll
     for (int qq = 0; qq < B; ++qq) th[qq] = thr[qq];
-    bool need = false;
 
-    uint32_t w[W];
-    int64_t pos = c0 + tid;
+    // Each thread evaluates U codes per step (positions base + u*NT + tid, coalesced),
+    // the next step's codes prefetched into registers.  Block barriers only every
+    // WIN steps: a window whose pushes overflow the fresh buffer is rolled back
+    // (its pushes dropped, the buffer compacted) and redone one step at a time,
+    // which cannot overflow (an empty buffer holds a whole step, NEWCAP >= NT*U).
+    constexpr int U = 2, STEP = NT * U, WIN = 4, SOFT = NEWCAP / 4;
+    static_assert(NEWCAP >= STEP, "a single step must fit the fresh buffer");
+    int *s_ovf = scratch + 1, *s_cnt0 = scratch + 2;  // flags, fill snapshot at the window start
+    uint32_t w[U][W];
+    auto load_step = [&](int64_t b, uint32_t(&dst)[U][W]) {
 #pragma unroll
-    for (int i = 0; i < W; ++i) w[i] = 0;
-    if (pos < c1) load_code<W>(codes + pos * M, w);
-    for (int64_t base = c0; base < c1; base += NT) {
-        const bool valid = pos < c1;
-        const int64_t npos = pos + NT;
-        uint32_t wn[W];
+        for (int u = 0; u < U; ++u) {
+            const int64_t p = b + u * NT + tid;
 #pragma unroll
-        for (int i = 0; i < W; ++i) wn[i] = 0;
-        if (npos < c1) load_code<W>(codes + npos * M, wn);
-        float2 acc2[NP];
-        adc_rotated<M, B>(lut, w, rw, sel, l8, acc2);
-        float acc[B];
+            for (int i = 0; i < W; ++i) dst[u][i] = 0;
+            if (p < c1) load_code<W>(codes + p * M, dst[u]);
+        }
+    };
+    int64_t base = c0;
+    load_step(base, w);
+    int safe = 0;
+    while (base < c1) {
+        const int64_t wstart = base;
+        const int nsteps = safe > 0 ? 1 : WIN;
+        bool ovf = false, need = false;
+        for (int s = 0; s < nsteps && base < c1; ++s) {
+            uint32_t wn[U][W];
+            load_step(base + STEP, wn);
 #pragma unroll
-        for (int p = 0; p < NP; ++p) { acc[2 * p] = acc2[p].x; acc[2 * p + 1] = acc2[p].y; }
+            for (int u = 0; u < U; ++u) {
+                const int64_t pos = base + u * NT + tid;
+                float2 acc2[NP];
+                adc_rotated<M, B>(lut, w[u], rw, sel, l8, acc2);
 #pragma unroll
-        for (int qq = 0; qq < B; ++qq)
-            push_candidate(valid && acc[qq] <= th[qq], make_key(acc[qq], (uint32_t)pos), fresh + qq * NEWCAP,
-                           cnt + qq, lane, need);
-        if (__syncthreads_or(need)) {
+                for (int p = 0; p < NP; ++p) {
+                    push_candidate_win(pos < c1 && acc2[p].x <= th[2 * p], make_key(acc2[p].x, (uint32_t)pos),
+                                       fresh + (2 * p) * NEWCAP, cnt + 2 * p, lane, SOFT, need, ovf);
+                    push_candidate_win(pos < c1 && acc2[p].y <= th[2 * p + 1], make_key(acc2[p].y, (uint32_t)pos),
+                                       fresh + (2 * p + 1) * NEWCAP, cnt + 2 * p + 1, lane, SOFT, need, ovf);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int i = 0; i < W; ++i) w[u][i] = wn[u][i];
+            base += STEP;
+        }
+        if (ovf) *s_ovf = 1;
+        if (__syncthreads_or(ovf || need)) {
+            const bool rolled = *s_ovf != 0;  // written before the barrier; reset below
+            if (rolled && tid < B) cnt[tid] = s_cnt0[tid];
             compact_topk(top, fresh, cnt, thr, B, kk, scratch);
+            if (tid == 0) *s_ovf = 0;
+            if (tid < B) s_cnt0[tid] = 0;
 #pragma unroll
             for (int qq = 0; qq < B; ++qq) th[qq] = thr[qq];
-            need = false;
+            if (rolled) {
+                base = wstart;
+                load_step(base, w);
+                safe = 4;
+                continue;
+            }
+        } else {
+            if (tid < B) s_cnt0[tid] = cnt[tid];
+            __syncthreads();  // snapshot taken before the next window pushes
         }
-#pragma unroll
-        for (int i = 0; i < W; ++i) w[i] = wn[i];
-        pos = npos;
+        if (safe > 0) --safe;
     }
     compact_topk(top, fresh, cnt, thr, B, kk, scratch);
 
@@ -218,7 +255,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
 }
 
-static size_t smem_fast(int B, int kk) { return (size_t)(B / 2) * LUT_PAIR_BYTES + (size_t)B * (kk + NEWCAP) * 8 + 64; }
+static size_t smem_fast(int B, int kk) { return (size_t)(B / 2) * LUT_PAIR_BYTES + (size_t)B * (kk + NEWCAP) * 8 + 64; }  // 64 B: cnt, thr, scratch[8]
 static size_t smem_generic(int B, int M, int kk) {
     return (size_t)B * M * KS * 4 + (size_t)B * (kk + NEWCAP) * 8 + 64;
 }

@@ -33,6 +33,29 @@ __device__ __forceinline__ void push_candidate(bool pred, uint64_t key, uint64_t
     }
 }
 
+// Windowed variant: never writes past NEWCAP; a push that does not fit sets
+// `ovf` (the caller rolls the window back and redoes it) and a fill above
+// `soft` sets `need` (compaction at the window end).
+__device__ __forceinline__ void push_candidate_win(bool pred, uint64_t key, uint64_t *fresh_q, int *cnt_q, int lane,
+                                                   int soft, bool &need, bool &ovf) {
+    unsigned bal = __ballot_sync(0xffffffffu, pred);
+    if (bal) {
+        int n = __popc(bal);
+        int leader = __ffs(bal) - 1;
+        int base = 0;
+        if (lane == leader) {
+            base = atomicAdd(cnt_q, n);
+            if (base + n > soft) need = true;
+        }
+        base = __shfl_sync(0xffffffffu, base, leader);
+        const int slot = base + __popc(bal & ((1u << lane) - 1u));
+        if (pred) {
+            if (slot < NEWCAP) fresh_q[slot] = key;
+            else ovf = true;
+        }
+    }
+}
+
 __device__ __forceinline__ void cas_asc(uint64_t *a, int i, int p) {
     uint64_t x = a[i], y = a[p];
     if (x > y) { a[i] = y; a[p] = x; }

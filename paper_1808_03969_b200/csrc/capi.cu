@@ -115,7 +115,7 @@ struct rii_index {
     int64_t theta = -1;
     // scratch (query side is const-callable: mutable)
     mutable Buf s_q, s_S, s_pos, s_sub, s_part, s_keys, s_gather, s_d0, s_probe, s_roff, s_rids, s_rkey, s_rval,
-        s_out_ids, s_out_dist, s_flag, s_x;
+        s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_items;
 };
 
 namespace {
@@ -339,9 +339,38 @@ void search_local(const rii_index *x, const QueryArgs &a, cudaStream_t st, int64
             off = roff;
             ids = rids;
         }
-        uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
-        launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st);
-        parts = pp;
+        // List-major (B queries share one list's codes) when lists are long and the
+        // [nq][P][kk] partials stay small; otherwise query-major (one LUT per query).
+        const int64_t n_cand = a.S ? std::max<int64_t>(a.nS, 1) : x->n_local;
+        const double avg_len = (double)n_cand / (double)x->K;
+        const int Bl = list_major_supported(x->M) ? list_major_B(kk) : 0;
+        const bool list_major = Bl > 0 && avg_len >= 768.0 && (double)a.nq * P * kk * 8 <= 4e9 &&
+                                (double)a.nq * P < 4e9;
+        if (list_major) {
+            const int64_t npairs = a.nq * P;
+            uint32_t *vals = x->s_lq.get<uint32_t>(npairs);
+            iota_u32_kernel<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(vals, npairs);
+            RII_LAUNCHED();
+            int64_t *qoff = x->s_qoff.get<int64_t>(x->K + 1);
+            uint32_t *qlist = x->s_ql.get<uint32_t>(npairs);
+            build_csr(probes, vals, npairs, x->K, qoff, qlist, st);  // (query, rank) pairs grouped by list
+            const int64_t cap = npairs / Bl + x->K + 1;
+            int4 *items = x->s_items.get<int4>(cap);
+            const int64_t n_items = build_list_items(qoff, x->K, Bl, items, cap, st);
+            uint64_t *pp = x->s_part.get<uint64_t>((size_t)npairs * kk);
+            ScanArgs sa{};
+            sa.codes = codes; sa.q = a.q; sa.nq = a.nq; sa.cb = cb; sa.ds = x->ds; sa.kk = kk; sa.out = pp;
+            sa.items = items; sa.qlist = qlist; sa.P = P; sa.offsets = off; sa.ids = ids;
+            launch_list_scan(x->M, sa, n_items, st);
+            parts = pp;
+            q_stride = P * kk;
+            p_stride = kk;
+            nparts = (int)P;
+        } else {
+            uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
+            launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st);
+            parts = pp;
+        }
     }
     launch_merge(parts, q_stride, p_stride, nparts, a.nq, kk, a.topk, map, out_ids, out_dist, out_keys, st);
 }

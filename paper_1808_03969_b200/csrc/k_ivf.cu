@@ -7,6 +7,8 @@
 //                  and codes (16-byte gathers from the linear array),
 //                  evaluate ADC with the lane-rotated table of k_scan.cu and keep
 //                  the top-kk in shared memory (L7-L16, mode A of reading R2).
+#include <cub/cub.cuh>
+
 #include "kernels.cuh"
 #include "lut.cuh"
 #include "topk.cuh"
@@ -132,6 +134,48 @@ void launch_select_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int
     if (nq <= 0) return;
     select_probes_kernel<<<(unsigned)nq, NT, 0, st>>>(d0, K, P, probes);
     RII_LAUNCHED();
+}
+
+// ------------------------------------------------------ list-major items ----
+__global__ void list_item_count_kernel(const int64_t *__restrict__ qoff, int64_t K, int B, int64_t *__restrict__ n) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < K) n[k] = (qoff[k + 1] - qoff[k] + B - 1) / B;
+    else if (k == K) n[k] = 0;
+}
+
+__global__ void list_item_fill_kernel(const int64_t *__restrict__ qoff, const int64_t *__restrict__ ioff, int64_t K,
+                                      int B, int4 *__restrict__ items) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const int64_t c = qoff[k + 1] - qoff[k];
+    for (int64_t i = 0; i * B < c; ++i) {
+        const int64_t n = c - i * B < B ? c - i * B : B;
+        items[ioff[k] + i] = make_int4((int)k, (int)(qoff[k] + i * B), (int)n, 0);
+    }
+}
+
+int64_t build_list_items(const int64_t *qoff, int64_t K, int B, int4 *items, int64_t cap, cudaStream_t st) {
+    int64_t *n = nullptr, *ioff = nullptr;
+    RII_CUDA(cudaMallocAsync(&n, (size_t)(K + 1) * 8, st));
+    RII_CUDA(cudaMallocAsync(&ioff, (size_t)(K + 1) * 8, st));
+    list_item_count_kernel<<<(unsigned)ceil_div(K + 1, 256), 256, 0, st>>>(qoff, K, B, n);
+    RII_LAUNCHED();
+    size_t tb = 0;
+    RII_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, n, ioff, K + 1, st));
+    void *tmp = nullptr;
+    RII_CUDA(cudaMallocAsync(&tmp, tb, st));
+    RII_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, n, ioff, K + 1, st));
+    count_launch(2);
+    int64_t total = 0;
+    RII_CUDA(cudaMemcpyAsync(&total, ioff + K, 8, cudaMemcpyDeviceToHost, st));
+    RII_CUDA(cudaStreamSynchronize(st));
+    if (total > cap) throw Error(4, "list-major item buffer too small");
+    list_item_fill_kernel<<<(unsigned)ceil_div(K, 256), 256, 0, st>>>(qoff, ioff, K, B, items);
+    RII_LAUNCHED();
+    RII_CUDA(cudaFreeAsync(tmp, st));
+    RII_CUDA(cudaFreeAsync(n, st));
+    RII_CUDA(cudaFreeAsync(ioff, st));
+    return total;
 }
 
 // ----------------------------------------------------------- list scan -----

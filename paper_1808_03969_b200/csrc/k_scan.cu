@@ -15,6 +15,8 @@
 // selects the query.  The lane-dependent summation order is undone by a
 // canonical (CA2, m ascending) rescore of the kept candidates, so the returned
 // distances equal the oracle's bit for bit.
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "lut.cuh"
 #include "topk.cuh"
@@ -62,30 +64,49 @@ __device__ __forceinline__ void adc_rotated(const uint8_t *lut, const uint32_t (
     }
 }
 
-template <int M, int B>
-__global__ void __launch_bounds__(NT, 1)
-    scan_fast_kernel(const uint8_t *__restrict__ codes, int64_t n_codes, const float *__restrict__ q, int64_t nq,
-                     const float *__restrict__ cb, int ds, int kk, int nb, int64_t chunk, int nc,
-                     uint64_t *__restrict__ out) {
+template <int M, int B, bool LISTS, int NTH, int U>
+__global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     constexpr int W = M / 4, NP = B / 2;
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t *lut = smem;
+    const int kk = a.kk;
     uint64_t *top = reinterpret_cast<uint64_t *>(smem + NP * LUT_PAIR_BYTES);
     uint64_t *fresh = top + B * kk;
     int *cnt = reinterpret_cast<int *>(fresh + B * NEWCAP);
     float *thr = reinterpret_cast<float *>(cnt + B);
     int *scratch = reinterpret_cast<int *>(thr + B);
+    const uint8_t *__restrict__ codes = a.codes;
 
-    const int item = blockIdx.x, ci = item / nb, qb = item - ci * nb;
-    const int64_t c0 = (int64_t)ci * chunk, c1 = min(n_codes, c0 + chunk);
-    const int D = M * ds, tid = threadIdx.x, lane = tid & 31;
+    // Work item: linear mode = (code chunk ci, query batch qb); list mode = (posting
+    // list, up to B of the queries that probe it) -- list-major Alg. 2 L7-L13.
+    int64_t c0, c1, qstart = 0;
+    int ci = 0, qb = 0, nqi = B;
+    if constexpr (LISTS) {
+        const int4 it = a.items[blockIdx.x];
+        c0 = a.offsets[it.x];
+        c1 = a.offsets[it.x + 1];
+        qstart = it.y;
+        nqi = it.z;
+    } else {
+        ci = blockIdx.x / a.nb;
+        qb = blockIdx.x - ci * a.nb;
+        c0 = (int64_t)ci * a.chunk;
+        c1 = min(a.n_codes, c0 + a.chunk);
+        const int64_t rem = a.nq - (int64_t)qb * B;
+        nqi = rem < B ? (int)rem : B;
+    }
+    auto query_of = [&](int qq) -> int64_t {  // global query index of slot qq
+        qq = qq < nqi ? qq : nqi - 1;
+        if constexpr (LISTS) return a.qlist[qstart + qq] / a.P;
+        else return (int64_t)qb * B + qq;
+    };
+    const int D = M * a.ds, tid = threadIdx.x, lane = tid & 31;
 
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-        const int64_t qa = min((int64_t)qb * B + 2 * p, nq - 1), qc = min((int64_t)qb * B + 2 * p + 1, nq - 1);
-        build_lut_pair<M>(reinterpret_cast<float *>(lut + p * LUT_PAIR_BYTES), q + qa * D, q + qc * D, cb, ds);
-    }
-    for (int e = tid; e < B * kk; e += NT) top[e] = KEY_MAX;
+    for (int p = 0; p < NP; ++p)
+        build_lut_pair<M>(reinterpret_cast<float *>(lut + p * LUT_PAIR_BYTES), a.q + query_of(2 * p) * D,
+                          a.q + query_of(2 * p + 1) * D, a.cb, a.ds);
+    for (int e = tid; e < B * kk; e += NTH) top[e] = KEY_MAX;
     if (tid < B) { cnt[tid] = 0; thr[tid] = __int_as_float(0x7f800000); scratch[2 + tid] = 0; }
     if (tid == 0) scratch[1] = 0;
     __syncthreads();
@@ -102,46 +123,54 @@ __global__ void __launch_bounds__(NT, 1)
     // WIN steps: a window whose pushes overflow the fresh buffer is rolled back
     // (its pushes dropped, the buffer compacted) and redone one step at a time,
     // which cannot overflow (an empty buffer holds a whole step, NEWCAP >= NT*U).
-    constexpr int U = 2, STEP = NT * U, WIN = 4, SOFT = NEWCAP / 4;
+    constexpr int STEP = NTH * U, WIN = 4, SOFT = NEWCAP / 4;
     static_assert(NEWCAP >= STEP, "a single step must fit the fresh buffer");
     int *s_ovf = scratch + 1, *s_cnt0 = scratch + 2;  // flags, fill snapshot at the window start
     uint32_t w[U][W];
-    auto load_step = [&](int64_t b, uint32_t(&dst)[U][W]) {
+    uint32_t cid[U];  // candidate id: position in `codes` (linear) or the list's id (lists)
+    auto load_step = [&](int64_t b, uint32_t(&dst)[U][W], uint32_t(&did)[U]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t p = b + u * NT + tid;
+            const int64_t p = b + u * NTH + tid;
 #pragma unroll
             for (int i = 0; i < W; ++i) dst[u][i] = 0;
-            if (p < c1) load_code<W>(codes + p * M, dst[u]);
+            did[u] = 0;
+            if (p < c1) {
+                if constexpr (LISTS) did[u] = __ldg(a.ids + p);
+                else did[u] = (uint32_t)p;
+                load_code<W>(codes + (size_t)did[u] * M, dst[u]);
+            }
         }
     };
     int64_t base = c0;
-    load_step(base, w);
+    load_step(base, w, cid);
     int safe = 0;
     while (base < c1) {
         const int64_t wstart = base;
         const int nsteps = safe > 0 ? 1 : WIN;
         bool ovf = false, need = false;
         for (int s = 0; s < nsteps && base < c1; ++s) {
-            uint32_t wn[U][W];
-            load_step(base + STEP, wn);
+            uint32_t wn[U][W], nid[U];
+            load_step(base + STEP, wn, nid);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int64_t pos = base + u * NT + tid;
+                const int64_t pos = base + u * NTH + tid;
                 float2 acc2[NP];
                 adc_rotated<M, B>(lut, w[u], rw, sel, l8, acc2);
 #pragma unroll
                 for (int p = 0; p < NP; ++p) {
-                    push_candidate_win(pos < c1 && acc2[p].x <= th[2 * p], make_key(acc2[p].x, (uint32_t)pos),
+                    push_candidate_win(pos < c1 && acc2[p].x <= th[2 * p], make_key(acc2[p].x, cid[u]),
                                        fresh + (2 * p) * NEWCAP, cnt + 2 * p, lane, SOFT, need, ovf);
-                    push_candidate_win(pos < c1 && acc2[p].y <= th[2 * p + 1], make_key(acc2[p].y, (uint32_t)pos),
+                    push_candidate_win(pos < c1 && acc2[p].y <= th[2 * p + 1], make_key(acc2[p].y, cid[u]),
                                        fresh + (2 * p + 1) * NEWCAP, cnt + 2 * p + 1, lane, SOFT, need, ovf);
                 }
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u)
+            for (int u = 0; u < U; ++u) {
+                cid[u] = nid[u];
 #pragma unroll
                 for (int i = 0; i < W; ++i) w[u][i] = wn[u][i];
+            }
             base += STEP;
         }
         if (ovf) *s_ovf = 1;
@@ -155,7 +184,7 @@ __global__ void __launch_bounds__(NT, 1)
             for (int qq = 0; qq < B; ++qq) th[qq] = thr[qq];
             if (rolled) {
                 base = wstart;
-                load_step(base, w);
+                load_step(base, w, cid);
                 safe = 4;
                 continue;
             }
@@ -168,7 +197,7 @@ __global__ void __launch_bounds__(NT, 1)
     compact_topk(top, fresh, cnt, thr, B, kk, scratch);
 
     // Canonical rescore (CA2: m ascending, replica 0) of the kept candidates.
-    for (int e = tid; e < B * kk; e += NT) {
+    for (int e = tid; e < B * kk; e += NTH) {
         const uint64_t k = top[e];
         if (k == KEY_MAX) continue;
         const int qq = e / kk;
@@ -182,10 +211,11 @@ __global__ void __launch_bounds__(NT, 1)
     }
     __syncthreads();
     bitonic_sort_rows(top, B, kk, kk);
-    for (int e = tid; e < B * kk; e += NT) {
+    for (int e = tid; e < B * kk; e += NTH) {
         const int qq = e / kk, i = e - qq * kk;
-        const int64_t qi = (int64_t)qb * B + qq;
-        if (qi < nq) out[(qi * nc + ci) * kk + i] = top[e];
+        if (qq >= nqi) continue;
+        if constexpr (LISTS) a.out[a.qlist[qstart + qq] * kk + i] = top[e];   // [q][probe rank][kk]
+        else a.out[(((int64_t)qb * B + qq) * a.nc + ci) * kk + i] = top[e];
     }
 }
 
@@ -291,14 +321,35 @@ ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms) {
     return p;
 }
 
+// Threads per CTA x codes per thread and step of the lane-rotated kernels
+// (RII_SCAN_CFG=0: 256 x 2, 1: 512 x 1; default below).
+static int scan_cfg() {
+    static int cfg = [] {
+        const char *e = getenv("RII_SCAN_CFG");
+        return e ? atoi(e) : 1;
+    }();
+    return cfg;
+}
+static int scan_threads() { return scan_cfg() == 0 ? 256 : 512; }
+
+template <int M, int B, bool LISTS>
+static void *fast_kernel_ptr() {
+    if (scan_cfg() == 0) return (void *)scan_fast_kernel<M, B, LISTS, 256, 2>;
+    return (void *)scan_fast_kernel<M, B, LISTS, 512, 1>;
+}
+
 template <int M, int B>
 static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
                           const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st) {
-    auto kern = scan_fast_kernel<M, B>;
+    void *kern = fast_kernel_ptr<M, B, false>();
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    ScanArgs a{};
+    a.codes = codes; a.n_codes = n; a.q = q; a.nq = nq; a.cb = cb; a.ds = ds; a.kk = kk;
+    a.nb = pl.nb; a.chunk = pl.chunk; a.nc = pl.nc; a.out = out;
+    void *args[] = {&a};
     KernelTimer t(TK_LINEAR, st);
-    kern<<<pl.nb * pl.nc, NT, pl.smem, st>>>(codes, n, q, nq, cb, ds, kk, pl.nb, pl.chunk, pl.nc, out);
-    RII_LAUNCHED();
+    RII_CUDA(cudaLaunchKernel(kern, dim3(pl.nb * pl.nc), dim3(scan_threads()), args, pl.smem, st));
+    count_launch();
 }
 
 template <int M>
@@ -317,6 +368,45 @@ static void launch_generic_t(const ScanPlan &pl, const uint8_t *codes, int64_t n
     KernelTimer t(TK_LINEAR, st);
     kern<<<pl.nb * pl.nc, NT, pl.smem, st>>>(codes, n, q, nq, cb, M, ds, kk, pl.nb, pl.chunk, pl.nc, out);
     RII_LAUNCHED();
+}
+
+bool list_major_supported(int M) { return M == 4 || M == 8 || M == 16 || M == 32; }
+
+int list_major_B(int kk) {
+    for (int B : {6, 4, 2})
+        if (smem_fast(B, kk) <= SMEM_CAP) return B;
+    return 0;
+}
+
+template <int M, int B>
+static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st) {
+    void *kern = fast_kernel_ptr<M, B, true>();
+    const size_t smem = smem_fast(B, a.kk);
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ScanArgs aa = a;
+    void *args[] = {&aa};
+    KernelTimer t(TK_IVF, st);
+    RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)n_items), dim3(scan_threads()), args, smem, st));
+    count_launch();
+}
+
+template <int M>
+static void launch_list_m(const ScanArgs &a, int64_t n_items, cudaStream_t st) {
+    const int B = list_major_B(a.kk);
+    if (B == 6) launch_list_t<M, 6>(a, n_items, st);
+    else if (B == 4) launch_list_t<M, 4>(a, n_items, st);
+    else launch_list_t<M, 2>(a, n_items, st);
+}
+
+void launch_list_scan(int M, const ScanArgs &a, int64_t n_items, cudaStream_t st) {
+    if (n_items <= 0) return;
+    if (list_major_B(a.kk) == 0) throw Error(1, "topk too large for the list-major scan");
+    switch (M) {
+        case 4: launch_list_m<4>(a, n_items, st); break;
+        case 8: launch_list_m<8>(a, n_items, st); break;
+        case 16: launch_list_m<16>(a, n_items, st); break;
+        default: launch_list_m<32>(a, n_items, st); break;
+    }
 }
 
 void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_codes, int M, const float *q, int64_t nq,

@@ -17,6 +17,35 @@ struct ScanPlan {
     size_t smem;
 };
 ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms);
+
+// Arguments of the lane-rotated scan kernel (linear mode, or list-major inverted
+// index mode where a work item is (posting list, up to B queries probing it)).
+struct ScanArgs {
+    const uint8_t *codes;
+    int64_t n_codes;
+    const float *q;
+    int64_t nq;
+    const float *cb;
+    int ds, kk;
+    int nb;            // linear: query batches
+    int64_t chunk;     // linear: codes per chunk
+    int nc;            // linear: chunks
+    uint64_t *out;     // linear: [nq][nc][kk]; lists: [nq][P][kk]
+    const int4 *items; // lists: {list, first entry in qlist, #queries, 0}
+    const uint32_t *qlist;  // lists: q * P + probe rank, grouped by list
+    int64_t P;
+    const int64_t *offsets;  // lists: CSR of the posting lists
+    const uint32_t *ids;
+};
+
+// List-major inverted-index scan: B queries per CTA share one posting list's codes.
+bool list_major_supported(int M);
+int list_major_B(int kk);
+void launch_list_scan(int M, const ScanArgs &a, int64_t n_items, cudaStream_t st);
+// Work items of the list-major scan: for every list k, ceil(#queries probing k / B)
+// items {k, first entry of qlist, count, 0}.  qoff = CSR of qlist by list.
+// Returns the number of items (synchronises the stream).
+int64_t build_list_items(const int64_t *qoff, int64_t K, int B, int4 *items, int64_t cap, cudaStream_t st);
 void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_codes, int M, const float *q, int64_t nq,
                         const float *cb, int D, int kk, uint64_t *out, cudaStream_t st);
 

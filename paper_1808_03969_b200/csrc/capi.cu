@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <mutex>
 #include <cstring>
 #include <new>
@@ -13,6 +14,7 @@
 #include "../../include/rii.h"
 #include "comm.hpp"
 #include "kernels.cuh"
+#include "lut.cuh"
 
 namespace rii {
 std::atomic<uint64_t> g_launches{0};
@@ -115,7 +117,7 @@ struct rii_index {
     int64_t theta = -1;
     // scratch (query side is const-callable: mutable)
     mutable Buf s_q, s_S, s_pos, s_sub, s_part, s_keys, s_gather, s_d0, s_probe, s_roff, s_rids, s_rkey, s_rval,
-        s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_items;
+        s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_items, s_gthr, s_tables, s_cpart, s_ckeys;
 };
 
 namespace {
@@ -277,29 +279,68 @@ int resolve_path(const rii_index *x, int64_t nS_global, bool has_S, int L, rii_p
     return ns < th ? RII_PATH_LINEAR : RII_PATH_IVF;  // Alg. 3 L1
 }
 
-// Local search; writes either the final result (world == 1, out_keys == nullptr)
-// or this rank's top-kk keys with global ids (out_keys, device [nq][kk]).
-void search_local(const rii_index *x, const QueryArgs &a, cudaStream_t st, int64_t *out_ids, float *out_dist,
-                  uint64_t *out_keys) {
+// Per-call preparation of the target set S on this rank (R7): the local slice of
+// S, its gathered codes (linear path) or the posting lists restricted to it (IVF).
+struct Targets {
+    const int64_t *S_loc = nullptr, *pos = nullptr;
+    int64_t n_loc = 0;
+    const uint8_t *sub_codes = nullptr;     // linear path
+    const int64_t *roff = nullptr;          // IVF path
+    const uint32_t *rids = nullptr;
+};
+
+Targets prepare_targets(const rii_index *x, const QueryArgs &a, cudaStream_t st) {
+    Targets t;
+    if (!a.S) return t;
+    t.n_loc = route_targets(x, a.S, a.nS, st, &t.S_loc, &t.pos);
+    if (a.path == RII_PATH_LINEAR) {
+        uint8_t *sub = x->s_sub.get<uint8_t>((size_t)std::max<int64_t>(t.n_loc, 1) * x->M + 64);
+        launch_gather_codes(x->codes.as<uint8_t>(), x->M, t.pos, t.n_loc, sub, st);
+        t.sub_codes = sub;
+    } else {
+        int32_t *rk = x->s_rkey.get<int32_t>(t.n_loc + 1);
+        uint32_t *rv = x->s_rval.get<uint32_t>(t.n_loc + 1);
+        if (t.n_loc > 0) {
+            gather_i32_kernel<<<(unsigned)ceil_div(t.n_loc, 256), 256, 0, st>>>(x->assign.as<int32_t>(), t.pos,
+                                                                               t.n_loc, rk, rv);
+            RII_LAUNCHED();
+        }
+        int64_t *roff = x->s_roff.get<int64_t>(x->K + 1);
+        uint32_t *rids = x->s_rids.get<uint32_t>(t.n_loc + 1);
+        build_csr(rk, rv, t.n_loc, x->K, roff, rids, st);
+        t.roff = roff;
+        t.rids = rids;
+    }
+    return t;
+}
+
+// One batch of queries (a.q, a.nq) against this rank's shard.  Writes either the
+// final result (world == 1, out_keys == nullptr) or this rank's top-kk keys with
+// global ids (out_keys, device [nq][kk]).
+void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cudaStream_t st, int64_t *out_ids,
+                  float *out_dist, uint64_t *out_keys) {
     const int kk = a.kk;
     const float *cb = x->cb.as<float>();
     const uint8_t *codes = x->codes.as<uint8_t>();
+    const bool fast = list_major_supported(x->M);
     IdMap map = local_map(x);
+    // per-query rotated ADC tables, built once per batch (a1)
+    const float *tables = nullptr;
+    if (fast) {
+        float *tb = x->s_tables.get<float>((size_t)a.nq * LUT_Q_FLOATS);
+        launch_lut_tables(a.q, a.nq, cb, x->D, x->M, tb, st);
+        tables = tb;
+    }
     const uint64_t *parts = nullptr;
     int64_t q_stride = kk, p_stride = kk;
     int nparts = 1;
-    if (a.path == RII_PATH_LINEAR) {
-        const uint8_t *scan_codes = codes;
-        int64_t n_codes = x->n_local;
+    if (a.path == RII_PATH_LINEAR) {  // Alg. 1
+        const uint8_t *scan_codes = a.S ? t.sub_codes : codes;
+        const int64_t n_codes = a.S ? t.n_loc : x->n_local;
         if (a.S) {
-            const int64_t *S_loc = nullptr, *pos = nullptr;
-            n_codes = route_targets(x, a.S, a.nS, st, &S_loc, &pos);
-            uint8_t *sub = x->s_sub.get<uint8_t>((size_t)std::max<int64_t>(n_codes, 1) * x->M + 64);
-            launch_gather_codes(codes, x->M, pos, n_codes, sub, st);
-            scan_codes = sub;
             map = IdMap();
             map.kind = 1;
-            map.table = S_loc;
+            map.table = t.S_loc;
         }
         if (n_codes == 0) {
             uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
@@ -308,42 +349,40 @@ void search_local(const rii_index *x, const QueryArgs &a, cudaStream_t st, int64
         } else {
             ScanPlan pl = plan_linear(x->M, kk, a.nq, n_codes, x->num_sms);
             uint64_t *pp = x->s_part.get<uint64_t>((size_t)pl.nb * pl.B * pl.nc * kk);
-            launch_linear_scan(pl, scan_codes, n_codes, x->M, a.q, a.nq, cb, x->D, kk, pp, st);
+            launch_linear_scan(pl, scan_codes, n_codes, x->M, a.q, a.nq, cb, x->D, kk, pp, st, tables);
             parts = pp;
             q_stride = (int64_t)pl.nc * kk;
             p_stride = kk;
             nparts = pl.nc;
         }
-    } else {
+    } else {  // Alg. 2
         const int64_t P = a.S ? std::min<int64_t>(x->K, ceil_div((int64_t)a.L * x->N, std::max<int64_t>(a.nS, 1)))
                               : std::min<int64_t>(a.L, x->K);  // P:492-502, R1
-        float *d0 = x->s_d0.get<float>((size_t)a.nq * x->K);
-        launch_coarse_dist(x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, d0, st);
         int32_t *probes = x->s_probe.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
-        launch_select_probes(d0, a.nq, x->K, P, probes, st);
-        const int64_t *off = x->offsets.as<int64_t>();
-        const uint32_t *ids = x->ids.as<uint32_t>();
-        if (a.S) {  // restrict the posting lists to S once per call (R7)
-            const int64_t *S_loc = nullptr, *pos = nullptr;
-            const int64_t n_loc = route_targets(x, a.S, a.nS, st, &S_loc, &pos);
-            int32_t *rk = x->s_rkey.get<int32_t>(n_loc + 1);
-            uint32_t *rv = x->s_rval.get<uint32_t>(n_loc + 1);
-            if (n_loc > 0) {
-                gather_i32_kernel<<<(unsigned)ceil_div(n_loc, 256), 256, 0, st>>>(x->assign.as<int32_t>(), pos, n_loc,
-                                                                                 rk, rv);
-                RII_LAUNCHED();
-            }
-            int64_t *roff = x->s_roff.get<int64_t>(x->K + 1);
-            uint32_t *rids = x->s_rids.get<uint32_t>(n_loc + 1);
-            build_csr(rk, rv, n_loc, x->K, roff, rids, st);
-            off = roff;
-            ids = rids;
+        const int kkc = partial_width((int)std::min<int64_t>(P, 1024));
+        if (P >= x->K) {
+            launch_select_probes(nullptr, a.nq, x->K, P, probes, st);  // every list
+        } else if (fast && P <= 1008) {
+            // coarse ranking (L2-L5) with the lane-rotated scan over the K centre codes,
+            // canonical rescore, top-P by (d0, k) (L6)
+            ScanPlan pc = plan_linear(x->M, kkc, a.nq, x->K, x->num_sms);
+            uint64_t *cp = x->s_cpart.get<uint64_t>((size_t)pc.nb * pc.B * pc.nc * kkc);
+            launch_linear_scan(pc, x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, kkc, cp, st, tables);
+            uint64_t *ck = x->s_ckeys.get<uint64_t>((size_t)a.nq * kkc);
+            launch_merge(cp, (int64_t)pc.nc * kkc, kkc, pc.nc, a.nq, kkc, (int)P, IdMap(), nullptr, nullptr, ck, st);
+            launch_keys_to_probes(ck, a.nq, kkc, P, probes, st);
+        } else {
+            float *d0 = x->s_d0.get<float>((size_t)a.nq * x->K);
+            launch_coarse_dist(x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, d0, st);
+            launch_select_probes(d0, a.nq, x->K, P, probes, st);
         }
+        const int64_t *off = a.S ? t.roff : x->offsets.as<int64_t>();
+        const uint32_t *ids = a.S ? t.rids : x->ids.as<uint32_t>();
         // List-major (B queries share one list's codes) when lists are long and the
-        // [nq][P][kk] partials stay small; otherwise query-major (one LUT per query).
-        const int64_t n_cand = a.S ? std::max<int64_t>(a.nS, 1) : x->n_local;
+        // [nq][P][kk] partials stay small; otherwise query-major (one table per query).
+        const int64_t n_cand = a.S ? std::max<int64_t>(t.n_loc, 1) : x->n_local;
         const double avg_len = (double)n_cand / (double)x->K;
-        const int Bl = list_major_supported(x->M) ? list_major_B(kk) : 0;
+        const int Bl = fast ? list_major_B(kk) : 0;
         const bool list_major = Bl > 0 && avg_len >= 768.0 && (double)a.nq * P * kk * 8 <= 4e9 &&
                                 (double)a.nq * P < 4e9;
         if (list_major) {
@@ -356,11 +395,14 @@ void search_local(const rii_index *x, const QueryArgs &a, cudaStream_t st, int64
             build_csr(probes, vals, npairs, x->K, qoff, qlist, st);  // (query, rank) pairs grouped by list
             const int64_t cap = npairs / Bl + x->K + 1;
             int4 *items = x->s_items.get<int4>(cap);
-            const int64_t n_items = build_list_items(qoff, x->K, Bl, items, cap, st);
+            const int64_t n_items = build_list_items(qoff, x->K, Bl, qlist, P, items, cap, st);
             uint64_t *pp = x->s_part.get<uint64_t>((size_t)npairs * kk);
+            float *gthr = x->s_gthr.get<float>(a.nq);
+            launch_fill_f32(gthr, a.nq, INFINITY, st);
             ScanArgs sa{};
             sa.codes = codes; sa.q = a.q; sa.nq = a.nq; sa.cb = cb; sa.ds = x->ds; sa.kk = kk; sa.out = pp;
-            sa.items = items; sa.qlist = qlist; sa.P = P; sa.offsets = off; sa.ids = ids;
+            sa.items = items; sa.qlist = qlist; sa.P = P; sa.offsets = off; sa.ids = ids; sa.gthr = gthr;
+            sa.tables = tables;
             launch_list_scan(x->M, sa, n_items, st);
             parts = pp;
             q_stride = P * kk;
@@ -368,11 +410,27 @@ void search_local(const rii_index *x, const QueryArgs &a, cudaStream_t st, int64
             nparts = (int)P;
         } else {
             uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
-            launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st);
+            launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st, tables);
             parts = pp;
         }
     }
     launch_merge(parts, q_stride, p_stride, nparts, a.nq, kk, a.topk, map, out_ids, out_dist, out_keys, st);
+}
+
+// Query batches of at most QBATCH queries bound the per-call scratch (tables:
+// 32 KB per query; partials).
+constexpr int64_t QBATCH = 16384;
+
+void search_local(const rii_index *x, const QueryArgs &a, cudaStream_t st, int64_t *out_ids, float *out_dist,
+                  uint64_t *out_keys) {
+    const Targets t = prepare_targets(x, a, st);
+    for (int64_t q0 = 0; q0 < a.nq; q0 += QBATCH) {
+        QueryArgs b = a;
+        b.q = a.q + q0 * x->D;
+        b.nq = std::min<int64_t>(QBATCH, a.nq - q0);
+        search_batch(x, b, t, st, out_ids ? out_ids + q0 * a.topk : nullptr, out_dist ? out_dist + q0 * a.topk : nullptr,
+                     out_keys ? out_keys + q0 * a.kk : nullptr);
+    }
 }
 
 void check_targets(const rii_index *x, const int64_t *S, int64_t nS, cudaStream_t st) {

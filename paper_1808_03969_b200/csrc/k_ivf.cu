@@ -130,6 +130,20 @@ __global__ void __launch_bounds__(NT) select_probes_kernel(const float *__restri
     }
 }
 
+__global__ void keys_to_probes_kernel(const uint64_t *__restrict__ keys, int64_t nq, int kk, int64_t P,
+                                      int32_t *__restrict__ probes) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nq * P) return;
+    const int64_t q = e / P, r = e - q * P;
+    probes[e] = (int32_t)key_id(keys[q * kk + r]);
+}
+
+void launch_keys_to_probes(const uint64_t *keys, int64_t nq, int kk, int64_t P, int32_t *probes, cudaStream_t st) {
+    if (nq * P <= 0) return;
+    keys_to_probes_kernel<<<(unsigned)ceil_div(nq * P, 256), 256, 0, st>>>(keys, nq, kk, P, probes);
+    RII_LAUNCHED();
+}
+
 void launch_select_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int32_t *probes, cudaStream_t st) {
     if (nq <= 0) return;
     select_probes_kernel<<<(unsigned)nq, NT, 0, st>>>(d0, K, P, probes);
@@ -154,7 +168,39 @@ __global__ void list_item_fill_kernel(const int64_t *__restrict__ qoff, const in
     }
 }
 
-int64_t build_list_items(const int64_t *qoff, int64_t K, int B, int4 *items, int64_t cap, cudaStream_t st) {
+__global__ void item_rank_kernel(const int4 *__restrict__ items, int64_t n, const uint32_t *__restrict__ qlist,
+                                 int64_t P, uint32_t *__restrict__ key, uint32_t *__restrict__ idx) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int4 it = items[i];
+    uint32_t r = 0xffffffffu;
+    for (int j = 0; j < it.z; ++j) {
+        const uint32_t rj = (uint32_t)(qlist[it.y + j] % P);
+        r = rj < r ? rj : r;
+    }
+    key[i] = r;
+    idx[i] = (uint32_t)i;
+}
+
+__global__ void permute_items_kernel(const int4 *__restrict__ in, const uint32_t *__restrict__ idx, int64_t n,
+                                     int4 *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[idx[i]];
+}
+
+__global__ void fill_f32_kernel(float *p, int64_t n, float v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+void launch_fill_f32(float *p, int64_t n, float v, cudaStream_t st) {
+    if (n <= 0) return;
+    fill_f32_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(p, n, v);
+    RII_LAUNCHED();
+}
+
+int64_t build_list_items(const int64_t *qoff, int64_t K, int B, const uint32_t *qlist, int64_t P, int4 *items,
+                         int64_t cap, cudaStream_t st) {
     int64_t *n = nullptr, *ioff = nullptr;
     RII_CUDA(cudaMallocAsync(&n, (size_t)(K + 1) * 8, st));
     RII_CUDA(cudaMallocAsync(&ioff, (size_t)(K + 1) * 8, st));
@@ -170,8 +216,32 @@ int64_t build_list_items(const int64_t *qoff, int64_t K, int B, int4 *items, int
     RII_CUDA(cudaMemcpyAsync(&total, ioff + K, 8, cudaMemcpyDeviceToHost, st));
     RII_CUDA(cudaStreamSynchronize(st));
     if (total > cap) throw Error(4, "list-major item buffer too small");
-    list_item_fill_kernel<<<(unsigned)ceil_div(K, 256), 256, 0, st>>>(qoff, ioff, K, B, items);
+    int4 *raw = nullptr;
+    RII_CUDA(cudaMallocAsync(&raw, (size_t)std::max<int64_t>(total, 1) * sizeof(int4), st));
+    list_item_fill_kernel<<<(unsigned)ceil_div(K, 256), 256, 0, st>>>(qoff, ioff, K, B, raw);
     RII_LAUNCHED();
+    if (total > 0) {
+        uint32_t *key = nullptr, *key2 = nullptr, *idx = nullptr, *idx2 = nullptr;
+        RII_CUDA(cudaMallocAsync(&key, (size_t)total * 4, st));
+        RII_CUDA(cudaMallocAsync(&key2, (size_t)total * 4, st));
+        RII_CUDA(cudaMallocAsync(&idx, (size_t)total * 4, st));
+        RII_CUDA(cudaMallocAsync(&idx2, (size_t)total * 4, st));
+        item_rank_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, st>>>(raw, total, qlist, P, key, idx);
+        RII_LAUNCHED();
+        int bits = 1;
+        while ((1ll << bits) <= P) ++bits;
+        size_t tb2 = 0;
+        RII_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, key, key2, idx, idx2, total, 0, bits, st));
+        void *tmp2 = nullptr;
+        RII_CUDA(cudaMallocAsync(&tmp2, tb2, st));
+        RII_CUDA(cub::DeviceRadixSort::SortPairs(tmp2, tb2, key, key2, idx, idx2, total, 0, bits, st));
+        count_launch(4);
+        permute_items_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, st>>>(raw, idx2, total, items);
+        RII_LAUNCHED();
+        for (void *pp : {(void *)tmp2, (void *)key, (void *)key2, (void *)idx, (void *)idx2})
+            RII_CUDA(cudaFreeAsync(pp, st));
+    }
+    RII_CUDA(cudaFreeAsync(raw, st));
     RII_CUDA(cudaFreeAsync(tmp, st));
     RII_CUDA(cudaFreeAsync(n, st));
     RII_CUDA(cudaFreeAsync(ioff, st));
@@ -228,7 +298,8 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
                                                       int64_t nq, const float *__restrict__ cb, int Mrt, int ds,
                                                       int kk, const int32_t *__restrict__ probes, int64_t P,
                                                       const int64_t *__restrict__ offsets,
-                                                      const uint32_t *__restrict__ ids, uint64_t *__restrict__ out) {
+                                                      const uint32_t *__restrict__ ids, uint64_t *__restrict__ out,
+                                                      const float *__restrict__ tables) {
     constexpr int W = FAST ? M / 4 : 1;
     const int MM = FAST ? M : Mrt;
     extern __shared__ __align__(16) uint8_t smem[];
@@ -245,7 +316,11 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
     const int D = MM * ds, tid = threadIdx.x, lane = tid & 31;
     const float *qa = q + min(q0, nq - 1) * D, *qb = q + min(q0 + 1, nq - 1) * D;
     if constexpr (FAST) {
-        build_lut_pair<M>(reinterpret_cast<float *>(lut), qa, qb, cb, ds);
+        if (tables)
+            load_lut_pair(reinterpret_cast<float *>(lut), tables + min(q0, nq - 1) * LUT_Q_FLOATS,
+                          tables + min(q0 + 1, nq - 1) * LUT_Q_FLOATS);
+        else
+            build_lut_pair<M>(reinterpret_cast<float *>(lut), qa, qb, cb, ds);
     } else {
         float *lp = reinterpret_cast<float *>(lut);
         for (int e = tid; e < 2 * MM * KS; e += NT) {
@@ -335,27 +410,28 @@ size_t ivf_smem(int M, int kk) {
 template <int M, bool FAST>
 static void ivf_launch_t(const uint8_t *codes, int Mrt, const float *q, int64_t nq, const float *cb, int ds, int kk,
                          const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
-                         cudaStream_t st) {
+                         cudaStream_t st, const float *tables) {
     const size_t smem = ivf_smem(Mrt, kk);
     auto kern = ivf_scan_kernel<M, FAST>;
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     KernelTimer t(TK_IVF, st);
-    kern<<<(unsigned)ceil_div(nq, 2), NT, smem, st>>>(codes, q, nq, cb, Mrt, ds, kk, probes, P, offsets, ids, out);
+    kern<<<(unsigned)ceil_div(nq, 2), NT, smem, st>>>(codes, q, nq, cb, Mrt, ds, kk, probes, P, offsets, ids, out,
+                                                      FAST ? tables : nullptr);
     RII_LAUNCHED();
 }
 
 void launch_ivf_scan(const uint8_t *codes, int M, const float *q, int64_t nq, const float *cb, int D, int kk,
                      const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
-                     cudaStream_t st) {
+                     cudaStream_t st, const float *tables) {
     if (nq <= 0) return;
     if (ivf_smem(M, kk) > 227 * 1024) throw Error(1, "topk too large for the inverted-index kernel");
     const int ds = D / M;
     switch (M) {
-        case 4: ivf_launch_t<4, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st); break;
-        case 8: ivf_launch_t<8, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st); break;
-        case 16: ivf_launch_t<16, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st); break;
-        case 32: ivf_launch_t<32, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st); break;
-        default: ivf_launch_t<1, false>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st); break;
+        case 4: ivf_launch_t<4, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables); break;
+        case 8: ivf_launch_t<8, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables); break;
+        case 16: ivf_launch_t<16, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables); break;
+        case 32: ivf_launch_t<32, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables); break;
+        default: ivf_launch_t<1, false>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables); break;
     }
 }
 

@@ -103,9 +103,13 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     const int D = M * a.ds, tid = threadIdx.x, lane = tid & 31;
 
 #pragma unroll
-    for (int p = 0; p < NP; ++p)
-        build_lut_pair<M>(reinterpret_cast<float *>(lut + p * LUT_PAIR_BYTES), a.q + query_of(2 * p) * D,
-                          a.q + query_of(2 * p + 1) * D, a.cb, a.ds);
+    for (int p = 0; p < NP; ++p) {
+        float *lp = reinterpret_cast<float *>(lut + p * LUT_PAIR_BYTES);
+        if (a.tables)
+            load_lut_pair(lp, a.tables + query_of(2 * p) * LUT_Q_FLOATS, a.tables + query_of(2 * p + 1) * LUT_Q_FLOATS);
+        else
+            build_lut_pair<M>(lp, a.q + query_of(2 * p) * D, a.q + query_of(2 * p + 1) * D, a.cb, a.ds);
+    }
     for (int e = tid; e < B * kk; e += NTH) top[e] = KEY_MAX;
     if (tid < B) { cnt[tid] = 0; thr[tid] = __int_as_float(0x7f800000); scratch[2 + tid] = 0; }
     if (tid == 0) scratch[1] = 0;
@@ -114,9 +118,17 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
     uint32_t sel[4];
     make_selectors(r, sel);
+    // List mode: the query's global bound (the best kk-th distance any finished item
+    // of this query saw, inflated by 1e-5 for the lane-rotated rounding) also filters.
+    float gq[B];
+#pragma unroll
+    for (int qq = 0; qq < B; ++qq) {
+        gq[qq] = __int_as_float(0x7f800000);
+        if constexpr (LISTS) gq[qq] = __ldcg(a.gthr + query_of(qq));
+    }
     float th[B];
 #pragma unroll
-    for (int qq = 0; qq < B; ++qq) th[qq] = thr[qq];
+    for (int qq = 0; qq < B; ++qq) th[qq] = fminf(thr[qq], gq[qq]);
 
     // Each thread evaluates U codes per step (positions base + u*NT + tid, coalesced),
     // the next step's codes prefetched into registers.  Block barriers only every
@@ -181,7 +193,10 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
             if (tid == 0) *s_ovf = 0;
             if (tid < B) s_cnt0[tid] = 0;
 #pragma unroll
-            for (int qq = 0; qq < B; ++qq) th[qq] = thr[qq];
+            for (int qq = 0; qq < B; ++qq) {
+                if constexpr (LISTS) gq[qq] = fminf(gq[qq], __ldcg(a.gthr + query_of(qq)));
+                th[qq] = fminf(thr[qq], gq[qq]);
+            }
             if (rolled) {
                 base = wstart;
                 load_step(base, w, cid);
@@ -190,11 +205,24 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
             }
         } else {
             if (tid < B) s_cnt0[tid] = cnt[tid];
+            if constexpr (LISTS) {
+#pragma unroll
+                for (int qq = 0; qq < B; ++qq) {
+                    gq[qq] = fminf(gq[qq], __ldcg(a.gthr + query_of(qq)));
+                    th[qq] = fminf(th[qq], gq[qq]);
+                }
+            }
             __syncthreads();  // snapshot taken before the next window pushes
         }
         if (safe > 0) --safe;
     }
     compact_topk(top, fresh, cnt, thr, B, kk, scratch);
+    if constexpr (LISTS) {  // publish this item's kk-th distance as a bound for the query
+        if (tid < nqi && thr[tid] < __int_as_float(0x7f800000)) {
+            const float bound = __fmul_ru(thr[tid], 1.00001f);
+            atomicMin(reinterpret_cast<int *>(a.gthr + query_of(tid)), __float_as_int(bound));
+        }
+    }
 
     // Canonical rescore (CA2: m ascending, replica 0) of the kept candidates.
     for (int e = tid; e < B * kk; e += NTH) {
@@ -340,12 +368,12 @@ static void *fast_kernel_ptr() {
 
 template <int M, int B>
 static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
-                          const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st) {
+                          const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st, const float *tables) {
     void *kern = fast_kernel_ptr<M, B, false>();
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     ScanArgs a{};
     a.codes = codes; a.n_codes = n; a.q = q; a.nq = nq; a.cb = cb; a.ds = ds; a.kk = kk;
-    a.nb = pl.nb; a.chunk = pl.chunk; a.nc = pl.nc; a.out = out;
+    a.nb = pl.nb; a.chunk = pl.chunk; a.nc = pl.nc; a.out = out; a.tables = tables;
     void *args[] = {&a};
     KernelTimer t(TK_LINEAR, st);
     RII_CUDA(cudaLaunchKernel(kern, dim3(pl.nb * pl.nc), dim3(scan_threads()), args, pl.smem, st));
@@ -354,10 +382,10 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
 
 template <int M>
 static void launch_fast_m(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
-                          const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st) {
-    if (pl.B == 6) launch_fast_t<M, 6>(pl, codes, n, q, nq, cb, ds, kk, out, st);
-    else if (pl.B == 4) launch_fast_t<M, 4>(pl, codes, n, q, nq, cb, ds, kk, out, st);
-    else launch_fast_t<M, 2>(pl, codes, n, q, nq, cb, ds, kk, out, st);
+                          const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st, const float *tables) {
+    if (pl.B == 6) launch_fast_t<M, 6>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables);
+    else if (pl.B == 4) launch_fast_t<M, 4>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables);
+    else launch_fast_t<M, 2>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables);
 }
 
 template <int B>
@@ -410,14 +438,14 @@ void launch_list_scan(int M, const ScanArgs &a, int64_t n_items, cudaStream_t st
 }
 
 void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_codes, int M, const float *q, int64_t nq,
-                        const float *cb, int D, int kk, uint64_t *out, cudaStream_t st) {
+                        const float *cb, int D, int kk, uint64_t *out, cudaStream_t st, const float *tables) {
     const int ds = D / M;
     if (pl.fast) {
         switch (M) {
-            case 4: launch_fast_m<4>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st); break;
-            case 8: launch_fast_m<8>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st); break;
-            case 16: launch_fast_m<16>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st); break;
-            default: launch_fast_m<32>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st); break;
+            case 4: launch_fast_m<4>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables); break;
+            case 8: launch_fast_m<8>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables); break;
+            case 16: launch_fast_m<16>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables); break;
+            default: launch_fast_m<32>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables); break;
         }
     } else if (pl.B == 4) {
         launch_generic_t<4>(pl, codes, n_codes, M, q, nq, cb, ds, kk, out, st);
@@ -426,6 +454,31 @@ void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_code
     } else {
         launch_generic_t<1>(pl, codes, n_codes, M, q, nq, cb, ds, kk, out, st);
     }
+}
+
+// ------------------------------------------------------------ LUT tables ---
+// One CTA per query: warp w fills rows z = w, w + 8, ...; lane c = column c,
+// A(c mod M, z) by CA1 (the code book stays in L1: this kernel has no smem).
+__global__ void __launch_bounds__(256) lut_tables_kernel(const float *__restrict__ q, int64_t nq,
+                                                         const float *__restrict__ cb, int M, int ds,
+                                                         float *__restrict__ tables) {
+    const int64_t qi = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int m = lane % M;
+    const float *qv = q + qi * (int64_t)M * ds + m * ds;
+    float *t = tables + qi * LUT_Q_FLOATS;
+    for (int z = warp; z < KS; z += 8) {
+        const float *cv = cb + ((size_t)m * KS + z) * ds;
+        float a = 0.f;
+        for (int j = 0; j < ds; ++j) a = ca1_step(a, qv[j], cv[j]);
+        t[z * 32 + lane] = a;
+    }
+}
+
+void launch_lut_tables(const float *q, int64_t nq, const float *cb, int D, int M, float *tables, cudaStream_t st) {
+    if (nq <= 0) return;
+    lut_tables_kernel<<<(unsigned)nq, 256, 0, st>>>(q, nq, cb, M, D / M, tables);
+    RII_LAUNCHED();
 }
 
 // ---------------------------------------------------------------- gather ---

@@ -21,6 +21,7 @@ ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms);
 // Arguments of the lane-rotated scan kernel (linear mode, or list-major inverted
 // index mode where a work item is (posting list, up to B queries probing it)).
 struct ScanArgs {
+    const float *tables;  // [nq][256][32] per-query tables (lut.cuh); when set, copied instead of built
     const uint8_t *codes;
     int64_t n_codes;
     const float *q;
@@ -36,6 +37,7 @@ struct ScanArgs {
     int64_t P;
     const int64_t *offsets;  // lists: CSR of the posting lists
     const uint32_t *ids;
+    float *gthr;             // lists: per-query upper bound on the global kk-th distance
 };
 
 // List-major inverted-index scan: B queries per CTA share one posting list's codes.
@@ -45,9 +47,17 @@ void launch_list_scan(int M, const ScanArgs &a, int64_t n_items, cudaStream_t st
 // Work items of the list-major scan: for every list k, ceil(#queries probing k / B)
 // items {k, first entry of qlist, count, 0}.  qoff = CSR of qlist by list.
 // Returns the number of items (synchronises the stream).
-int64_t build_list_items(const int64_t *qoff, int64_t K, int B, int4 *items, int64_t cap, cudaStream_t st);
+// Items are ordered by the smallest probe rank of their queries, so every query's
+// nearest lists run first and tighten its global threshold early.
+int64_t build_list_items(const int64_t *qoff, int64_t K, int B, const uint32_t *qlist, int64_t P, int4 *items,
+                         int64_t cap, cudaStream_t st);
+void launch_fill_f32(float *p, int64_t n, float v, cudaStream_t st);
 void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_codes, int M, const float *q, int64_t nq,
-                        const float *cb, int D, int kk, uint64_t *out, cudaStream_t st);
+                        const float *cb, int D, int kk, uint64_t *out, cudaStream_t st,
+                        const float *tables = nullptr);
+
+// Per-query rotated tables [nq][256][32] (M in {4,8,16,32}), CA1 values.
+void launch_lut_tables(const float *q, int64_t nq, const float *cb, int D, int M, float *tables, cudaStream_t st);
 
 // out[i] = codes[pos[i]] for i < n (subset gather, Alg. 1 "pick up target PQ-codes").
 void launch_gather_codes(const uint8_t *codes, int M, const int64_t *pos, int64_t n, uint8_t *out, cudaStream_t st);
@@ -68,11 +78,13 @@ void launch_coarse_dist(const uint8_t *centers, int64_t K, int M, const float *q
                         float *d0, cudaStream_t st);
 // probes[q][0..P) = the P centres with the smallest (d0, k) (Alg. 2 L6), ascending k.
 void launch_select_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int32_t *probes, cudaStream_t st);
+// probes[q][r] = id of the r-th key of the sorted per-query keys [nq][kk] (r < P).
+void launch_keys_to_probes(const uint64_t *keys, int64_t nq, int kk, int64_t P, int32_t *probes, cudaStream_t st);
 // Posting-list traversal (Alg. 2 L7-L16, mode A): out[nq][kk] keys, ids = local positions.
 size_t ivf_smem(int M, int kk);
 void launch_ivf_scan(const uint8_t *codes, int M, const float *q, int64_t nq, const float *cb, int D, int kk,
                      const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
-                     cudaStream_t st);
+                     cudaStream_t st, const float *tables = nullptr);
 
 // ---- build side (k_build.cu) -------------------------------------------------
 void launch_encode(const float *x, int64_t n, int D, int M, const float *cb, uint8_t *codes, cudaStream_t st);

@@ -29,6 +29,23 @@ __device__ __forceinline__ void build_lut_pair(float *lutp, const float *q0, con
     }
 }
 
+// Per-query table in HBM (built once per call by lut_tables_kernel): row z holds
+// 32 fp32 columns, column c = A(c mod M, z).  32 KB per query for every M <= 32.
+constexpr int LUT_Q_FLOATS = KS * 32;
+
+// Copy the HBM tables of queries qa, qb into the interleaved pair layout:
+// coalesced 16-byte loads, 16-byte conflict-free stores.
+__device__ __forceinline__ void load_lut_pair(float *lutp, const float *__restrict__ ta,
+                                              const float *__restrict__ tb) {
+    const float4 *a4 = reinterpret_cast<const float4 *>(ta), *b4 = reinterpret_cast<const float4 *>(tb);
+    float4 *d4 = reinterpret_cast<float4 *>(lutp);
+    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 4; e += blockDim.x) {
+        const float4 a = __ldg(a4 + e), b = __ldg(b4 + e);
+        d4[2 * e] = make_float4(a.x, b.x, a.y, b.y);
+        d4[2 * e + 1] = make_float4(a.z, b.z, a.w, b.w);
+    }
+}
+
 // Canonical (replica 0) entry A_h(m, z) of the pair table.
 __device__ __forceinline__ float lut_pair_entry(const float *lutp, int h, int m, int z) {
     return lutp[z * 64 + 2 * m + h];

@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 #include <cstring>
@@ -279,6 +282,21 @@ int resolve_path(const rii_index *x, int64_t nS_global, bool has_S, int L, rii_p
     return ns < th ? RII_PATH_LINEAR : RII_PATH_IVF;  // Alg. 3 L1
 }
 
+// RII_TRACE=1: synchronise and print the host-side duration of each query phase.
+struct PhaseTrace {
+    bool on;
+    cudaStream_t st;
+    std::chrono::steady_clock::time_point t;
+    explicit PhaseTrace(cudaStream_t s) : on(getenv("RII_TRACE") != nullptr), st(s), t(std::chrono::steady_clock::now()) {}
+    void mark(const char *what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "[rii] %-24s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+
 // Per-call preparation of the target set S on this rank (R7): the local slice of
 // S, its gathered codes (linear path) or the posting lists restricted to it (IVF).
 struct Targets {
@@ -324,6 +342,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
     const uint8_t *codes = x->codes.as<uint8_t>();
     const bool fast = list_major_supported(x->M);
     IdMap map = local_map(x);
+    PhaseTrace tr(st);
     // per-query rotated ADC tables, built once per batch (a1)
     const float *tables = nullptr;
     if (fast) {
@@ -331,6 +350,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
         launch_lut_tables(a.q, a.nq, cb, x->D, x->M, tb, st);
         tables = tb;
     }
+    tr.mark("tables");
     const uint64_t *parts = nullptr;
     int64_t q_stride = kk, p_stride = kk;
     int nparts = 1;
@@ -376,6 +396,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             launch_coarse_dist(x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, d0, st);
             launch_select_probes(d0, a.nq, x->K, P, probes, st);
         }
+        tr.mark("coarse+probes");
         const int64_t *off = a.S ? t.roff : x->offsets.as<int64_t>();
         const uint32_t *ids = a.S ? t.rids : x->ids.as<uint32_t>();
         // List-major (B queries share one list's codes) when lists are long and the
@@ -395,15 +416,19 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             build_csr(probes, vals, npairs, x->K, qoff, qlist, st);  // (query, rank) pairs grouped by list
             const int64_t cap = npairs / Bl + x->K + 1;
             int4 *items = x->s_items.get<int4>(cap);
+            tr.mark("pairs csr");
             const int64_t n_items = build_list_items(qoff, x->K, Bl, qlist, P, items, cap, st);
+            tr.mark("items");
             uint64_t *pp = x->s_part.get<uint64_t>((size_t)npairs * kk);
             float *gthr = x->s_gthr.get<float>(a.nq);
             launch_fill_f32(gthr, a.nq, INFINITY, st);
+            tr.mark("alloc partials");
             ScanArgs sa{};
             sa.codes = codes; sa.q = a.q; sa.nq = a.nq; sa.cb = cb; sa.ds = x->ds; sa.kk = kk; sa.out = pp;
             sa.items = items; sa.qlist = qlist; sa.P = P; sa.offsets = off; sa.ids = ids; sa.gthr = gthr;
             sa.tables = tables;
             launch_list_scan(x->M, sa, n_items, st);
+            tr.mark("list scan");
             parts = pp;
             q_stride = P * kk;
             p_stride = kk;
@@ -414,7 +439,9 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             parts = pp;
         }
     }
+    tr.mark("scan");
     launch_merge(parts, q_stride, p_stride, nparts, a.nq, kk, a.topk, map, out_ids, out_dist, out_keys, st);
+    tr.mark("merge");
 }
 
 // Query batches of at most QBATCH queries bound the per-call scratch (tables:
@@ -520,6 +547,12 @@ rii_status rii_create(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t 
         x->rank = rank;
         x->world = world;
         RII_CUDA(cudaDeviceGetAttribute(&x->num_sms, cudaDevAttrMultiProcessorCount, device));
+        // keep memory freed by cudaFreeAsync cached in the pool (no re-mapping per call)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
         try {
             x->cb.get<float>((size_t)M * KS * x->ds);
             if (world > 1 && nccl_id) x->comm = nccl_init(nccl_id, rank, world);

@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "kernels.cuh"
+#include "lut.cuh"
 
 namespace rii {
 
@@ -113,8 +114,8 @@ __global__ void __launch_bounds__(256) assign_kernel(const uint8_t *__restrict__
     }
 }
 
-void launch_assign(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, int M, const float *T,
-                   int32_t *assign, float *dist, cudaStream_t st) {
+static void launch_assign_canonical(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, int M,
+                                    const float *T, int32_t *assign, float *dist, cudaStream_t st) {
     if (n <= 0) return;
     int Bc = (int)((190 * 1024 - 256 * AR * M) / ((size_t)M * KS * 4));
     if (Bc < 1) Bc = 1;
@@ -124,6 +125,177 @@ void launch_assign(const uint8_t *codes, int64_t n, const uint8_t *centers, int6
     RII_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     assign_kernel<<<(unsigned)ceil_div(n, 256 * AR), 256, smem, st>>>(codes, n, centers, K, M, T, Bc, assign, dist);
     RII_LAUNCHED();
+}
+
+// ------------------------------------------------------------ fast assign --
+// The "table" of centre k is the row set T_m[cbar_k^m][.] (d_S(x, c) = sum_m
+// T_m[c^m][x^m]), laid out like a query table (lut.cuh): row z, column c =
+// T_{c mod M}[cbar_k^{c mod M}][z].
+__global__ void __launch_bounds__(256) centre_tables_kernel(const float *__restrict__ T,
+                                                            const uint8_t *__restrict__ centers, int M,
+                                                            float *__restrict__ tables) {
+    const int64_t k = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int m = lane % M;
+    const float *row = T + ((size_t)m * KS + centers[k * M + m]) * KS;
+    float *t = tables + k * LUT_Q_FLOATS;
+    for (int z = warp; z < KS; z += 8) t[z * 32 + lane] = __ldg(row + z);
+}
+
+// a(n) with the lane-rotated tables: 6 centres per pass (3 pairs), AR2 codes per
+// thread kept pre-permuted in registers.  The rotated fp32 order can differ from
+// CA2 by < 4e-6 relative (31 roundings of non-negative terms each way), so a code
+// whose runner-up is within 1e-5 of its best is re-assigned canonically (exact);
+// every other code's argmin is the canonical one.
+template <int M>
+__host__ __device__ constexpr int ar2() { return M >= 32 ? 4 : 8; }
+template <int M>
+__global__ void __launch_bounds__(256, 1)
+    assign_fast_kernel(const uint8_t *__restrict__ codes, int64_t n, const float *__restrict__ tables, int64_t K,
+                       const float *__restrict__ T, const uint8_t *__restrict__ centers, int32_t *__restrict__ assign,
+                       float *__restrict__ dist, int64_t *__restrict__ fb, unsigned long long *__restrict__ fb_n) {
+    constexpr int W = M / 4, B = 6, NP = 3, AR2 = ar2<M>();
+    extern __shared__ __align__(16) uint8_t lut[];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t i0 = (int64_t)blockIdx.x * 256 * AR2;
+    const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
+    uint32_t sel[4];
+    make_selectors(r, sel);
+    uint32_t wp[AR2][W];
+    float best[AR2];
+    int bk[AR2];
+    bool amb[AR2];
+#pragma unroll
+    for (int u = 0; u < AR2; ++u) {
+        const int64_t i = i0 + u * 256 + tid;
+#pragma unroll
+        for (int j = 0; j < W; ++j) wp[u][j] = 0;
+        if (i < n) {
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(codes + i * M);
+#pragma unroll
+            for (int j = 0; j < W; ++j) wp[u][j] = __ldg(src + j);
+        }
+        permute_words<W>(wp[u], rw);
+        best[u] = __int_as_float(0x7f800000);
+        bk[u] = 0;
+        amb[u] = false;
+    }
+    const float TOLF = 1.00001f;
+    for (int64_t k0 = 0; k0 < K; k0 += B) {
+        __syncthreads();
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const int64_t ka = min(k0 + 2 * p, K - 1), kb = min(k0 + 2 * p + 1, K - 1);
+            load_lut_pair(reinterpret_cast<float *>(lut + p * LUT_PAIR_BYTES), tables + ka * LUT_Q_FLOATS,
+                          tables + kb * LUT_Q_FLOATS);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < AR2; ++u) {
+            float2 acc[NP];
+            adc_rotated_pre<M, B>(lut, wp[u], sel, l8, acc);
+#pragma unroll
+            for (int jj = 0; jj < B; ++jj) {
+                const float d = (jj & 1) ? acc[jj >> 1].y : acc[jj >> 1].x;
+                const int64_t k = k0 + jj;
+                if (k < K) {
+                    if (d < best[u]) {
+                        amb[u] = best[u] <= d * TOLF;
+                        best[u] = d;
+                        bk[u] = (int)k;
+                    } else if (d <= best[u] * TOLF) {
+                        amb[u] = true;
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < AR2; ++u) {
+        const int64_t i = i0 + u * 256 + tid;
+        if (i >= n) continue;
+        if (amb[u]) {
+            const unsigned long long slot = atomicAdd(fb_n, 1ull);
+            fb[slot] = i;
+            continue;
+        }
+        assign[i] = bk[u];
+        if (dist) {  // canonical (CA2) distance to the chosen centre
+            const uint8_t *x = codes + i * M;
+            const uint8_t *c = centers + (int64_t)bk[u] * M;
+            float d = 0.f;
+            for (int m = 0; m < M; ++m) d = __fadd_rn(d, __ldg(T + ((size_t)m * KS + c[m]) * KS + x[m]));
+            dist[i] = d;
+        }
+    }
+}
+
+__global__ void scatter_fallback_kernel(const int64_t *__restrict__ fb, int64_t nfb, const int32_t *__restrict__ a_fb,
+                                        const float *__restrict__ d_fb, int32_t *__restrict__ assign,
+                                        float *__restrict__ dist) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nfb) return;
+    assign[fb[j]] = a_fb[j];
+    if (dist) dist[fb[j]] = d_fb[j];
+}
+
+template <int M>
+static void assign_fast_t(const uint8_t *codes, int64_t n, const float *tables, int64_t K, const float *T,
+                          const uint8_t *centers, int32_t *assign, float *dist, int64_t *fb,
+                          unsigned long long *fb_n, cudaStream_t st) {
+    auto kern = assign_fast_kernel<M>;
+    const size_t smem = (size_t)3 * LUT_PAIR_BYTES;
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)ceil_div(n, 256 * ar2<M>()), 256, smem, st>>>(codes, n, tables, K, T, centers, assign, dist, fb,
+                                                              fb_n);
+    RII_LAUNCHED();
+}
+
+void launch_assign(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, int M, const float *T,
+                   int32_t *assign, float *dist, cudaStream_t st) {
+    if (n <= 0) return;
+    const bool fast = (M == 4 || M == 8 || M == 16 || M == 32) && K >= 12 && n >= 4096;
+    if (!fast) {
+        launch_assign_canonical(codes, n, centers, K, M, T, assign, dist, st);
+        return;
+    }
+    float *tables = nullptr;
+    int64_t *fb = nullptr;
+    unsigned long long *fb_n = nullptr;
+    RII_CUDA(cudaMallocAsync(&tables, (size_t)K * LUT_Q_FLOATS * 4, st));
+    RII_CUDA(cudaMallocAsync(&fb, (size_t)n * 8, st));
+    RII_CUDA(cudaMallocAsync(&fb_n, 8, st));
+    RII_CUDA(cudaMemsetAsync(fb_n, 0, 8, st));
+    centre_tables_kernel<<<(unsigned)K, 256, 0, st>>>(T, centers, M, tables);
+    RII_LAUNCHED();
+    switch (M) {
+        case 4: assign_fast_t<4>(codes, n, tables, K, T, centers, assign, dist, fb, fb_n, st); break;
+        case 8: assign_fast_t<8>(codes, n, tables, K, T, centers, assign, dist, fb, fb_n, st); break;
+        case 16: assign_fast_t<16>(codes, n, tables, K, T, centers, assign, dist, fb, fb_n, st); break;
+        default: assign_fast_t<32>(codes, n, tables, K, T, centers, assign, dist, fb, fb_n, st); break;
+    }
+    unsigned long long nfb = 0;
+    RII_CUDA(cudaMemcpyAsync(&nfb, fb_n, 8, cudaMemcpyDeviceToHost, st));
+    RII_CUDA(cudaStreamSynchronize(st));
+    if (nfb > 0) {  // exact canonical re-assignment of the near-tie codes
+        uint8_t *sub = nullptr;
+        int32_t *a_fb = nullptr;
+        float *d_fb = nullptr;
+        RII_CUDA(cudaMallocAsync(&sub, (size_t)nfb * M, st));
+        RII_CUDA(cudaMallocAsync(&a_fb, (size_t)nfb * 4, st));
+        RII_CUDA(cudaMallocAsync(&d_fb, (size_t)nfb * 4, st));
+        launch_gather_codes(codes, M, fb, (int64_t)nfb, sub, st);
+        launch_assign_canonical(sub, (int64_t)nfb, centers, K, M, T, a_fb, dist ? d_fb : nullptr, st);
+        scatter_fallback_kernel<<<(unsigned)ceil_div((int64_t)nfb, 256), 256, 0, st>>>(fb, (int64_t)nfb, a_fb, d_fb,
+                                                                                       assign, dist);
+        RII_LAUNCHED();
+        RII_CUDA(cudaFreeAsync(sub, st));
+        RII_CUDA(cudaFreeAsync(a_fb, st));
+        RII_CUDA(cudaFreeAsync(d_fb, st));
+    }
+    RII_CUDA(cudaFreeAsync(tables, st));
+    RII_CUDA(cudaFreeAsync(fb, st));
+    RII_CUDA(cudaFreeAsync(fb_n, st));
 }
 
 // -------------------------------------------------------------------- CSR --

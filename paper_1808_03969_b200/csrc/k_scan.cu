@@ -42,28 +42,6 @@ __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
     }
 }
 
-// Lane-rotated ADC of one code (M bytes in w) against the B tables of the CTA:
-// per step j one PRMT builds (z << 8) | 8*(l ^ j); per query pair one LDS.64 +
-// one FADD2.
-template <int M, int B>
-__device__ __forceinline__ void adc_rotated(const uint8_t *lut, const uint32_t (&w)[M / 4], uint32_t rw,
-                                            const uint32_t (&sel)[4], uint32_t l8, float2 (&acc)[B / 2]) {
-    constexpr int W = M / 4, NP = B / 2;
-    uint32_t wp[W];
-#pragma unroll
-    for (int i = 0; i < W; ++i) wp[i] = w[i];
-    permute_words<W>(wp, rw);
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-        const uint32_t off = __byte_perm(wp[j >> 2], l8 ^ (uint32_t)(j << 3), sel[j & 3]);
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            const float2 v = *reinterpret_cast<const float2 *>(lut + p * LUT_PAIR_BYTES + off);
-            acc[p] = j == 0 ? v : fadd2(acc[p], v);  // 0 + v == v for v >= +0
-        }
-    }
-}
-
 template <int M, int B, bool LISTS, int NTH, int U>
 __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     constexpr int W = M / 4, NP = B / 2;

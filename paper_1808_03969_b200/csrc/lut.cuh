@@ -87,4 +87,35 @@ __device__ __forceinline__ void make_selectors(uint32_t r, uint32_t (&sel)[4]) {
     for (int t = 0; t < 4; ++t) sel[t] = 0x5504u | ((((uint32_t)t ^ r) & 3u) << 4);
 }
 
+// Lane-rotated ADC of one code (M bytes in w) against the B tables of the CTA:
+// per step j one PRMT builds (z << 8) | 8*(l ^ j); per query pair one LDS.64 +
+// one FADD2.
+// `wp` = the code words already permuted by permute_words (lane rotation).
+template <int M, int B>
+__device__ __forceinline__ void adc_rotated_pre(const uint8_t *lut, const uint32_t (&wp)[M / 4],
+                                                const uint32_t (&sel)[4], uint32_t l8, float2 (&acc)[B / 2]) {
+    constexpr int NP = B / 2;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        const uint32_t off = __byte_perm(wp[j >> 2], l8 ^ (uint32_t)(j << 3), sel[j & 3]);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const float2 v = *reinterpret_cast<const float2 *>(lut + p * LUT_PAIR_BYTES + off);
+            acc[p] = j == 0 ? v : fadd2(acc[p], v);  // 0 + v == v for v >= +0
+        }
+    }
+}
+
+
+template <int M, int B>
+__device__ __forceinline__ void adc_rotated(const uint8_t *lut, const uint32_t (&w)[M / 4], uint32_t rw,
+                                            const uint32_t (&sel)[4], uint32_t l8, float2 (&acc)[B / 2]) {
+    constexpr int W = M / 4;
+    uint32_t wp[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) wp[i] = w[i];
+    permute_words<W>(wp, rw);
+    adc_rotated_pre<M, B>(lut, wp, sel, l8, acc);
+}
+
 }  // namespace rii

@@ -404,8 +404,11 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
         const int64_t n_cand = a.S ? std::max<int64_t>(t.n_loc, 1) : x->n_local;
         const double avg_len = (double)n_cand / (double)x->K;
         const int Bl = fast ? list_major_B(kk) : 0;
-        const bool list_major = Bl > 0 && avg_len >= 768.0 && (double)a.nq * P * kk * 8 <= 4e9 &&
-                                (double)a.nq * P < 4e9;
+        bool list_major = Bl > 0 && avg_len >= 768.0 && (double)a.nq * P * kk * 8 <= 4e9 && (double)a.nq * P < 4e9;
+        if (const char *mode = getenv("RII_IVF_MODE")) {  // test / tuning override: "list" or "query"
+            if (!strcmp(mode, "list")) list_major = Bl > 0 && (double)a.nq * P < 4e9;
+            if (!strcmp(mode, "query")) list_major = false;
+        }
         if (list_major) {
             const int64_t npairs = a.nq * P;
             uint32_t *vals = x->s_lq.get<uint32_t>(npairs);

@@ -93,6 +93,24 @@ def test_paths_match_oracle(rii, ref, kind, N, D, M, K, nq, topk):
                 assert_topk_parity(ref, o.cb, o.codes, q, gr, orr, S=sub, what=f"{kind} M={M} {path} L={L}")
 
 
+@pytest.mark.parametrize("mode", ["list", "query"])
+@pytest.mark.parametrize("kind,N,D,M,K", [("deep", 30_011, 96, 32, 20), ("sift", 25_000, 128, 16, 16),
+                                          ("deep", 20_003, 96, 8, 12)])
+def test_ivf_list_major_and_query_major(rii, ref, monkeypatch, mode, kind, N, D, M, K):
+    """Both posting-list traversals (list-major: B queries share a list; query-major:
+    one table per query) against the oracle's Alg. 2, whole and subset."""
+    monkeypatch.setenv("RII_IVF_MODE", mode)
+    x = gen.base(kind, N, D, seed=N)
+    q = gen.base(kind, 41, D, seed=N, stream=gen.STREAM_QUERY)
+    g, o = _build_pair(rii, ref, x, M, K, n_iter=3, train_rows=x[:3000], train_iter=3)
+    _check_state(g, o)
+    for sub in (None, gen.subset(N, N // 3, seed=5)):
+        for L in (1, 3, K):
+            gr = g.query(q, 100, target_ids=sub, L=L, path="ivf")
+            orr = o.query(q, 100, S=sub, L=L, path=2)
+            assert_topk_parity(ref, o.cb, o.codes, q, gr, orr, S=sub, what=f"ivf-{mode} {kind} M={M} L={L}")
+
+
 def test_device_memory_path_matches_host_path(rii, ref):
     import torch
     x = gen.deep_like(12_345, 96, seed=3)

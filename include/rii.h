@@ -173,6 +173,22 @@ rii_status rii_get_codes(const rii_index *idx, int64_t first, int64_t n, uint8_t
 rii_status rii_get_centers(const rii_index *idx, uint8_t *out);
 rii_status rii_get_postings(const rii_index *idx, int64_t *offsets, int64_t *ids);
 
+/* Threshold calibration (Alg. 3 / P:589-598: "we simply run the search with several
+ * parameter combinations when the data structure is constructed ... fit a 1D line
+ * in the parameter space"; the supplement with the details is missing, reading R3).
+ * For every L in L_grid (n_L >= 1 values) and target-set sizes |S| = 2^7, 2^9, ...
+ * <= N (evenly spaced sorted ids), times rii_query on the GPU with path LINEAR and
+ * path IVF (CUDA events, one warm-up each; max over ranks), locates the crossover
+ * |S|*(L) by log-linear interpolation (N if the linear scan always wins, 0 if the
+ * inverted index always wins) and fits theta(L) = a*L + b by least squares.
+ * AUTO then uses max(0, a*L + b) at each call's L until rii_set_theta or
+ * rii_reconfigure.  q: nq x D queries (`where`).  Needs K > 0 (RII_ERR_STATE).
+ * a_out / b_out / crossovers (n_L values) may be NULL.  The value is
+ * machine-dependent by construction (parity unpinned). */
+rii_status rii_calibrate_theta(rii_index *idx, const float *q, int64_t nq, int32_t topk, const int32_t *L_grid,
+                               int32_t n_L, rii_mem where, void *stream, double *a_out, double *b_out,
+                               double *crossovers);
+
 /* theta of Alg. 3 (reading R3).  theta < 0 restores the default
  * theta(L) = ceil(L*N/K) + K evaluated at each call's L. */
 rii_status rii_set_theta(rii_index *idx, int64_t theta);

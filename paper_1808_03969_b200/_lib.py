@@ -41,6 +41,8 @@ SIGNATURES = {
     "rii_get_centers": (C.c_int, [_p, _p]),
     "rii_get_postings": (C.c_int, [_p, _p, _p]),
     "rii_set_theta": (C.c_int, [_p, _i64]),
+    "rii_calibrate_theta": (C.c_int, [_p, _p, _i64, _i32, _p, _i32, C.c_int, _p, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double), _p]),
     "rii_get_info": (C.c_int, [_p, C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_i64),
                                C.POINTER(_i64)]),
 }

@@ -118,6 +118,8 @@ struct rii_index {
     int64_t K = 0;
     Buf centers, offsets, ids;
     int64_t theta = -1;
+    bool theta_fit = false;  // rii_calibrate_theta result in use (theta(L) = fit_a * L + fit_b)
+    double fit_a = 0.0, fit_b = 0.0;
     // scratch (query side is const-callable: mutable)
     mutable Buf s_q, s_S, s_pos, s_sub, s_part, s_keys, s_gather, s_d0, s_probe, s_roff, s_rids, s_rkey, s_rval,
         s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_items, s_gthr, s_tables, s_cpart, s_ckeys;
@@ -278,7 +280,8 @@ int resolve_path(const rii_index *x, int64_t nS_global, bool has_S, int L, rii_p
     }
     if (path != RII_PATH_AUTO) return path;
     const int64_t ns = has_S ? nS_global : x->N;
-    const int64_t th = x->theta >= 0 ? x->theta : ceil_div((int64_t)L * x->N, x->K) + x->K;  // R3
+    int64_t th = x->theta >= 0 ? x->theta : ceil_div((int64_t)L * x->N, x->K) + x->K;  // R3
+    if (x->theta < 0 && x->theta_fit) th = (int64_t)std::max(0.0, std::ceil(x->fit_a * L + x->fit_b));
     return ns < th ? RII_PATH_LINEAR : RII_PATH_IVF;  // Alg. 3 L1
 }
 
@@ -354,6 +357,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
     const uint64_t *parts = nullptr;
     int64_t q_stride = kk, p_stride = kk;
     int nparts = 1;
+    Rescore rs;  // set when the partials hold lane-rotated (not yet canonical) distances
     if (a.path == RII_PATH_LINEAR) {  // Alg. 1
         const uint8_t *scan_codes = a.S ? t.sub_codes : codes;
         const int64_t n_codes = a.S ? t.n_loc : x->n_local;
@@ -433,6 +437,9 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             launch_list_scan(x->M, sa, n_items, st);
             tr.mark("list scan");
             parts = pp;
+            rs.codes = codes;
+            rs.tables = tables;
+            rs.M = x->M;
             q_stride = P * kk;
             p_stride = kk;
             nparts = (int)P;
@@ -443,7 +450,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
         }
     }
     tr.mark("scan");
-    launch_merge(parts, q_stride, p_stride, nparts, a.nq, kk, a.topk, map, out_ids, out_dist, out_keys, st);
+    launch_merge(parts, q_stride, p_stride, nparts, a.nq, kk, a.topk, map, out_ids, out_dist, out_keys, st, rs);
     tr.mark("merge");
 }
 
@@ -729,6 +736,7 @@ rii_status rii_reconfigure(rii_index *x, int32_t nlist, int32_t n_iter, uint64_t
         uint8_t *cent = x->centers.get<uint8_t>((size_t)nlist * M);
         RII_CUDA(cudaMemcpyAsync(cent, C, (size_t)nlist * M, cudaMemcpyDeviceToDevice, st));
         x->K = nlist;
+        x->theta_fit = false;
         int32_t *as = x->assign.get<int32_t>(x->n_local + 1);
         launch_assign(x->codes.as<uint8_t>(), x->n_local, cent, x->K, M, x->T.as<float>(), as, nullptr, st);
         rebuild_csr(x, st);
@@ -866,6 +874,108 @@ rii_status rii_set_theta(rii_index *x, int64_t theta) {
     return guarded([&] {
         arg_check(x != nullptr, "index is NULL");
         x->theta = theta < 0 ? -1 : theta;
+        x->theta_fit = false;
+    });
+}
+
+__global__ void strided_ids_kernel(int64_t *out, int64_t s, int64_t N) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < s) out[i] = (int64_t)(((__int128)i * N) / s);
+}
+
+rii_status rii_calibrate_theta(rii_index *x, const float *q, int64_t nq, int32_t topk, const int32_t *L_grid,
+                               int32_t n_L, rii_mem where, void *stream, double *a_out, double *b_out,
+                               double *crossovers) {
+    return guarded([&] {
+        arg_check(x && q && L_grid && n_L >= 1 && nq >= 1, "bad arguments");
+        state_check(x->trained && x->K > 0, "calibration needs coarse centres (K > 0)");
+        arg_check(topk >= 1 && topk <= 1024, "topk must be in [1, 1024]");
+        DeviceGuard g(x->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        const float *dq = q;
+        Buf qb, Sb, oi, od, kb;
+        if (where == RII_MEM_HOST) {
+            float *b = qb.get<float>((size_t)nq * x->D);
+            RII_CUDA(cudaMemcpyAsync(b, q, (size_t)nq * x->D * 4, cudaMemcpyHostToDevice, st));
+            dq = b;
+        }
+        std::vector<int64_t> sizes;
+        for (int64_t s = 128; s <= x->N; s *= 4) sizes.push_back(s);
+        if (sizes.empty() || sizes.back() != x->N) sizes.push_back(x->N);
+        int64_t *S = Sb.get<int64_t>(x->N);
+        int64_t *ids = oi.get<int64_t>((size_t)nq * topk);
+        float *dist = od.get<float>((size_t)nq * topk);
+        cudaEvent_t e0, e1;
+        RII_CUDA(cudaEventCreate(&e0));
+        RII_CUDA(cudaEventCreate(&e1));
+        auto time_query = [&](int64_t s, int L, int path) -> int64_t {  // ns, max over ranks
+            for (int rep = 0; rep < 2; ++rep) {
+                if (rep == 1) RII_CUDA(cudaEventRecord(e0, st));
+                const rii_status r = query_impl(x, dq, nq, topk, S, s, L, (rii_path)path, RII_MEM_DEVICE, st, ids,
+                                                dist, nullptr, nullptr);
+                if (r != RII_OK) throw Error(r, t_err);
+                if (rep == 1) RII_CUDA(cudaEventRecord(e1, st));
+            }
+            RII_CUDA(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            RII_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            int64_t ns = (int64_t)(ms * 1e6), mx = ns;
+            if (x->world > 1 && x->comm) {
+                int64_t *d = kb.get<int64_t>(2);
+                RII_CUDA(cudaMemcpyAsync(d, &ns, 8, cudaMemcpyHostToDevice, st));
+                nccl_allreduce_max_i64(x->comm, d, d + 1, 1, st);
+                RII_CUDA(cudaMemcpyAsync(&mx, d + 1, 8, cudaMemcpyDeviceToHost, st));
+                RII_CUDA(cudaStreamSynchronize(st));
+            }
+            return mx;
+        };
+        std::vector<double> Ls, cross;
+        for (int li = 0; li < n_L; ++li) {
+            const int L = L_grid[li];
+            arg_check(L >= 1, "L_grid values must be >= 1");
+            double prev_s = 0.0, prev_r = 0.0, c = -1.0;
+            for (size_t si = 0; si < sizes.size(); ++si) {
+                const int64_t s = sizes[si];
+                strided_ids_kernel<<<(unsigned)ceil_div(s, 256), 256, 0, st>>>(S, s, x->N);
+                RII_LAUNCHED();
+                const double tl = (double)time_query(s, L, RII_PATH_LINEAR);
+                const double ti = (double)time_query(s, L, RII_PATH_IVF);
+                const double r = std::log(tl / std::max(ti, 1.0));  // > 0: the inverted index is faster
+                if (r > 0) {
+                    if (si == 0) c = 0.0;
+                    else {  // log-linear interpolation of the sign change of log(t_lin / t_ivf)
+                        const double f = prev_r / (prev_r - r);
+                        c = std::exp(std::log(prev_s) + f * (std::log((double)s) - std::log(prev_s)));
+                    }
+                    break;
+                }
+                prev_s = (double)s;
+                prev_r = r;
+            }
+            if (c < 0) c = (double)x->N;
+            Ls.push_back((double)L);
+            cross.push_back(c);
+            if (crossovers) crossovers[li] = c;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        double a = 0.0, b = cross[0];
+        if (n_L > 1) {  // least squares theta = a L + b
+            double mL = 0, mC = 0;
+            for (int i = 0; i < n_L; ++i) { mL += Ls[i]; mC += cross[i]; }
+            mL /= n_L;
+            mC /= n_L;
+            double sxy = 0, sxx = 0;
+            for (int i = 0; i < n_L; ++i) { sxy += (Ls[i] - mL) * (cross[i] - mC); sxx += (Ls[i] - mL) * (Ls[i] - mL); }
+            a = sxx > 0 ? sxy / sxx : 0.0;
+            b = mC - a * mL;
+        }
+        x->fit_a = a;
+        x->fit_b = b;
+        x->theta_fit = true;
+        x->theta = -1;
+        if (a_out) *a_out = a;
+        if (b_out) *b_out = b;
     });
 }
 

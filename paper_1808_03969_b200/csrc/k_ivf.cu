@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
         for (int e = tid; e < 2 * kk; e += NT) {
             const uint64_t k = top[e];
             if (k == KEY_MAX) continue;
-            const int qq = e / kk;
+            const int qq = e >= kk;
             const uint32_t id = key_id(k);
             const uint8_t *cp = codes + (size_t)id * M;
             const float *lq = reinterpret_cast<const float *>(lut);
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
         bitonic_sort_rows(top, 2, kk, kk);
     }
     for (int e = tid; e < 2 * kk; e += NT) {
-        const int qq = e / kk, i = e - qq * kk;
+        const int qq = e >= kk ? 1 : 0, i = e - qq * kk;
         if (q0 + qq < nq) out[(q0 + qq) * kk + i] = top[e];
     }
 }

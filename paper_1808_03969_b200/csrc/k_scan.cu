@@ -202,11 +202,13 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
         }
     }
 
-    // Canonical rescore (CA2: m ascending, replica 0) of the kept candidates.
-    for (int e = tid; e < B * kk; e += NTH) {
+    // Canonical rescore (CA2: m ascending, replica 0) of the kept candidates.  List
+    // mode defers it to the per-query merge (merge_kernel with a Rescore).
+    const int lkk = ilog2_pow2(kk);
+    for (int e = tid; e < (LISTS ? 0 : B * kk); e += NTH) {
         const uint64_t k = top[e];
         if (k == KEY_MAX) continue;
-        const int qq = e / kk;
+        const int qq = e >> lkk;
         const uint32_t id = key_id(k);
         const uint8_t *cp = codes + (size_t)id * M;
         const float *lq = reinterpret_cast<const float *>(lut + (qq >> 1) * LUT_PAIR_BYTES);
@@ -216,9 +218,9 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
         top[e] = make_key(d, id);
     }
     __syncthreads();
-    bitonic_sort_rows(top, B, kk, kk);
+    if constexpr (!LISTS) bitonic_sort_rows(top, B, kk, kk);
     for (int e = tid; e < B * kk; e += NTH) {
-        const int qq = e / kk, i = e - qq * kk;
+        const int qq = e >> lkk, i = e & (kk - 1);
         if (qq >= nqi) continue;
         if constexpr (LISTS) a.out[a.qlist[qstart + qq] * kk + i] = top[e];   // [q][probe rank][kk]
         else a.out[(((int64_t)qb * B + qq) * a.nc + ci) * kk + i] = top[e];
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
     compact_topk(top, fresh, cnt, thr, B, kk, scratch);
     for (int e = tid; e < B * kk; e += NT) {
-        const int qq = e / kk, i = e - qq * kk;
+        const int qq = e >> ilog2_pow2(kk), i = e & (kk - 1);
         const int64_t qi = (int64_t)qb * B + qq;
         if (qi < nq) out[(qi * nc + ci) * kk + i] = top[e];
     }
@@ -497,7 +499,7 @@ void launch_validate_targets(const int64_t *ids, int64_t n, int64_t N, int *flag
 __global__ void __launch_bounds__(NT) merge_kernel(const uint64_t *__restrict__ keys, int64_t q_stride,
                                                    int64_t p_stride, int parts, int kk, int topk, IdMap map,
                                                    int64_t *__restrict__ out_ids, float *__restrict__ out_dist,
-                                                   uint64_t *__restrict__ out_keys) {
+                                                   uint64_t *__restrict__ out_keys, Rescore rs) {
     extern __shared__ __align__(16) uint64_t msm[];
     uint64_t *top = msm, *prt = msm + kk;
     const int64_t q = blockIdx.x;
@@ -514,6 +516,20 @@ __global__ void __launch_bounds__(NT) merge_kernel(const uint64_t *__restrict__ 
         __syncthreads();
         bitonic_merge_rows(top, 1, kk, kk);
     }
+    if (rs.tables) {  // canonical (CA2) rescore from the query's HBM table, then re-sort
+        const float *tq = rs.tables + q * LUT_Q_FLOATS;
+        for (int i = threadIdx.x; i < kk; i += blockDim.x) {
+            const uint64_t k = top[i];
+            if (k == KEY_MAX) continue;
+            const uint32_t id = key_id(k);
+            const uint8_t *cp = rs.codes + (size_t)id * rs.M;
+            float d = 0.f;
+            for (int m = 0; m < rs.M; ++m) d = __fadd_rn(d, __ldg(tq + (int)cp[m] * 32 + m));
+            top[i] = make_key(d, id);
+        }
+        __syncthreads();
+        bitonic_sort_rows(top, 1, kk, kk);
+    }
     if (out_keys) {
         for (int i = threadIdx.x; i < kk; i += blockDim.x) {
             const uint64_t k = top[i];
@@ -529,11 +545,12 @@ __global__ void __launch_bounds__(NT) merge_kernel(const uint64_t *__restrict__ 
 }
 
 void launch_merge(const uint64_t *keys, int64_t q_stride, int64_t p_stride, int parts, int64_t nq, int kk, int topk,
-                  const IdMap &map, int64_t *out_ids, float *out_dist, uint64_t *out_keys, cudaStream_t st) {
+                  const IdMap &map, int64_t *out_ids, float *out_dist, uint64_t *out_keys, cudaStream_t st,
+                  const Rescore &rs) {
     if (nq <= 0) return;
     KernelTimer t(TK_MERGE, st);
     merge_kernel<<<(unsigned)nq, NT, (size_t)2 * kk * 8, st>>>(keys, q_stride, p_stride, parts, kk, topk, map,
-                                                               out_ids, out_dist, out_keys);
+                                                               out_ids, out_dist, out_keys, rs);
     RII_LAUNCHED();
 }
 

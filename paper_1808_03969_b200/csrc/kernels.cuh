@@ -69,8 +69,16 @@ void launch_validate_targets(const int64_t *ids, int64_t n, int64_t N, int *flag
 // keys addressed as base[q * q_stride + p * p_stride + i].  Either writes
 // (out_ids, out_dist) [nq][topk] or, if out_keys != nullptr, [nq][kk] keys with
 // ids mapped to global ids.
+// Optional canonical rescore inside the merge: key ids are positions in `codes`,
+// tables are the per-query HBM tables (lut.cuh layout).
+struct Rescore {
+    const uint8_t *codes = nullptr;
+    const float *tables = nullptr;
+    int M = 0;
+};
 void launch_merge(const uint64_t *keys, int64_t q_stride, int64_t p_stride, int parts, int64_t nq, int kk, int topk,
-                  const IdMap &map, int64_t *out_ids, float *out_dist, uint64_t *out_keys, cudaStream_t st);
+                  const IdMap &map, int64_t *out_ids, float *out_dist, uint64_t *out_keys, cudaStream_t st,
+                  const Rescore &rs = Rescore());
 
 // ---- inverted index (k_ivf.cu) -----------------------------------------------
 // d0[q][k] = CA2 ADC of query q to centre code k (Alg. 2 L2-L5).

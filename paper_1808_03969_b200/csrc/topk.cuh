@@ -61,13 +61,15 @@ __device__ __forceinline__ void cas_asc(uint64_t *a, int i, int p) {
     if (x > y) { a[i] = y; a[p] = x; }
 }
 
+__device__ __forceinline__ int ilog2_pow2(int v) { return __ffs(v) - 1; }  // v a power of two
+
 // Bitonic sort of `nq` independent arrays a[q*stride .. + S), S a power of two.
 __device__ inline void bitonic_sort_rows(uint64_t *a, int nq, int stride, int S) {
-    const int half = S >> 1;
+    const int half = S >> 1, lh = ilog2_pow2(half > 0 ? half : 1);
     for (int k = 2; k <= S; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             for (int e = threadIdx.x; e < nq * half; e += blockDim.x) {
-                int q = e / half, t = e - q * half;
+                int q = e >> lh, t = e & (half - 1);
                 int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
                 int p = i | j;
                 uint64_t *r = a + (size_t)q * stride;
@@ -82,10 +84,10 @@ __device__ inline void bitonic_sort_rows(uint64_t *a, int nq, int stride, int S)
 
 // Sort a bitonic sequence a[q*stride .. + S) ascending (merge network).
 __device__ inline void bitonic_merge_rows(uint64_t *a, int nq, int stride, int S) {
-    const int half = S >> 1;
+    const int half = S >> 1, lh = ilog2_pow2(half > 0 ? half : 1);
     for (int len = half; len > 0; len >>= 1) {
         for (int e = threadIdx.x; e < nq * half; e += blockDim.x) {
-            int q = e / half, t = e - q * half;
+            int q = e >> lh, t = e & (half - 1);
             int i = ((t & ~(len - 1)) << 1) | (t & (len - 1));
             cas_asc(a + (size_t)q * stride, i, i | len);
         }
@@ -108,14 +110,16 @@ __device__ inline void compact_topk(uint64_t *top, uint64_t *fresh, int *cnt, fl
     if (mx > 0) {
         int S = 2;
         while (S < mx) S <<= 1;
+        const int ls = ilog2_pow2(S);
         for (int e = threadIdx.x; e < nq * S; e += blockDim.x) {
-            int q = e / S, i = e - q * S;
+            int q = e >> ls, i = e & (S - 1);
             if (i >= cnt[q]) fresh[(size_t)q * NEWCAP + i] = KEY_MAX;
         }
         __syncthreads();
         bitonic_sort_rows(fresh, nq, NEWCAP, S);
+        const int lk = ilog2_pow2(kk);
         for (int e = threadIdx.x; e < nq * kk; e += blockDim.x) {
-            int q = e / kk, i = e - q * kk;
+            int q = e >> lk, i = e & (kk - 1);
             int x = kk - 1 - i;
             uint64_t v = x < S ? fresh[(size_t)q * NEWCAP + x] : KEY_MAX;
             uint64_t *t = top + (size_t)q * kk + i;

@@ -212,6 +212,22 @@ class Index:
         _rl.check(self._lib.rii_get_postings(self._h, _ptr(off), _ptr(ids)))
         return off, ids
 
+    def calibrate_theta(self, q, topk: int = 100, L_grid=(1, 4, 16, 64)):
+        """Fit theta(L) = a L + b from GPU timings of both paths (Alg. 3).
+        Returns (a, b, crossovers per L)."""
+        Lg = np.ascontiguousarray(L_grid, dtype=np.int32)
+        cross = np.empty(len(Lg), np.float64)
+        a, b = C.c_double(), C.c_double()
+        if _is_cuda_tensor(q):
+            q = _dev(q, np.float32)
+            where, st = _rl.MEM_DEVICE, _stream_ptr(None)
+        else:
+            q = _host(q, np.float32)
+            where, st = _rl.MEM_HOST, None
+        _rl.check(self._lib.rii_calibrate_theta(self._h, _ptr(q), q.shape[0], topk, _ptr(Lg), len(Lg), where, st,
+                                                C.byref(a), C.byref(b), _ptr(cross)))
+        return a.value, b.value, cross
+
     def set_theta(self, theta: int):
         _rl.check(self._lib.rii_set_theta(self._h, theta))
 

@@ -252,3 +252,30 @@ def test_logical_shards_equal_single_index(rii, ref):
     with pytest.raises(rii.RiiError) as e:
         shards[0].query(q, 5)
     assert e.value.status == 2
+
+
+def test_theta_calibration(rii, ref):
+    """Alg. 3 threshold fitted from GPU timings: a line theta(L) = aL + b
+    whose value is machine-dependent (parity unpinned); checked for sanity and for the
+    rule |S| < theta -> linear, applied with the fitted value."""
+    import torch
+    N, D, M = 200_000, 96, 32
+    x = torch.from_numpy(gen.deep_like(N, D, seed=31)).cuda()
+    q = torch.from_numpy(gen.deep_like(256, D, seed=31, stream=gen.STREAM_QUERY)).cuda()
+    g = rii.Index(D, M)
+    g.train(x[:20_000], n_iter=2, seed=0)
+    g.add(x)
+    g.reconfigure(447, n_iter=3, seed=0)
+    a, b, cross = g.calibrate_theta(q, topk=100, L_grid=(1, 4, 16))
+    assert np.isfinite(a) and np.isfinite(b)
+    assert ((cross >= 0) & (cross <= N)).all()
+    for L in (1, 4, 16):
+        th = int(max(0.0, np.ceil(a * L + b)))
+        if th >= 8:
+            S = np.arange(0, N, N // (th // 2))[: th // 2].astype(np.int64)
+            assert g.query(q[:4], 10, target_ids=S, L=L)[2] == rii.PATH_LINEAR
+        if 2 * th <= N:
+            S = np.arange(0, N, max(1, N // (2 * th)))[: 2 * th].astype(np.int64)
+            assert g.query(q[:4], 10, target_ids=S, L=L)[2] == rii.PATH_IVF
+    g.set_theta(-1)  # back to the analytic default (R3)
+    assert g.query(q[:4], 10, L=1)[2] == rii.PATH_IVF

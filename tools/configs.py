@@ -1,0 +1,147 @@
+"""Measure the other BASELINE.json configs on one GPU and print
+one JSON line per row.  Timing: CUDA events on the launching stream, >= 1 warm-up,
+queries resident in HBM, median of `reps` runs.
+
+    python tools/configs.py [--only tiny,sift1m,growth,deep10m] [--reps 3]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1808_03969_b200 as rii  # noqa: E402
+from synth import generators as gen  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def timed(fn, reps):
+    fn()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    out = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn()
+        b.record(st)
+        torch.cuda.synchronize()
+        out.append(a.elapsed_time(b))
+    return statistics.median(out)
+
+
+def emit(**kw):
+    print(json.dumps(kw), flush=True)
+
+
+def rows_for(name, g, q, topk, Ls, subsets, N, nlist, reps):
+    nq = q.shape[0]
+    ms = timed(lambda: g.query(q, topk, None, L=1, path="linear"), reps)
+    emit(config=name, row="linear whole", N=N, nq=nq, topk=topk, ms=ms, qps=nq / ms * 1e3,
+         scanned_codes_per_s=nq * N / ms * 1e3)
+    for L in Ls:
+        ms = timed(lambda: g.query(q, topk, None, L=L, path="ivf"), reps)
+        emit(config=name, row=f"ivf whole L={L}", N=N, nq=nq, topk=topk, ms=ms, qps=nq / ms * 1e3,
+             approx_candidates_per_query=L * N / nlist)
+    for s in subsets:
+        S = gen.subset_torch(N, s, DEV, seed=s)
+        for L in Ls[-1:]:
+            for path in ("auto", "linear", "ivf"):
+                used = {}
+
+                def f():
+                    used["p"] = g.query(q, topk, S, L=L, path=path)[2]
+                ms = timed(f, reps)
+                emit(config=name, row=f"subset |S|={s} L={L} {path}", path_used=["auto", "linear", "ivf"][used["p"]],
+                     ms=ms, qps=nq / ms * 1e3)
+
+
+def build(kind, N, D, M, nlist, n_train, train_iter=20):
+    g = rii.Index(D, M, device=0)
+    t0 = time.perf_counter()
+    g.train(bench._device_data(kind, n_train, D, DEV, 0, gen.STREAM_TRAIN), n_iter=train_iter, seed=0)
+    torch.cuda.synchronize()
+    t_train = time.perf_counter() - t0
+    x = bench._device_data(kind, N, D, DEV, 0, gen.STREAM_BASE)
+    t0 = time.perf_counter()
+    g.add(x)
+    torch.cuda.synchronize()
+    t_add = time.perf_counter() - t0
+    del x
+    t0 = time.perf_counter()
+    g.reconfigure(nlist, n_iter=10, seed=0)
+    torch.cuda.synchronize()
+    t_rec = time.perf_counter() - t0
+    return g, dict(train_s=t_train, add_s=t_add, reconfigure_s=t_rec)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="tiny,sift1m,growth")
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    only = a.only.split(",")
+    if "tiny" in only:
+        c = gen.CONFIGS["tiny"]
+        g, b = build("gaussian", c["N"], c["D"], c["M"], c["nlist"], c["N"])
+        emit(config="tiny", row="build", **b)
+        q = bench._device_data("gaussian", c["nq"], c["D"], DEV, 0, gen.STREAM_QUERY)
+        rows_for("tiny", g, q, 10, [8], [1000], c["N"], c["nlist"], a.reps)
+    if "sift1m" in only:
+        c = gen.CONFIGS["sift1m"]
+        g, b = build("sift", c["N"], c["D"], c["M"], c["nlist"], c["n_train"])
+        emit(config="sift1m", row="build", **b)
+        q = bench._device_data("sift", c["nq"], c["D"], DEV, 0, gen.STREAM_QUERY)
+        th = g.calibrate_theta(q[:1000], topk=100, L_grid=(1, 4, 16, 64))
+        emit(config="sift1m", row="theta calibration", a=th[0], b=th[1], crossovers=th[2].tolist())
+        rows_for("sift1m", g, q, 100, [1, 4, 16, 64], c["subsets"], c["N"], c["nlist"], a.reps)
+    if "growth" in only:  # configs[3]: start 10k, nlist 100, add 9 x 1,111,111, reconfigure to sqrt(N)
+        c = gen.CONFIGS["growth"]
+        D, M = c["D"], c["M"]
+        g = rii.Index(D, M, device=0)
+        g.train(bench._device_data("sift", c["n_train"], D, DEV, 0, gen.STREAM_TRAIN), n_iter=20, seed=0)
+        x0 = bench._device_data("sift", c["N"], D, DEV, 0, gen.STREAM_BASE)
+        g.add(x0)
+        g.reconfigure(c["nlist"], n_iter=10, seed=0)
+        q = bench._device_data("sift", c["nq"], D, DEV, 0, gen.STREAM_QUERY)
+        for i in range(c["add_batches"]):
+            xb = bench._device_data("sift", c["add_size"], D, DEV, 1 + i, gen.STREAM_BASE)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            g.add(xb)
+            torch.cuda.synchronize()
+            emit(config="growth", row=f"add batch {i}", n=c["add_size"], add_s=time.perf_counter() - t0,
+                 N=g.info()["N"])
+        N = g.info()["N"]
+        for L in c["L"]:
+            ms = timed(lambda: g.query(q, c["topk"], None, L=L, path="ivf"), a.reps)
+            emit(config="growth", row=f"before reconfigure ivf L={L}", K=g.info()["K"], ms=ms, qps=c["nq"] / ms * 1e3)
+        K2 = gen.nlist_for(N)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g.reconfigure(K2, n_iter=10, seed=0)
+        torch.cuda.synchronize()
+        emit(config="growth", row="reconfigure", N=N, nlist=K2, reconfigure_s=time.perf_counter() - t0)
+        for L in c["L"]:
+            ms = timed(lambda: g.query(q, c["topk"], None, L=L, path="ivf"), a.reps)
+            emit(config="growth", row=f"after reconfigure ivf L={L}", K=K2, ms=ms, qps=c["nq"] / ms * 1e3)
+    if "deep10m" in only:
+        kind, N, D, M, nlist, nq, topk, n_train, _ = bench.WORKLOADS["deep10m"]
+        g, b = build(kind, N, D, M, nlist, n_train)
+        emit(config="deep10m", row="build", **b)
+        q = bench._device_data(kind, nq, D, DEV, 0, gen.STREAM_QUERY)
+        th = g.calibrate_theta(q[:1000], topk=100, L_grid=(1, 4, 16, 64))
+        emit(config="deep10m", row="theta calibration", a=th[0], b=th[1], crossovers=th[2].tolist())
+        rows_for("deep10m", g, q, topk, [1, 4, 16, 64], [100_000, 1_000_000], N, nlist, a.reps)
+
+
+if __name__ == "__main__":
+    main()

@@ -371,7 +371,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             RII_CUDA(cudaMemsetAsync(pp, 0xff, (size_t)a.nq * kk * 8, st));
             parts = pp;
         } else {
-            ScanPlan pl = plan_linear(x->M, kk, a.nq, n_codes, x->num_sms);
+            ScanPlan pl = plan_linear(x->M, kk, a.nq, n_codes, x->num_sms, tables != nullptr);
             uint64_t *pp = x->s_part.get<uint64_t>((size_t)pl.nb * pl.B * pl.nc * kk);
             launch_linear_scan(pl, scan_codes, n_codes, x->M, a.q, a.nq, cb, x->D, kk, pp, st, tables);
             parts = pp;
@@ -389,7 +389,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
         } else if (fast && P <= 1008) {
             // coarse ranking (L2-L5) with the lane-rotated scan over the K centre codes,
             // canonical rescore, top-P by (d0, k) (L6)
-            ScanPlan pc = plan_linear(x->M, kkc, a.nq, x->K, x->num_sms);
+            ScanPlan pc = plan_linear(x->M, kkc, a.nq, x->K, x->num_sms, tables != nullptr);
             uint64_t *cp = x->s_cpart.get<uint64_t>((size_t)pc.nb * pc.B * pc.nc * kkc);
             launch_linear_scan(pc, x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, kkc, cp, st, tables);
             uint64_t *ck = x->s_ckeys.get<uint64_t>((size_t)a.nq * kkc);
@@ -437,9 +437,11 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             launch_list_scan(x->M, sa, n_items, st);
             tr.mark("list scan");
             parts = pp;
-            rs.codes = codes;
-            rs.tables = tables;
-            rs.M = x->M;
+            if (Bl != 8) {  // fp32-pair items keep lane-rotated keys: rescore in the merge
+                rs.codes = codes;
+                rs.tables = tables;
+                rs.M = x->M;
+            }
             q_stride = P * kk;
             p_stride = kk;
             nparts = (int)P;

@@ -42,13 +42,14 @@ __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
     }
 }
 
-template <int M, int B, bool LISTS, int NTH, int U>
+template <int M, int B, bool LISTS, int NTH, int U, bool PACKED>
 __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
-    constexpr int W = M / 4, NP = B / 2;
+    constexpr int W = M / 4, NP = B / 2, NQ = B / 4;
+    static_assert(!PACKED || B % 4 == 0, "packed tables hold 4 queries each");
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t *lut = smem;
     const int kk = a.kk;
-    uint64_t *top = reinterpret_cast<uint64_t *>(smem + NP * LUT_PAIR_BYTES);
+    uint64_t *top = reinterpret_cast<uint64_t *>(smem + (PACKED ? NQ * QUAD_BYTES : NP * LUT_PAIR_BYTES));
     uint64_t *fresh = top + B * kk;
     int *cnt = reinterpret_cast<int *>(fresh + B * NEWCAP);
     float *thr = reinterpret_cast<float *>(cnt + B);
@@ -80,13 +81,22 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     };
     const int D = M * a.ds, tid = threadIdx.x, lane = tid & 31;
 
+    if constexpr (PACKED) {
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-        float *lp = reinterpret_cast<float *>(lut + p * LUT_PAIR_BYTES);
-        if (a.tables)
-            load_lut_pair(lp, a.tables + query_of(2 * p) * LUT_Q_FLOATS, a.tables + query_of(2 * p + 1) * LUT_Q_FLOATS);
-        else
-            build_lut_pair<M>(lp, a.q + query_of(2 * p) * D, a.q + query_of(2 * p + 1) * D, a.cb, a.ds);
+        for (int p = 0; p < NQ; ++p)
+            load_lut_quad(reinterpret_cast<uint32_t *>(lut + p * QUAD_BYTES), a.tables + query_of(4 * p) * LUT_Q_FLOATS,
+                          a.tables + query_of(4 * p + 1) * LUT_Q_FLOATS, a.tables + query_of(4 * p + 2) * LUT_Q_FLOATS,
+                          a.tables + query_of(4 * p + 3) * LUT_Q_FLOATS);
+    } else {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            float *lp = reinterpret_cast<float *>(lut + p * LUT_PAIR_BYTES);
+            if (a.tables)
+                load_lut_pair(lp, a.tables + query_of(2 * p) * LUT_Q_FLOATS,
+                              a.tables + query_of(2 * p + 1) * LUT_Q_FLOATS);
+            else
+                build_lut_pair<M>(lp, a.q + query_of(2 * p) * D, a.q + query_of(2 * p + 1) * D, a.cb, a.ds);
+        }
     }
     for (int e = tid; e < B * kk; e += NTH) top[e] = KEY_MAX;
     if (tid < B) { cnt[tid] = 0; thr[tid] = __int_as_float(0x7f800000); scratch[2 + tid] = 0; }
@@ -104,9 +114,32 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
         gq[qq] = __int_as_float(0x7f800000);
         if constexpr (LISTS) gq[qq] = __ldcg(a.gthr + query_of(qq));
     }
+    // Filter thresholds: the exact kk-th distance (and list bound); relaxed by
+    // PACK_SLACK for the approximate packed sums.
+    auto relax = [](float t) { return PACKED ? __fmul_ru(t, PACK_SLACK) : t; };
     float th[B];
 #pragma unroll
-    for (int qq = 0; qq < B; ++qq) th[qq] = fminf(thr[qq], gq[qq]);
+    for (int qq = 0; qq < B; ++qq) th[qq] = relax(fminf(thr[qq], gq[qq]));
+    // Packed mode: canonical (CA2) rescore of the fresh entries from the queries'
+    // fp32 HBM tables before they are compacted into the exact top lists.
+    auto rescore_fresh = [&]() {
+        if constexpr (PACKED) {
+            for (int qq = 0; qq < B; ++qq) {
+                const float *tq = a.tables + query_of(qq) * LUT_Q_FLOATS;
+                const int n = cnt[qq];
+                for (int i = tid; i < n; i += NTH) {
+                    uint64_t *f = fresh + qq * NEWCAP + i;
+                    const uint32_t id = key_id(*f);
+                    const uint8_t *cp = codes + (size_t)id * M;
+                    float d = 0.f;
+#pragma unroll
+                    for (int m = 0; m < M; ++m) d = __fadd_rn(d, __ldg(tq + (int)cp[m] * 32 + m));
+                    *f = make_key(d, id);
+                }
+            }
+            __syncthreads();
+        }
+    };
 
     // Each thread evaluates U codes per step (positions base + u*NT + tid, coalesced),
     // the next step's codes prefetched into registers.  Block barriers only every
@@ -145,15 +178,30 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t pos = base + u * NTH + tid;
-                float2 acc2[NP];
-                adc_rotated<M, B>(lut, w[u], rw, sel, l8, acc2);
+                float d[B];
+                if constexpr (PACKED) {
+                    float2 ab[NQ], cd[NQ];
+                    adc_packed<M, NQ>(lut, w[u], rw, sel, l8, ab, cd);
 #pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    push_candidate_win(pos < c1 && acc2[p].x <= th[2 * p], make_key(acc2[p].x, cid[u]),
-                                       fresh + (2 * p) * NEWCAP, cnt + 2 * p, lane, SOFT, need, ovf);
-                    push_candidate_win(pos < c1 && acc2[p].y <= th[2 * p + 1], make_key(acc2[p].y, cid[u]),
-                                       fresh + (2 * p + 1) * NEWCAP, cnt + 2 * p + 1, lane, SOFT, need, ovf);
+                    for (int p = 0; p < NQ; ++p) {
+                        d[4 * p] = ab[p].x;
+                        d[4 * p + 1] = ab[p].y;
+                        d[4 * p + 2] = cd[p].x;
+                        d[4 * p + 3] = cd[p].y;
+                    }
+                } else {
+                    float2 acc2[NP];
+                    adc_rotated<M, B>(lut, w[u], rw, sel, l8, acc2);
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        d[2 * p] = acc2[p].x;
+                        d[2 * p + 1] = acc2[p].y;
+                    }
                 }
+#pragma unroll
+                for (int qq = 0; qq < B; ++qq)
+                    push_candidate_win(pos < c1 && d[qq] <= th[qq], make_key(d[qq], cid[u]), fresh + qq * NEWCAP,
+                                       cnt + qq, lane, SOFT, need, ovf);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -167,13 +215,15 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
         if (__syncthreads_or(ovf || need)) {
             const bool rolled = *s_ovf != 0;  // written before the barrier; reset below
             if (rolled && tid < B) cnt[tid] = s_cnt0[tid];
+            __syncthreads();
+            rescore_fresh();
             compact_topk(top, fresh, cnt, thr, B, kk, scratch);
             if (tid == 0) *s_ovf = 0;
             if (tid < B) s_cnt0[tid] = 0;
 #pragma unroll
             for (int qq = 0; qq < B; ++qq) {
                 if constexpr (LISTS) gq[qq] = fminf(gq[qq], __ldcg(a.gthr + query_of(qq)));
-                th[qq] = fminf(thr[qq], gq[qq]);
+                th[qq] = relax(fminf(thr[qq], gq[qq]));
             }
             if (rolled) {
                 base = wstart;
@@ -187,13 +237,15 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
 #pragma unroll
                 for (int qq = 0; qq < B; ++qq) {
                     gq[qq] = fminf(gq[qq], __ldcg(a.gthr + query_of(qq)));
-                    th[qq] = fminf(th[qq], gq[qq]);
+                    th[qq] = fminf(th[qq], relax(gq[qq]));
                 }
             }
             __syncthreads();  // snapshot taken before the next window pushes
         }
         if (safe > 0) --safe;
     }
+    __syncthreads();
+    rescore_fresh();
     compact_topk(top, fresh, cnt, thr, B, kk, scratch);
     if constexpr (LISTS) {  // publish this item's kk-th distance as a bound for the query
         if (tid < nqi && thr[tid] < __int_as_float(0x7f800000)) {
@@ -203,9 +255,10 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     }
 
     // Canonical rescore (CA2: m ascending, replica 0) of the kept candidates.  List
-    // mode defers it to the per-query merge (merge_kernel with a Rescore).
+    // mode defers it to the per-query merge (merge_kernel with a Rescore); packed
+    // mode's top lists are exact already.
     const int lkk = ilog2_pow2(kk);
-    for (int e = tid; e < (LISTS ? 0 : B * kk); e += NTH) {
+    for (int e = tid; e < ((LISTS || PACKED) ? 0 : B * kk); e += NTH) {
         const uint64_t k = top[e];
         if (k == KEY_MAX) continue;
         const int qq = e >> lkk;
@@ -218,7 +271,7 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
         top[e] = make_key(d, id);
     }
     __syncthreads();
-    if constexpr (!LISTS) bitonic_sort_rows(top, B, kk, kk);
+    if constexpr (!LISTS && !PACKED) bitonic_sort_rows(top, B, kk, kk);
     for (int e = tid; e < B * kk; e += NTH) {
         const int qq = e >> lkk, i = e & (kk - 1);
         if (qq >= nqi) continue;
@@ -293,19 +346,33 @@ __global__ void __launch_bounds__(NT, 1)
     }
 }
 
-static size_t smem_fast(int B, int kk) { return (size_t)(B / 2) * LUT_PAIR_BYTES + (size_t)B * (kk + NEWCAP) * 8 + 64; }  // 64 B: cnt, thr, scratch[8]
+// B == 8 means the bf16-packed variant (2 quad tables); otherwise B / 2 fp32 pair tables.
+static size_t smem_fast(int B, int kk) {
+    const size_t lut = B == 8 ? (size_t)2 * QUAD_BYTES : (size_t)(B / 2) * LUT_PAIR_BYTES;
+    return lut + (size_t)B * (kk + NEWCAP) * 8 + 128;  // 128 B: cnt, thr, scratch[16]
+}
+// RII_PACKED=0 disables the bf16-packed tables (A/B measurements).
+static bool packed_enabled() {
+    static bool on = [] {
+        const char *e = getenv("RII_PACKED");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 static size_t smem_generic(int B, int M, int kk) {
     return (size_t)B * M * KS * 4 + (size_t)B * (kk + NEWCAP) * 8 + 64;
 }
 static constexpr size_t SMEM_CAP = 227 * 1024;
 
-ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms) {
+ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available) {
     ScanPlan p{};
     p.fast = (M == 4 || M == 8 || M == 16 || M == 32);
     p.B = 0;
     if (p.fast) {
-        for (int B : {6, 4, 2})
+        for (int B : {8, 6, 4, 2}) {
+            if (B == 8 && (!packed_enabled() || !tables_available)) continue;
             if (smem_fast(B, kk) <= SMEM_CAP) { p.B = B; p.smem = smem_fast(B, kk); break; }
+        }
     } else {
         for (int B : {4, 2, 1})
             if (smem_generic(B, M, kk) <= SMEM_CAP) { p.B = B; p.smem = smem_generic(B, M, kk); break; }
@@ -342,8 +409,12 @@ static int scan_threads() { return scan_cfg() == 0 ? 256 : 512; }
 
 template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr() {
-    if (scan_cfg() == 0) return (void *)scan_fast_kernel<M, B, LISTS, 256, 2>;
-    return (void *)scan_fast_kernel<M, B, LISTS, 512, 1>;
+    if constexpr (B == 8) {
+        return (void *)scan_fast_kernel<M, 8, LISTS, 512, 1, true>;
+    } else {
+        if (scan_cfg() == 0) return (void *)scan_fast_kernel<M, B, LISTS, 256, 2, false>;
+        return (void *)scan_fast_kernel<M, B, LISTS, 512, 1, false>;
+    }
 }
 
 template <int M, int B>
@@ -363,7 +434,8 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
 template <int M>
 static void launch_fast_m(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
                           const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st, const float *tables) {
-    if (pl.B == 6) launch_fast_t<M, 6>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables);
+    if (pl.B == 8) launch_fast_t<M, 8>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables);
+    else if (pl.B == 6) launch_fast_t<M, 6>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables);
     else if (pl.B == 4) launch_fast_t<M, 4>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables);
     else launch_fast_t<M, 2>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables);
 }
@@ -381,8 +453,10 @@ static void launch_generic_t(const ScanPlan &pl, const uint8_t *codes, int64_t n
 bool list_major_supported(int M) { return M == 4 || M == 8 || M == 16 || M == 32; }
 
 int list_major_B(int kk) {
-    for (int B : {6, 4, 2})
+    for (int B : {8, 6, 4, 2}) {
+        if (B == 8 && !packed_enabled()) continue;
         if (smem_fast(B, kk) <= SMEM_CAP) return B;
+    }
     return 0;
 }
 
@@ -401,7 +475,8 @@ static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st) {
 template <int M>
 static void launch_list_m(const ScanArgs &a, int64_t n_items, cudaStream_t st) {
     const int B = list_major_B(a.kk);
-    if (B == 6) launch_list_t<M, 6>(a, n_items, st);
+    if (B == 8) launch_list_t<M, 8>(a, n_items, st);
+    else if (B == 6) launch_list_t<M, 6>(a, n_items, st);
     else if (B == 4) launch_list_t<M, 4>(a, n_items, st);
     else launch_list_t<M, 2>(a, n_items, st);
 }

@@ -16,7 +16,7 @@ struct ScanPlan {
     bool fast;    // lane-rotated conflict-free LUT layout
     size_t smem;
 };
-ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms);
+ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available = false);
 
 // Arguments of the lane-rotated scan kernel (linear mode, or list-major inverted
 // index mode where a work item is (posting list, up to B queries probing it)).

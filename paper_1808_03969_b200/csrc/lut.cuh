@@ -5,6 +5,8 @@
 // Lane l reads column c = l ^ j at step j: 32 distinct columns -> every 16-lane
 // half-warp covers 32 distinct banks whatever the code bytes are.
 #pragma once
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace rii {
@@ -116,6 +118,57 @@ __device__ __forceinline__ void adc_rotated(const uint8_t *lut, const uint32_t (
     for (int i = 0; i < W; ++i) wp[i] = w[i];
     permute_words<W>(wp, rw);
     adc_rotated_pre<M, B>(lut, wp, sel, l8, acc);
+}
+
+// ---- bf16-packed quad tables (4 queries per 8-byte column) ------------------
+// Word 0 of column c in row z = trunc_bf16(A) << 16 | rn_bf16(C), word 1 = the same
+// for (B, D).  Read raw as fp32, the high halves give A and B with the low 16
+// mantissa bits as noise; shifted left by 16 the low halves give C and D exactly
+// as bf16.  Every approximate table value lies within 2^-7 relative of the fp32
+// entry, so an approximate ADC sum is within 2^-7 (+ fp32 rounding) of the
+// canonical one: the kernels filter with the threshold relaxed by PACK_SLACK and
+// rescore every pushed candidate canonically before it can enter a top list.
+constexpr int QUAD_BYTES = 256 * 256;
+constexpr float PACK_SLACK = 1.008f;  // > (1 + 2^-7) (1 + 1e-5)
+
+__device__ __forceinline__ void load_lut_quad(uint32_t *dst, const float *__restrict__ ta,
+                                              const float *__restrict__ tb, const float *__restrict__ tc,
+                                              const float *__restrict__ td) {
+    const float4 *a4 = reinterpret_cast<const float4 *>(ta), *b4 = reinterpret_cast<const float4 *>(tb);
+    const float4 *c4 = reinterpret_cast<const float4 *>(tc), *d4 = reinterpret_cast<const float4 *>(td);
+    uint4 *o = reinterpret_cast<uint4 *>(dst);
+    auto hi = [](float v) { return __float_as_uint(v) & 0xffff0000u; };
+    auto lo = [](float v) { return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v)); };
+    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 4; e += blockDim.x) {
+        const float4 A = __ldg(a4 + e), B = __ldg(b4 + e), C = __ldg(c4 + e), D = __ldg(d4 + e);
+        o[2 * e] = make_uint4(hi(A.x) | lo(C.x), hi(B.x) | lo(D.x), hi(A.y) | lo(C.y), hi(B.y) | lo(D.y));
+        o[2 * e + 1] = make_uint4(hi(A.z) | lo(C.z), hi(B.z) | lo(D.z), hi(A.w) | lo(C.w), hi(B.w) | lo(D.w));
+    }
+}
+
+// Approximate lane-rotated ADC of one pre-loaded code against NQ quad tables:
+// per step j one PRMT, per quad one LDS.64, two SHF and two FADD2 (4 lookups).
+template <int M, int NQ>
+__device__ __forceinline__ void adc_packed(const uint8_t *lut, const uint32_t (&w)[M / 4], uint32_t rw,
+                                           const uint32_t (&sel)[4], uint32_t l8, float2 (&ab)[NQ],
+                                           float2 (&cd)[NQ]) {
+    constexpr int W = M / 4;
+    uint32_t wp[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) wp[i] = w[i];
+    permute_words<W>(wp, rw);
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        const uint32_t off = __byte_perm(wp[j >> 2], l8 ^ (uint32_t)(j << 3), sel[j & 3]);
+#pragma unroll
+        for (int p = 0; p < NQ; ++p) {
+            const uint2 v = *reinterpret_cast<const uint2 *>(lut + p * QUAD_BYTES + off);
+            const float2 x = make_float2(__uint_as_float(v.x), __uint_as_float(v.y));
+            const float2 y = make_float2(__uint_as_float(v.x << 16), __uint_as_float(v.y << 16));
+            ab[p] = j == 0 ? x : fadd2(ab[p], x);
+            cd[p] = j == 0 ? y : fadd2(cd[p], y);
+        }
+    }
 }
 
 }  // namespace rii

@@ -407,7 +407,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
         // [nq][P][kk] partials stay small; otherwise query-major (one table per query).
         const int64_t n_cand = a.S ? std::max<int64_t>(t.n_loc, 1) : x->n_local;
         const double avg_len = (double)n_cand / (double)x->K;
-        const int Bl = fast ? list_major_B(kk) : 0;
+        const int Bl = fast ? list_major_B(kk, avg_len) : 0;
         bool list_major = Bl > 0 && avg_len >= 768.0 && (double)a.nq * P * kk * 8 <= 4e9 && (double)a.nq * P < 4e9;
         if (const char *mode = getenv("RII_IVF_MODE")) {  // test / tuning override: "list" or "query"
             if (!strcmp(mode, "list")) list_major = Bl > 0 && (double)a.nq * P < 4e9;
@@ -434,7 +434,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             sa.codes = codes; sa.q = a.q; sa.nq = a.nq; sa.cb = cb; sa.ds = x->ds; sa.kk = kk; sa.out = pp;
             sa.items = items; sa.qlist = qlist; sa.P = P; sa.offsets = off; sa.ids = ids; sa.gthr = gthr;
             sa.tables = tables;
-            launch_list_scan(x->M, sa, n_items, st);
+            launch_list_scan(x->M, Bl, sa, n_items, st);
             tr.mark("list scan");
             parts = pp;
             if (Bl != 8) {  // fp32-pair items keep lane-rotated keys: rescore in the merge

@@ -363,14 +363,17 @@ static size_t smem_generic(int B, int M, int kk) {
     return (size_t)B * M * KS * 4 + (size_t)B * (kk + NEWCAP) * 8 + 64;
 }
 static constexpr size_t SMEM_CAP = 227 * 1024;
+static constexpr int PACKED_MIN_CODES = 16384;  // codes per CTA below which fp32 pair tables win
 
 ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available) {
     ScanPlan p{};
     p.fast = (M == 4 || M == 8 || M == 16 || M == 32);
     p.B = 0;
     if (p.fast) {
+        // Packed tables cost a larger per-CTA table build: only for long code ranges.
+        const bool pk = packed_enabled() && tables_available && n_codes >= (int64_t)PACKED_MIN_CODES;
         for (int B : {8, 6, 4, 2}) {
-            if (B == 8 && (!packed_enabled() || !tables_available)) continue;
+            if (B == 8 && !pk) continue;
             if (smem_fast(B, kk) <= SMEM_CAP) { p.B = B; p.smem = smem_fast(B, kk); break; }
         }
     } else {
@@ -452,9 +455,9 @@ static void launch_generic_t(const ScanPlan &pl, const uint8_t *codes, int64_t n
 
 bool list_major_supported(int M) { return M == 4 || M == 8 || M == 16 || M == 32; }
 
-int list_major_B(int kk) {
+int list_major_B(int kk, double avg_len) {
     for (int B : {8, 6, 4, 2}) {
-        if (B == 8 && !packed_enabled()) continue;
+        if (B == 8 && (!packed_enabled() || avg_len < (double)PACKED_MIN_CODES)) continue;
         if (smem_fast(B, kk) <= SMEM_CAP) return B;
     }
     return 0;
@@ -473,22 +476,21 @@ static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st) {
 }
 
 template <int M>
-static void launch_list_m(const ScanArgs &a, int64_t n_items, cudaStream_t st) {
-    const int B = list_major_B(a.kk);
+static void launch_list_m(int B, const ScanArgs &a, int64_t n_items, cudaStream_t st) {
     if (B == 8) launch_list_t<M, 8>(a, n_items, st);
     else if (B == 6) launch_list_t<M, 6>(a, n_items, st);
     else if (B == 4) launch_list_t<M, 4>(a, n_items, st);
     else launch_list_t<M, 2>(a, n_items, st);
 }
 
-void launch_list_scan(int M, const ScanArgs &a, int64_t n_items, cudaStream_t st) {
+void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStream_t st) {
     if (n_items <= 0) return;
-    if (list_major_B(a.kk) == 0) throw Error(1, "topk too large for the list-major scan");
+    if (B == 0) throw Error(1, "topk too large for the list-major scan");
     switch (M) {
-        case 4: launch_list_m<4>(a, n_items, st); break;
-        case 8: launch_list_m<8>(a, n_items, st); break;
-        case 16: launch_list_m<16>(a, n_items, st); break;
-        default: launch_list_m<32>(a, n_items, st); break;
+        case 4: launch_list_m<4>(B, a, n_items, st); break;
+        case 8: launch_list_m<8>(B, a, n_items, st); break;
+        case 16: launch_list_m<16>(B, a, n_items, st); break;
+        default: launch_list_m<32>(B, a, n_items, st); break;
     }
 }
 

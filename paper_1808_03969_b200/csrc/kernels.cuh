@@ -42,8 +42,8 @@ struct ScanArgs {
 
 // List-major inverted-index scan: B queries per CTA share one posting list's codes.
 bool list_major_supported(int M);
-int list_major_B(int kk);
-void launch_list_scan(int M, const ScanArgs &a, int64_t n_items, cudaStream_t st);
+int list_major_B(int kk, double avg_len);
+void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStream_t st);
 // Work items of the list-major scan: for every list k, ceil(#queries probing k / B)
 // items {k, first entry of qlist, count, 0}.  qoff = CSR of qlist by list.
 // Returns the number of items (synchronises the stream).

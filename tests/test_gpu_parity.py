@@ -95,10 +95,11 @@ def test_paths_match_oracle(rii, ref, kind, N, D, M, K, nq, topk):
 
 @pytest.mark.parametrize("mode", ["list", "query"])
 @pytest.mark.parametrize("kind,N,D,M,K", [("deep", 30_011, 96, 32, 20), ("sift", 25_000, 128, 16, 16),
-                                          ("deep", 20_003, 96, 8, 12)])
+                                          ("deep", 20_003, 96, 8, 12), ("deep", 40_000, 96, 32, 2)])
 def test_ivf_list_major_and_query_major(rii, ref, monkeypatch, mode, kind, N, D, M, K):
     """Both posting-list traversals (list-major: B queries share a list; query-major:
-    one table per query) against the oracle's Alg. 2, whole and subset."""
+    one table per query) against the oracle's Alg. 2, whole and subset.  K = 2 makes
+    the lists long enough for the bf16-packed list-major kernel."""
     monkeypatch.setenv("RII_IVF_MODE", mode)
     x = gen.base(kind, N, D, seed=N)
     q = gen.base(kind, 41, D, seed=N, stream=gen.STREAM_QUERY)

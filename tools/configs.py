@@ -133,6 +133,47 @@ def main():
         for L in c["L"]:
             ms = timed(lambda: g.query(q, c["topk"], None, L=L, path="ivf"), a.reps)
             emit(config="growth", row=f"after reconfigure ivf L={L}", K=K2, ms=ms, qps=c["nq"] / ms * 1e3)
+    if "scale1b" in only:  # configs[4] on ONE B200 (8 GB of codes fit): 1e9 x 96 unit-norm mixture, M=8
+        c = gen.CONFIGS["scale1b"]
+        N, D, M, K = c["N"], c["D"], c["M"], c["nlist"]
+        g = rii.Index(D, M, device=0)
+        t0 = time.perf_counter()
+        g.train(bench._device_data("deep", c["n_train"], D, DEV, 0, gen.STREAM_TRAIN), n_iter=20, seed=0)
+        torch.cuda.synchronize()
+        emit(config="scale1b", row="train", n=c["n_train"], train_s=time.perf_counter() - t0)
+        chunk = 1 << 24
+        t0 = time.perf_counter()
+        for s0 in range(0, N, chunk):  # streamed: the raw vectors are never stored
+            xb = gen.deep_like_torch(min(chunk, N - s0), DEV, D=D, seed=1000 + s0 // chunk, stream=gen.STREAM_BASE)
+            g.add(xb)
+            del xb
+        torch.cuda.synchronize()
+        emit(config="scale1b", row="add (generate + encode, streamed)", N=g.info()["N"], add_s=time.perf_counter() - t0)
+        torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        g.reconfigure(K, n_iter=10, seed=0)
+        torch.cuda.synchronize()
+        emit(config="scale1b", row="reconfigure", nlist=K, reconfigure_s=time.perf_counter() - t0,
+             bytes=g.info()["bytes"])
+        qb = c["q_batch"]
+        q = gen.deep_like_torch(c["nq"], DEV, D=D, seed=0, stream=gen.STREAM_QUERY)
+        ms = timed(lambda: [g.query(q[i:i + qb], c["topk"], None, L=64, path="ivf") for i in range(0, c["nq"], qb)],
+                   a.reps)
+        emit(config="scale1b", row="ivf whole L=64 (batches of 1024)", ms=ms, qps=c["nq"] / ms * 1e3)
+        S = gen.subset_torch(N, 1_000_000, DEV, seed=1)
+        for path in ("auto", "linear", "ivf"):
+            used = {}
+
+            def f():
+                for i in range(0, c["nq"], qb):
+                    used["p"] = g.query(q[i:i + qb], c["topk"], S, L=64, path=path)[2]
+            ms = timed(f, a.reps)
+            emit(config="scale1b", row=f"subset |S|=1e6 L=64 {path}", path_used=["auto", "linear", "ivf"][used["p"]],
+                 ms=ms, qps=c["nq"] / ms * 1e3)
+        q1 = q[:qb]
+        ms = timed(lambda: g.query(q1, c["topk"], None, L=1, path="linear"), 1)
+        emit(config="scale1b", row="linear whole (1024 queries)", ms=ms, qps=qb / ms * 1e3,
+             scanned_codes_per_s=qb * N / ms * 1e3)
     if "deep10m" in only:
         kind, N, D, M, nlist, nq, topk, n_train, _ = bench.WORKLOADS["deep10m"]
         g, b = build(kind, N, D, M, nlist, n_train)

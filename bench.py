@@ -232,6 +232,9 @@ def run_ours(args, rank, world, local):
     rii_lib.rii_kernel_timing_read(0, C.byref(kms), C.byref(kn))
     mms, mn = C.c_double(), C.c_int64()
     rii_lib.rii_kernel_timing_read(2, C.byref(mms), C.byref(mn))
+    pms, pn = C.c_double(), C.c_int64()
+    rii_lib.rii_kernel_timing_read(3, C.byref(pms), C.byref(pn))
+    packed = pn.value > 0 and pn.value == kn.value
     rii_lib.rii_kernel_timing(0)
     torch.cuda.synchronize()
     _barrier(world)
@@ -243,7 +246,10 @@ def run_ours(args, rank, world, local):
 
     peaks, peak_src = _peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    lut_peak = SMS * LUT_LOOKUPS_PER_CLK_PER_SM * sm_max * 1e6  # lookups/s
+    # one 128-B shared-memory wavefront per clock per SM: 32 fp32 lookups, or 64
+    # lookups with the bf16-packed tables (2 B per lookup)
+    per_clk = LUT_LOOKUPS_PER_CLK_PER_SM * (2 if packed else 1)
+    lut_peak = SMS * per_clk * sm_max * 1e6  # lookups/s
     lookups = nq * n_local * M
     achieved = lookups / (kernel_ms / 1e3)
     traffic = None
@@ -252,10 +258,13 @@ def run_ours(args, rank, world, local):
         with open(tp) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
     roofline = {
-        "bound": "alu", "kernel": "scan_fast_kernel<32,6> (linear ADC scan + top-k)",
+        "bound": "alu",
+        "kernel": ("scan_fast_kernel<32,8,packed> (linear ADC scan + top-k, bf16-packed tables + exact rescore)"
+                   if packed else "scan_fast_kernel<32,6> (linear ADC scan + top-k, fp32 tables)"),
         "achieved": achieved / 1e9, "peak": lut_peak / 1e9, "unit": "Glookup/s",
         "frac": achieved / lut_peak, "traffic": traffic,
-        "peak_basis": f"shared-memory LUT pipe: {LUT_LOOKUPS_PER_CLK_PER_SM} fp32 lookups/clk/SM x {SMS} SMs x "
+        "peak_basis": f"shared-memory LUT pipe: one 128-B wavefront/clk/SM = {per_clk} "
+                      f"{'bf16-packed (2 B)' if packed else 'fp32 (4 B)'} lookups/clk/SM x {SMS} SMs x "
                       f"{sm_max:.0f} MHz (sm_max_mhz, {peak_src})",
         "algorithmic_units": f"{nq} queries x {n_local} codes x {M} lookups per launch",
         "kernel_ms_per_launch": kernel_ms, "kernel_share_of_step": kernel_ms / (total_ms / args.steps),

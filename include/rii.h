@@ -70,7 +70,8 @@ uint64_t rii_launch_count(void);
  * kernel is launched on (used by bench.py for the roofline's "achieved").
  * rii_kernel_timing(1) clears the totals and starts recording; (0) stops.
  * which: 0 = linear ADC scan kernel, 1 = inverted-index list-scan kernel,
- * 2 = top-k merge kernel.  total_ms / launches cover every launch since the
+ * 2 = top-k merge kernel, 3 = the linear-scan launches that used the
+ * bf16-packed tables (a subset of 0).  total_ms / launches cover every launch since the
  * last clear (read synchronises with the recorded events). */
 void rii_kernel_timing(int32_t enable);
 rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *launches);
@@ -188,6 +189,18 @@ rii_status rii_get_postings(const rii_index *idx, int64_t *offsets, int64_t *ids
 rii_status rii_calibrate_theta(rii_index *idx, const float *q, int64_t nq, int32_t topk, const int32_t *L_grid,
                                int32_t n_L, rii_mem where, void *stream, double *a_out, double *b_out,
                                double *crossovers);
+
+/* Meaning of L in the inverted index (reading R2).
+ *  RII_IVF_LISTS (default, mode A): L = the number of nearest coarse lists; every
+ *    member of S in them is evaluated (BASELINE.json's "posting lists of the L
+ *    nearest coarse centres").
+ *  RII_IVF_PAPER (mode B, Alg. 2 exactly as printed): L = the number of
+ *    candidates; the ceil(K*L/|S|) (<= K) nearest lists by (d0, k) are traversed
+ *    in that order, ids ascending in each list, non-members of S skipped, and the
+ *    traversal stops once L candidates were evaluated.  AUTO's default threshold
+ *    becomes theta(L) = L + K.  Single-GPU only (world > 1 -> RII_ERR_STATE at query). */
+typedef enum { RII_IVF_LISTS = 0, RII_IVF_PAPER = 1 } rii_ivf_mode;
+rii_status rii_set_ivf_mode(rii_index *idx, int32_t mode);
 
 /* theta of Alg. 3 (reading R3).  theta < 0 restores the default
  * theta(L) = ceil(L*N/K) + K evaluated at each call's L. */

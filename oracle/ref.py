@@ -56,6 +56,8 @@ def lib():
             "rref_num_probe": (i64, [i64, i64, i64, C.c_int, i64]),
             "rref_ivf": (C.c_int, [p, C.c_int, C.c_int, C.c_int, p, i64, p, i64, p, p, p, i64, C.c_int,
                                    p, i64, i64, p, p]),
+            "rref_ivf_paper": (C.c_int, [p, C.c_int, C.c_int, C.c_int, p, i64, p, i64, p, p, p, i64, C.c_int,
+                                         p, i64, i64, p, p]),
             "rref_default_theta": (i64, [i64, i64, i64]),
             "rref_query": (C.c_int, [p, C.c_int, C.c_int, C.c_int, p, i64, p, i64, p, p, p, i64, C.c_int,
                                      p, i64, i64, i64, C.c_int, p, p, p]),
@@ -195,6 +197,21 @@ def ivf(cb, codes, centers, offsets, ids_csr, q, topk, L, S=None, Z=Z_DEFAULT):
     dist = np.empty((nq, topk), np.float32)
     _chk(lib().rref_ivf(_p(cb), D, M, Z, _p(codes), N, _p(centers), K, _p(offsets), _p(ids_csr), _p(q), nq,
                         topk, _p(S), nS, L, _p(ids), _p(dist)), "ivf")
+    return ids, dist
+
+
+def ivf_paper(cb, codes, centers, offsets, ids_csr, q, topk, L, S=None, Z=Z_DEFAULT):
+    """Alg. 2 as printed: L = candidate budget with the early stop (R2 mode B)."""
+    cb, codes, q = _c(cb, np.float32), _c(codes, np.uint8), _c(q, np.float32)
+    centers, offsets, ids_csr = _c(centers, np.uint8), _c(offsets, np.int64), _c(ids_csr, np.int64)
+    N, M = codes.shape
+    K = centers.shape[0]
+    nq, D = q.shape
+    S, nS = _targets(S)
+    ids = np.empty((nq, topk), np.int64)
+    dist = np.empty((nq, topk), np.float32)
+    _chk(lib().rref_ivf_paper(_p(cb), D, M, Z, _p(codes), N, _p(centers), K, _p(offsets), _p(ids_csr), _p(q), nq,
+                              topk, _p(S), nS, L, _p(ids), _p(dist)), "ivf_paper")
     return ids, dist
 
 

@@ -277,6 +277,50 @@ int rref_ivf(const float *cb, int D, int M, int Z, const uint8_t *codes, int64_t
     return REF_OK;
 }
 
+/* Alg. 2 InvertedIndex exactly as printed (reading R2 mode B, "paper"):
+ * L is the number of candidates.  The ceil(K L / |S|) (capped at K, P:492-502;
+ * |S| = N for S = ALL) nearest lists by (d0, k) are traversed in that order, ids
+ * ascending inside a list (R11), non-members of S skipped (L10-11), and the
+ * traversal returns as soon as |U| = L (L14-16); if the lists run out first, what
+ * was collected is returned. */
+int rref_ivf_paper(const float *cb, int D, int M, int Z, const uint8_t *codes, int64_t N,
+                   const uint8_t *centers, int64_t K, const int64_t *offsets, const int64_t *ids,
+                   const float *q, int64_t nq, int topk, const int64_t *S, int64_t nS, int64_t L,
+                   int64_t *out_ids, float *out_dist) {
+    if (topk < 1 || K < 1 || L < 1) return REF_ERR_ARG;
+    if (S && check_targets(S, nS, N) != REF_OK) return REF_ERR_ARG;
+    float *A = (float *)malloc(sizeof(float) * M * Z);
+    dk_t *T = (dk_t *)malloc(sizeof(dk_t) * K);
+    topr_t t = {topk, 0, (float *)malloc(sizeof(float) * topk), (int64_t *)malloc(sizeof(int64_t) * topk)};
+    if (!A || !T || !t.d || !t.id) { free(A); free(T); free(t.d); free(t.id); return REF_ERR_OOM; }
+    int64_t ns = S ? nS : N;
+    int64_t P = ns > 0 ? (K * L + ns - 1) / ns : K;
+    if (P > K) P = K;
+    for (int64_t qi = 0; qi < nq; ++qi) {
+        rref_lut(cb, D, M, Z, q + qi * D, A);                         /* L1 */
+        for (int64_t k = 0; k < K; ++k) {                             /* L3-L5 */
+            T[k].d = rref_adc(A, M, Z, centers + k * M);
+            T[k].k = k;
+        }
+        qsort(T, (size_t)K, sizeof(dk_t), dk_cmp);                    /* L6 */
+        t.count = 0;                                                  /* L7 */
+        int64_t got = 0;
+        for (int64_t r = 0; r < P && got < L; ++r) {                  /* L8 */
+            int64_t k = T[r].k;
+            for (int64_t p = offsets[k]; p < offsets[k + 1] && got < L; ++p) {  /* L9 */
+                int64_t n = ids[p];
+                if (S && !is_member(S, nS, n)) continue;              /* L10-L11 */
+                float d = rref_adc(A, M, Z, codes + n * M);           /* L12 */
+                topr_push(&t, d, n);                                  /* L13 */
+                ++got;                                                /* L14: stop at |U| = L */
+            }
+        }
+        topr_take(&t, out_ids + qi * topk, out_dist + qi * topk);     /* L15-L16 */
+    }
+    free(A); free(T); free(t.d); free(t.id);
+    return REF_OK;
+}
+
 /* Default threshold (reading R3): theta(L) = ceil(L*N/K) + K. */
 int64_t rref_default_theta(int64_t N, int64_t K, int64_t L) {
     if (K <= 0) return INT64_MAX;

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "librii_b200.so")
 
 RII_OK, RII_ERR_ARG, RII_ERR_STATE, RII_ERR_OOM, RII_ERR_CUDA, RII_ERR_NCCL, RII_ERR_TRAIN = range(7)
 PATH_AUTO, PATH_LINEAR, PATH_IVF = 0, 1, 2
+IVF_LISTS, IVF_PAPER = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
 NCCL_ID_BYTES = 128
 
@@ -41,6 +42,7 @@ SIGNATURES = {
     "rii_get_centers": (C.c_int, [_p, _p]),
     "rii_get_postings": (C.c_int, [_p, _p, _p]),
     "rii_set_theta": (C.c_int, [_p, _i64]),
+    "rii_set_ivf_mode": (C.c_int, [_p, _i32]),
     "rii_calibrate_theta": (C.c_int, [_p, _p, _i64, _i32, _p, _i32, C.c_int, _p, C.POINTER(C.c_double),
                                       C.POINTER(C.c_double), _p]),
     "rii_get_info": (C.c_int, [_p, C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_i64),

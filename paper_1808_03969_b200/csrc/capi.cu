@@ -27,8 +27,8 @@ std::mutex g_tmu;
 bool g_timing = false;
 struct TimedPair { int which; cudaEvent_t a, b; };
 std::vector<TimedPair> g_pairs;
-double g_total_ms[TK_COUNT] = {0, 0, 0};
-int64_t g_count[TK_COUNT] = {0, 0, 0};
+double g_total_ms[TK_COUNT] = {0, 0, 0, 0};
+int64_t g_count[TK_COUNT] = {0, 0, 0, 0};
 
 void drain_pairs() {  // caller holds g_tmu
     for (auto &p : g_pairs) {
@@ -47,7 +47,7 @@ using namespace timing;
 
 KernelTimer::KernelTimer(int w, cudaStream_t s) : st(s), which(w) {
     std::lock_guard<std::mutex> lk(g_tmu);
-    if (!g_timing) return;
+    if (!g_timing || w < 0) return;
     if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) { a = b = nullptr; return; }
     cudaEventRecord(a, st);
 }
@@ -118,11 +118,12 @@ struct rii_index {
     int64_t K = 0;
     Buf centers, offsets, ids;
     int64_t theta = -1;
+    int ivf_mode = 0;        // RII_IVF_LISTS / RII_IVF_PAPER
     bool theta_fit = false;  // rii_calibrate_theta result in use (theta(L) = fit_a * L + fit_b)
     double fit_a = 0.0, fit_b = 0.0;
     // scratch (query side is const-callable: mutable)
     mutable Buf s_q, s_S, s_pos, s_sub, s_part, s_keys, s_gather, s_d0, s_probe, s_roff, s_rids, s_rkey, s_rval,
-        s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_items, s_gthr, s_tables, s_cpart, s_ckeys;
+        s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_items, s_gthr, s_tables, s_cpart, s_ckeys, s_take;
 };
 
 namespace {
@@ -280,7 +281,9 @@ int resolve_path(const rii_index *x, int64_t nS_global, bool has_S, int L, rii_p
     }
     if (path != RII_PATH_AUTO) return path;
     const int64_t ns = has_S ? nS_global : x->N;
-    int64_t th = x->theta >= 0 ? x->theta : ceil_div((int64_t)L * x->N, x->K) + x->K;  // R3
+    int64_t th = x->theta >= 0 ? x->theta
+                 : x->ivf_mode == RII_IVF_PAPER ? (int64_t)L + x->K          // L candidates + K coarse
+                                                : ceil_div((int64_t)L * x->N, x->K) + x->K;  // R3
     if (x->theta < 0 && x->theta_fit) th = (int64_t)std::max(0.0, std::ceil(x->fit_a * L + x->fit_b));
     return ns < th ? RII_PATH_LINEAR : RII_PATH_IVF;  // Alg. 3 L1
 }
@@ -379,7 +382,21 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             p_stride = kk;
             nparts = pl.nc;
         }
-    } else {  // Alg. 2
+    } else if (x->ivf_mode == RII_IVF_PAPER) {  // Alg. 2 exactly as printed (mode B)
+        const int64_t ns = a.S ? std::max<int64_t>(a.nS, 1) : x->N;
+        const int64_t P = std::min<int64_t>(x->K, ceil_div(x->K * (int64_t)a.L, ns));  // ceil(KL/|S|)
+        int32_t *probes = x->s_probe.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
+        float *d0 = x->s_d0.get<float>((size_t)a.nq * x->K);
+        launch_coarse_dist(x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, d0, st);  // L2-L5
+        launch_sorted_probes(d0, a.nq, x->K, P, probes, st);                                     // L6
+        const int64_t *off = a.S ? t.roff : x->offsets.as<int64_t>();
+        const uint32_t *ids = a.S ? t.rids : x->ids.as<uint32_t>();
+        int32_t *take = x->s_take.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
+        launch_paper_takes(probes, a.nq, P, off, a.L, take, st);                                  // L14 cut
+        uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
+        launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st, tables, take);
+        parts = pp;
+    } else {  // Alg. 2, mode A (reading R2)
         const int64_t P = a.S ? std::min<int64_t>(x->K, ceil_div((int64_t)a.L * x->N, std::max<int64_t>(a.nS, 1)))
                               : std::min<int64_t>(a.L, x->K);  // P:492-502, R1
         int32_t *probes = x->s_probe.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
@@ -512,7 +529,7 @@ void rii_kernel_timing(int32_t enable) {
 
 rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *launches) {
     return guarded([&] {
-        arg_check(which >= 0 && which < TK_COUNT, "which must be 0, 1 or 2");
+        arg_check(which >= 0 && which < TK_COUNT, "which must be 0, 1, 2 or 3");
         std::lock_guard<std::mutex> lk(g_tmu);
         drain_pairs();
         if (total_ms) *total_ms = g_total_ms[which];
@@ -755,6 +772,8 @@ static rii_status query_impl(const rii_index *x, const float *q, int64_t nq, int
         DeviceGuard g(x->device);
         cudaStream_t st = (cudaStream_t)stream;
         const int used = resolve_path(x, nS, S != nullptr, L, path);
+        state_check(!(used == RII_PATH_IVF && x->ivf_mode == RII_IVF_PAPER && x->world > 1),
+                    "RII_IVF_PAPER (global early stop) is single-GPU only");
         if (path_used) *path_used = used;
         if (nq == 0) return;
         arg_check(q && (out_keys || (out_ids && out_dist)), "NULL argument");
@@ -869,6 +888,15 @@ rii_status rii_get_postings(const rii_index *x, int64_t *offsets, int64_t *ids) 
             RII_LAUNCHED();
             RII_CUDA(cudaMemcpy(ids, d, (size_t)x->n_local * 8, cudaMemcpyDeviceToHost));
         }
+    });
+}
+
+rii_status rii_set_ivf_mode(rii_index *x, int32_t mode) {
+    return guarded([&] {
+        arg_check(x != nullptr, "index is NULL");
+        arg_check(mode == RII_IVF_LISTS || mode == RII_IVF_PAPER, "mode must be RII_IVF_LISTS or RII_IVF_PAPER");
+        x->ivf_mode = mode;
+        x->theta_fit = false;
     });
 }
 

@@ -150,6 +150,73 @@ void launch_select_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int
     RII_LAUNCHED();
 }
 
+// --------------------------------------------------- paper mode (Alg. 2) ----
+__global__ void seg_offsets_kernel(int64_t *off, int64_t nseg, int64_t len) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i <= nseg) off[i] = i * len;
+}
+
+__global__ void seg_iota_kernel(int32_t *v, int64_t n, int64_t len) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = (int32_t)(i % len);
+}
+
+__global__ void seg_head_kernel(const int32_t *sorted, int64_t nq, int64_t K, int64_t P, int32_t *probes) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nq * P) return;
+    const int64_t q = e / P, r = e - q * P;
+    probes[e] = sorted[q * K + r];
+}
+
+void launch_sorted_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int32_t *probes, cudaStream_t st) {
+    if (nq <= 0 || P <= 0) return;
+    const int64_t n = nq * K;
+    uint32_t *kout = nullptr;
+    int32_t *vin = nullptr, *vout = nullptr;
+    int64_t *off = nullptr;
+    RII_CUDA(cudaMallocAsync(&kout, (size_t)n * 4, st));
+    RII_CUDA(cudaMallocAsync(&vin, (size_t)n * 4, st));
+    RII_CUDA(cudaMallocAsync(&vout, (size_t)n * 4, st));
+    RII_CUDA(cudaMallocAsync(&off, (size_t)(nq + 1) * 8, st));
+    seg_offsets_kernel<<<(unsigned)ceil_div(nq + 1, 256), 256, 0, st>>>(off, nq, K);
+    RII_LAUNCHED();
+    seg_iota_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(vin, n, K);
+    RII_LAUNCHED();
+    const uint32_t *kin = reinterpret_cast<const uint32_t *>(d0);  // d0 >= +0: bit order == value order
+    size_t tb = 0;
+    RII_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, nq, off, off + 1, 0, 32,
+                                                      st));
+    void *tmp = nullptr;
+    RII_CUDA(cudaMallocAsync(&tmp, tb, st));
+    RII_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, n, nq, off, off + 1, 0, 32,
+                                                      st));  // stable: ties keep ascending k (CA4)
+    count_launch(4);
+    seg_head_kernel<<<(unsigned)ceil_div(nq * P, 256), 256, 0, st>>>(vout, nq, K, P, probes);
+    RII_LAUNCHED();
+    for (void *pp : {(void *)tmp, (void *)kout, (void *)vin, (void *)vout, (void *)off}) RII_CUDA(cudaFreeAsync(pp, st));
+}
+
+__global__ void paper_takes_kernel(const int32_t *__restrict__ probes, int64_t nq, int64_t P,
+                                   const int64_t *__restrict__ offsets, int64_t L, int32_t *__restrict__ take) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    int64_t acc = 0;
+    for (int64_t r = 0; r < P; ++r) {  // L8-L9 in rank order, stop at |U| = L (L14)
+        const int32_t k = probes[q * P + r];
+        const int64_t len = offsets[k + 1] - offsets[k];
+        const int64_t t = acc >= L ? 0 : (len < L - acc ? len : L - acc);
+        take[q * P + r] = (int32_t)t;
+        acc += t;
+    }
+}
+
+void launch_paper_takes(const int32_t *probes, int64_t nq, int64_t P, const int64_t *offsets, int64_t L,
+                        int32_t *take, cudaStream_t st) {
+    if (nq <= 0 || P <= 0) return;
+    paper_takes_kernel<<<(unsigned)ceil_div(nq, 128), 128, 0, st>>>(probes, nq, P, offsets, L, take);
+    RII_LAUNCHED();
+}
+
 // ------------------------------------------------------ list-major items ----
 __global__ void list_item_count_kernel(const int64_t *__restrict__ qoff, int64_t K, int B, int64_t *__restrict__ n) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -277,7 +344,8 @@ struct ListCursor {
 };
 
 __device__ __forceinline__ void next_list(ListCursor &c, int *s_next, int64_t P, int64_t q0, int64_t nq,
-                                          const int32_t *probes, const int64_t *offsets, int lane) {
+                                          const int32_t *probes, const int64_t *offsets, const int32_t *take,
+                                          int lane) {
     while (!c.done && c.beg >= c.end) {
         int it = 0;
         if (lane == 0) it = atomicAdd(s_next, 1);
@@ -289,7 +357,7 @@ __device__ __forceinline__ void next_list(ListCursor &c, int *s_next, int64_t P,
         const int32_t k = probes[qi * P + r];
         c.qq = qq;
         c.beg = offsets[k];
-        c.end = offsets[k + 1];
+        c.end = take ? c.beg + take[qi * P + r] : offsets[k + 1];
     }
 }
 
@@ -299,7 +367,8 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
                                                       int kk, const int32_t *__restrict__ probes, int64_t P,
                                                       const int64_t *__restrict__ offsets,
                                                       const uint32_t *__restrict__ ids, uint64_t *__restrict__ out,
-                                                      const float *__restrict__ tables) {
+                                                      const float *__restrict__ tables,
+                                                      const int32_t *__restrict__ take) {
     constexpr int W = FAST ? M / 4 : 1;
     const int MM = FAST ? M : Mrt;
     extern __shared__ __align__(16) uint8_t smem[];
@@ -343,7 +412,7 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
     bool need = false;
     ListCursor cur{0, 0, 0, false};
     while (true) {
-        next_list(cur, s_next, P, q0, nq, probes, offsets, lane);
+        next_list(cur, s_next, P, q0, nq, probes, offsets, take, lane);
         if (!__syncthreads_or(!cur.done)) break;
         if (!cur.done) {
             const int64_t p = cur.beg + lane;
@@ -410,28 +479,28 @@ size_t ivf_smem(int M, int kk) {
 template <int M, bool FAST>
 static void ivf_launch_t(const uint8_t *codes, int Mrt, const float *q, int64_t nq, const float *cb, int ds, int kk,
                          const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
-                         cudaStream_t st, const float *tables) {
+                         cudaStream_t st, const float *tables, const int32_t *take) {
     const size_t smem = ivf_smem(Mrt, kk);
     auto kern = ivf_scan_kernel<M, FAST>;
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     KernelTimer t(TK_IVF, st);
     kern<<<(unsigned)ceil_div(nq, 2), NT, smem, st>>>(codes, q, nq, cb, Mrt, ds, kk, probes, P, offsets, ids, out,
-                                                      FAST ? tables : nullptr);
+                                                      FAST ? tables : nullptr, take);
     RII_LAUNCHED();
 }
 
 void launch_ivf_scan(const uint8_t *codes, int M, const float *q, int64_t nq, const float *cb, int D, int kk,
                      const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
-                     cudaStream_t st, const float *tables) {
+                     cudaStream_t st, const float *tables, const int32_t *take) {
     if (nq <= 0) return;
     if (ivf_smem(M, kk) > 227 * 1024) throw Error(1, "topk too large for the inverted-index kernel");
     const int ds = D / M;
     switch (M) {
-        case 4: ivf_launch_t<4, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables); break;
-        case 8: ivf_launch_t<8, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables); break;
-        case 16: ivf_launch_t<16, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables); break;
-        case 32: ivf_launch_t<32, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables); break;
-        default: ivf_launch_t<1, false>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables); break;
+        case 4: ivf_launch_t<4, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take); break;
+        case 8: ivf_launch_t<8, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take); break;
+        case 16: ivf_launch_t<16, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take); break;
+        case 32: ivf_launch_t<32, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take); break;
+        default: ivf_launch_t<1, false>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take); break;
     }
 }
 

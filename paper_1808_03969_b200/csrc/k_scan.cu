@@ -429,8 +429,8 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
     a.codes = codes; a.n_codes = n; a.q = q; a.nq = nq; a.cb = cb; a.ds = ds; a.kk = kk;
     a.nb = pl.nb; a.chunk = pl.chunk; a.nc = pl.nc; a.out = out; a.tables = tables;
     void *args[] = {&a};
-    KernelTimer t(TK_LINEAR, st);
-    RII_CUDA(cudaLaunchKernel(kern, dim3(pl.nb * pl.nc), dim3(scan_threads()), args, pl.smem, st));
+    KernelTimer t(TK_LINEAR, st), tp(B == 8 ? TK_PACKED : -1, st);
+    RII_CUDA(cudaLaunchKernel(kern, dim3(pl.nb * pl.nc), dim3(B == 8 ? 512 : scan_threads()), args, pl.smem, st));
     count_launch();
 }
 
@@ -471,7 +471,7 @@ static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st) {
     ScanArgs aa = a;
     void *args[] = {&aa};
     KernelTimer t(TK_IVF, st);
-    RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)n_items), dim3(scan_threads()), args, smem, st));
+    RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)n_items), dim3(B == 8 ? 512 : scan_threads()), args, smem, st));
     count_launch();
 }
 

@@ -88,11 +88,17 @@ void launch_coarse_dist(const uint8_t *centers, int64_t K, int M, const float *q
 void launch_select_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int32_t *probes, cudaStream_t st);
 // probes[q][r] = id of the r-th key of the sorted per-query keys [nq][kk] (r < P).
 void launch_keys_to_probes(const uint64_t *keys, int64_t nq, int kk, int64_t P, int32_t *probes, cudaStream_t st);
+// probes[q][0..P) = the P nearest lists in (d0, k) order (CUB segmented sort of d0).
+void launch_sorted_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int32_t *probes, cudaStream_t st);
+// Alg. 2 early stop (mode B): take[q][r] = members of list probes[q][r] evaluated
+// before the budget L runs out (ranks in order).
+void launch_paper_takes(const int32_t *probes, int64_t nq, int64_t P, const int64_t *offsets, int64_t L,
+                        int32_t *take, cudaStream_t st);
 // Posting-list traversal (Alg. 2 L7-L16, mode A): out[nq][kk] keys, ids = local positions.
 size_t ivf_smem(int M, int kk);
 void launch_ivf_scan(const uint8_t *codes, int M, const float *q, int64_t nq, const float *cb, int D, int kk,
                      const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
-                     cudaStream_t st, const float *tables = nullptr);
+                     cudaStream_t st, const float *tables = nullptr, const int32_t *take = nullptr);
 
 // ---- build side (k_build.cu) -------------------------------------------------
 void launch_encode(const float *x, int64_t n, int D, int M, const float *cb, uint8_t *codes, cudaStream_t st);

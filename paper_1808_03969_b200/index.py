@@ -228,6 +228,12 @@ class Index:
                                                 C.byref(a), C.byref(b), _ptr(cross)))
         return a.value, b.value, cross
 
+    def set_ivf_mode(self, mode):
+        """'lists' (L = nearest lists, every member evaluated; default) or 'paper'
+        (Alg. 2 as printed: L = candidate budget with the early stop)."""
+        m = {"lists": _rl.IVF_LISTS, "paper": _rl.IVF_PAPER}.get(mode, mode)
+        _rl.check(self._lib.rii_set_ivf_mode(self._h, int(m)))
+
     def set_theta(self, theta: int):
         _rl.check(self._lib.rii_set_theta(self._h, theta))
 

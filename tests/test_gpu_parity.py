@@ -280,3 +280,26 @@ def test_theta_calibration(rii, ref):
             assert g.query(q[:4], 10, target_ids=S, L=L)[2] == rii.PATH_IVF
     g.set_theta(-1)  # back to the analytic default (R3)
     assert g.query(q[:4], 10, L=1)[2] == rii.PATH_IVF
+
+
+@pytest.mark.parametrize("kind,N,D,M,K", [("deep", 20_011, 96, 32, 30), ("sift", 15_000, 128, 16, 40),
+                                          ("deep", 9_001, 96, 12, 10)])
+def test_ivf_paper_mode(rii, ref, kind, N, D, M, K):
+    """Alg. 2 as printed (RII_IVF_PAPER): L = candidate budget, ceil(KL/|S|) lists in
+    (d0, k) order, early stop at |U| = L -- against oracle rref_ivf_paper."""
+    x = gen.base(kind, N, D, seed=N + 1)
+    q = gen.base(kind, 23, D, seed=N + 1, stream=gen.STREAM_QUERY)
+    g, o = _build_pair(rii, ref, x, M, K, n_iter=3, train_rows=x[:3000], train_iter=3)
+    g.set_ivf_mode("paper")
+    for sub in (None, gen.subset(N, N // 4, seed=9), gen.subset(N, 150, seed=10)):
+        for L in (1, 50, 700, N):
+            gr = g.query(q, 50, target_ids=sub, L=L, path="ivf")
+            orr = ref.ivf_paper(o.cb, o.codes, o.centers, o.offsets, o.ids, q, 50, L, S=sub)
+            assert_topk_parity(ref, o.cb, o.codes, q, gr, orr, S=sub, what=f"paper {kind} L={L}")
+    # AUTO default threshold in paper mode: theta(L) = L + K
+    S = gen.subset(N, 200 + K - 1, seed=11)
+    assert g.query(q[:2], 5, target_ids=S, L=200)[2] == rii.PATH_LINEAR
+    S = gen.subset(N, 200 + K, seed=12)
+    assert g.query(q[:2], 5, target_ids=S, L=200)[2] == rii.PATH_IVF
+    g.set_ivf_mode("lists")
+    assert g.query(q[:2], 5, L=2)[2] == rii.PATH_IVF

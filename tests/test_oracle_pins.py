@@ -397,3 +397,37 @@ def test_train_rejects_too_few_rows(ref):
     with pytest.raises(ref.OracleError) as e:
         ref.train(np.zeros((10, 4), np.float32), M=2, n_iter=1, seed=0)
     assert e.value.status == 6
+
+
+# ------------------------------------------------------ paper-exact Alg. 2 ---
+def test_ivf_paper_budget_and_early_stop(ref):
+    """Alg. 2 as printed (P:543-576): L = candidates, ceil(KL/|S|) lists (P:492-502),
+    early stop at |U| = L.  Pinned by: (a) an unlimited budget over every list equals
+    the linear scan; (b) K = 1: the first L members of S in id order (R11),
+    ranked — i.e. the linear scan over exactly those ids; (c) the returned ids are
+    always within the traversal prefix."""
+    idx, _ = _small_index(ref, K=1)
+    q = gen.gaussian(8, idx.D, seed=41, stream=gen.STREAM_QUERY)
+    for S in (None, gen.subset(idx.N, 900, seed=42)):
+        members = np.arange(idx.N) if S is None else S
+        for L in (1, 37, 500):
+            pid, pd = ref.ivf_paper(idx.cb, idx.codes, idx.centers, idx.offsets, idx.ids, q, 20, L, S=S)
+            lid, ld = ref.linear(idx.cb, idx.codes, q, 20, S=members[:L])
+            assert np.array_equal(pid, lid) and np.array_equal(pd, ld)
+    idx, _ = _small_index(ref, K=25)
+    q = gen.gaussian(8, idx.D, seed=43, stream=gen.STREAM_QUERY)
+    pid, pd = ref.ivf_paper(idx.cb, idx.codes, idx.centers, idx.offsets, idx.ids, q, 30, L=idx.N)
+    lid, ld = ref.linear(idx.cb, idx.codes, q, 30)
+    assert np.array_equal(pid, lid) and np.array_equal(pd, ld)
+    # traversal prefix: ranks by fp64 reconstruction distance of the centres (skip near-ties)
+    rec = ref.decode(idx.cb, idx.centers, idx.D).astype(np.float64)
+    L = 150
+    P = -(-idx.K * L // idx.N)
+    pid, _ = ref.ivf_paper(idx.cb, idx.codes, idx.centers, idx.offsets, idx.ids, q, 30, L)
+    for i in range(len(q)):
+        d0 = ((rec - q[i].astype(np.float64)) ** 2).sum(1)
+        order = np.argsort(d0, kind="stable")
+        if np.min(np.diff(np.sort(d0))[: P + 1]) < 1e-6 * d0.max():
+            continue
+        prefix = np.concatenate([idx.ids[idx.offsets[k]:idx.offsets[k + 1]] for k in order[:P]])[:L]
+        assert np.isin(pid[i][pid[i] >= 0], prefix).all()

@@ -174,6 +174,12 @@ rii_status rii_get_codes(const rii_index *idx, int64_t first, int64_t n, uint8_t
 rii_status rii_get_centers(const rii_index *idx, uint8_t *out);
 rii_status rii_get_postings(const rii_index *idx, int64_t *offsets, int64_t *ids);
 
+/* Install K coarse centres (K x M PQ codes, host memory) instead of running
+ * rii_reconfigure -- e.g. to restore a saved index: every stored code is assigned
+ * to its SDC-nearest centre (ties to the lowest k) and the posting
+ * lists are rebuilt (Alg. 4 L2-L4).  1 <= K < 2^31; resets theta to the default. */
+rii_status rii_set_centers(rii_index *idx, const uint8_t *centers, int32_t K, void *stream);
+
 /* Threshold calibration (Alg. 3 / P:589-598: "we simply run the search with several
  * parameter combinations when the data structure is constructed ... fit a 1D line
  * in the parameter space"; the supplement with the details is missing, reading R3).

@@ -41,6 +41,7 @@ SIGNATURES = {
     "rii_get_codes": (C.c_int, [_p, _i64, _i64, _p]),
     "rii_get_centers": (C.c_int, [_p, _p]),
     "rii_get_postings": (C.c_int, [_p, _p, _p]),
+    "rii_set_centers": (C.c_int, [_p, _p, _i32, _p]),
     "rii_set_theta": (C.c_int, [_p, _i64]),
     "rii_set_ivf_mode": (C.c_int, [_p, _i32]),
     "rii_calibrate_theta": (C.c_int, [_p, _p, _i64, _i32, _p, _i32, C.c_int, _p, C.POINTER(C.c_double),

@@ -891,6 +891,26 @@ rii_status rii_get_postings(const rii_index *x, int64_t *offsets, int64_t *ids) 
     });
 }
 
+rii_status rii_set_centers(rii_index *x, const uint8_t *centers, int32_t K, void *stream) {
+    return guarded([&] {
+        arg_check(x && centers, "NULL argument");
+        arg_check(K >= 1, "K must be >= 1");
+        state_check(x->trained, "index has no code book");
+        DeviceGuard g(x->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        ensure_T(x, st);
+        uint8_t *cent = x->centers.get<uint8_t>((size_t)K * x->M);
+        RII_CUDA(cudaMemcpyAsync(cent, centers, (size_t)K * x->M, cudaMemcpyHostToDevice, st));
+        x->K = K;
+        int32_t *as = x->assign.get<int32_t>(x->n_local + 1);
+        launch_assign(x->codes.as<uint8_t>(), x->n_local, cent, x->K, x->M, x->T.as<float>(), as, nullptr, st);
+        rebuild_csr(x, st);
+        x->theta = -1;
+        x->theta_fit = false;
+        RII_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 rii_status rii_set_ivf_mode(rii_index *x, int32_t mode) {
     return guarded([&] {
         arg_check(x != nullptr, "index is NULL");

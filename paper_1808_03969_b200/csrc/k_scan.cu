@@ -15,6 +15,7 @@
 // selects the query.  The lane-dependent summation order is undone by a
 // canonical (CA2, m ascending) rescore of the kept candidates, so the returned
 // distances equal the oracle's bit for bit.
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -83,10 +84,16 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
 
     if constexpr (PACKED) {
 #pragma unroll
-        for (int p = 0; p < NQ; ++p)
-            load_lut_quad(reinterpret_cast<uint32_t *>(lut + p * QUAD_BYTES), a.tables + query_of(4 * p) * LUT_Q_FLOATS,
-                          a.tables + query_of(4 * p + 1) * LUT_Q_FLOATS, a.tables + query_of(4 * p + 2) * LUT_Q_FLOATS,
-                          a.tables + query_of(4 * p + 3) * LUT_Q_FLOATS);
+        for (int p = 0; p < NQ; ++p) {
+            uint32_t *dq = reinterpret_cast<uint32_t *>(lut + p * QUAD_BYTES);
+            if (a.sdcT)
+                load_lut_quad_sdc<M>(dq, a.sdcT, a.qcodes + query_of(4 * p) * M, a.qcodes + query_of(4 * p + 1) * M,
+                                     a.qcodes + query_of(4 * p + 2) * M, a.qcodes + query_of(4 * p + 3) * M);
+            else
+                load_lut_quad(dq, a.tables + query_of(4 * p) * LUT_Q_FLOATS, a.tables + query_of(4 * p + 1) * LUT_Q_FLOATS,
+                              a.tables + query_of(4 * p + 2) * LUT_Q_FLOATS,
+                              a.tables + query_of(4 * p + 3) * LUT_Q_FLOATS);
+        }
     } else {
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -125,8 +132,22 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     auto rescore_fresh = [&]() {
         if constexpr (PACKED) {
             for (int qq = 0; qq < B; ++qq) {
-                const float *tq = a.tables + query_of(qq) * LUT_Q_FLOATS;
                 const int n = cnt[qq];
+                if (a.sdcT) {  // d_S(x, c) = sum_m T_m[x^m][c^m] (CA2)
+                    const uint8_t *xq = a.qcodes + query_of(qq) * M;
+                    for (int i = tid; i < n; i += NTH) {
+                        uint64_t *f = fresh + qq * NEWCAP + i;
+                        const uint32_t id = key_id(*f);
+                        const uint8_t *cp = codes + (size_t)id * M;
+                        float d = 0.f;
+#pragma unroll
+                        for (int m = 0; m < M; ++m)
+                            d = __fadd_rn(d, __ldg(a.sdcT + ((size_t)m * KS + xq[m]) * KS + cp[m]));
+                        *f = make_key(d, id);
+                    }
+                    continue;
+                }
+                const float *tq = a.tables + query_of(qq) * LUT_Q_FLOATS;
                 for (int i = tid; i < n; i += NTH) {
                     uint64_t *f = fresh + qq * NEWCAP + i;
                     const uint32_t id = key_id(*f);
@@ -510,6 +531,57 @@ void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_code
         launch_generic_t<2>(pl, codes, n_codes, M, q, nq, cb, ds, kk, out, st);
     } else {
         launch_generic_t<1>(pl, codes, n_codes, M, q, nq, cb, ds, kk, out, st);
+    }
+}
+
+// ---------------------------------------------------- SDC-mode assignment ---
+bool assign_scan_supported(int M, int64_t K) {
+    return (M == 4 || M == 8 || M == 16 || M == 32) && packed_enabled() && K >= 8192 &&
+           smem_fast(8, 32) <= SMEM_CAP;
+}
+
+__global__ void top1_kernel(const uint64_t *__restrict__ keys, int64_t n, int kk, int32_t *__restrict__ assign,
+                            float *__restrict__ dist) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t k = keys[i * kk];
+    assign[i] = (int32_t)key_id(k);
+    if (dist) dist[i] = key_dist(k);
+}
+
+template <int M>
+static void assign_scan_m(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, const float *T,
+                          int32_t *assign, float *dist, cudaStream_t st) {
+    const int kk = 32, B = 8;
+    const size_t smem = smem_fast(B, kk);
+    void *kern = fast_kernel_ptr<M, B, false>();
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t CH = (int64_t)1 << 23;  // codes per launch: bounds the [chunk][kk] keys
+    uint64_t *keys = nullptr;
+    RII_CUDA(cudaMallocAsync(&keys, (size_t)std::min(n, CH) * kk * 8, st));
+    for (int64_t s0 = 0; s0 < n; s0 += CH) {
+        const int64_t cn = std::min(CH, n - s0);
+        ScanArgs a{};
+        a.codes = centers; a.n_codes = K; a.nq = cn; a.ds = 0; a.kk = kk; a.out = keys;
+        a.nb = (int)ceil_div(cn, B); a.chunk = K; a.nc = 1;
+        a.sdcT = T; a.qcodes = codes + s0 * M;
+        void *args[] = {&a};
+        RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)a.nb), dim3(512), args, smem, st));
+        count_launch();
+        top1_kernel<<<(unsigned)ceil_div(cn, 256), 256, 0, st>>>(keys, cn, kk, assign + s0, dist ? dist + s0 : nullptr);
+        RII_LAUNCHED();
+    }
+    RII_CUDA(cudaFreeAsync(keys, st));
+}
+
+void launch_assign_scan(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, int M, const float *T,
+                        int32_t *assign, float *dist, int, cudaStream_t st) {
+    if (n <= 0) return;
+    switch (M) {
+        case 4: assign_scan_m<4>(codes, n, centers, K, T, assign, dist, st); break;
+        case 8: assign_scan_m<8>(codes, n, centers, K, T, assign, dist, st); break;
+        case 16: assign_scan_m<16>(codes, n, centers, K, T, assign, dist, st); break;
+        default: assign_scan_m<32>(codes, n, centers, K, T, assign, dist, st); break;
     }
 }
 

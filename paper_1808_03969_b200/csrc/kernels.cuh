@@ -38,6 +38,10 @@ struct ScanArgs {
     const int64_t *offsets;  // lists: CSR of the posting lists
     const uint32_t *ids;
     float *gthr;             // lists: per-query upper bound on the global kk-th distance
+    // SDC mode (assignment): the "queries" are PQ codes qcodes[nq][M] whose
+    // tables are rows of the SDC tables T (T_m[x^m][.]); the scanned codes are centres.
+    const float *sdcT;
+    const uint8_t *qcodes;
 };
 
 // List-major inverted-index scan: B queries per CTA share one posting list's codes.
@@ -79,6 +83,13 @@ struct Rescore {
 void launch_merge(const uint64_t *keys, int64_t q_stride, int64_t p_stride, int parts, int64_t nq, int kk, int topk,
                   const IdMap &map, int64_t *out_ids, float *out_dist, uint64_t *out_keys, cudaStream_t st,
                   const Rescore &rs = Rescore());
+
+// a[i] = argmin_k d_S(codes[i], centers[k]) with the packed scan kernel in SDC mode
+// (exact: top-1 of an exactly rescored top-32).  For large K (the per-centre tables
+// of launch_assign would not stay in L2).
+bool assign_scan_supported(int M, int64_t K);
+void launch_assign_scan(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, int M, const float *T,
+                        int32_t *assign, float *dist, int num_sms, cudaStream_t st);
 
 // ---- inverted index (k_ivf.cu) -----------------------------------------------
 // d0[q][k] = CA2 ADC of query q to centre code k (Alg. 2 L2-L5).

@@ -146,6 +146,32 @@ __device__ __forceinline__ void load_lut_quad(uint32_t *dst, const float *__rest
     }
 }
 
+// SDC-mode quad: the table of a PQ code x is T_m[x^m][z] (column c = m = c mod M).
+template <int M>
+__device__ __forceinline__ void load_lut_quad_sdc(uint32_t *dst, const float *__restrict__ T,
+                                                  const uint8_t *__restrict__ xa, const uint8_t *__restrict__ xb,
+                                                  const uint8_t *__restrict__ xc, const uint8_t *__restrict__ xd) {
+    uint4 *o = reinterpret_cast<uint4 *>(dst);
+    auto hi = [](float v) { return __float_as_uint(v) & 0xffff0000u; };
+    auto lo = [](float v) { return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v)); };
+    auto val = [&](const uint8_t *x, int c, int z) {
+        const int m = c & (M - 1);
+        return __ldg(T + ((size_t)m * KS + __ldg(x + m)) * KS + z);
+    };
+    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 4; e += blockDim.x) {
+        const int z = e >> 3, c0 = (e & 7) * 4;
+        uint32_t w[8];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int c = c0 + t;
+            w[2 * t] = hi(val(xa, c, z)) | lo(val(xc, c, z));
+            w[2 * t + 1] = hi(val(xb, c, z)) | lo(val(xd, c, z));
+        }
+        o[2 * e] = make_uint4(w[0], w[1], w[2], w[3]);
+        o[2 * e + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+}
+
 // Approximate lane-rotated ADC of one pre-loaded code against NQ quad tables:
 // per step j one PRMT, per quad one LDS.64, two SHF and two FADD2 (4 lookups).
 template <int M, int NQ>

@@ -205,6 +205,12 @@ class Index:
         _rl.check(self._lib.rii_get_centers(self._h, _ptr(out)))
         return out
 
+    def set_centers(self, centers):
+        """Install coarse centres (K x M codes): assigns every code, rebuilds W."""
+        c = _host(centers, np.uint8)
+        assert c.ndim == 2 and c.shape[1] == self.M
+        _rl.check(self._lib.rii_set_centers(self._h, _ptr(c), c.shape[0], None))
+
     def get_postings(self):
         inf = self.info()
         off = np.empty(inf["K"] + 1, np.int64)

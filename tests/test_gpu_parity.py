@@ -303,3 +303,28 @@ def test_ivf_paper_mode(rii, ref, kind, N, D, M, K):
     assert g.query(q[:2], 5, target_ids=S, L=200)[2] == rii.PATH_IVF
     g.set_ivf_mode("lists")
     assert g.query(q[:2], 5, L=2)[2] == rii.PATH_IVF
+
+
+@pytest.mark.parametrize("M,K", [(8, 9_000), (16, 8_192), (32, 1_000)])
+def test_assignment_paths_large_k(rii, ref, M, K):
+    """a(n) = argmin_k d_S for installed centres: K >= 8192 takes the
+    SDC-mode packed scan (codes as queries over the centre codes), smaller K the
+    rotated-table kernel with canonical near-tie fallback.  Bit-exact vs the oracle."""
+    D = 96 if M != 16 else 128
+    kind = "deep" if M != 16 else "sift"
+    x = gen.base(kind, 20_000, D, seed=K + M)
+    g = rii.Index(D, M)
+    g.train(x[:4000], n_iter=2, seed=0)
+    cb = g.get_codebook()
+    g.add(x)
+    codes = g.get_codes()
+    assert np.array_equal(codes, ref.encode(cb, x, M))
+    rng = np.random.default_rng(K)
+    centers = codes[rng.choice(len(codes), K, replace=False)].copy()
+    centers[1] = centers[0]            # duplicate centre: exact ties must go to the lower k
+    g.set_centers(centers)
+    T = ref.sdc_tables(cb, D, M)
+    a, _ = ref.assign(T, codes, centers)
+    off, ids = g.get_postings()
+    want_off, want_ids = ref.build_postings(a, K)
+    assert np.array_equal(off, want_off) and np.array_equal(ids, want_ids)

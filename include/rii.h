@@ -196,6 +196,19 @@ rii_status rii_calibrate_theta(rii_index *idx, const float *q, int64_t nq, int32
                                int32_t n_L, rii_mem where, void *stream, double *a_out, double *b_out,
                                double *crossovers);
 
+/* Persistence (the paper pickles the index; SPEC's "RII1" layout,
+ * S:382-397).  Little-endian file: magic "RII1", u32 version (1), u32 D, M, Ks,
+ * world, rank, ivf_mode, flags (bit 0: fitted theta), u32 n_segments; i64 N,
+ * n_local, K, theta; f64 fit_a, fit_b; then the code book (M*Ks*(D/M) f32),
+ * n_segments x (i64 local offset, i64 global first id, i64 count), the codes
+ * (n_local*M u8), the centres (K*M u8) and the posting lists (offsets (K+1) i64,
+ * ids n_local u32 local positions; the assignment is rebuilt from them, Eq. 4),
+ * i.e. (N+K)M + 4N bytes plus header, code book and offsets.  Each rank saves
+ * its own shard.  rii_load creates an index from such a file (the same rank/world
+ * layout; nccl_id as in rii_create).  Format errors -> RII_ERR_ARG. */
+rii_status rii_save(const rii_index *idx, const char *path);
+rii_status rii_load(const char *path, int32_t device, const void *nccl_id, rii_index **out);
+
 /* Meaning of L in the inverted index (reading R2).
  *  RII_IVF_LISTS (default, mode A): L = the number of nearest coarse lists; every
  *    member of S in them is evaluated (BASELINE.json's "posting lists of the L

@@ -42,6 +42,8 @@ SIGNATURES = {
     "rii_get_centers": (C.c_int, [_p, _p]),
     "rii_get_postings": (C.c_int, [_p, _p, _p]),
     "rii_set_centers": (C.c_int, [_p, _p, _i32, _p]),
+    "rii_save": (C.c_int, [_p, C.c_char_p]),
+    "rii_load": (C.c_int, [C.c_char_p, _i32, _p, C.POINTER(_p)]),
     "rii_set_theta": (C.c_int, [_p, _i64]),
     "rii_set_ivf_mode": (C.c_int, [_p, _i32]),
     "rii_calibrate_theta": (C.c_int, [_p, _p, _i64, _i32, _p, _i32, C.c_int, _p, C.POINTER(C.c_double),

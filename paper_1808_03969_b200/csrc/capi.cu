@@ -206,6 +206,12 @@ __global__ void gather_i32_kernel(const int32_t *src, const int64_t *pos, int64_
     if (i < n) { dst[i] = src[pos[i]]; val[i] = (uint32_t)pos[i]; }
 }
 
+__global__ void assign_from_csr_kernel(const int64_t *off, int64_t K, const uint32_t *ids, int32_t *a) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    for (int64_t p = off[k]; p < off[k + 1]; ++p) a[ids[p]] = (int32_t)k;
+}
+
 __global__ void widen_ids_kernel(const uint32_t *src, int64_t n, IdMap map, int64_t *dst) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) dst[i] = map_id(map, src[i]);
@@ -888,6 +894,147 @@ rii_status rii_get_postings(const rii_index *x, int64_t *offsets, int64_t *ids) 
             RII_LAUNCHED();
             RII_CUDA(cudaMemcpy(ids, d, (size_t)x->n_local * 8, cudaMemcpyDeviceToHost));
         }
+    });
+}
+
+}  // extern "C"
+
+namespace {
+struct FileW {
+    FILE *f;
+    void put(const void *p, size_t n) {
+        if (n && fwrite(p, 1, n, f) != n) throw Error(RII_ERR_ARG, "write failed");
+    }
+    template <class T>
+    void val(T v) { put(&v, sizeof(T)); }
+};
+struct FileR {
+    FILE *f;
+    void get(void *p, size_t n, const char *what) {
+        if (n && fread(p, 1, n, f) != n) throw Error(RII_ERR_ARG, std::string("truncated index file: ") + what);
+    }
+    template <class T>
+    T val(const char *what) { T v; get(&v, sizeof(T), what); return v; }
+};
+template <class T>
+void dev_to_file(FileW &w, const T *d, size_t n) {
+    std::vector<T> h(n);
+    if (n) RII_CUDA(cudaMemcpy(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost));
+    w.put(h.data(), n * sizeof(T));
+}
+template <class T>
+void file_to_dev(FileR &r, T *d, size_t n, const char *what) {
+    std::vector<T> h(n);
+    r.get(h.data(), n * sizeof(T), what);
+    if (n) RII_CUDA(cudaMemcpy(d, h.data(), n * sizeof(T), cudaMemcpyHostToDevice));
+}
+}  // namespace
+
+extern "C" {
+
+rii_status rii_save(const rii_index *x, const char *path) {
+    return guarded([&] {
+        arg_check(x && path, "NULL argument");
+        state_check(x->trained, "nothing to save: no code book");
+        DeviceGuard g(x->device);
+        FILE *f = fopen(path, "wb");
+        arg_check(f != nullptr, "cannot open file for writing");
+        FileW w{f};
+        try {
+            w.put("RII1", 4);
+            w.val<uint32_t>(1);
+            for (uint32_t v : {(uint32_t)x->D, (uint32_t)x->M, (uint32_t)KS, (uint32_t)x->world, (uint32_t)x->rank,
+                               (uint32_t)x->ivf_mode, (uint32_t)(x->theta_fit ? 1 : 0), (uint32_t)x->segs.size()})
+                w.val(v);
+            for (int64_t v : {x->N, x->n_local, x->K, x->theta}) w.val(v);
+            w.val(x->fit_a);
+            w.val(x->fit_b);
+            dev_to_file(w, x->cb.as<float>(), (size_t)x->M * KS * x->ds);
+            for (auto &sg : x->segs) { w.val(sg.local_off); w.val(sg.global_first); w.val(sg.count); }
+            dev_to_file(w, x->codes.as<uint8_t>(), (size_t)x->n_local * x->M);
+            if (x->K > 0) {
+                dev_to_file(w, x->centers.as<uint8_t>(), (size_t)x->K * x->M);
+                dev_to_file(w, x->offsets.as<int64_t>(), (size_t)x->K + 1);
+                dev_to_file(w, x->ids.as<uint32_t>(), (size_t)x->n_local);
+            }
+        } catch (...) {
+            fclose(f);
+            throw;
+        }
+        arg_check(fclose(f) == 0, "close failed");
+    });
+}
+
+rii_status rii_load(const char *path, int32_t device, const void *nccl_id, rii_index **out) {
+    if (out) *out = nullptr;
+    return guarded([&] {
+        arg_check(path && out, "NULL argument");
+        FILE *f = fopen(path, "rb");
+        arg_check(f != nullptr, "cannot open index file");
+        FileR r{f};
+        rii_index *x = nullptr;
+        try {
+            char magic[4];
+            r.get(magic, 4, "magic");
+            arg_check(memcmp(magic, "RII1", 4) == 0, "not an RII1 index file (bad magic)");
+            arg_check(r.val<uint32_t>("version") == 1, "unsupported index file version");
+            const uint32_t D = r.val<uint32_t>("header"), M = r.val<uint32_t>("header"), Ks = r.val<uint32_t>("header");
+            const uint32_t world = r.val<uint32_t>("header"), rank = r.val<uint32_t>("header");
+            const uint32_t mode = r.val<uint32_t>("header"), flags = r.val<uint32_t>("header");
+            const uint32_t nseg = r.val<uint32_t>("header");
+            const int64_t N = r.val<int64_t>("header"), n_local = r.val<int64_t>("header");
+            const int64_t K = r.val<int64_t>("header"), theta = r.val<int64_t>("header");
+            const double fa = r.val<double>("header"), fb = r.val<double>("header");
+            arg_check(Ks == KS && M >= 1 && M <= 64 && D % M == 0 && D / M <= 64, "bad shape in header");
+            arg_check(world >= 1 && rank < world && n_local >= 0 && n_local <= N && K >= 0 && mode <= 1,
+                      "bad header");
+            const rii_status st = rii_create((int32_t)D, (int32_t)M, (int32_t)Ks, device, (int32_t)rank,
+                                             (int32_t)world, nccl_id, &x);
+            if (st != RII_OK) throw Error(st, t_err);
+            DeviceGuard g(device);
+            file_to_dev(r, x->cb.as<float>(), (size_t)M * KS * (D / M), "code book");
+            x->trained = true;
+            for (uint32_t i = 0; i < nseg; ++i) {
+                Seg sg;
+                sg.local_off = r.val<int64_t>("segments");
+                sg.global_first = r.val<int64_t>("segments");
+                sg.count = r.val<int64_t>("segments");
+                x->segs.push_back(sg);
+            }
+            x->N = N;
+            x->n_local = n_local;
+            file_to_dev(r, x->codes.get<uint8_t>((size_t)std::max<int64_t>(n_local, 1) * M), (size_t)n_local * M,
+                        "codes");
+            x->K = K;
+            if (K > 0) {
+                file_to_dev(r, x->centers.get<uint8_t>((size_t)K * M), (size_t)K * M, "centres");
+                file_to_dev(r, x->offsets.get<int64_t>((size_t)K + 1), (size_t)K + 1, "posting offsets");
+                file_to_dev(r, x->ids.get<uint32_t>((size_t)std::max<int64_t>(n_local, 1)), (size_t)n_local,
+                            "posting ids");
+                // a(n) is implied by W (Eq. 4): rebuilt on the device, not stored
+                int32_t *as = x->assign.get<int32_t>((size_t)std::max<int64_t>(n_local, 1));
+                if (K > 0 && n_local > 0) {
+                    assign_from_csr_kernel<<<(unsigned)ceil_div(K, 64), 64>>>(x->offsets.as<int64_t>(), K,
+                                                                             x->ids.as<uint32_t>(), as);
+                    RII_LAUNCHED();
+                    RII_CUDA(cudaDeviceSynchronize());
+                }
+            }
+            char extra;
+            arg_check(fread(&extra, 1, 1, f) == 0, "trailing bytes after the index");
+            x->theta = theta;
+            x->ivf_mode = (int)mode;
+            x->theta_fit = (flags & 1) != 0;
+            x->fit_a = fa;
+            x->fit_b = fb;
+            upload_segs(x, nullptr);
+        } catch (...) {
+            fclose(f);
+            rii_destroy(x);
+            throw;
+        }
+        fclose(f);
+        *out = x;
     });
 }
 

@@ -219,10 +219,16 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
                         d[2 * p + 1] = acc2[p].y;
                     }
                 }
+                // one warp vote per code; per-query ballots only when some lane has a candidate
+                bool any = false;
 #pragma unroll
-                for (int qq = 0; qq < B; ++qq)
-                    push_candidate_win(pos < c1 && d[qq] <= th[qq], make_key(d[qq], cid[u]), fresh + qq * NEWCAP,
-                                       cnt + qq, lane, SOFT, need, ovf);
+                for (int qq = 0; qq < B; ++qq) any |= d[qq] <= th[qq];
+                if (__any_sync(0xffffffffu, any && pos < c1)) {
+#pragma unroll
+                    for (int qq = 0; qq < B; ++qq)
+                        push_candidate_win(pos < c1 && d[qq] <= th[qq], make_key(d[qq], cid[u]), fresh + qq * NEWCAP,
+                                           cnt + qq, lane, SOFT, need, ovf);
+                }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {

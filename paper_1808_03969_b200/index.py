@@ -8,6 +8,7 @@ arrays and CPU tensors as host memory (RII_MEM_HOST).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -204,6 +205,30 @@ class Index:
         out = np.empty((self.info()["K"], self.M), np.uint8)
         _rl.check(self._lib.rii_get_centers(self._h, _ptr(out)))
         return out
+
+    def save(self, path: str):
+        """Write this rank's shard as an RII1 file (include/rii.h)."""
+        _rl.check(self._lib.rii_save(self._h, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path: str, device: int | None = None, nccl_id: bytes | None = None) -> "Index":
+        """Create an index from an RII1 file written by save()."""
+        lib = _rl.load()
+        if device is None:
+            try:
+                device = _torch().cuda.current_device()
+            except Exception:
+                device = 0
+        h = C.c_void_p()
+        idbuf = None if nccl_id is None else (C.c_uint8 * _rl.NCCL_ID_BYTES).from_buffer_copy(nccl_id)
+        _rl.check(lib.rii_load(os.fsencode(path), device, C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
+                               C.byref(h)))
+        self = cls.__new__(cls)
+        self._lib, self._h, self.device = lib, h, device
+        with open(path, "rb") as f:
+            hdr = np.frombuffer(f.read(40), dtype="<u4")
+        self.D, self.M, self.Ks, self.world, self.rank = (int(v) for v in hdr[2:7])
+        return self
 
     def set_centers(self, centers):
         """Install coarse centres (K x M codes): assigns every code, rebuilds W."""

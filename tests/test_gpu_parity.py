@@ -328,3 +328,36 @@ def test_assignment_paths_large_k(rii, ref, M, K):
     off, ids = g.get_postings()
     want_off, want_ids = ref.build_postings(a, K)
     assert np.array_equal(off, want_off) and np.array_equal(ids, want_ids)
+
+
+def test_save_load_roundtrip(rii, ref, tmp_path):
+    """Persistence: load(save(idx)) answers identically; save -> load ->
+    save is byte-identical; the payload is (N+K)M + 4N bytes plus header,
+    code book and list offsets; malformed files are rejected."""
+    N, D, M, K = 20_000, 128, 16, 64
+    x = gen.sift_like(N, D, seed=51)
+    q = gen.sift_like(17, D, seed=51, stream=gen.STREAM_QUERY)
+    g = rii.Index(D, M)
+    g.train(x[:5000], n_iter=3, seed=0)
+    g.add(x)
+    g.reconfigure(K, n_iter=3, seed=0)
+    g.set_theta(4321)
+    p1, p2 = str(tmp_path / "a.rii"), str(tmp_path / "b.rii")
+    g.save(p1)
+    h = rii.Index.load(p1)
+    assert h.info() == g.info()
+    for path, L, S in (("linear", 1, None), ("ivf", 3, None), ("auto", 2, gen.subset(N, 4000, seed=1))):
+        a, b = g.query(q, 20, S, L=L, path=path), h.query(q, 20, S, L=L, path=path)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+    h.save(p2)
+    assert open(p1, "rb").read() == open(p2, "rb").read()
+    import os
+    header = 4 + 4 * 9 + 8 * 4 + 8 * 2 + 3 * 8          # magic, u32 fields, i64 fields, fit a/b, one segment
+    assert os.path.getsize(p1) == header + 256 * D * 4 + (N + K) * M + 4 * N + 8 * (K + 1)
+    raw = open(p1, "rb").read()
+    (tmp_path / "t.rii").write_bytes(raw[:-10])
+    (tmp_path / "m.rii").write_bytes(b"XXXX" + raw[4:])
+    for bad in ("t.rii", "m.rii"):
+        with pytest.raises(rii.RiiError) as e:
+            rii.Index.load(str(tmp_path / bad))
+        assert e.value.status == 1

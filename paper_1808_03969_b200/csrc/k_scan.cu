@@ -391,6 +391,7 @@ static size_t smem_generic(int B, int M, int kk) {
 }
 static constexpr size_t SMEM_CAP = 227 * 1024;
 static constexpr int PACKED_MIN_CODES = 16384;  // codes per CTA below which fp32 pair tables win
+static constexpr int PACKED_NTH = 384;           // threads of the packed kernels (<= 170 registers)
 
 ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available) {
     ScanPlan p{};
@@ -409,13 +410,16 @@ ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bo
     }
     if (p.B == 0) throw Error(1, "topk too large for the scan kernel's shared-memory budget");
     p.nb = (int)ceil_div(nq, p.B);
-    // Code chunks: minimise waves(nc) / nc (per-CTA work ~ n_codes / nc), >= 8192 codes per chunk.
+    // Code chunks: minimise waves(nc) / nc (per-CTA work ~ n_codes / nc), >= 8192 codes per
+    // chunk, and at most ~40 MB of codes per chunk so that the CTAs of a wave (which all
+    // stream the same chunk) hit in the 126 MB L2 even when they drift apart.
     int64_t nc_max = n_codes / 8192;
     if (nc_max < 1) nc_max = 1;
-    if (nc_max > 64) nc_max = 64;
+    if (nc_max > 256) nc_max = 256;
+    const int64_t nc_min = std::min<int64_t>(nc_max, ceil_div(n_codes * M, (int64_t)40 << 20));
     double best = 1e300;
-    int bnc = 1;
-    for (int nc = 1; nc <= nc_max; ++nc) {
+    int bnc = (int)nc_min;
+    for (int nc = (int)nc_min; nc <= nc_max; ++nc) {
         const double waves = (double)ceil_div((int64_t)p.nb * nc, num_sms);
         const double t = waves / nc * (1.0 + 0.002 * nc);
         if (t < best * 0.999) { best = t; bnc = nc; }
@@ -440,7 +444,7 @@ static int scan_threads() { return scan_cfg() == 0 ? 256 : 512; }
 template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr() {
     if constexpr (B == 8) {
-        return (void *)scan_fast_kernel<M, 8, LISTS, 512, 1, true>;
+        return (void *)scan_fast_kernel<M, 8, LISTS, PACKED_NTH, 1, true>;
     } else {
         if (scan_cfg() == 0) return (void *)scan_fast_kernel<M, B, LISTS, 256, 2, false>;
         return (void *)scan_fast_kernel<M, B, LISTS, 512, 1, false>;
@@ -457,7 +461,7 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
     a.nb = pl.nb; a.chunk = pl.chunk; a.nc = pl.nc; a.out = out; a.tables = tables;
     void *args[] = {&a};
     KernelTimer t(TK_LINEAR, st), tp(B == 8 ? TK_PACKED : -1, st);
-    RII_CUDA(cudaLaunchKernel(kern, dim3(pl.nb * pl.nc), dim3(B == 8 ? 512 : scan_threads()), args, pl.smem, st));
+    RII_CUDA(cudaLaunchKernel(kern, dim3(pl.nb * pl.nc), dim3(B == 8 ? PACKED_NTH : scan_threads()), args, pl.smem, st));
     count_launch();
 }
 
@@ -498,7 +502,7 @@ static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st) {
     ScanArgs aa = a;
     void *args[] = {&aa};
     KernelTimer t(TK_IVF, st);
-    RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)n_items), dim3(B == 8 ? 512 : scan_threads()), args, smem, st));
+    RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)n_items), dim3(B == 8 ? PACKED_NTH : scan_threads()), args, smem, st));
     count_launch();
 }
 
@@ -572,7 +576,7 @@ static void assign_scan_m(const uint8_t *codes, int64_t n, const uint8_t *center
         a.nb = (int)ceil_div(cn, B); a.chunk = K; a.nc = 1;
         a.sdcT = T; a.qcodes = codes + s0 * M;
         void *args[] = {&a};
-        RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)a.nb), dim3(512), args, smem, st));
+        RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)a.nb), dim3(PACKED_NTH), args, smem, st));
         count_launch();
         top1_kernel<<<(unsigned)ceil_div(cn, 256), 256, 0, st>>>(keys, cn, kk, assign + s0, dist ? dist + s0 : nullptr);
         RII_LAUNCHED();

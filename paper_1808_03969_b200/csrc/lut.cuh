@@ -190,7 +190,10 @@ __device__ __forceinline__ void adc_packed(const uint8_t *lut, const uint32_t (&
         for (int p = 0; p < NQ; ++p) {
             const uint2 v = *reinterpret_cast<const uint2 *>(lut + p * QUAD_BYTES + off);
             const float2 x = make_float2(__uint_as_float(v.x), __uint_as_float(v.y));
-            const float2 y = make_float2(__uint_as_float(v.x << 16), __uint_as_float(v.y << 16));
+            // low halves -> high halves with PRMT (ALU pipe; a shift would be lowered to an
+            // IMAD on the FMA pipe, which the FADD2s already saturate)
+            const float2 y = make_float2(__uint_as_float(__byte_perm(v.x, 0u, 0x1044)),
+                                         __uint_as_float(__byte_perm(v.y, 0u, 0x1044)));
             ab[p] = j == 0 ? x : fadd2(ab[p], x);
             cd[p] = j == 0 ? y : fadd2(cd[p], y);
         }

@@ -43,7 +43,7 @@ __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
     }
 }
 
-template <int M, int B, bool LISTS, int NTH, int U, bool PACKED>
+template <int M, int B, bool LISTS, int NTH, int U, bool PACKED, int VARIANT = 0>
 __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     constexpr int W = M / 4, NP = B / 2, NQ = B / 4;
     static_assert(!PACKED || B % 4 == 0, "packed tables hold 4 queries each");
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
                 float d[B];
                 if constexpr (PACKED) {
                     float2 ab[NQ], cd[NQ];
-                    adc_packed<M, NQ>(lut, w[u], rw, sel, l8, ab, cd);
+                    adc_packed<M, NQ, VARIANT>(lut, w[u], rw, sel, l8, ab, cd);
 #pragma unroll
                     for (int p = 0; p < NQ; ++p) {
                         d[4 * p] = ab[p].x;
@@ -391,7 +391,18 @@ static size_t smem_generic(int B, int M, int kk) {
 }
 static constexpr size_t SMEM_CAP = 227 * 1024;
 static constexpr int PACKED_MIN_CODES = 16384;  // codes per CTA below which fp32 pair tables win
-static constexpr int PACKED_NTH = 384;           // threads of the packed kernels (<= 170 registers)
+// Packed-kernel configuration (RII_PACK_CFG, for A/B measurements): 0 = 512 threads,
+// shift unpack; 1 = 384 threads, PRMT unpack; 2 = 512 threads, PRMT unpack,
+// recomputed column offsets; 3 = 384 threads, shift unpack.
+static int pack_cfg() {
+    static int cfg = [] {
+        const char *e = getenv("RII_PACK_CFG");
+        return e ? atoi(e) : 0;
+    }();
+    return cfg;
+}
+static int packed_nth() { return (pack_cfg() == 1 || pack_cfg() == 3) ? 384 : 512; }
+#define PACKED_NTH packed_nth()
 
 ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available) {
     ScanPlan p{};
@@ -416,7 +427,11 @@ ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bo
     int64_t nc_max = n_codes / 8192;
     if (nc_max < 1) nc_max = 1;
     if (nc_max > 256) nc_max = 256;
-    const int64_t nc_min = std::min<int64_t>(nc_max, ceil_div(n_codes * M, (int64_t)40 << 20));
+    static const int64_t chunk_mb = [] {
+        const char *e = getenv("RII_CHUNK_MB");  // A/B: 0 disables the L2 chunk cap
+        return (int64_t)(e ? atoi(e) : 40);
+    }();
+    const int64_t nc_min = chunk_mb > 0 ? std::min<int64_t>(nc_max, ceil_div(n_codes * M, chunk_mb << 20)) : 1;
     double best = 1e300;
     int bnc = (int)nc_min;
     for (int nc = (int)nc_min; nc <= nc_max; ++nc) {
@@ -444,7 +459,12 @@ static int scan_threads() { return scan_cfg() == 0 ? 256 : 512; }
 template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr() {
     if constexpr (B == 8) {
-        return (void *)scan_fast_kernel<M, 8, LISTS, PACKED_NTH, 1, true>;
+        switch (pack_cfg()) {
+            case 1: return (void *)scan_fast_kernel<M, 8, LISTS, 384, 1, true, 1>;
+            case 2: return (void *)scan_fast_kernel<M, 8, LISTS, 512, 1, true, 3>;
+            case 3: return (void *)scan_fast_kernel<M, 8, LISTS, 384, 1, true, 0>;
+            default: return (void *)scan_fast_kernel<M, 8, LISTS, 512, 1, true, 0>;
+        }
     } else {
         if (scan_cfg() == 0) return (void *)scan_fast_kernel<M, B, LISTS, 256, 2, false>;
         return (void *)scan_fast_kernel<M, B, LISTS, 512, 1, false>;

@@ -173,8 +173,11 @@ __device__ __forceinline__ void load_lut_quad_sdc(uint32_t *dst, const float *__
 }
 
 // Approximate lane-rotated ADC of one pre-loaded code against NQ quad tables:
-// per step j one PRMT, per quad one LDS.64, two SHF and two FADD2 (4 lookups).
-template <int M, int NQ>
+// per step j one PRMT, per quad one LDS.64, two unpacks and two FADD2 (4 lookups).
+// VARIANT bit 0: unpack the low halves with PRMT (ALU pipe) instead of a shift
+// (lowered to IMAD on the FMA pipe); bit 1: recompute the column offset l8 ^ 8j per
+// step (one LOP) instead of letting the compiler hoist 32 constants into registers.
+template <int M, int NQ, int VARIANT>
 __device__ __forceinline__ void adc_packed(const uint8_t *lut, const uint32_t (&w)[M / 4], uint32_t rw,
                                            const uint32_t (&sel)[4], uint32_t l8, float2 (&ab)[NQ],
                                            float2 (&cd)[NQ]) {
@@ -185,15 +188,19 @@ __device__ __forceinline__ void adc_packed(const uint8_t *lut, const uint32_t (&
     permute_words<W>(wp, rw);
 #pragma unroll
     for (int j = 0; j < M; ++j) {
-        const uint32_t off = __byte_perm(wp[j >> 2], l8 ^ (uint32_t)(j << 3), sel[j & 3]);
+        uint32_t col;
+        if constexpr (VARIANT & 2) asm volatile("xor.b32 %0, %1, %2;" : "=r"(col) : "r"(l8), "r"((uint32_t)(j << 3)));
+        else col = l8 ^ (uint32_t)(j << 3);
+        const uint32_t off = __byte_perm(wp[j >> 2], col, sel[j & 3]);
 #pragma unroll
         for (int p = 0; p < NQ; ++p) {
             const uint2 v = *reinterpret_cast<const uint2 *>(lut + p * QUAD_BYTES + off);
             const float2 x = make_float2(__uint_as_float(v.x), __uint_as_float(v.y));
-            // low halves -> high halves with PRMT (ALU pipe; a shift would be lowered to an
-            // IMAD on the FMA pipe, which the FADD2s already saturate)
-            const float2 y = make_float2(__uint_as_float(__byte_perm(v.x, 0u, 0x1044)),
-                                         __uint_as_float(__byte_perm(v.y, 0u, 0x1044)));
+            float2 y;
+            if constexpr (VARIANT & 1)
+                y = make_float2(__uint_as_float(__byte_perm(v.x, 0u, 0x1044)), __uint_as_float(__byte_perm(v.y, 0u, 0x1044)));
+            else
+                y = make_float2(__uint_as_float(v.x << 16), __uint_as_float(v.y << 16));
             ab[p] = j == 0 ? x : fadd2(ab[p], x);
             cd[p] = j == 0 ? y : fadd2(cd[p], y);
         }

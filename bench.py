@@ -234,7 +234,12 @@ def run_ours(args, rank, world, local):
     rii_lib.rii_kernel_timing_read(2, C.byref(mms), C.byref(mn))
     pms, pn = C.c_double(), C.c_int64()
     rii_lib.rii_kernel_timing_read(3, C.byref(pms), C.byref(pn))
-    packed = pn.value > 0 and pn.value == kn.value
+    bms, bn = C.c_double(), C.c_int64()
+    rii_lib.rii_kernel_timing_read(4, C.byref(bms), C.byref(bn))
+    qms, qn16 = C.c_double(), C.c_int64()
+    rii_lib.rii_kernel_timing_read(5, C.byref(qms), C.byref(qn16))
+    q16 = qn16.value > 0 and qn16.value == kn.value
+    packed = q16 or (pn.value > 0 and pn.value == kn.value)
     rii_lib.rii_kernel_timing(0)
     torch.cuda.synchronize()
     _barrier(world)
@@ -242,12 +247,13 @@ def run_ours(args, rank, world, local):
     total_ms = _max_over_ranks(sum(step_ms), world)
     kernel_ms = _max_over_ranks(kms.value / max(kn.value, 1), world)
     merge_ms = _max_over_ranks(mms.value / max(mn.value, 1), world)
+    bound_ms = _max_over_ranks(bms.value / max(bn.value, 1), world)
     qps = nq * args.steps / (total_ms / 1e3)
 
     peaks, peak_src = _peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     # one 128-B shared-memory wavefront per clock per SM: 32 fp32 lookups, or 64
-    # lookups with the bf16-packed tables (2 B per lookup)
+    # lookups with the bf16-packed or u16 fixed-point tables (2 B per lookup)
     per_clk = LUT_LOOKUPS_PER_CLK_PER_SM * (2 if packed else 1)
     lut_peak = SMS * per_clk * sm_max * 1e6  # lookups/s
     lookups = nq * n_local * M
@@ -259,16 +265,19 @@ def run_ours(args, rank, world, local):
             traffic = json.load(f).get("dram_bytes_per_launch")
     roofline = {
         "bound": "alu",
-        "kernel": ("scan_fast_kernel<32,8,packed> (linear ADC scan + top-k, bf16-packed tables + exact rescore)"
+        "kernel": ("scan_fast_kernel<32,8,u16> (linear ADC scan + top-k, u16 fixed-point SWAR tables + exact rescore)"
+                   if q16 else
+                   "scan_fast_kernel<32,8,packed> (linear ADC scan + top-k, bf16-packed tables + exact rescore)"
                    if packed else "scan_fast_kernel<32,6> (linear ADC scan + top-k, fp32 tables)"),
         "achieved": achieved / 1e9, "peak": lut_peak / 1e9, "unit": "Glookup/s",
         "frac": achieved / lut_peak, "traffic": traffic,
         "peak_basis": f"shared-memory LUT pipe: one 128-B wavefront/clk/SM = {per_clk} "
-                      f"{'bf16-packed (2 B)' if packed else 'fp32 (4 B)'} lookups/clk/SM x {SMS} SMs x "
+                      f"{'u16 (2 B)' if q16 else 'bf16-packed (2 B)' if packed else 'fp32 (4 B)'} lookups/clk/SM x {SMS} SMs x "
                       f"{sm_max:.0f} MHz (sm_max_mhz, {peak_src})",
         "algorithmic_units": f"{nq} queries x {n_local} codes x {M} lookups per launch",
         "kernel_ms_per_launch": kernel_ms, "kernel_share_of_step": kernel_ms / (total_ms / args.steps),
         "merge_ms_per_launch": merge_ms,
+        "bound_pass_ms_per_step": bound_ms if bn.value else None,
         "hbm_equiv": {"code_bytes_per_s": achieved, "of_measured_hbm": achieved / (float(peaks["hbm_gbs"]) * 1e9),
                       "hbm_gbs": float(peaks["hbm_gbs"]),
                       "note": "north_star's 'fraction of HBM on code bytes': Q*N*M effective code bytes/s over the "

@@ -27,8 +27,8 @@ std::mutex g_tmu;
 bool g_timing = false;
 struct TimedPair { int which; cudaEvent_t a, b; };
 std::vector<TimedPair> g_pairs;
-double g_total_ms[TK_COUNT] = {0, 0, 0, 0};
-int64_t g_count[TK_COUNT] = {0, 0, 0, 0};
+double g_total_ms[TK_COUNT] = {};
+int64_t g_count[TK_COUNT] = {};
 
 void drain_pairs() {  // caller holds g_tmu
     for (auto &p : g_pairs) {
@@ -123,7 +123,8 @@ struct rii_index {
     double fit_a = 0.0, fit_b = 0.0;
     // scratch (query side is const-callable: mutable)
     mutable Buf s_q, s_S, s_pos, s_sub, s_part, s_keys, s_gather, s_d0, s_probe, s_roff, s_rids, s_rkey, s_rval,
-        s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_items, s_gthr, s_tables, s_cpart, s_ckeys, s_take;
+        s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_items, s_gthr, s_tables, s_cpart, s_ckeys, s_take,
+        s_samp, s_spart, s_bound;
 };
 
 namespace {
@@ -344,6 +345,21 @@ Targets prepare_targets(const rii_index *x, const QueryArgs &a, cudaStream_t st)
     return t;
 }
 
+// u16 tables: scans of at least RII_Q16_MIN (default 2^19) codes; the bound comes
+// from min(Q16_SAMPLE, n / 4) strided codes.
+static int64_t q16_sample() {
+    const char *e = getenv("RII_Q16_SAMPLE");
+    return e ? atoll(e) : ((int64_t)1 << 15);
+}
+static int ns_chunks() {
+    const char *e = getenv("RII_Q16_SAMPLE_NC");
+    return e ? atoi(e) : 1;
+}
+static int64_t q16_min_codes() {
+    const char *e = getenv("RII_Q16_MIN");
+    return e ? atoll(e) : ((int64_t)1 << 19);
+}
+
 // One batch of queries (a.q, a.nq) against this rank's shard.  Writes either the
 // final result (world == 1, out_keys == nullptr) or this rank's top-kk keys with
 // global ids (out_keys, device [nq][kk]).
@@ -381,8 +397,32 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             parts = pp;
         } else {
             ScanPlan pl = plan_linear(x->M, kk, a.nq, n_codes, x->num_sms, tables != nullptr);
+            // u16 fixed-point tables for long scans: the exact kk-th distance over a
+            // strided sample of the codes bounds each query's final kk-th distance
+            // (the sample is a subset), which scales the tables and seeds the filter.
+            // every CTA filters with, and publishes its kk-th distance into, gthr
+            float *gthr = x->s_gthr.get<float>(a.nq);
+            const int64_t ns = std::min<int64_t>(q16_sample(), n_codes / 4);
+            const bool q16 = pl.B == 8 && pl.fast && q16_enabled() && n_codes >= q16_min_codes() && ns >= 4 * kk;
+            if (!q16) {
+                if (pl.fast) launch_fill_f32(gthr, a.nq, INFINITY, st);
+                else gthr = nullptr;
+            } else {
+                KernelTimer tb(TK_BOUND, st);
+                const int64_t stride = n_codes / ns;
+                uint8_t *samp = x->s_samp.get<uint8_t>((size_t)ns * x->M);
+                launch_strided_gather(scan_codes, x->M, stride, ns, samp, st);
+                // one chunk per query batch: the sample is short, so per-CTA top-k work dominates
+                ScanPlan ps = plan_linear(x->M, kk, a.nq, ns, x->num_sms, true, ns_chunks());
+                uint64_t *sp = x->s_spart.get<uint64_t>((size_t)ps.nb * ps.B * ps.nc * kk);
+                launch_linear_scan(ps, samp, ns, x->M, a.q, a.nq, cb, x->D, kk, sp, st, tables, nullptr, false, -1);
+                uint64_t *sk = x->s_ckeys.get<uint64_t>((size_t)a.nq * kk);
+                launch_merge(sp, (int64_t)ps.nc * kk, kk, ps.nc, a.nq, kk, kk, IdMap(), nullptr, nullptr, sk, st);
+                launch_kth_bound(sk, a.nq, kk, gthr, st);
+                tr.mark("q16 bound");
+            }
             uint64_t *pp = x->s_part.get<uint64_t>((size_t)pl.nb * pl.B * pl.nc * kk);
-            launch_linear_scan(pl, scan_codes, n_codes, x->M, a.q, a.nq, cb, x->D, kk, pp, st, tables);
+            launch_linear_scan(pl, scan_codes, n_codes, x->M, a.q, a.nq, cb, x->D, kk, pp, st, tables, gthr, q16);
             parts = pp;
             q_stride = (int64_t)pl.nc * kk;
             p_stride = kk;
@@ -535,7 +575,7 @@ void rii_kernel_timing(int32_t enable) {
 
 rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *launches) {
     return guarded([&] {
-        arg_check(which >= 0 && which < TK_COUNT, "which must be 0, 1, 2 or 3");
+        arg_check(which >= 0 && which < TK_COUNT, "which must be in [0, 6)");
         std::lock_guard<std::mutex> lk(g_tmu);
         drain_pairs();
         if (total_ms) *total_ms = g_total_ms[which];

@@ -43,18 +43,35 @@ __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
     }
 }
 
-template <int M, int B, bool LISTS, int NTH, int U, bool PACKED, int VARIANT = 0>
+// Top lists, fresh buffers, counters, thresholds, scratch[16] and the q16 scales.
+__host__ __device__ constexpr int smem_aux_bytes(int B, int kk) { return B * (kk + NEWCAP) * 8 + B * 8 + 64 + B * 8; }
+
+// TAB: 0 = fp32 pair tables, 1 = bf16-packed quad tables, 2 = u16 fixed-point quad
+// tables (integer SWAR sums, linear mode with a per-query bound).
+template <int M, int B, bool LISTS, int NTH, int U, int TAB, int VARIANT = 0>
 __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     constexpr int W = M / 4, NP = B / 2, NQ = B / 4;
+    constexpr bool PACKED = TAB != 0, Q16 = TAB == 2;
     static_assert(!PACKED || B % 4 == 0, "packed tables hold 4 queries each");
+    static_assert(!(Q16 && LISTS), "u16 tables need a per-query bound (linear mode)");
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t *lut = smem;
     const int kk = a.kk;
-    uint64_t *top = reinterpret_cast<uint64_t *>(smem + (PACKED ? NQ * QUAD_BYTES : NP * LUT_PAIR_BYTES));
+    uint8_t *aux = smem + (PACKED ? NQ * QUAD_BYTES : NP * LUT_PAIR_BYTES);
+    if constexpr (Q16) {
+        // The u16 tables start at a 64 KB-aligned shared address, so that one PRMT
+        // yields the complete LDS address (bytes 2-3 = table base >> 16); the top
+        // lists and buffers go into the padding below it when they fit, else above.
+        const uint32_t pad = (0u - (uint32_t)__cvta_generic_to_shared(smem)) & 0xffffu;
+        lut = smem + pad;
+        aux = pad >= (uint32_t)smem_aux_bytes(B, kk) ? smem : lut + NQ * QUAD_BYTES;
+    }
+    uint64_t *top = reinterpret_cast<uint64_t *>(aux);
     uint64_t *fresh = top + B * kk;
     int *cnt = reinterpret_cast<int *>(fresh + B * NEWCAP);
     float *thr = reinterpret_cast<float *>(cnt + B);
     int *scratch = reinterpret_cast<int *>(thr + B);
+    float *qsc = reinterpret_cast<float *>(scratch + 16);  // q16: per-query scale [B]
     const uint8_t *__restrict__ codes = a.codes;
 
     // Work item: linear mode = (code chunk ci, query batch qb); list mode = (posting
@@ -82,7 +99,23 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     };
     const int D = M * a.ds, tid = threadIdx.x, lane = tid & 31;
 
-    if constexpr (PACKED) {
+    if constexpr (Q16) {
+        // u16 tables: per-query scale s = CAP / T (T = +inf -> s = 0: everything passes)
+        float qs[B];
+#pragma unroll
+        for (int qq = 0; qq < B; ++qq) {
+            const float T = __ldcg(a.gthr + query_of(qq));  // current bound on the kk-th distance
+            qs[qq] = __fdiv_rd((float)q16_cap<M>(), fmaxf(T, 1e-30f));
+            if (tid == 0) qsc[qq] = qs[qq];
+        }
+#pragma unroll
+        for (int p = 0; p < NQ; ++p)
+            load_lut_quad_q16<M>(reinterpret_cast<uint32_t *>(lut + p * QUAD_BYTES),
+                                 a.tables + query_of(4 * p) * LUT_Q_FLOATS, a.tables + query_of(4 * p + 1) * LUT_Q_FLOATS,
+                                 a.tables + query_of(4 * p + 2) * LUT_Q_FLOATS,
+                                 a.tables + query_of(4 * p + 3) * LUT_Q_FLOATS, qs[4 * p], qs[4 * p + 1],
+                                 qs[4 * p + 2], qs[4 * p + 3]);
+    } else if constexpr (PACKED) {
 #pragma unroll
         for (int p = 0; p < NQ; ++p) {
             uint32_t *dq = reinterpret_cast<uint32_t *>(lut + p * QUAD_BYTES);
@@ -112,21 +145,35 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
 
     const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
     uint32_t sel[4];
-    make_selectors(r, sel);
+    if constexpr (Q16) make_selectors_q16(r, sel);
+    else make_selectors(r, sel);
+    // q16 column registers: bytes 0-1 = 8 (l ^ t) for t = 0,1 (colA) and 2,3 (colB),
+    // bytes 2-3 = the table's shared address >> 16
+    const uint32_t lut_hi = (uint32_t)__cvta_generic_to_shared(lut) & 0xffff0000u;
+    const uint32_t colA = lut_hi | (((uint32_t)lane ^ 0u) << 3) | (((uint32_t)lane ^ 1u) << 11);
+    const uint32_t colB = lut_hi | (((uint32_t)lane ^ 2u) << 3) | (((uint32_t)lane ^ 3u) << 11);
     // List mode: the query's global bound (the best kk-th distance any finished item
     // of this query saw, inflated by 1e-5 for the lane-rotated rounding) also filters.
     float gq[B];
 #pragma unroll
     for (int qq = 0; qq < B; ++qq) {
         gq[qq] = __int_as_float(0x7f800000);
-        if constexpr (LISTS) gq[qq] = __ldcg(a.gthr + query_of(qq));
+        if (a.gthr) gq[qq] = __ldcg(a.gthr + query_of(qq));
     }
     // Filter thresholds: the exact kk-th distance (and list bound); relaxed by
     // PACK_SLACK for the approximate packed sums.
     auto relax = [](float t) { return PACKED ? __fmul_ru(t, PACK_SLACK) : t; };
     float th[B];
+    uint32_t thq[Q16 ? B : 1];
+    auto set_thq = [&]() {
+        if constexpr (Q16) {
+#pragma unroll
+            for (int qq = 0; qq < B; ++qq) thq[qq] = q16_threshold(fminf(thr[qq], gq[qq]), qsc[qq]);
+        }
+    };
 #pragma unroll
     for (int qq = 0; qq < B; ++qq) th[qq] = relax(fminf(thr[qq], gq[qq]));
+    set_thq();
     // Packed mode: canonical (CA2) rescore of the fresh entries from the queries'
     // fp32 HBM tables before they are compacted into the exact top lists.
     auto rescore_fresh = [&]() {
@@ -167,7 +214,8 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     // WIN steps: a window whose pushes overflow the fresh buffer is rolled back
     // (its pushes dropped, the buffer compacted) and redone one step at a time,
     // which cannot overflow (an empty buffer holds a whole step, NEWCAP >= NT*U).
-    constexpr int STEP = NTH * U, WIN = 4, SOFT = NEWCAP / 4;
+    // (u16 tables start from the sampled bound, so few pushes: VARIANT bits 2/3 widen the window)
+    constexpr int STEP = NTH * U, WIN = (VARIANT & 0xfc) ? (VARIANT & 0xfc) * 2 : 4, SOFT = NEWCAP / 4;
     static_assert(NEWCAP >= STEP, "a single step must fit the fresh buffer");
     int *s_ovf = scratch + 1, *s_cnt0 = scratch + 2;  // flags, fill snapshot at the window start
     uint32_t w[U][W];
@@ -199,6 +247,29 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t pos = base + u * NTH + tid;
+                if constexpr (Q16) {
+                    uint32_t acc0[NQ], acc1[NQ];
+                    adc_q16<M, NQ>(w[u], rw, sel, colA, colB, acc0, acc1);
+                    uint32_t dq[B];
+#pragma unroll
+                    for (int p = 0; p < NQ; ++p) {
+                        dq[4 * p] = acc0[p] & 0xffffu;
+                        dq[4 * p + 2] = acc0[p] >> 16;
+                        dq[4 * p + 1] = acc1[p] & 0xffffu;
+                        dq[4 * p + 3] = acc1[p] >> 16;
+                    }
+                    bool any = false;
+#pragma unroll
+                    for (int qq = 0; qq < B; ++qq) any |= dq[qq] <= thq[qq];
+                    if (__any_sync(0xffffffffu, any && pos < c1)) {
+                        // the key's distance field is replaced by the canonical rescore
+#pragma unroll
+                        for (int qq = 0; qq < B; ++qq)
+                            push_candidate_win(pos < c1 && dq[qq] <= thq[qq], (uint64_t)cid[u], fresh + qq * NEWCAP,
+                                               cnt + qq, lane, SOFT, need, ovf);
+                    }
+                    continue;
+                }
                 float d[B];
                 if constexpr (PACKED) {
                     float2 ab[NQ], cd[NQ];
@@ -249,9 +320,10 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
             if (tid < B) s_cnt0[tid] = 0;
 #pragma unroll
             for (int qq = 0; qq < B; ++qq) {
-                if constexpr (LISTS) gq[qq] = fminf(gq[qq], __ldcg(a.gthr + query_of(qq)));
+                if (a.gthr) gq[qq] = fminf(gq[qq], __ldcg(a.gthr + query_of(qq)));
                 th[qq] = relax(fminf(thr[qq], gq[qq]));
             }
+            set_thq();
             if (rolled) {
                 base = wstart;
                 load_step(base, w, cid);
@@ -260,12 +332,13 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
             }
         } else {
             if (tid < B) s_cnt0[tid] = cnt[tid];
-            if constexpr (LISTS) {
+            if (a.gthr) {
 #pragma unroll
                 for (int qq = 0; qq < B; ++qq) {
                     gq[qq] = fminf(gq[qq], __ldcg(a.gthr + query_of(qq)));
                     th[qq] = fminf(th[qq], relax(gq[qq]));
                 }
+                set_thq();
             }
             __syncthreads();  // snapshot taken before the next window pushes
         }
@@ -274,7 +347,7 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     __syncthreads();
     rescore_fresh();
     compact_topk(top, fresh, cnt, thr, B, kk, scratch);
-    if constexpr (LISTS) {  // publish this item's kk-th distance as a bound for the query
+    if (a.gthr) {  // publish this item's kk-th distance as a bound for the query
         if (tid < nqi && thr[tid] < __int_as_float(0x7f800000)) {
             const float bound = __fmul_ru(thr[tid], 1.00001f);
             atomicMin(reinterpret_cast<int *>(a.gthr + query_of(tid)), __float_as_int(bound));
@@ -374,9 +447,11 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 // B == 8 means the bf16-packed variant (2 quad tables); otherwise B / 2 fp32 pair tables.
+// u16 variant: 64 KB-aligned tables + the aux block below or above them (kernel).
+static size_t smem_q16(int kk) { return (size_t)2 * QUAD_BYTES + 2 * (size_t)smem_aux_bytes(8, kk) + 16; }
 static size_t smem_fast(int B, int kk) {
     const size_t lut = B == 8 ? (size_t)2 * QUAD_BYTES : (size_t)(B / 2) * LUT_PAIR_BYTES;
-    return lut + (size_t)B * (kk + NEWCAP) * 8 + 128;  // 128 B: cnt, thr, scratch[16]
+    return lut + smem_aux_bytes(B, kk);
 }
 // RII_PACKED=0 disables the bf16-packed tables (A/B measurements).
 static bool packed_enabled() {
@@ -404,7 +479,7 @@ static int pack_cfg() {
 static int packed_nth() { return (pack_cfg() == 1 || pack_cfg() == 3) ? 384 : 512; }
 #define PACKED_NTH packed_nth()
 
-ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available) {
+ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available, int max_nc) {
     ScanPlan p{};
     p.fast = (M == 4 || M == 8 || M == 16 || M == 32);
     p.B = 0;
@@ -425,6 +500,7 @@ ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bo
     // chunk, and at most ~40 MB of codes per chunk so that the CTAs of a wave (which all
     // stream the same chunk) hit in the 126 MB L2 even when they drift apart.
     int64_t nc_max = n_codes / 8192;
+    if (nc_max > max_nc) nc_max = max_nc;
     if (nc_max < 1) nc_max = 1;
     if (nc_max > 256) nc_max = 256;
     static const int64_t chunk_mb = [] {
@@ -456,42 +532,71 @@ static int scan_cfg() {
 }
 static int scan_threads() { return scan_cfg() == 0 ? 256 : 512; }
 
+static int q16_cfg() {
+    const char *e = getenv("RII_Q16_CFG");
+    return e ? atoi(e) : 0;
+}
+static int q16_nth() {
+    const int c = q16_cfg();
+    return c == 2 ? 256 : c == 3 ? 512 : 384;
+}
+
 template <int M, int B, bool LISTS>
-static void *fast_kernel_ptr() {
+static void *fast_kernel_ptr(bool q16 = false) {
     if constexpr (B == 8) {
+        if constexpr (!LISTS) {
+            if (q16) {
+                // RII_Q16_CFG (A/B): threads x codes per step, barrier window (steps).
+                // 384 threads keep the kernel spill-free (168 registers); the window
+                // is long because the bound makes pushes rare (B200, deep10m: 4 steps
+                // 272 ms, 8: 251 ms, 32: 223 ms, 128: 219 ms per 10k-query launch).
+                switch (q16_cfg()) {
+                    case 1: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 2, 16>;  // window 32
+                    case 2: return (void *)scan_fast_kernel<M, 8, false, 256, 2, 2, 64>;
+                    case 3: return (void *)scan_fast_kernel<M, 8, false, 512, 1, 2, 64>;
+                    default: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 2, 64>;  // window 128
+                }
+            }
+        }
         switch (pack_cfg()) {
-            case 1: return (void *)scan_fast_kernel<M, 8, LISTS, 384, 1, true, 1>;
-            case 2: return (void *)scan_fast_kernel<M, 8, LISTS, 512, 1, true, 3>;
-            case 3: return (void *)scan_fast_kernel<M, 8, LISTS, 384, 1, true, 0>;
-            default: return (void *)scan_fast_kernel<M, 8, LISTS, 512, 1, true, 0>;
+            case 1: return (void *)scan_fast_kernel<M, 8, LISTS, 384, 1, 1, 1>;
+            case 2: return (void *)scan_fast_kernel<M, 8, LISTS, 512, 1, 1, 3>;
+            case 3: return (void *)scan_fast_kernel<M, 8, LISTS, 384, 1, 1, 0>;
+            default: return (void *)scan_fast_kernel<M, 8, LISTS, 512, 1, 1, 0>;
         }
     } else {
-        if (scan_cfg() == 0) return (void *)scan_fast_kernel<M, B, LISTS, 256, 2, false>;
-        return (void *)scan_fast_kernel<M, B, LISTS, 512, 1, false>;
+        if (scan_cfg() == 0) return (void *)scan_fast_kernel<M, B, LISTS, 256, 2, 0>;
+        return (void *)scan_fast_kernel<M, B, LISTS, 512, 1, 0>;
     }
 }
 
 template <int M, int B>
 static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
-                          const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st, const float *tables) {
-    void *kern = fast_kernel_ptr<M, B, false>();
-    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+                          const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st, const float *tables,
+                          float *gthr, bool q16_req, int timer) {
+    const bool q16 = B == 8 && q16_req && gthr != nullptr;
+    void *kern = fast_kernel_ptr<M, B, false>(q16);
+    const size_t smem = q16 ? smem_q16(kk) : pl.smem;
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ScanArgs a{};
     a.codes = codes; a.n_codes = n; a.q = q; a.nq = nq; a.cb = cb; a.ds = ds; a.kk = kk;
     a.nb = pl.nb; a.chunk = pl.chunk; a.nc = pl.nc; a.out = out; a.tables = tables;
+    a.gthr = gthr;
     void *args[] = {&a};
-    KernelTimer t(TK_LINEAR, st), tp(B == 8 ? TK_PACKED : -1, st);
-    RII_CUDA(cudaLaunchKernel(kern, dim3(pl.nb * pl.nc), dim3(B == 8 ? PACKED_NTH : scan_threads()), args, pl.smem, st));
+    KernelTimer t(timer, st), tp(B == 8 && timer == TK_LINEAR ? (q16 ? TK_Q16 : TK_PACKED) : -1, st);
+    const int nth = q16 ? q16_nth() : (B == 8 ? PACKED_NTH : scan_threads());
+    RII_CUDA(cudaLaunchKernel(kern, dim3(pl.nb * pl.nc), dim3(nth), args, smem, st));
     count_launch();
 }
 
 template <int M>
 static void launch_fast_m(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
-                          const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st, const float *tables) {
-    if (pl.B == 8) launch_fast_t<M, 8>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables);
-    else if (pl.B == 6) launch_fast_t<M, 6>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables);
-    else if (pl.B == 4) launch_fast_t<M, 4>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables);
-    else launch_fast_t<M, 2>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables);
+                          const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st, const float *tables,
+                          float *gthr, bool q16, int timer) {
+    if (pl.B == 8) launch_fast_t<M, 8>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
+    else if (pl.B == 6) launch_fast_t<M, 6>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
+    else if (pl.B == 4) launch_fast_t<M, 4>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
+    else launch_fast_t<M, 2>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
 }
 
 template <int B>
@@ -546,14 +651,15 @@ void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStre
 }
 
 void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_codes, int M, const float *q, int64_t nq,
-                        const float *cb, int D, int kk, uint64_t *out, cudaStream_t st, const float *tables) {
+                        const float *cb, int D, int kk, uint64_t *out, cudaStream_t st, const float *tables,
+                        float *gthr, bool q16, int timer) {
     const int ds = D / M;
     if (pl.fast) {
         switch (M) {
-            case 4: launch_fast_m<4>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables); break;
-            case 8: launch_fast_m<8>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables); break;
-            case 16: launch_fast_m<16>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables); break;
-            default: launch_fast_m<32>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables); break;
+            case 4: launch_fast_m<4>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
+            case 8: launch_fast_m<8>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
+            case 16: launch_fast_m<16>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
+            default: launch_fast_m<32>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
         }
     } else if (pl.B == 4) {
         launch_generic_t<4>(pl, codes, n_codes, M, q, nq, cb, ds, kk, out, st);
@@ -584,7 +690,7 @@ static void assign_scan_m(const uint8_t *codes, int64_t n, const uint8_t *center
                           int32_t *assign, float *dist, cudaStream_t st) {
     const int kk = 32, B = 8;
     const size_t smem = smem_fast(B, kk);
-    void *kern = fast_kernel_ptr<M, B, false>();
+    void *kern = fast_kernel_ptr<M, B, false>(false);
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t CH = (int64_t)1 << 23;  // codes per launch: bounds the [chunk][kk] keys
     uint64_t *keys = nullptr;
@@ -637,6 +743,43 @@ __global__ void __launch_bounds__(256) lut_tables_kernel(const float *__restrict
 void launch_lut_tables(const float *q, int64_t nq, const float *cb, int D, int M, float *tables, cudaStream_t st) {
     if (nq <= 0) return;
     lut_tables_kernel<<<(unsigned)nq, 256, 0, st>>>(q, nq, cb, M, D / M, tables);
+    RII_LAUNCHED();
+}
+
+// ------------------------------------------------- u16 tables: the bound ---
+// RII_Q16=0 disables the u16 fixed-point tables (A/B measurements).
+bool q16_enabled() {
+    const char *e = getenv("RII_Q16");
+    return !(e && e[0] == '0');
+}
+
+// out[i] = codes[i * stride] (a strided sample of the scanned codes).
+__global__ void strided_gather_kernel(const uint8_t *__restrict__ codes, int M, int64_t stride, int64_t n,
+                                      uint8_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(codes + i * stride * M);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(out + i * M);
+    for (int b = 0; b < M / 4; ++b) dst[b] = __ldg(src + b);
+}
+
+void launch_strided_gather(const uint8_t *codes, int M, int64_t stride, int64_t n, uint8_t *out, cudaStream_t st) {
+    if (n <= 0) return;
+    strided_gather_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(codes, M, stride, n, out);
+    RII_LAUNCHED();
+}
+
+// bound[q] = distance of the kk-th key of keys[q][kk] (+inf when the list is short).
+__global__ void kth_bound_kernel(const uint64_t *__restrict__ keys, int64_t nq, int kk, float *__restrict__ bound) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const uint64_t k = keys[q * kk + kk - 1];
+    bound[q] = k == KEY_MAX ? __int_as_float(0x7f800000) : key_dist(k);
+}
+
+void launch_kth_bound(const uint64_t *keys, int64_t nq, int kk, float *bound, cudaStream_t st) {
+    if (nq <= 0) return;
+    kth_bound_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, st>>>(keys, nq, kk, bound);
     RII_LAUNCHED();
 }
 

@@ -16,7 +16,8 @@ struct ScanPlan {
     bool fast;    // lane-rotated conflict-free LUT layout
     size_t smem;
 };
-ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available = false);
+ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available = false,
+                     int max_nc = 1 << 30);
 
 // Arguments of the lane-rotated scan kernel (linear mode, or list-major inverted
 // index mode where a work item is (posting list, up to B queries probing it)).
@@ -37,7 +38,7 @@ struct ScanArgs {
     int64_t P;
     const int64_t *offsets;  // lists: CSR of the posting lists
     const uint32_t *ids;
-    float *gthr;             // lists: per-query upper bound on the global kk-th distance
+    float *gthr;             // per-query upper bound on the global kk-th distance (optional in linear mode)
     // SDC mode (assignment): the "queries" are PQ codes qcodes[nq][M] whose
     // tables are rows of the SDC tables T (T_m[x^m][.]); the scanned codes are centres.
     const float *sdcT;
@@ -56,9 +57,18 @@ void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStre
 int64_t build_list_items(const int64_t *qoff, int64_t K, int B, const uint32_t *qlist, int64_t P, int4 *items,
                          int64_t cap, cudaStream_t st);
 void launch_fill_f32(float *p, int64_t n, float v, cudaStream_t st);
+// gthr (fast kernels): per-query upper bound on the global kk-th distance, read by
+// every CTA as a filter and lowered (atomicMin) with each CTA's final kk-th distance,
+// so chunks scanned later start from the bound of the earlier ones.  q16 (B == 8
+// plans only, gthr required): u16 fixed-point tables scaled by the bound at CTA start.
 void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_codes, int M, const float *q, int64_t nq,
                         const float *cb, int D, int kk, uint64_t *out, cudaStream_t st,
-                        const float *tables = nullptr);
+                        const float *tables = nullptr, float *gthr = nullptr, bool q16 = false,
+                        int timer = TK_LINEAR);
+// u16 tables (RII_Q16 != 0), the strided code sample and the kk-th-distance bound.
+bool q16_enabled();
+void launch_strided_gather(const uint8_t *codes, int M, int64_t stride, int64_t n, uint8_t *out, cudaStream_t st);
+void launch_kth_bound(const uint64_t *keys, int64_t nq, int kk, float *bound, cudaStream_t st);
 
 // Per-query rotated tables [nq][256][32] (M in {4,8,16,32}), CA1 values.
 void launch_lut_tables(const float *q, int64_t nq, const float *cb, int D, int M, float *tables, cudaStream_t st);

@@ -207,4 +207,102 @@ __device__ __forceinline__ void adc_packed(const uint8_t *lut, const uint32_t (&
     }
 }
 
+// ---- u16 fixed-point quad tables (4 queries per 8-byte column, integer SWAR) --
+// Entry q(v) = floor(min(v (x)_rd s, CAP)) with a per-query scale s = CAP / T (T an
+// upper bound on the query's final kk-th distance, from a sampled exact pass).
+// Word 0 of column c in row z = q(A) | q(C) << 16, word 1 = q(B) | q(D) << 16.
+// CAP = floor(65535 / M), so a 16-bit lane holding the sum of M entries never
+// carries into its neighbour: one IADD3 adds two lookups of two queries.
+// Since q(v) <= v*s (real), sum_m q <= s * d_exact (1 + M 2^-24): a code whose
+// exact distance is <= thr has quantised sum <= floor(s (x)_ru thr (x)_ru (1 + 2^-16)),
+// so the integer filter never drops a candidate that can enter the exact top list
+// (every pushed candidate is rescored canonically before compaction).
+template <int M>
+__host__ __device__ constexpr uint32_t q16_cap() { return 65535u / (uint32_t)M; }
+
+__device__ __forceinline__ uint32_t q16_entry(float v, float s, float cap) {
+    return __float2uint_rd(fminf(__fmul_rd(v, s), cap));
+}
+
+// Integer threshold of an fp32 distance threshold t (+inf -> pass everything).
+__device__ __forceinline__ uint32_t q16_threshold(float t, float s) {
+    const float x = __fmul_ru(__fmul_ru(t, s), 1.0000153f);  // (1 + 2^-16), rounded up
+    return x >= 4294967040.f ? 0xffffffffu : __float2uint_rd(x);
+}
+
+template <int M>
+__device__ __forceinline__ void load_lut_quad_q16(uint32_t *dst, const float *__restrict__ ta,
+                                                  const float *__restrict__ tb, const float *__restrict__ tc,
+                                                  const float *__restrict__ td, float sa, float sb, float sc,
+                                                  float sd) {
+    const float4 *a4 = reinterpret_cast<const float4 *>(ta), *b4 = reinterpret_cast<const float4 *>(tb);
+    const float4 *c4 = reinterpret_cast<const float4 *>(tc), *d4 = reinterpret_cast<const float4 *>(td);
+    uint4 *o = reinterpret_cast<uint4 *>(dst);
+    const float cap = (float)q16_cap<M>();
+    auto pk = [&](float lo, float slo, float hi, float shi) {
+        return q16_entry(lo, slo, cap) | (q16_entry(hi, shi, cap) << 16);
+    };
+    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 4; e += blockDim.x) {
+        const float4 A = __ldg(a4 + e), B = __ldg(b4 + e), C = __ldg(c4 + e), D = __ldg(d4 + e);
+        o[2 * e] = make_uint4(pk(A.x, sa, C.x, sc), pk(B.x, sb, D.x, sd), pk(A.y, sa, C.y, sc), pk(B.y, sb, D.y, sd));
+        o[2 * e + 1] =
+            make_uint4(pk(A.z, sa, C.z, sc), pk(B.z, sb, D.z, sd), pk(A.w, sa, C.w, sc), pk(B.w, sb, D.w, sd));
+    }
+}
+
+// PRMT selectors of the q16 kernel: byte0 <- byte (t & 1) of the column register
+// (two column offsets per register), byte1 <- code byte ((t ^ r) & 3) of the
+// permuted word, bytes 2-3 <- bytes 2-3 of the column register (table base >> 16).
+__device__ __forceinline__ void make_selectors_q16(uint32_t r, uint32_t (&sel)[4]) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) sel[t] = 0x7600u | ((((uint32_t)t ^ r) & 3u) << 4) | (4u + ((uint32_t)t & 1u));
+}
+
+// 8-byte shared load at address off + p * QUAD_BYTES (p an unrolled constant).
+__device__ __forceinline__ uint2 lds64_quad(uint32_t off, int p) {
+    uint2 v;
+    if (p == 0) asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(off));
+    else if (p == 1) asm volatile("ld.shared.v2.u32 {%0, %1}, [%2+65536];" : "=r"(v.x), "=r"(v.y) : "r"(off));
+    else if (p == 2) asm volatile("ld.shared.v2.u32 {%0, %1}, [%2+131072];" : "=r"(v.x), "=r"(v.y) : "r"(off));
+    else asm volatile("ld.shared.v2.u32 {%0, %1}, [%2+196608];" : "=r"(v.x), "=r"(v.y) : "r"(off));
+    return v;
+}
+
+// Quantised lane-rotated ADC of one code against NQ u16 quad tables.  colA / colB
+// hold the byte offsets 8 (l ^ t) of steps t = 0,1 / 2,3 (bytes 0-1); step
+// j = 4a + t reads column (l ^ t) ^ 4a, i.e. the register XOR a * 0x2020.
+// acc0[p] = sums of queries (4p, 4p+2) in (low, high) halves; acc1[p] = (4p+1, 4p+3).
+template <int M, int NQ>
+__device__ __forceinline__ void adc_q16(const uint32_t (&w)[M / 4], uint32_t rw,
+                                        const uint32_t (&sel)[4], uint32_t colA, uint32_t colB,
+                                        uint32_t (&acc0)[NQ], uint32_t (&acc1)[NQ]) {
+    constexpr int W = M / 4;
+    uint32_t wp[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) wp[i] = w[i];
+    permute_words<W>(wp, rw);
+    uint2 h[NQ];
+#pragma unroll
+    for (int aw = 0; aw < W; ++aw) {
+        const uint32_t ca = colA ^ (uint32_t)(aw * 0x2020), cb = colB ^ (uint32_t)(aw * 0x2020);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t off = __byte_perm(wp[aw], t < 2 ? ca : cb, sel[t]);
+#pragma unroll
+            for (int p = 0; p < NQ; ++p) {
+                const uint2 v = lds64_quad(off, p);  // off = the complete shared address
+                if ((t & 1) == 0) {
+                    h[p] = v;
+                } else if (aw == 0 && t == 1) {
+                    acc0[p] = h[p].x + v.x;
+                    acc1[p] = h[p].y + v.y;
+                } else {
+                    acc0[p] = acc0[p] + h[p].x + v.x;
+                    acc1[p] = acc1[p] + h[p].y + v.y;
+                }
+            }
+        }
+    }
+}
+
 }  // namespace rii

@@ -361,3 +361,50 @@ def test_save_load_roundtrip(rii, ref, tmp_path):
         with pytest.raises(rii.RiiError) as e:
             rii.Index.load(str(tmp_path / bad))
         assert e.value.status == 1
+
+
+# ------------------------------------------------- u16 fixed-point tables ---
+@pytest.mark.parametrize("kind,N,D,M,nq,topk", [("deep", 40_009, 96, 32, 45, 100), ("sift", 33_333, 128, 16, 19, 64),
+                                                ("deep", 20_011, 96, 8, 23, 10), ("gaussian", 17_003, 32, 4, 9, 100)])
+def test_linear_u16_tables(rii, ref, monkeypatch, kind, N, D, M, nq, topk):
+    """The u16 fixed-point SWAR scan (sampled kk-th bound, integer filter, canonical
+    rescore) must return exactly the oracle's Alg. 1 result, whole and subset; the
+    threshold RII_Q16_MIN=1 forces it onto these small sizes (several chunks, ragged
+    tails, query batches not a multiple of 8)."""
+    monkeypatch.setenv("RII_Q16_MIN", "1")
+    x = gen.base(kind, N, D, seed=N)
+    q = gen.base(kind, nq, D, seed=N, stream=gen.STREAM_QUERY)
+    g, o = _build_pair(rii, ref, x, M, 0, train_rows=x[:4000], train_iter=3)
+    for sub in (None, gen.subset(N, N // 2 + 1, seed=3)):
+        gr = g.query(q, topk, target_ids=sub, path="linear")
+        orr = o.query(q, topk, S=sub, path=1)
+        assert_topk_parity(ref, o.cb, o.codes, q, gr, orr, S=sub, what=f"u16 {kind} M={M}")
+        monkeypatch.setenv("RII_Q16", "0")  # the bf16 / fp32 path gives the identical answer
+        g2 = g.query(q, topk, target_ids=sub, path="linear")
+        monkeypatch.delenv("RII_Q16")
+        assert np.array_equal(gr[0], g2[0]) and np.array_equal(gr[1], g2[1])
+
+
+def test_linear_u16_duplicates_and_zero_distance(rii, ref, monkeypatch):
+    """Ties and T = 0: every code repeated 60 times (one 8-query batch sees > NEWCAP
+    equal candidates per step window) and queries equal to stored vectors in the
+    lossless case (kk-th bound 0, scale clamp)."""
+    monkeypatch.setenv("RII_Q16_MIN", "1")
+    base = gen.deep_like(300, 96, seed=9)
+    x = np.concatenate([base] * 60)
+    q = np.concatenate([gen.deep_like(7, 96, seed=9, stream=gen.STREAM_QUERY), base[:5]])
+    g, o = _build_pair(rii, ref, x, 32, 0, train_rows=x[:3000], train_iter=2)
+    gr = g.query(q, 100, path="linear")
+    orr = o.query(q, 100, path=1)
+    assert np.array_equal(gr[0], orr[0]) and np.array_equal(gr[1], orr[1])
+    xl = np.concatenate([gen.lossless(300, 16, seed=5)] * 200)  # >= 32 zero-distance copies in the sample
+    cb = np.tile(np.arange(256, dtype=np.float32)[None, :, None], (16, 1, 1))
+    gl = rii.Index(16, 16)
+    gl.set_codebook(cb)
+    gl.add(xl)
+    ql = np.concatenate([xl[:6], np.random.default_rng(5).integers(0, 256, size=(6, 16)).astype(np.float32)])
+    ids, dist, _ = gl.query(ql, 10, path="linear")
+    for i in range(len(ql)):
+        d = ((xl.astype(np.int64) - ql[i].astype(np.int64)) ** 2).sum(1)
+        order = np.lexsort((np.arange(len(xl)), d))[:10]
+        assert np.array_equal(ids[i], order) and np.array_equal(dist[i], d[order].astype(np.float32))

@@ -526,10 +526,17 @@ constexpr int64_t QBATCH = 16384;
 void search_local(const rii_index *x, const QueryArgs &a, cudaStream_t st, int64_t *out_ids, float *out_dist,
                   uint64_t *out_keys) {
     const Targets t = prepare_targets(x, a, st);
-    for (int64_t q0 = 0; q0 < a.nq; q0 += QBATCH) {
+    // IVF: smaller batches keep the batch's per-query tables (32 KB each) L2-resident
+    // while the list-major items re-read them once per probed list.
+    int64_t qb = QBATCH;
+    if (a.path == RII_PATH_IVF) {
+        const char *e = getenv("RII_IVF_QBATCH");
+        qb = e ? std::max<int64_t>(atoll(e), 1) : QBATCH;
+    }
+    for (int64_t q0 = 0; q0 < a.nq; q0 += qb) {
         QueryArgs b = a;
         b.q = a.q + q0 * x->D;
-        b.nq = std::min<int64_t>(QBATCH, a.nq - q0);
+        b.nq = std::min<int64_t>(qb, a.nq - q0);
         search_batch(x, b, t, st, out_ids ? out_ids + q0 * a.topk : nullptr, out_dist ? out_dist + q0 * a.topk : nullptr,
                      out_keys ? out_keys + q0 * a.kk : nullptr);
     }

@@ -92,9 +92,18 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
         const int64_t rem = a.nq - (int64_t)qb * B;
         nqi = rem < B ? (int)rem : B;
     }
+    // List mode: the item's query indices are read from qlist once into shared memory.
+    int *qid_s = reinterpret_cast<int *>(qsc + B);
+    if constexpr (LISTS) {
+        if (threadIdx.x < B) {
+            const int qq = (int)threadIdx.x < nqi ? (int)threadIdx.x : nqi - 1;
+            qid_s[threadIdx.x] = (int)(a.qlist[qstart + qq] / a.P);
+        }
+        __syncthreads();
+    }
     auto query_of = [&](int qq) -> int64_t {  // global query index of slot qq
         qq = qq < nqi ? qq : nqi - 1;
-        if constexpr (LISTS) return a.qlist[qstart + qq] / a.P;
+        if constexpr (LISTS) return qid_s[qq];
         else return (int64_t)qb * B + qq;
     };
     const int D = M * a.ds, tid = threadIdx.x, lane = tid & 31;
@@ -220,6 +229,18 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     int *s_ovf = scratch + 1, *s_cnt0 = scratch + 2;  // flags, fill snapshot at the window start
     uint32_t w[U][W];
     uint32_t cid[U];  // candidate id: position in `codes` (linear) or the list's id (lists)
+    // List mode: the posting-list ids are prefetched one step ahead of the codes they
+    // address (idn = ids of step b), so the two dependent loads overlap across steps.
+    uint32_t idn[U];
+    auto load_ids = [&](int64_t b) {
+        if constexpr (LISTS) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t p = b + u * NTH + tid;
+                idn[u] = p < c1 ? __ldg(a.ids + p) : 0u;
+            }
+        }
+    };
     auto load_step = [&](int64_t b, uint32_t(&dst)[U][W], uint32_t(&did)[U]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -228,13 +249,15 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
             for (int i = 0; i < W; ++i) dst[u][i] = 0;
             did[u] = 0;
             if (p < c1) {
-                if constexpr (LISTS) did[u] = __ldg(a.ids + p);
+                if constexpr (LISTS) did[u] = idn[u];
                 else did[u] = (uint32_t)p;
                 load_code<W>(codes + (size_t)did[u] * M, dst[u]);
             }
         }
+        load_ids(b + STEP);
     };
     int64_t base = c0;
+    load_ids(base);
     load_step(base, w, cid);
     int safe = 0;
     while (base < c1) {
@@ -326,6 +349,7 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
             set_thq();
             if (rolled) {
                 base = wstart;
+                load_ids(base);
                 load_step(base, w, cid);
                 safe = 4;
                 continue;
@@ -612,8 +636,10 @@ static void launch_generic_t(const ScanPlan &pl, const uint8_t *codes, int64_t n
 bool list_major_supported(int M) { return M == 4 || M == 8 || M == 16 || M == 32; }
 
 int list_major_B(int kk, double avg_len) {
+    const char *pe = getenv("RII_LIST_PACKED_MIN");  // A/B knob
+    const double pmin = pe ? atof(pe) : (double)PACKED_MIN_CODES;
     for (int B : {8, 6, 4, 2}) {
-        if (B == 8 && (!packed_enabled() || avg_len < (double)PACKED_MIN_CODES)) continue;
+        if (B == 8 && (!packed_enabled() || avg_len < pmin)) continue;
         if (smem_fast(B, kk) <= SMEM_CAP) return B;
     }
     return 0;

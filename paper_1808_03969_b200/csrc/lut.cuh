@@ -41,10 +41,24 @@ __device__ __forceinline__ void load_lut_pair(float *lutp, const float *__restri
                                               const float *__restrict__ tb) {
     const float4 *a4 = reinterpret_cast<const float4 *>(ta), *b4 = reinterpret_cast<const float4 *>(tb);
     float4 *d4 = reinterpret_cast<float4 *>(lutp);
-    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 4; e += blockDim.x) {
-        const float4 a = __ldg(a4 + e), b = __ldg(b4 + e);
-        d4[2 * e] = make_float4(a.x, b.x, a.y, b.y);
-        d4[2 * e + 1] = make_float4(a.z, b.z, a.w, b.w);
+    // 8 independent 16-byte loads in flight per thread before the stores (the copy is
+    // latency-bound otherwise: one CTA per SM waits on it before scanning)
+    constexpr int UNR = 4;
+    for (int e0 = threadIdx.x; e0 < LUT_Q_FLOATS / 4; e0 += UNR * blockDim.x) {
+        float4 a[UNR], b[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < LUT_Q_FLOATS / 4) { a[u] = __ldg(a4 + e); b[u] = __ldg(b4 + e); }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < LUT_Q_FLOATS / 4) {
+                d4[2 * e] = make_float4(a[u].x, b[u].x, a[u].y, b[u].y);
+                d4[2 * e + 1] = make_float4(a[u].z, b[u].z, a[u].w, b[u].w);
+            }
+        }
     }
 }
 
@@ -139,10 +153,23 @@ __device__ __forceinline__ void load_lut_quad(uint32_t *dst, const float *__rest
     uint4 *o = reinterpret_cast<uint4 *>(dst);
     auto hi = [](float v) { return __float_as_uint(v) & 0xffff0000u; };
     auto lo = [](float v) { return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v)); };
-    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 4; e += blockDim.x) {
-        const float4 A = __ldg(a4 + e), B = __ldg(b4 + e), C = __ldg(c4 + e), D = __ldg(d4 + e);
-        o[2 * e] = make_uint4(hi(A.x) | lo(C.x), hi(B.x) | lo(D.x), hi(A.y) | lo(C.y), hi(B.y) | lo(D.y));
-        o[2 * e + 1] = make_uint4(hi(A.z) | lo(C.z), hi(B.z) | lo(D.z), hi(A.w) | lo(C.w), hi(B.w) | lo(D.w));
+    constexpr int UNR = 2;  // 8 independent 16-byte loads in flight per thread
+    for (int e0 = threadIdx.x; e0 < LUT_Q_FLOATS / 4; e0 += UNR * blockDim.x) {
+        float4 A[UNR], B[UNR], C[UNR], D[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < LUT_Q_FLOATS / 4) { A[u] = __ldg(a4 + e); B[u] = __ldg(b4 + e); C[u] = __ldg(c4 + e); D[u] = __ldg(d4 + e); }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e >= LUT_Q_FLOATS / 4) continue;
+            o[2 * e] = make_uint4(hi(A[u].x) | lo(C[u].x), hi(B[u].x) | lo(D[u].x), hi(A[u].y) | lo(C[u].y),
+                                  hi(B[u].y) | lo(D[u].y));
+            o[2 * e + 1] = make_uint4(hi(A[u].z) | lo(C[u].z), hi(B[u].z) | lo(D[u].z), hi(A[u].w) | lo(C[u].w),
+                                      hi(B[u].w) | lo(D[u].w));
+        }
     }
 }
 
@@ -242,11 +269,23 @@ __device__ __forceinline__ void load_lut_quad_q16(uint32_t *dst, const float *__
     auto pk = [&](float lo, float slo, float hi, float shi) {
         return q16_entry(lo, slo, cap) | (q16_entry(hi, shi, cap) << 16);
     };
-    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 4; e += blockDim.x) {
-        const float4 A = __ldg(a4 + e), B = __ldg(b4 + e), C = __ldg(c4 + e), D = __ldg(d4 + e);
-        o[2 * e] = make_uint4(pk(A.x, sa, C.x, sc), pk(B.x, sb, D.x, sd), pk(A.y, sa, C.y, sc), pk(B.y, sb, D.y, sd));
-        o[2 * e + 1] =
-            make_uint4(pk(A.z, sa, C.z, sc), pk(B.z, sb, D.z, sd), pk(A.w, sa, C.w, sc), pk(B.w, sb, D.w, sd));
+    constexpr int UNR = 2;  // 8 independent 16-byte loads in flight per thread
+    for (int e0 = threadIdx.x; e0 < LUT_Q_FLOATS / 4; e0 += UNR * blockDim.x) {
+        float4 A[UNR], B[UNR], C[UNR], D[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < LUT_Q_FLOATS / 4) { A[u] = __ldg(a4 + e); B[u] = __ldg(b4 + e); C[u] = __ldg(c4 + e); D[u] = __ldg(d4 + e); }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e >= LUT_Q_FLOATS / 4) continue;
+            o[2 * e] = make_uint4(pk(A[u].x, sa, C[u].x, sc), pk(B[u].x, sb, D[u].x, sd), pk(A[u].y, sa, C[u].y, sc),
+                                  pk(B[u].y, sb, D[u].y, sd));
+            o[2 * e + 1] = make_uint4(pk(A[u].z, sa, C[u].z, sc), pk(B[u].z, sb, D[u].z, sd),
+                                      pk(A[u].w, sa, C[u].w, sc), pk(B[u].w, sb, D[u].w, sd));
+        }
     }
 }
 

@@ -124,7 +124,7 @@ struct rii_index {
     // scratch (query side is const-callable: mutable)
     mutable Buf s_q, s_S, s_pos, s_sub, s_part, s_keys, s_gather, s_d0, s_probe, s_roff, s_rids, s_rkey, s_rval,
         s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_items, s_gthr, s_tables, s_cpart, s_ckeys, s_take,
-        s_samp, s_spart, s_bound;
+        s_samp, s_spart, s_bound, s_skey, s_tab16, s_qscale;
 };
 
 namespace {
@@ -200,6 +200,14 @@ void ensure_T(rii_index *x, cudaStream_t st) {
 __global__ void iota_u32_kernel(uint32_t *v, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) v[i] = (uint32_t)i;
+}
+
+// List-major two-phase split: pairs (q, r) with rank r < r0 keep bucket probes[q][r],
+// the others go to bucket K + probes[q][r] (phase B, u16 tables with bounds).
+__global__ void split_keys_kernel(const int32_t *probes, int64_t npairs, int64_t P, int64_t r0, int64_t K,
+                                  int32_t *keys) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < npairs) keys[i] = probes[i] + (i % P < r0 ? 0 : (int32_t)K);
 }
 
 __global__ void gather_i32_kernel(const int32_t *src, const int64_t *pos, int64_t n, int32_t *dst, uint32_t *val) {
@@ -347,6 +355,10 @@ Targets prepare_targets(const rii_index *x, const QueryArgs &a, cudaStream_t st)
 
 // u16 tables: scans of at least RII_Q16_MIN (default 2^19) codes; the bound comes
 // from min(Q16_SAMPLE, n / 4) strided codes.
+static double list_q16_min_len() {  // RII_LIST_Q16_MIN: average list length for two-phase u16
+    const char *e = getenv("RII_LIST_Q16_MIN");
+    return e ? atof(e) : 1024.0;
+}
 static int64_t q16_sample() {
     const char *e = getenv("RII_Q16_SAMPLE");
     return e ? atoll(e) : ((int64_t)1 << 15);
@@ -403,7 +415,8 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             // every CTA filters with, and publishes its kk-th distance into, gthr
             float *gthr = x->s_gthr.get<float>(a.nq);
             const int64_t ns = std::min<int64_t>(q16_sample(), n_codes / 4);
-            const bool q16 = pl.B == 8 && pl.fast && q16_enabled() && n_codes >= q16_min_codes() && ns >= 4 * kk;
+            const bool q16 = pl.B == 8 && pl.fast && q16_enabled() && q16_supported(kk) && n_codes >= q16_min_codes() &&
+                             ns >= 4 * kk;
             if (!q16) {
                 if (pl.fast) launch_fill_f32(gthr, a.nq, INFINITY, st);
                 else gthr = nullptr;
@@ -481,13 +494,28 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             uint32_t *vals = x->s_lq.get<uint32_t>(npairs);
             iota_u32_kernel<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(vals, npairs);
             RII_LAUNCHED();
-            int64_t *qoff = x->s_qoff.get<int64_t>(x->K + 1);
+            // Two phases (u16 tables): the pairs of the r0 nearest lists of every query run
+            // first with fp32 / bf16 tables and publish each query's kk-th distance as its
+            // bound; the remaining pairs run with u16 tables scaled by those bounds.
+            const int64_t r0 = std::max<int64_t>(1, std::min<int64_t>(P, ceil_div(4 * kk, (int64_t)std::max(avg_len, 1.0))));
+            const bool q16l = q16_enabled() && q16_supported(kk) && P > r0 && avg_len >= list_q16_min_len();
+            const int64_t nb = q16l ? 2 * x->K : x->K;
+            const int32_t *keys = probes;
+            if (q16l) {
+                int32_t *k2 = x->s_skey.get<int32_t>(npairs);
+                split_keys_kernel<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(probes, npairs, P, r0, x->K, k2);
+                RII_LAUNCHED();
+                keys = k2;
+            }
+            int64_t *qoff = x->s_qoff.get<int64_t>(nb + 1);
             uint32_t *qlist = x->s_ql.get<uint32_t>(npairs);
-            build_csr(probes, vals, npairs, x->K, qoff, qlist, st);  // (query, rank) pairs grouped by list
-            const int64_t cap = npairs / Bl + x->K + 1;
+            build_csr(keys, vals, npairs, nb, qoff, qlist, st);  // (query, rank) pairs grouped by list
+            const int64_t cap = npairs / std::min(Bl, 8) + nb + 1;
             int4 *items = x->s_items.get<int4>(cap);
             tr.mark("pairs csr");
             const int64_t n_items = build_list_items(qoff, x->K, Bl, qlist, P, items, cap, st);
+            const int64_t n_items_b = q16l ? build_list_items(qoff + x->K, x->K, 8, qlist, P, items + n_items,
+                                                              cap - n_items, st) : 0;
             tr.mark("items");
             uint64_t *pp = x->s_part.get<uint64_t>((size_t)npairs * kk);
             float *gthr = x->s_gthr.get<float>(a.nq);
@@ -498,6 +526,16 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             sa.items = items; sa.qlist = qlist; sa.P = P; sa.offsets = off; sa.ids = ids; sa.gthr = gthr;
             sa.tables = tables;
             launch_list_scan(x->M, Bl, sa, n_items, st);
+            if (n_items_b > 0) {
+                tr.mark("list scan A");
+                uint16_t *t16 = x->s_tab16.get<uint16_t>((size_t)a.nq * LUT_Q_FLOATS);
+                float *qsc = x->s_qscale.get<float>(a.nq);
+                launch_q16_tables(tables, gthr, a.nq, x->M, t16, qsc, st);
+                sa.qtab16 = t16;
+                sa.qscale = qsc;
+                sa.items = items + n_items;
+                launch_list_scan(x->M, 8, sa, n_items_b, st, true);
+            }
             tr.mark("list scan");
             parts = pp;
             if (Bl != 8) {  // fp32-pair items keep lane-rotated keys: rescore in the merge

@@ -53,7 +53,6 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     constexpr int W = M / 4, NP = B / 2, NQ = B / 4;
     constexpr bool PACKED = TAB != 0, Q16 = TAB == 2;
     static_assert(!PACKED || B % 4 == 0, "packed tables hold 4 queries each");
-    static_assert(!(Q16 && LISTS), "u16 tables need a per-query bound (linear mode)");
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t *lut = smem;
     const int kk = a.kk;
@@ -108,7 +107,15 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     };
     const int D = M * a.ds, tid = threadIdx.x, lane = tid & 31;
 
-    if constexpr (Q16) {
+    if (Q16 && a.qtab16) {
+        // precomputed per-query u16 tables (q16_tables_kernel) with their scales
+        if (tid < B) qsc[tid] = __ldg(a.qscale + query_of(tid));
+#pragma unroll
+        for (int p = 0; p < NQ; ++p)
+            load_lut_quad_u16(reinterpret_cast<uint32_t *>(lut + p * QUAD_BYTES), a.qtab16 + query_of(4 * p) * LUT_Q_FLOATS,
+                              a.qtab16 + query_of(4 * p + 1) * LUT_Q_FLOATS, a.qtab16 + query_of(4 * p + 2) * LUT_Q_FLOATS,
+                              a.qtab16 + query_of(4 * p + 3) * LUT_Q_FLOATS);
+    } else if constexpr (Q16) {
         // u16 tables: per-query scale s = CAP / T (T = +inf -> s = 0: everything passes)
         float qs[B];
 #pragma unroll
@@ -473,6 +480,7 @@ __global__ void __launch_bounds__(NT, 1)
 // B == 8 means the bf16-packed variant (2 quad tables); otherwise B / 2 fp32 pair tables.
 // u16 variant: 64 KB-aligned tables + the aux block below or above them (kernel).
 static size_t smem_q16(int kk) { return (size_t)2 * QUAD_BYTES + 2 * (size_t)smem_aux_bytes(8, kk) + 16; }
+bool q16_supported(int kk) { return smem_q16(kk) <= 227 * 1024; }
 static size_t smem_fast(int B, int kk) {
     const size_t lut = B == 8 ? (size_t)2 * QUAD_BYTES : (size_t)(B / 2) * LUT_PAIR_BYTES;
     return lut + smem_aux_bytes(B, kk);
@@ -568,7 +576,9 @@ static int q16_nth() {
 template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr(bool q16 = false) {
     if constexpr (B == 8) {
-        if constexpr (!LISTS) {
+        if constexpr (LISTS) {
+            if (q16) return (void *)scan_fast_kernel<M, 8, true, 384, 1, 2, 64>;  // window 128
+        } else {
             if (q16) {
                 // RII_Q16_CFG (A/B): threads x codes per step, barrier window (steps).
                 // 384 threads keep the kernel spill-free (168 registers); the window
@@ -646,33 +656,36 @@ int list_major_B(int kk, double avg_len) {
 }
 
 template <int M, int B>
-static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st) {
-    void *kern = fast_kernel_ptr<M, B, true>();
-    const size_t smem = smem_fast(B, a.kk);
+static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
+    q16 = q16 && B == 8;
+    void *kern = fast_kernel_ptr<M, B, true>(q16);
+    const size_t smem = q16 ? smem_q16(a.kk) : smem_fast(B, a.kk);
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ScanArgs aa = a;
     void *args[] = {&aa};
     KernelTimer t(TK_IVF, st);
-    RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)n_items), dim3(B == 8 ? PACKED_NTH : scan_threads()), args, smem, st));
+    const int nth = q16 ? 384 : (B == 8 ? PACKED_NTH : scan_threads());
+    RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)n_items), dim3(nth), args, smem, st));
     count_launch();
 }
 
 template <int M>
-static void launch_list_m(int B, const ScanArgs &a, int64_t n_items, cudaStream_t st) {
-    if (B == 8) launch_list_t<M, 8>(a, n_items, st);
-    else if (B == 6) launch_list_t<M, 6>(a, n_items, st);
-    else if (B == 4) launch_list_t<M, 4>(a, n_items, st);
-    else launch_list_t<M, 2>(a, n_items, st);
+static void launch_list_m(int B, const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
+    if (B == 8) launch_list_t<M, 8>(a, n_items, st, q16);
+    else if (B == 6) launch_list_t<M, 6>(a, n_items, st, false);
+    else if (B == 4) launch_list_t<M, 4>(a, n_items, st, false);
+    else launch_list_t<M, 2>(a, n_items, st, false);
 }
 
-void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStream_t st) {
+void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
     if (n_items <= 0) return;
     if (B == 0) throw Error(1, "topk too large for the list-major scan");
+    if (q16 && (B != 8 || !q16_supported(a.kk) || !a.gthr)) throw Error(1, "u16 list scan needs B = 8, kk <= 256, gthr");
     switch (M) {
-        case 4: launch_list_m<4>(B, a, n_items, st); break;
-        case 8: launch_list_m<8>(B, a, n_items, st); break;
-        case 16: launch_list_m<16>(B, a, n_items, st); break;
-        default: launch_list_m<32>(B, a, n_items, st); break;
+        case 4: launch_list_m<4>(B, a, n_items, st, q16); break;
+        case 8: launch_list_m<8>(B, a, n_items, st, q16); break;
+        case 16: launch_list_m<16>(B, a, n_items, st, q16); break;
+        default: launch_list_m<32>(B, a, n_items, st, q16); break;
     }
 }
 
@@ -806,6 +819,36 @@ __global__ void kth_bound_kernel(const uint64_t *__restrict__ keys, int64_t nq, 
 void launch_kth_bound(const uint64_t *keys, int64_t nq, int kk, float *bound, cudaStream_t st) {
     if (nq <= 0) return;
     kth_bound_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, st>>>(keys, nq, kk, bound);
+    RII_LAUNCHED();
+}
+
+// Per-query u16 tables (lut.cuh q16 entries) from the fp32 tables and the current
+// bounds: scale[q] = CAP / gthr[q] (rounded down), out[q] = q16(tables[q]).
+template <int M>
+__global__ void __launch_bounds__(256) q16_tables_kernel(const float *__restrict__ tables, const float *__restrict__ gthr,
+                                                         int64_t nq, uint16_t *__restrict__ out, float *__restrict__ scale) {
+    const int64_t q = blockIdx.x;
+    const float s = __fdiv_rd((float)q16_cap<M>(), fmaxf(__ldcg(gthr + q), 1e-30f));
+    if (threadIdx.x == 0) scale[q] = s;
+    const float cap = (float)q16_cap<M>();
+    const float4 *t4 = reinterpret_cast<const float4 *>(tables + q * LUT_Q_FLOATS);
+    uint2 *o = reinterpret_cast<uint2 *>(out + q * LUT_Q_FLOATS);
+    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 4; e += blockDim.x) {
+        const float4 v = __ldg(t4 + e);
+        o[e] = make_uint2(q16_entry(v.x, s, cap) | (q16_entry(v.y, s, cap) << 16),
+                          q16_entry(v.z, s, cap) | (q16_entry(v.w, s, cap) << 16));
+    }
+}
+
+void launch_q16_tables(const float *tables, const float *gthr, int64_t nq, int M, uint16_t *out, float *scale,
+                       cudaStream_t st) {
+    if (nq <= 0) return;
+    switch (M) {
+        case 4: q16_tables_kernel<4><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
+        case 8: q16_tables_kernel<8><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
+        case 16: q16_tables_kernel<16><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
+        default: q16_tables_kernel<32><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
+    }
     RII_LAUNCHED();
 }
 

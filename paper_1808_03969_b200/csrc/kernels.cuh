@@ -43,12 +43,17 @@ struct ScanArgs {
     // tables are rows of the SDC tables T (T_m[x^m][.]); the scanned codes are centres.
     const float *sdcT;
     const uint8_t *qcodes;
+    // u16 list mode: precomputed per-query u16 tables [nq][256][32] and their scales
+    const uint16_t *qtab16;
+    const float *qscale;
 };
 
 // List-major inverted-index scan: B queries per CTA share one posting list's codes.
 bool list_major_supported(int M);
 int list_major_B(int kk, double avg_len);
-void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStream_t st);
+// q16: u16 fixed-point tables (B == 8, kk <= 256), scaled per item by the queries'
+// gthr bounds (items whose queries have no bound yet should run without q16).
+void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16 = false);
 // Work items of the list-major scan: for every list k, ceil(#queries probing k / B)
 // items {k, first entry of qlist, count, 0}.  qoff = CSR of qlist by list.
 // Returns the number of items (synchronises the stream).
@@ -67,6 +72,10 @@ void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_code
                         int timer = TK_LINEAR);
 // u16 tables (RII_Q16 != 0), the strided code sample and the kk-th-distance bound.
 bool q16_enabled();
+bool q16_supported(int kk);  // shared-memory budget of the u16 kernels (kk <= 256)
+// out[q] = u16 entries of tables[q] with scale[q] = CAP / gthr[q] (u16 list scan).
+void launch_q16_tables(const float *tables, const float *gthr, int64_t nq, int M, uint16_t *out, float *scale,
+                       cudaStream_t st);
 void launch_strided_gather(const uint8_t *codes, int M, int64_t stride, int64_t n, uint8_t *out, cudaStream_t st);
 void launch_kth_bound(const uint64_t *keys, int64_t nq, int kk, float *bound, cudaStream_t st);
 

@@ -289,6 +289,38 @@ __device__ __forceinline__ void load_lut_quad_q16(uint32_t *dst, const float *__
     }
 }
 
+// Quad layout from four precomputed per-query u16 tables ([z][32 columns] u16, as
+// written by q16_tables_kernel): column word 0 = A | C << 16, word 1 = B | D << 16.
+__device__ __forceinline__ void load_lut_quad_u16(uint32_t *dst, const uint16_t *__restrict__ ta,
+                                                  const uint16_t *__restrict__ tb, const uint16_t *__restrict__ tc,
+                                                  const uint16_t *__restrict__ td) {
+    const uint4 *a4 = reinterpret_cast<const uint4 *>(ta), *b4 = reinterpret_cast<const uint4 *>(tb);
+    const uint4 *c4 = reinterpret_cast<const uint4 *>(tc), *d4 = reinterpret_cast<const uint4 *>(td);
+    uint4 *o = reinterpret_cast<uint4 *>(dst);
+    constexpr int N16 = LUT_Q_FLOATS / 8;  // 16-byte chunks (8 columns) per table
+    constexpr int UNR = 2;
+    for (int e0 = threadIdx.x; e0 < N16; e0 += UNR * blockDim.x) {
+        uint4 A[UNR], B[UNR], C[UNR], D[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < N16) { A[u] = __ldg(a4 + e); B[u] = __ldg(b4 + e); C[u] = __ldg(c4 + e); D[u] = __ldg(d4 + e); }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e >= N16) continue;
+            // chunk e = columns 8e'..8e'+7 of one row; output 8 columns x 8 bytes = 4 uint4
+            const uint32_t a[4] = {A[u].x, A[u].y, A[u].z, A[u].w}, b[4] = {B[u].x, B[u].y, B[u].z, B[u].w};
+            const uint32_t c[4] = {C[u].x, C[u].y, C[u].z, C[u].w}, d[4] = {D[u].x, D[u].y, D[u].z, D[u].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)  // word k holds columns 2k (low) and 2k+1 (high)
+                o[4 * e + k] = make_uint4(__byte_perm(a[k], c[k], 0x5410), __byte_perm(b[k], d[k], 0x5410),
+                                          __byte_perm(a[k], c[k], 0x7632), __byte_perm(b[k], d[k], 0x7632));
+        }
+    }
+}
+
 // PRMT selectors of the q16 kernel: byte0 <- byte (t & 1) of the column register
 // (two column offsets per register), byte1 <- code byte ((t ^ r) & 3) of the
 // permuted word, bytes 2-3 <- bytes 2-3 of the column register (table base >> 16).

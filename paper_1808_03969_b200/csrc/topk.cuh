@@ -95,18 +95,111 @@ __device__ inline void bitonic_merge_rows(uint64_t *a, int nq, int stride, int S
     }
 }
 
+// ---- warp-level compaction (few fresh candidates: no block barriers) -------
+// Element i of a warp-distributed array of 32*E keys sits in lane i / E, slot i % E.
+template <int E>
+__device__ __forceinline__ void warp_cas_stage(uint64_t (&v)[E], int lane, int k, int j) {
+    if (j < E) {  // partner in the same lane
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int p = e ^ j;
+            if (p <= e) continue;
+            const bool up = ((lane * E + e) & k) == 0;
+            const uint64_t x = v[e], y = v[p];
+            if ((x > y) == up) { v[e] = y; v[p] = x; }
+        }
+    } else {
+        const int lj = j / E;
+        const bool lower = (lane & lj) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const uint64_t y = __shfl_xor_sync(0xffffffffu, v[e], lj);
+            const bool up = ((lane * E + e) & k) == 0;
+            v[e] = (lower == up) ? (v[e] < y ? v[e] : y) : (v[e] > y ? v[e] : y);
+        }
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void warp_bitonic_sort(uint64_t (&v)[E], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) warp_cas_stage<E>(v, lane, k, j);
+}
+
+// Ascending sort of a bitonic warp-distributed sequence (merge network only).
+template <int E>
+__device__ __forceinline__ void warp_bitonic_merge(uint64_t (&v)[E], int lane) {
+#pragma unroll
+    for (int j = 16 * E; j > 0; j >>= 1) warp_cas_stage<E>(v, lane, 32 * E, j);
+}
+
+// One warp folds fresh_q[0..n) (n <= 64) into top_q[kk] (kk = 32 * E, ascending):
+// sort the fresh keys (2 per lane), then top[i] = min(top[i], fresh[kk-1-i]) keeps
+// the kk smallest of the union as a bitonic sequence, which the merge sorts.
+template <int E>
+__device__ __forceinline__ float warp_compact_query(uint64_t *top_q, uint64_t *fresh_q, int n, int lane) {
+    uint64_t f[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) f[e] = lane * 2 + e < n ? fresh_q[lane * 2 + e] : KEY_MAX;
+    warp_bitonic_sort<2>(f, lane);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) fresh_q[lane * 2 + e] = f[e];
+    __syncwarp();
+    uint64_t v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane * E + e, x = 32 * E - 1 - i;
+        const uint64_t t = top_q[i], c = x < 64 ? fresh_q[x] : KEY_MAX;
+        v[e] = c < t ? c : t;
+    }
+    warp_bitonic_merge<E>(v, lane);
+#pragma unroll
+    for (int e = 0; e < E; ++e) top_q[lane * E + e] = v[e];
+    const uint64_t last = __shfl_sync(0xffffffffu, v[E - 1], 31);
+    return last == KEY_MAX ? __int_as_float(0x7f800000) : key_dist(last);
+}
+
+template <int E>
+__device__ __forceinline__ void warp_compact_all(uint64_t *top, uint64_t *fresh, int *cnt, float *thr, int nq) {
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int q = threadIdx.x >> 5; q < nq; q += nw) {
+        const int n = cnt[q];
+        if (n > 0) {
+            const float t = warp_compact_query<E>(top + (size_t)q * (32 * E), fresh + (size_t)q * NEWCAP, n, lane);
+            if (lane == 0) thr[q] = t;
+        }
+        __syncwarp();
+    }
+}
+
 // Fold the fresh candidates of `nq` queries into their top lists.
 // top: [nq][kk] ascending; fresh: [nq][NEWCAP]; cnt[nq]; thr[nq] updated.
 __device__ inline void compact_topk(uint64_t *top, uint64_t *fresh, int *cnt, float *thr, int nq, int kk,
                                     int *scratch) {
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int mx = 0;
-        for (int q = 0; q < nq; ++q) mx = cnt[q] > mx ? cnt[q] : mx;
-        scratch[0] = mx;
+    if (threadIdx.x < 32) {
+        int m = 0;
+        for (int q = threadIdx.x; q < nq; q += 32) m = max(m, cnt[q]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (threadIdx.x == 0) scratch[0] = m;
     }
     __syncthreads();
     const int mx = scratch[0];
+    if (mx > 0 && mx <= 64 && kk >= 32 && kk <= 256) {  // warp per query
+        switch (kk) {
+            case 32: warp_compact_all<1>(top, fresh, cnt, thr, nq); break;
+            case 64: warp_compact_all<2>(top, fresh, cnt, thr, nq); break;
+            case 128: warp_compact_all<4>(top, fresh, cnt, thr, nq); break;
+            default: warp_compact_all<8>(top, fresh, cnt, thr, nq); break;
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < nq; q += blockDim.x) cnt[q] = 0;
+        __syncthreads();
+        return;
+    }
     if (mx > 0) {
         int S = 2;
         while (S < mx) S <<= 1;

@@ -110,6 +110,11 @@ def test_ivf_list_major_and_query_major(rii, ref, monkeypatch, mode, kind, N, D,
             gr = g.query(q, 100, target_ids=sub, L=L, path="ivf")
             orr = o.query(q, 100, S=sub, L=L, path=2)
             assert_topk_parity(ref, o.cb, o.codes, q, gr, orr, S=sub, what=f"ivf-{mode} {kind} M={M} L={L}")
+            if mode == "list":  # two-phase u16 items (default) == single-phase fp32 / bf16 items
+                monkeypatch.setenv("RII_Q16", "0")
+                g2 = g.query(q, 100, target_ids=sub, L=L, path="ivf")
+                monkeypatch.delenv("RII_Q16")
+                assert np.array_equal(gr[0], g2[0]) and np.array_equal(gr[1], g2[1])
 
 
 def test_device_memory_path_matches_host_path(rii, ref):

@@ -113,6 +113,31 @@ void rii_destroy(rii_index *idx);
 rii_status rii_train(rii_index *idx, const float *x, int64_t n, int32_t n_iter, uint64_t seed, rii_mem where,
                      void *stream);
 
+/* OPQ variant (Rii-OPQ, Sec. "Advanced Encoding"; Table 2 P:1002,
+ * P:1008): "In the search phase, an input vector is first rotated with the
+ * matrix.  The remaining process is exactly the same as PQ".
+ * rii_set_rotation: R = D x D fp32 row-major host array (copied; NULL removes the
+ * rotation).  From then on every vector given to rii_train, rii_add, rii_query,
+ * rii_query_partial and rii_calibrate_theta is replaced by y = R x computed in the
+ * canonical order y_i = ((0 + R_i0 x_0) + R_i1 x_1) + ... (fp32, no FMA; DESIGN.md
+ * CR).  R is not checked for orthogonality.  Only while the index is empty
+ * (N == 0, else RII_ERR_STATE); clears the code book (train or set it again).
+ * rii_get_rotation: copies R into R (D x D; identity when none) and sets
+ * *has_rotation (either pointer may be NULL).
+ * rii_rotate: out = R in for n device rows (a copy when no rotation); synchronises.
+ * rii_train_opq: non-parametric OPQ (the rotation is "preliminarily trained to
+ * minimize the error"): R_0 = I; n_opq_iter times: train a code book on
+ * R x (max(1, n_iter / 2) Lloyd iterations, seed + it), reconstruct y = decode(
+ * encode(R x)), R <- U V^T for the SVD C = sum y x^T = U S V^T (orthogonal
+ * Procrustes; the D x D SVD runs on the host, C on the device); then sets R and
+ * trains the final code book on R x with n_iter iterations and `seed` (rii_train).
+ * Same requirements and errors as rii_train. */
+rii_status rii_set_rotation(rii_index *idx, const float *R);
+rii_status rii_get_rotation(const rii_index *idx, float *R, int32_t *has_rotation);
+rii_status rii_rotate(const rii_index *idx, const float *in, int64_t n, float *out, void *stream);
+rii_status rii_train_opq(rii_index *idx, const float *x, int64_t n, int32_t n_opq_iter, int32_t n_iter, uint64_t seed,
+                         rii_mem where, void *stream);
+
 /* Data addition (Sec. 4.3 "Data addition"): encodes x (n x D fp32,
  * Eq. 1) and appends the codes to the linear array (PushBack(Xbar, y));
  * if the index has coarse centres (K > 0) each new id is appended to the posting

@@ -46,6 +46,7 @@ def lib():
             "rref_splitmix64": (u64, [u64]),
             "rref_encode": (C.c_int, [p, C.c_int, C.c_int, C.c_int, p, i64, p]),
             "rref_decode": (None, [p, C.c_int, C.c_int, C.c_int, p, i64, p]),
+            "rref_rotate": (None, [p, C.c_int, p, i64, p]),
             "rref_lut": (None, [p, C.c_int, C.c_int, C.c_int, p, p]),
             "rref_lut64": (None, [p, C.c_int, C.c_int, C.c_int, p, p]),
             "rref_adc": (C.c_float, [p, C.c_int, C.c_int, p]),
@@ -116,6 +117,17 @@ def decode(cb, codes, D, Z=Z_DEFAULT):
     out = np.empty((n, D), np.float32)
     lib().rref_decode(_p(cb), D, M, Z, _p(codes), n, _p(out))
     return out
+
+
+def rotate(R, x):
+    """OPQ input rotation y = R x, canonical fp32 order CR."""
+    R = _c(R, np.float32)
+    x = _c(np.atleast_2d(x), np.float32)
+    D = R.shape[0]
+    assert R.shape == (D, D) and x.shape[1] == D
+    y = np.empty_like(x)
+    lib().rref_rotate(_p(R), D, _p(x), x.shape[0], _p(y))
+    return y
 
 
 def lut(cb, q, M, Z=Z_DEFAULT):
@@ -311,6 +323,10 @@ class OracleIndex:
         self.offsets = np.zeros(1, np.int64)
         self.ids = np.zeros(0, np.int64)
         self.theta = -1
+        self.R = None  # OPQ rotation; inputs become R x
+
+    def _in(self, x):
+        return x if self.R is None else rotate(self.R, x)
 
     @property
     def N(self):
@@ -321,12 +337,12 @@ class OracleIndex:
         return self.centers.shape[0]
 
     def train(self, x, n_iter=20, seed=0):
-        self.cb = train(x, self.M, n_iter, seed, self.Z)
+        self.cb = train(self._in(x), self.M, n_iter, seed, self.Z)
 
     def add(self, x):
         """Data addition: PushBack codes; PushBack(W_a(n), n)."""
         first = self.N
-        new = encode(self.cb, x, self.M, self.Z)
+        new = encode(self.cb, self._in(x), self.M, self.Z)
         self.codes = np.concatenate([self.codes, new])
         if self.K > 0:
             T = sdc_tables(self.cb, self.D, self.M, self.Z)
@@ -341,7 +357,7 @@ class OracleIndex:
         return obj
 
     def query(self, q, topk, S=None, L=1, path=PATH_AUTO):
-        return query(self.cb, self.codes, self.centers if self.K else None, self.offsets, self.ids, q, topk, L,
+        return query(self.cb, self.codes, self.centers if self.K else None, self.offsets, self.ids, self._in(q), topk, L,
                      S, self.theta, path, self.Z)
 
     def memory_bytes(self):

@@ -102,6 +102,22 @@ void rref_decode(const float *cb, int D, int M, int Z, const uint8_t *codes, int
                 x[i * D + m * ds + j] = cb[((int64_t)m * Z + codes[i * M + m]) * ds + j];
 }
 
+/* OPQ rotation (Rii-OPQ: "an input vector is first rotated with the
+ * matrix.  The remaining process is exactly the same as PQ"): y = R x for n rows,
+ * R row-major D x D.  Canonical order CR: y_i = ((0 + R_i0 x_0) +
+ * R_i1 x_1) + ..., j ascending, one fp32 multiply and one fp32 add per term. */
+void rref_rotate(const float *R, int D, const float *x, int64_t n, float *y) {
+    for (int64_t v = 0; v < n; ++v)
+        for (int i = 0; i < D; ++i) {
+            float acc = 0.0f;
+            for (int j = 0; j < D; ++j) {
+                float t = R[(int64_t)i * D + j] * x[v * D + j];
+                acc = acc + t;
+            }
+            y[v * D + i] = acc;
+        }
+}
+
 /* Distance table A in R^{M x Z} (Alg. 1 L1 "CompareCodewords"). */
 void rref_lut(const float *cb, int D, int M, int Z, const float *q, float *A) {
     int ds = D / M;

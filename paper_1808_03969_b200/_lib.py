@@ -31,6 +31,10 @@ SIGNATURES = {
     "rii_destroy": (None, [_p]),
     "rii_train": (C.c_int, [_p, _p, _i64, _i32, _u64, C.c_int, _p]),
     "rii_add": (C.c_int, [_p, _p, _i64, C.c_int, _p, C.POINTER(_i64)]),
+    "rii_set_rotation": (C.c_int, [_p, _p]),
+    "rii_get_rotation": (C.c_int, [_p, _p, C.POINTER(_i32)]),
+    "rii_rotate": (C.c_int, [_p, _p, _i64, _p, _p]),
+    "rii_train_opq": (C.c_int, [_p, _p, _i64, _i32, _i32, _u64, C.c_int, _p]),
     "rii_reconfigure": (C.c_int, [_p, _i32, _i32, _u64, _p]),
     "rii_query": (C.c_int, [_p, _p, _i64, _i32, _p, _i64, _i32, C.c_int, C.c_int, _p, _p, _p, C.POINTER(_i32)]),
     "rii_partial_width": (_i32, [_i32]),

@@ -17,6 +17,7 @@
 #include "../../include/rii.h"
 #include "comm.hpp"
 #include "kernels.cuh"
+#include "opq.hpp"
 #include "lut.cuh"
 
 namespace rii {
@@ -120,11 +121,14 @@ struct rii_index {
     int64_t theta = -1;
     int ivf_mode = 0;        // RII_IVF_LISTS / RII_IVF_PAPER
     bool theta_fit = false;  // rii_calibrate_theta result in use (theta(L) = fit_a * L + fit_b)
+    bool has_rot = false;    // OPQ rotation (rii_set_rotation / rii_train_opq): R and R^T, D x D fp32
+    Buf rot, rotT;
+    std::vector<float> rot_host;
     double fit_a = 0.0, fit_b = 0.0;
     // scratch (query side is const-callable: mutable)
     mutable Buf s_q, s_S, s_pos, s_sub, s_part, s_keys, s_gather, s_d0, s_probe, s_roff, s_rids, s_rkey, s_rval,
         s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_items, s_gthr, s_tables, s_cpart, s_ckeys, s_take,
-        s_samp, s_spart, s_bound, s_skey, s_tab16, s_qscale;
+        s_samp, s_spart, s_bound, s_skey, s_tab16, s_qscale, s_qrot, s_xrot;
 };
 
 namespace {
@@ -288,6 +292,15 @@ struct QueryArgs {
     int L;
     int path;                // resolved LINEAR / IVF
 };
+
+// OPQ: the rotated copy R x of n device rows in `buf`, or x itself
+// when the index has no rotation.
+const float *rotate_input(const rii_index *x, Buf &buf, const float *dx, int64_t n, cudaStream_t st) {
+    if (!x->has_rot || n <= 0) return dx;
+    float *o = buf.get<float>((size_t)n * x->D);
+    launch_rotate(x->rotT.as<float>(), dx, n, x->D, o, st);
+    return o;
+}
 
 int resolve_path(const rii_index *x, int64_t nS_global, bool has_S, int L, rii_path path) {
     if (x->K == 0) {
@@ -709,6 +722,7 @@ rii_status rii_train(rii_index *x, const float *xs, int64_t n, int32_t n_iter, u
             RII_CUDA(cudaMemcpyAsync(b, xs, (size_t)n * x->D * 4, cudaMemcpyHostToDevice, st));
             dx = b;
         }
+        dx = rotate_input(x, x->s_xrot, dx, n, st);  // OPQ: train on R x
         int *err = x->s_flag.get<int>(1);
         RII_CUDA(cudaMemsetAsync(err, 0, 4, st));
         Buf tmp;
@@ -722,6 +736,101 @@ rii_status rii_train(rii_index *x, const float *xs, int64_t n, int32_t n_iter, u
         RII_CUDA(cudaStreamSynchronize(st));
         x->trained = true;
         x->T_valid = false;
+    });
+}
+
+rii_status rii_set_rotation(rii_index *x, const float *R) {
+    return guarded([&] {
+        arg_check(x != nullptr, "index is NULL");
+        state_check(x->N == 0, "the rotation can only be set while the index is empty");
+        DeviceGuard g(x->device);
+        if (!R) {
+            x->has_rot = false;
+        } else {
+            const size_t DD = (size_t)x->D * x->D;
+            x->rot_host.assign(R, R + DD);
+            std::vector<float> Rt(DD);
+            for (int i = 0; i < x->D; ++i)
+                for (int j = 0; j < x->D; ++j) Rt[(size_t)j * x->D + i] = R[(size_t)i * x->D + j];
+            RII_CUDA(cudaMemcpy(x->rot.get<float>(DD), R, DD * 4, cudaMemcpyHostToDevice));
+            RII_CUDA(cudaMemcpy(x->rotT.get<float>(DD), Rt.data(), DD * 4, cudaMemcpyHostToDevice));
+            x->has_rot = true;
+        }
+        x->trained = false;  // the code book lives in the rotated space: train or set it afterwards
+        x->T_valid = false;
+    });
+}
+
+rii_status rii_get_rotation(const rii_index *x, float *R, int32_t *has_rotation) {
+    return guarded([&] {
+        arg_check(x != nullptr, "index is NULL");
+        if (has_rotation) *has_rotation = x->has_rot ? 1 : 0;
+        if (R) {
+            for (int i = 0; i < x->D; ++i)
+                for (int j = 0; j < x->D; ++j)
+                    R[(size_t)i * x->D + j] = x->has_rot ? x->rot_host[(size_t)i * x->D + j] : (i == j ? 1.f : 0.f);
+        }
+    });
+}
+
+rii_status rii_rotate(const rii_index *x, const float *in, int64_t n, float *out, void *stream) {
+    return guarded([&] {
+        arg_check(x && (n == 0 || (in && out)) && n >= 0, "bad arguments");
+        DeviceGuard g(x->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        if (n == 0) return;
+        if (x->has_rot) launch_rotate(x->rotT.as<float>(), in, n, x->D, out, st);
+        else RII_CUDA(cudaMemcpyAsync(out, in, (size_t)n * x->D * 4, cudaMemcpyDeviceToDevice, st));
+        RII_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+rii_status rii_train_opq(rii_index *x, const float *xs, int64_t n, int32_t n_opq_iter, int32_t n_iter,
+                         uint64_t seed, rii_mem where, void *stream) {
+    return guarded([&] {
+        arg_check(x && xs, "NULL argument");
+        arg_check(n_opq_iter >= 0 && n_iter >= 0, "iteration counts must be >= 0");
+        state_check(x->N == 0, "the rotation can only be trained while the index is empty");
+        if (n < KS) throw Error(RII_ERR_TRAIN, "training needs n >= 256 rows");
+        DeviceGuard g(x->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        const int D = x->D;
+        const size_t DD = (size_t)D * D;
+        Buf xb, yb, xr, cbb, cod, Cb;
+        const float *dx = xs;
+        if (where == RII_MEM_HOST) {
+            float *b = xb.get<float>((size_t)n * D);
+            RII_CUDA(cudaMemcpyAsync(b, xs, (size_t)n * D * 4, cudaMemcpyHostToDevice, st));
+            dx = b;
+        }
+        std::vector<float> R(DD, 0.f);
+        for (int i = 0; i < D; ++i) R[(size_t)i * D + i] = 1.f;  // R_0 = I
+        std::vector<double> Ch(DD);
+        int *err = x->s_flag.get<int>(1);
+        float *cb = cbb.get<float>((size_t)x->M * KS * x->ds);
+        uint8_t *codes = cod.get<uint8_t>((size_t)n * x->M);
+        float *y = yb.get<float>((size_t)n * D);
+        double *Cd = Cb.get<double>(DD);
+        for (int it = 0; it < n_opq_iter; ++it) {
+            // (1) PQ on the rotated data, (2) orthogonal Procrustes R = argmin sum ||y - R x||^2
+            RII_CUDA(cudaStreamSynchronize(st));
+            const rii_status s1 = rii_set_rotation(x, R.data());
+            if (s1 != RII_OK) throw Error(s1, t_err);
+            const float *rx = rotate_input(x, xr, dx, n, st);
+            RII_CUDA(cudaMemsetAsync(err, 0, 4, st));
+            run_train(rx, n, D, x->M, std::max(1, n_iter / 2), seed + (uint64_t)it, cb, err, st);
+            launch_encode(rx, n, D, x->M, cb, codes, st);
+            launch_decode(codes, n, x->M, D, cb, y, st);
+            launch_cross(y, dx, n, D, Cd, st);
+            RII_CUDA(cudaMemcpyAsync(Ch.data(), Cd, DD * 8, cudaMemcpyDeviceToHost, st));
+            RII_CUDA(cudaStreamSynchronize(st));
+            procrustes_rotation(Ch.data(), D, R.data());
+        }
+        RII_CUDA(cudaStreamSynchronize(st));
+        const rii_status s2 = rii_set_rotation(x, R.data());
+        if (s2 != RII_OK) throw Error(s2, t_err);
+        const rii_status s3 = rii_train(x, dx, n, n_iter, seed, RII_MEM_DEVICE, stream);  // final code book on R x
+        if (s3 != RII_OK) throw Error(s3, t_err);
     });
 }
 
@@ -769,6 +878,7 @@ rii_status rii_add(rii_index *x, const float *xs, int64_t n, rii_mem where, void
                     RII_CUDA(cudaMemcpyAsync(b, dx, (size_t)(e - s) * x->D * 4, cudaMemcpyHostToDevice, st));
                     dx = b;
                 }
+                dx = rotate_input(x, x->s_xrot, dx, e - s, st);  // OPQ: encode R x
                 launch_encode(dx, e - s, x->D, x->M, x->cb.as<float>(), codes + (x->n_local + (s - lo)) * x->M, st);
             }
             if (x->K > 0) {
@@ -882,6 +992,7 @@ static rii_status query_impl(const rii_index *x, const float *q, int64_t nq, int
             }
         }
         check_targets(x, dS, S ? nS : 0, st);
+        dq = rotate_input(x, x->s_qrot, dq, nq, st);  // OPQ: "an input vector is first rotated"
         QueryArgs a{dq, nq, topk, partial_width(topk), S ? dS : nullptr, S ? nS : 0, L, used};
         if (S && nS == 0) {  // empty subset: nothing to return but padding
             a.S = dS;
@@ -1029,11 +1140,13 @@ rii_status rii_save(const rii_index *x, const char *path) {
             w.put("RII1", 4);
             w.val<uint32_t>(1);
             for (uint32_t v : {(uint32_t)x->D, (uint32_t)x->M, (uint32_t)KS, (uint32_t)x->world, (uint32_t)x->rank,
-                               (uint32_t)x->ivf_mode, (uint32_t)(x->theta_fit ? 1 : 0), (uint32_t)x->segs.size()})
+                               (uint32_t)x->ivf_mode, (uint32_t)((x->theta_fit ? 1 : 0) | (x->has_rot ? 2 : 0)),
+                               (uint32_t)x->segs.size()})
                 w.val(v);
             for (int64_t v : {x->N, x->n_local, x->K, x->theta}) w.val(v);
             w.val(x->fit_a);
             w.val(x->fit_b);
+            if (x->has_rot) w.put(x->rot_host.data(), x->rot_host.size() * 4);  // flags bit 1: OPQ rotation
             dev_to_file(w, x->cb.as<float>(), (size_t)x->M * KS * x->ds);
             for (auto &sg : x->segs) { w.val(sg.local_off); w.val(sg.global_first); w.val(sg.count); }
             dev_to_file(w, x->codes.as<uint8_t>(), (size_t)x->n_local * x->M);
@@ -1077,6 +1190,12 @@ rii_status rii_load(const char *path, int32_t device, const void *nccl_id, rii_i
                                              (int32_t)world, nccl_id, &x);
             if (st != RII_OK) throw Error(st, t_err);
             DeviceGuard g(device);
+            if (flags & 2u) {  // OPQ rotation
+                std::vector<float> R((size_t)D * D);
+                r.get(R.data(), R.size() * 4, "rotation");
+                const rii_status sr = rii_set_rotation(x, R.data());
+                if (sr != RII_OK) throw Error(sr, t_err);
+            }
             file_to_dev(r, x->cb.as<float>(), (size_t)M * KS * (D / M), "code book");
             x->trained = true;
             for (uint32_t i = 0; i < nseg; ++i) {

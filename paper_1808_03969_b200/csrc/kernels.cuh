@@ -130,6 +130,14 @@ void launch_ivf_scan(const uint8_t *codes, int M, const float *q, int64_t nq, co
                      const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
                      cudaStream_t st, const float *tables = nullptr, const int32_t *take = nullptr);
 
+// ---- OPQ (k_opq.cu) ----------------------------------------------------------
+// y[n] = R x[n] with Rt = R^T (D x D), canonical order (CR: j ascending, no FMA).
+void launch_rotate(const float *Rt, const float *x, int64_t n, int D, float *y, cudaStream_t st);
+// y[n] = decode(codes[n]) (PQ reconstruction).
+void launch_decode(const uint8_t *codes, int64_t n, int M, int D, const float *cb, float *y, cudaStream_t st);
+// C (D x D, fp64) = sum_n y_n x_n^T.
+void launch_cross(const float *y, const float *x, int64_t n, int D, double *C, cudaStream_t st);
+
 // ---- build side (k_build.cu) -------------------------------------------------
 void launch_encode(const float *x, int64_t n, int D, int M, const float *cb, uint8_t *codes, cudaStream_t st);
 void launch_sdc_tables(const float *cb, int D, int M, float *T, cudaStream_t st);

@@ -127,6 +127,37 @@ class Index:
         x, n, where, st = self._rows(x)
         _rl.check(self._lib.rii_train(self._h, _ptr(x), n, n_iter, seed, where, st))
 
+    # --------------------------------------------------------------- OPQ ---
+    def set_rotation(self, R):
+        """OPQ rotation: every later train / add / query input x becomes R x."""
+        if R is None:
+            _rl.check(self._lib.rii_set_rotation(self._h, None))
+            return
+        R = _host(R, np.float32)
+        if R.shape != (self.D, self.D):
+            raise ValueError(f"R must be {self.D} x {self.D}")
+        _rl.check(self._lib.rii_set_rotation(self._h, _ptr(R)))
+
+    def get_rotation(self):
+        """(R, has_rotation); R is the identity when the index has no rotation."""
+        R = np.empty((self.D, self.D), np.float32)
+        has = C.c_int32(0)
+        _rl.check(self._lib.rii_get_rotation(self._h, _ptr(R), C.byref(has)))
+        return R, bool(has.value)
+
+    def rotate(self, x):
+        """R x for device rows (a torch CUDA tensor); returns a new tensor."""
+        torch = _torch()
+        x = _dev(x, np.float32)
+        out = torch.empty_like(x)
+        _rl.check(self._lib.rii_rotate(self._h, _ptr(x), x.shape[0], _ptr(out), _stream_ptr(None)))
+        return out
+
+    def train_opq(self, x, n_opq_iter: int = 8, n_iter: int = 20, seed: int = 0):
+        """Non-parametric OPQ: rotation + code book (rii_train_opq)."""
+        x, n, where, st = self._rows(x)
+        _rl.check(self._lib.rii_train_opq(self._h, _ptr(x), n, n_opq_iter, n_iter, seed, where, st))
+
     def add(self, x) -> int:
         x, n, where, st = self._rows(x)
         first = C.c_int64(0)

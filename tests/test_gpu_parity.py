@@ -413,3 +413,87 @@ def test_linear_u16_duplicates_and_zero_distance(rii, ref, monkeypatch):
         d = ((xl.astype(np.int64) - ql[i].astype(np.int64)) ** 2).sum(1)
         order = np.lexsort((np.arange(len(xl)), d))[:10]
         assert np.array_equal(ids[i], order) and np.array_equal(dist[i], d[order].astype(np.float32))
+
+
+# ------------------------------------------------------------ OPQ (Rii-OPQ) ---
+def _orthogonal(D, seed):
+    Q, _ = np.linalg.qr(np.random.default_rng(seed).normal(size=(D, D)))
+    return Q.astype(np.float32)
+
+
+@pytest.mark.parametrize("D,n", [(96, 1001), (128, 37), (30, 300)])
+def test_rotate_kernel_bit_exact(rii, ref, D, n):
+    """rotate_kernel (canonical order CR) equals the oracle's rref_rotate bit for bit."""
+    import torch
+    R = _orthogonal(D, D)
+    x = gen.base("deep", n, D, seed=D)
+    g = rii.Index(D, 1 if D == 30 else 32 if D == 96 else 16)
+    g.set_rotation(R)
+    y = g.rotate(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(y, ref.rotate(R, x))
+    Rg, has = g.get_rotation()
+    assert has and np.array_equal(Rg, R)
+
+
+def test_opq_pipeline_matches_oracle(rii, ref):
+    """Rii-OPQ with a given rotation: train, add, reconfigure and every
+    query path on R x equal the oracle's, bit for bit where bit-exact is required."""
+    D, M, K, N = 96, 32, 12, 20_011
+    R = _orthogonal(D, 5)
+    x = gen.base("deep", N, D, seed=5)
+    q = gen.base("deep", 23, D, seed=5, stream=gen.STREAM_QUERY)
+    g = rii.Index(D, M)
+    g.set_rotation(R)
+    g.train(x[:4000], n_iter=3, seed=0)
+    g.add(x)
+    g.reconfigure(K, n_iter=3, seed=0)
+    o = ref.OracleIndex(D, M)
+    o.R = R
+    o.train(x[:4000], n_iter=3, seed=0)
+    o.add(x)
+    o.reconfigure(K, n_iter=3, seed=0)
+    assert np.array_equal(g.get_codebook(), o.cb)
+    assert np.array_equal(g.get_codes(), o.codes)
+    assert np.array_equal(g.get_centers(), o.centers)
+    S = gen.subset(N, 3001, seed=1)
+    for path in ("linear", "ivf"):
+        for sub in (None, S):
+            gr = g.query(q, 50, target_ids=sub, L=3, path=path)
+            orr = o.query(q, 50, S=sub, L=3, path=1 if path == "linear" else 2)
+            assert_topk_parity(ref, o.cb, o.codes, ref.rotate(R, q), gr, orr, S=sub, what=f"opq {path}")
+
+
+def test_train_opq_properties(rii, ref, tmp_path):
+    """rii_train_opq: R orthogonal, deterministic, and the quantisation distortion
+    of R x is below plain PQ's on data whose energy is concentrated in a few
+    rotated directions (the case OPQ targets); save/load keeps R."""
+    D, M, n = 32, 8, 8000
+    rng = np.random.default_rng(3)
+    scales = (2.0 ** (-np.arange(D) / 3.0)).astype(np.float32)
+    x = ((rng.normal(size=(n, D)) * scales) @ _orthogonal(D, 9).T).astype(np.float32) * 10
+    g = rii.Index(D, M)
+    g.train_opq(x, n_opq_iter=6, n_iter=10, seed=1)
+    R, has = g.get_rotation()
+    assert has and np.abs(R.astype(np.float64) @ R.T.astype(np.float64) - np.eye(D)).max() < 1e-4
+    g2 = rii.Index(D, M)
+    g2.train_opq(x, n_opq_iter=6, n_iter=10, seed=1)
+    assert np.array_equal(g2.get_rotation()[0], R) and np.array_equal(g2.get_codebook(), g.get_codebook())
+    p = rii.Index(D, M)
+    p.train(x, n_iter=10, seed=1)
+
+    def distortion(idx, rot):
+        cb = idx.get_codebook()
+        xr = ref.rotate(rot, x) if rot is not None else x
+        rec = ref.decode(cb, ref.encode(cb, xr, M), D)
+        return float(((xr.astype(np.float64) - rec) ** 2).sum(1).mean())
+
+    d_opq, d_pq = distortion(g, R), distortion(p, None)
+    assert d_opq < 0.9 * d_pq, (d_opq, d_pq)
+    g.add(x)
+    q = x[:5]
+    r1 = g.query(q, 10, path="linear")
+    g.save(str(tmp_path / "opq.rii"))
+    h = rii.Index.load(str(tmp_path / "opq.rii"))
+    assert np.array_equal(h.get_rotation()[0], R)
+    r2 = h.query(q, 10, path="linear")
+    assert np.array_equal(r1[0], r2[0]) and np.array_equal(r1[1], r2[1])

@@ -431,3 +431,52 @@ def test_ivf_paper_budget_and_early_stop(ref):
             continue
         prefix = np.concatenate([idx.ids[idx.offsets[k]:idx.offsets[k + 1]] for k in order[:P]])[:L]
         assert np.isin(pid[i][pid[i] >= 0], prefix).all()
+
+
+# --------------------------------------------------------------- OPQ rotation --
+def test_rotate_closed_forms(ref):
+    """rref_rotate (canonical order CR): identity, permutations and sign
+    flips are exact; a 3-4-5 rotation matches its fp64 value to fp32 rounding; an
+    orthogonal R preserves norms and R^T undoes R (within fp32 accumulation error)."""
+    rng = np.random.default_rng(11)
+    D = 24
+    x = rng.normal(size=(50, D)).astype(np.float32)
+    assert np.array_equal(ref.rotate(np.eye(D, dtype=np.float32), x), x)
+    perm = rng.permutation(D)
+    P = np.zeros((D, D), np.float32)
+    P[np.arange(D), perm] = 1.0                      # (P x)_i = x_perm[i]
+    assert np.array_equal(ref.rotate(P, x), x[:, perm])
+    S = np.diag(np.where(rng.random(D) < 0.5, -1.0, 1.0)).astype(np.float32)
+    assert np.array_equal(ref.rotate(S, x), x * np.diag(S)[None, :])
+    G = np.array([[0.6, -0.8], [0.8, 0.6]], np.float32)  # cos/sin of the 3-4-5 triangle
+    y = ref.rotate(G, np.array([[5.0, 10.0]], np.float32))[0]
+    exact = np.array([-5.0, 10.0])
+    assert np.all(np.abs(y - exact) <= 4e-6 * np.abs(exact)), y
+    Q, _ = np.linalg.qr(rng.normal(size=(D, D)))
+    Q = Q.astype(np.float32)
+    yq = ref.rotate(Q, x).astype(np.float64)
+    assert np.allclose(np.linalg.norm(yq, axis=1), np.linalg.norm(x.astype(np.float64), axis=1), rtol=2e-5)
+    back = ref.rotate(np.ascontiguousarray(Q.T), ref.rotate(Q, x))
+    assert np.allclose(back, x, atol=2e-5 * np.abs(x).max())
+
+
+def test_rotated_index_is_pq_on_rotated_data(ref):
+    """Rii-OPQ "remaining process is exactly the same as PQ": an oracle
+    index with rotation R returns what a plain index over R x returns for R q."""
+    rng = np.random.default_rng(12)
+    D, M = 16, 4
+    x = rng.normal(size=(3000, D)).astype(np.float32)
+    q = rng.normal(size=(5, D)).astype(np.float32)
+    Q, _ = np.linalg.qr(rng.normal(size=(D, D)))
+    Q = Q.astype(np.float32)
+    a = ref.OracleIndex(D, M)
+    a.R = Q
+    a.train(x, n_iter=3)
+    a.add(x)
+    b = ref.OracleIndex(D, M)
+    xr = ref.rotate(Q, x)
+    b.train(xr, n_iter=3)
+    b.add(xr)
+    assert np.array_equal(a.codes, b.codes) and np.array_equal(a.cb, b.cb)
+    ra, rb = a.query(q, 7, path=ref.PATH_LINEAR), b.query(ref.rotate(Q, q), 7, path=ref.PATH_LINEAR)
+    assert np.array_equal(ra[0], rb[0]) and np.array_equal(ra[1], rb[1])

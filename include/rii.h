@@ -89,7 +89,8 @@ rii_status rii_shard_range(int64_t n, int32_t rank, int32_t world, int64_t *lo, 
 rii_status rii_nccl_unique_id(void *out);
 
 /* Create an empty index (Sec. 4.1) of D-dim vectors with M subspaces.
- *  D % M == 0, 1 <= M <= 64, Ks == 256, D/M <= 64 (else RII_ERR_ARG).
+ *  D % M == 0, 1 <= M <= 256, Ks == 256, D/M <= 64 (else RII_ERR_ARG).  M > 64
+ *  (GIST-like shapes) runs the one-query-per-CTA large-M kernels.
  *  device: CUDA ordinal this index lives on.  rank/world: this process's place
  *  in a one-process-per-GPU job (world == 1: single GPU).  nccl_id: the 128-byte
  *  id from rii_nccl_unique_id (all ranks identical) or NULL; with world > 1 and

@@ -23,7 +23,7 @@ LIB = os.path.join(HERE, "librii_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["capi.cu", "k_scan.cu", "k_ivf.cu", "k_build.cu", "k_opq.cu", "comm.cpp", "opq.cpp"]
+SOURCES = ["capi.cu", "k_scan.cu", "k_ivf.cu", "k_build.cu", "k_opq.cu", "k_large.cu", "comm.cpp", "opq.cpp"]
 
 
 def _headers_mtime():

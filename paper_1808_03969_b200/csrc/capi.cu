@@ -398,9 +398,14 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
     PhaseTrace tr(st);
     // per-query rotated ADC tables, built once per batch (a1)
     const float *tables = nullptr;
+    const bool large = x->M > 64;  // k_large.cu: one query per CTA, bf16 resident table
     if (fast) {
         float *tb = x->s_tables.get<float>((size_t)a.nq * LUT_Q_FLOATS);
         launch_lut_tables(a.q, a.nq, cb, x->D, x->M, tb, st);
+        tables = tb;
+    } else if (large) {
+        float *tb = x->s_tables.get<float>((size_t)a.nq * x->M * KS);
+        launch_lut_large(a.q, a.nq, cb, x->D, x->M, tb, st);
         tables = tb;
     }
     tr.mark("tables");
@@ -420,6 +425,14 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
             RII_CUDA(cudaMemsetAsync(pp, 0xff, (size_t)a.nq * kk * 8, st));
             parts = pp;
+        } else if (large) {
+            const int nc = large_linear_chunks(a.nq, n_codes, x->num_sms);
+            uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * nc * kk);
+            launch_large_linear(scan_codes, n_codes, x->M, tables, a.nq, kk, nc, pp, st);
+            parts = pp;
+            q_stride = (int64_t)nc * kk;
+            p_stride = kk;
+            nparts = nc;
         } else {
             ScanPlan pl = plan_linear(x->M, kk, a.nq, n_codes, x->num_sms, tables != nullptr);
             // u16 fixed-point tables for long scans: the exact kk-th distance over a
@@ -466,7 +479,8 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
         int32_t *take = x->s_take.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
         launch_paper_takes(probes, a.nq, P, off, a.L, take, st);                                  // L14 cut
         uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
-        launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st, tables, take);
+        if (large) launch_large_ivf(codes, x->M, tables, a.nq, kk, probes, P, off, ids, take, pp, st);
+        else launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st, tables, take);
         parts = pp;
     } else {  // Alg. 2, mode A (reading R2)
         const int64_t P = a.S ? std::min<int64_t>(x->K, ceil_div((int64_t)a.L * x->N, std::max<int64_t>(a.nS, 1)))
@@ -561,7 +575,8 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             nparts = (int)P;
         } else {
             uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
-            launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st, tables);
+            if (large) launch_large_ivf(codes, x->M, tables, a.nq, kk, probes, P, off, ids, nullptr, pp, st);
+            else launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st, tables);
             parts = pp;
         }
     }
@@ -663,7 +678,7 @@ rii_status rii_create(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t 
     if (out) *out = nullptr;
     return guarded([&] {
         arg_check(out != nullptr, "out is NULL");
-        arg_check(M >= 1 && M <= 64, "M must be in [1, 64]");
+        arg_check(M >= 1 && M <= 256, "M must be in [1, 256]");
         arg_check(D >= M && D % M == 0, "D must be a positive multiple of M");
         arg_check(D / M <= 64, "D / M must be <= 64");
         arg_check(Ks == 256, "Ks must be 256 (one byte per subspace, P:287)");
@@ -1183,7 +1198,7 @@ rii_status rii_load(const char *path, int32_t device, const void *nccl_id, rii_i
             const int64_t N = r.val<int64_t>("header"), n_local = r.val<int64_t>("header");
             const int64_t K = r.val<int64_t>("header"), theta = r.val<int64_t>("header");
             const double fa = r.val<double>("header"), fb = r.val<double>("header");
-            arg_check(Ks == KS && M >= 1 && M <= 64 && D % M == 0 && D / M <= 64, "bad shape in header");
+            arg_check(Ks == KS && M >= 1 && M <= 256 && D % M == 0 && D / M <= 64, "bad shape in header");
             arg_check(world >= 1 && rank < world && n_local >= 0 && n_local <= N && K >= 0 && mode <= 1,
                       "bad header");
             const rii_status st = rii_create((int32_t)D, (int32_t)M, (int32_t)Ks, device, (int32_t)rank,

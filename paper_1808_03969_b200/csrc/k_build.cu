@@ -254,6 +254,10 @@ static void assign_fast_t(const uint8_t *codes, int64_t n, const float *tables, 
 void launch_assign(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, int M, const float *T,
                    int32_t *assign, float *dist, cudaStream_t st) {
     if (n <= 0) return;
+    if (M > 64) {  // large M: one code per CTA, bf16 SDC rows + exact rescore (k_large.cu)
+        launch_large_assign(codes, n, centers, K, M, T, assign, dist, st);
+        return;
+    }
     if (assign_scan_supported(M, K) && n >= 8192) {  // large K: codes as queries over the centre codes
         launch_assign_scan(codes, n, centers, K, M, T, assign, dist, 148, st);
         return;

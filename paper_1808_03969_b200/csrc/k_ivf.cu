@@ -15,34 +15,46 @@
 
 namespace rii {
 
-constexpr int CQ = 4;  // queries per CTA in coarse_dist
+constexpr int CQ = 4;   // queries per CTA in coarse_dist
+constexpr int CMC = 32; // subspaces per table chunk in coarse_dist
 
+// d0[q][k] (Alg. 2 L2-L5): CTA = (256 centres, CQ queries); the CA1 table is built
+// in chunks of CMC subspaces ([CQ][CMC][256] fp32 in smem), each thread keeps its
+// centre's CQ running sums across the chunks, so the sums stay in the canonical m
+// order (CA2) for any M (up to 256).
 __global__ void __launch_bounds__(NT) coarse_dist_kernel(const uint8_t *__restrict__ centers, int64_t K, int M,
                                                          const float *__restrict__ q, int64_t nq,
                                                          const float *__restrict__ cb, int ds,
                                                          float *__restrict__ d0) {
-    extern __shared__ __align__(16) float clut[];  // [CQ][M][256]
+    extern __shared__ __align__(16) float clut[];  // [CQ][CMC][256]
     const int64_t q0 = (int64_t)blockIdx.y * CQ;
+    const int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x;
     const int D = M * ds;
-    for (int e = threadIdx.x; e < CQ * M * KS; e += blockDim.x) {
-        const int qq = e / (M * KS), m = (e / KS) % M, z = e % KS;
-        const int64_t qi = min(q0 + qq, nq - 1);
-        const float *qv = q + qi * D + m * ds, *cv = cb + ((size_t)m * KS + z) * ds;
-        float a = 0.f;
-        for (int j = 0; j < ds; ++j) a = ca1_step(a, qv[j], cv[j]);
-        clut[e] = a;
-    }
-    __syncthreads();
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
-        const uint8_t *cp = centers + k * M;
-        float acc[CQ];
+    const uint8_t *cp = centers + min(k, K - 1) * M;
+    float acc[CQ];
 #pragma unroll
-        for (int qq = 0; qq < CQ; ++qq) acc[qq] = 0.f;
-        for (int m = 0; m < M; ++m) {
-            const int z = cp[m];
-#pragma unroll
-            for (int qq = 0; qq < CQ; ++qq) acc[qq] = __fadd_rn(acc[qq], clut[(qq * M + m) * KS + z]);
+    for (int qq = 0; qq < CQ; ++qq) acc[qq] = 0.f;
+    for (int m0 = 0; m0 < M; m0 += CMC) {
+        const int mc = min(CMC, M - m0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < CQ * mc * KS; e += blockDim.x) {
+            const int qq = e / (mc * KS), m = (e / KS) % mc, z = e % KS;
+            const int64_t qi = min(q0 + qq, nq - 1);
+            const float *qv = q + qi * D + (m0 + m) * ds, *cv = cb + ((size_t)(m0 + m) * KS + z) * ds;
+            float a = 0.f;
+            for (int j = 0; j < ds; ++j) a = ca1_step(a, qv[j], cv[j]);
+            clut[(qq * CMC + m) * KS + z] = a;
         }
+        __syncthreads();
+        if (k < K) {
+            for (int m = 0; m < mc; ++m) {
+                const int z = cp[m0 + m];
+#pragma unroll
+                for (int qq = 0; qq < CQ; ++qq) acc[qq] = __fadd_rn(acc[qq], clut[(qq * CMC + m) * KS + z]);
+            }
+        }
+    }
+    if (k < K) {
 #pragma unroll
         for (int qq = 0; qq < CQ; ++qq)
             if (q0 + qq < nq) d0[(q0 + qq) * K + k] = acc[qq];
@@ -52,9 +64,9 @@ __global__ void __launch_bounds__(NT) coarse_dist_kernel(const uint8_t *__restri
 void launch_coarse_dist(const uint8_t *centers, int64_t K, int M, const float *q, int64_t nq, const float *cb, int D,
                         float *d0, cudaStream_t st) {
     if (nq <= 0 || K <= 0) return;
-    const size_t smem = (size_t)CQ * M * KS * 4;
+    const size_t smem = (size_t)CQ * CMC * KS * 4;
     RII_CUDA(cudaFuncSetAttribute(coarse_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dim3 grid((unsigned)std::min<int64_t>(ceil_div(K, NT), 16), (unsigned)ceil_div(nq, CQ));
+    dim3 grid((unsigned)ceil_div(K, NT), (unsigned)ceil_div(nq, CQ));
     coarse_dist_kernel<<<grid, NT, smem, st>>>(centers, K, M, q, nq, cb, D / M, d0);
     RII_LAUNCHED();
 }

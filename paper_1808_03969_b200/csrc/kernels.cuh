@@ -130,6 +130,23 @@ void launch_ivf_scan(const uint8_t *codes, int M, const float *q, int64_t nq, co
                      const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
                      cudaStream_t st, const float *tables = nullptr, const int32_t *take = nullptr);
 
+// ---- large M (k_large.cu; M > 64, up to 256) ---------------------------------
+// One query per CTA, bf16 table resident in smem, exact (CA2) rescore of pushes.
+bool large_supported(int M, int kk);
+// tables[nq][M][256] = CA1 entries (canonical layout).
+void launch_lut_large(const float *q, int64_t nq, const float *cb, int D, int M, float *tables, cudaStream_t st);
+int large_linear_chunks(int64_t nq, int64_t n_codes, int num_sms);
+// out[nq][nc][kk] keys (ids = positions in codes) of Alg. 1 over n_codes codes.
+void launch_large_linear(const uint8_t *codes, int64_t n_codes, int M, const float *tables, int64_t nq, int kk, int nc,
+                         uint64_t *out, cudaStream_t st);
+// out[nq][kk] keys of Alg. 2 over each query's P probed lists (take: optional budget cut).
+void launch_large_ivf(const uint8_t *codes, int M, const float *tables, int64_t nq, int kk, const int32_t *probes,
+                      int64_t P, const int64_t *offsets, const uint32_t *ids, const int32_t *take, uint64_t *out,
+                      cudaStream_t st);
+// a[i] = argmin_k d_S(codes[i], centers[k]) (CA2 SDC, ties lowest k); dist optional.
+void launch_large_assign(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, int M, const float *T,
+                         int32_t *assign, float *dist, cudaStream_t st);
+
 // ---- OPQ (k_opq.cu) ----------------------------------------------------------
 // y[n] = R x[n] with Rt = R^T (D x D), canonical order (CR: j ascending, no FMA).
 void launch_rotate(const float *Rt, const float *x, int64_t n, int D, float *y, cudaStream_t st);

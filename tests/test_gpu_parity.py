@@ -497,3 +497,29 @@ def test_train_opq_properties(rii, ref, tmp_path):
     assert np.array_equal(h.get_rotation()[0], R)
     r2 = h.query(q, 10, path="linear")
     assert np.array_equal(r1[0], r2[0]) and np.array_equal(r1[1], r2[1])
+
+
+# ------------------------------------------------------- large M (F3) -------
+@pytest.mark.parametrize("kind,N,D,M,K,nq,topk", [("deep", 3_001, 960, 240, 6, 7, 20),  # GIST1M shape
+                                                  ("sift", 4_003, 384, 192, 8, 9, 50),  # MET-like M = 192
+                                                  ("gaussian", 2_503, 140, 70, 5, 5, 10)])  # M % 4 != 0
+def test_large_m_shapes(rii, ref, kind, N, D, M, K, nq, topk):
+    """M > 64 (the paper's range reaches M = 240): train,
+    add, reconfigure (large-M SDC assignment) and every query path (linear whole /
+    subset, IVF mode A, IVF paper mode with its early stop) equal the oracle's."""
+    x = gen.base(kind, N, D, seed=N)
+    q = gen.base(kind, nq, D, seed=N, stream=gen.STREAM_QUERY)
+    g, o = _build_pair(rii, ref, x, M, K, n_iter=2, train_rows=x, train_iter=2)
+    _check_state(g, o)
+    S = gen.subset(N, N // 3, seed=4)
+    for path in ("linear", "ivf"):
+        for sub in (None, S):
+            for L in (1, 3):
+                gr = g.query(q, topk, target_ids=sub, L=L, path=path)
+                orr = o.query(q, topk, S=sub, L=L, path=1 if path == "linear" else 2)
+                assert_topk_parity(ref, o.cb, o.codes, q, gr, orr, S=sub, what=f"M={M} {path} L={L}")
+    g.set_ivf_mode("paper")
+    Lc = N // K
+    gr = g.query(q, topk, L=Lc, path="ivf")
+    orr = ref.ivf_paper(o.cb, o.codes, o.centers, o.offsets, o.ids, q, topk, Lc)
+    assert_topk_parity(ref, o.cb, o.codes, q, gr, orr, what=f"M={M} paper L={Lc}")

@@ -195,8 +195,15 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     build["reconfigure_s"] = time.perf_counter() - t1
     build["total_s"] = time.perf_counter() - t0
-    info = g.info()
     q = _device_data(kind, nq, D, dev, 0, gen.STREAM_QUERY)
+    # theta (Alg. 3's linear / inverted-index switch) is fitted by timing both paths
+    # on this GPU, as the paper does on its CPU; AUTO rows below use it
+    t1 = time.perf_counter()
+    th = g.calibrate_theta(q[:1000], topk=topk, L_grid=(1, 4, 16, 64))
+    torch.cuda.synchronize()
+    build["theta_calibration_s"] = time.perf_counter() - t1
+    build["theta_fit"] = {"a": th[0], "b": th[1], "crossovers_at_L_1_4_16_64": [float(v) for v in th[2]]}
+    info = g.info()
     stream = torch.cuda.current_stream()
     ids = torch.empty((nq, topk), dtype=torch.int64, device=dev)
     dist_ = torch.empty((nq, topk), dtype=torch.float32, device=dev)
@@ -239,7 +246,10 @@ def run_ours(args, rank, world, local):
     qms, qn16 = C.c_double(), C.c_int64()
     rii_lib.rii_kernel_timing_read(5, C.byref(qms), C.byref(qn16))
     q16 = qn16.value > 0 and qn16.value == kn.value
-    packed = q16 or (pn.value > 0 and pn.value == kn.value)
+    ums, un6 = C.c_double(), C.c_int64()
+    rii_lib.rii_kernel_timing_read(6, C.byref(ums), C.byref(un6))
+    u6 = un6.value > 0 and un6.value == kn.value
+    packed = u6 or q16 or (pn.value > 0 and pn.value == kn.value)
     rii_lib.rii_kernel_timing(0)
     torch.cuda.synchronize()
     _barrier(world)
@@ -254,7 +264,7 @@ def run_ours(args, rank, world, local):
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     # one 128-B shared-memory wavefront per clock per SM: 32 fp32 lookups, or 64
     # lookups with the bf16-packed or u16 fixed-point tables (2 B per lookup)
-    per_clk = LUT_LOOKUPS_PER_CLK_PER_SM * (2 if packed else 1)
+    per_clk = LUT_LOOKUPS_PER_CLK_PER_SM * (4 if u6 else 2 if packed else 1)
     lut_peak = SMS * per_clk * sm_max * 1e6  # lookups/s
     lookups = nq * n_local * M
     achieved = lookups / (kernel_ms / 1e3)
@@ -265,14 +275,17 @@ def run_ours(args, rank, world, local):
             traffic = json.load(f).get("dram_bytes_per_launch")
     roofline = {
         "bound": "alu",
-        "kernel": ("scan_fast_kernel<32,8,u16> (linear ADC scan + top-k, u16 fixed-point SWAR tables + exact rescore)"
+        "kernel": ("scan_fast_kernel<32,8,u6> (linear ADC scan + top-k, u6 fixed-point oct tables, bytewise SWAR "
+                   "sums + exact rescore)" if u6 else
+                   "scan_fast_kernel<32,8,u16> (linear ADC scan + top-k, u16 fixed-point SWAR tables + exact rescore)"
                    if q16 else
                    "scan_fast_kernel<32,8,packed> (linear ADC scan + top-k, bf16-packed tables + exact rescore)"
                    if packed else "scan_fast_kernel<32,6> (linear ADC scan + top-k, fp32 tables)"),
         "achieved": achieved / 1e9, "peak": lut_peak / 1e9, "unit": "Glookup/s",
         "frac": achieved / lut_peak, "traffic": traffic,
         "peak_basis": f"shared-memory LUT pipe: one 128-B wavefront/clk/SM = {per_clk} "
-                      f"{'u16 (2 B)' if q16 else 'bf16-packed (2 B)' if packed else 'fp32 (4 B)'} lookups/clk/SM x {SMS} SMs x "
+                      f"{'u6 (1 B)' if u6 else 'u16 (2 B)' if q16 else 'bf16-packed (2 B)' if packed else 'fp32 (4 B)'} "
+                      f"lookups/clk/SM x {SMS} SMs x "
                       f"{sm_max:.0f} MHz (sm_max_mhz, {peak_src})",
         "algorithmic_units": f"{nq} queries x {n_local} codes x {M} lookups per launch",
         "kernel_ms_per_launch": kernel_ms, "kernel_share_of_step": kernel_ms / (total_ms / args.steps),

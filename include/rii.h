@@ -73,9 +73,10 @@ uint64_t rii_launch_count(void);
  * 2 = top-k merge kernel, 3 = the linear-scan launches that used the
  * bf16-packed tables (a subset of 0), 4 = the u16-table bound pass (strided code
  * sample: gather + exact scan + merge + kk-th distance; one record per call),
- * 5 = the linear-scan launches that used the u16 fixed-point tables (a subset of 0).
- * total_ms / launches cover every launch since the last clear (read synchronises
- * with the recorded events).  which outside [0, 6) -> RII_ERR_ARG. */
+ * 5 = the linear-scan launches that used the u16 fixed-point tables, 6 = those that
+ * used the u6 fixed-point tables (each a subset of 0).  total_ms / launches cover
+ * every launch since the last clear (read synchronises with the recorded events).
+ * which outside [0, 7) -> RII_ERR_ARG. */
 void rii_kernel_timing(int32_t enable);
 rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *launches);
 

@@ -648,7 +648,7 @@ void rii_kernel_timing(int32_t enable) {
 
 rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *launches) {
     return guarded([&] {
-        arg_check(which >= 0 && which < TK_COUNT, "which must be in [0, 6)");
+        arg_check(which >= 0 && which < TK_COUNT, "which must be in [0, 7)");
         std::lock_guard<std::mutex> lk(g_tmu);
         drain_pairs();
         if (total_ms) *total_ms = g_total_ms[which];

@@ -35,7 +35,7 @@ inline void count_launch(int n = 1) { g_launches.fetch_add((uint64_t)n, std::mem
     } while (0)
 
 // Optional per-kernel event timing (rii_kernel_timing).
-enum TimedKernel { TK_LINEAR = 0, TK_IVF = 1, TK_MERGE = 2, TK_PACKED = 3, TK_BOUND = 4, TK_Q16 = 5, TK_COUNT = 6 };
+enum TimedKernel { TK_LINEAR = 0, TK_IVF = 1, TK_MERGE = 2, TK_PACKED = 3, TK_BOUND = 4, TK_Q16 = 5, TK_U6 = 6, TK_COUNT = 7 };
 struct KernelTimer {
     cudaStream_t st;
     int which;

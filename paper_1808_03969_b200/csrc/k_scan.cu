@@ -51,8 +51,15 @@ __host__ __device__ constexpr int smem_aux_bytes(int B, int kk) { return B * (kk
 template <int M, int B, bool LISTS, int NTH, int U, int TAB, int VARIANT = 0>
 __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     constexpr int W = M / 4, NP = B / 2, NQ = B / 4;
-    constexpr bool PACKED = TAB != 0, Q16 = TAB == 2;
+    constexpr bool PACKED = TAB != 0, U6 = TAB == 3, Q16 = TAB == 2 || U6;  // U6: integer path as Q16
     static_assert(!PACKED || B % 4 == 0, "packed tables hold 4 queries each");
+    static_assert(!U6 || (B == 8 && !LISTS), "u6 oct tables: 8 queries, linear mode");
+    // u6 options (VARIANT bit 0: 5-bit entries summed over 8 steps; bit 1: two table
+    // copies so that the code-word permutation needs one select stage, M = 32 only)
+    constexpr int U6_GJ = ((VARIANT & 1) && M >= 8) ? 8 : 4;
+    constexpr bool U6_R2 = U6 && (VARIANT & 2) && M == 32;
+    constexpr float U6_CAP = U6_GJ == 8 ? 31.0f : 63.0f;
+    constexpr int LUTB = U6 ? (U6_R2 ? 2 : 1) * OCT_BYTES : NQ * QUAD_BYTES;  // 64 KB-aligned integer tables
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t *lut = smem;
     const int kk = a.kk;
@@ -63,7 +70,7 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
         // lists and buffers go into the padding below it when they fit, else above.
         const uint32_t pad = (0u - (uint32_t)__cvta_generic_to_shared(smem)) & 0xffffu;
         lut = smem + pad;
-        aux = pad >= (uint32_t)smem_aux_bytes(B, kk) ? smem : lut + NQ * QUAD_BYTES;
+        aux = pad >= (uint32_t)smem_aux_bytes(B, kk) ? smem : lut + LUTB;
     }
     uint64_t *top = reinterpret_cast<uint64_t *>(aux);
     uint64_t *fresh = top + B * kk;
@@ -107,7 +114,19 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     };
     const int D = M * a.ds, tid = threadIdx.x, lane = tid & 31;
 
-    if (Q16 && a.qtab16) {
+    if constexpr (U6) {
+        // u6 tables: per-query scale s = 63 * ALPHA / T (T = +inf -> s = 0: everything passes)
+        float qs[8];
+        const float *tq[8];
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) {
+            const float T = __ldcg(a.gthr + query_of(qq));
+            qs[qq] = __fdiv_rd(U6_CAP * U6_ALPHA, fmaxf(T, 1e-30f));
+            if (tid == 0) qsc[qq] = qs[qq];
+            tq[qq] = a.tables + query_of(qq) * LUT_Q_FLOATS;
+        }
+        load_lut_oct_u6<U6_R2>(reinterpret_cast<uint32_t *>(lut), tq, qs, U6_CAP);
+    } else if (Q16 && a.qtab16) {
         // precomputed per-query u16 tables (q16_tables_kernel) with their scales
         if (tid < B) qsc[tid] = __ldg(a.qscale + query_of(tid));
 #pragma unroll
@@ -166,8 +185,18 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     // q16 column registers: bytes 0-1 = 8 (l ^ t) for t = 0,1 (colA) and 2,3 (colB),
     // bytes 2-3 = the table's shared address >> 16
     const uint32_t lut_hi = (uint32_t)__cvta_generic_to_shared(lut) & 0xffff0000u;
-    const uint32_t colA = lut_hi | (((uint32_t)lane ^ 0u) << 3) | (((uint32_t)lane ^ 1u) << 11);
-    const uint32_t colB = lut_hi | (((uint32_t)lane ^ 2u) << 3) | (((uint32_t)lane ^ 3u) << 11);
+    uint32_t colA = lut_hi | (((uint32_t)lane ^ 0u) << 3) | (((uint32_t)lane ^ 1u) << 11);
+    uint32_t colB = lut_hi | (((uint32_t)lane ^ 2u) << 3) | (((uint32_t)lane ^ 3u) << 11);
+    // two-copy u6 layout: word rotation by bit 2 of the lane only; bit 3 picks the copy
+    // (64 KB higher, columns XOR 8), so a half-warp still covers all 32 banks once
+    const uint32_t rw2 = ((uint32_t)lane >> 2) & 1u;
+    if constexpr (U6_R2) {
+        const uint32_t rep = ((uint32_t)lane >> 3) & 1u, r3 = (uint32_t)lane & 3u;
+        auto cb = [&](uint32_t t) { return ((rw2 << 5) | (((t ^ r3) & 3u) << 3)) ^ (rep << 6); };
+        const uint32_t hi = lut_hi + (rep << 16);
+        colA = hi | cb(0) | (cb(1) << 8);
+        colB = hi | cb(2) | (cb(3) << 8);
+    }
     // List mode: the query's global bound (the best kk-th distance any finished item
     // of this query saw, inflated by 1e-5 for the lane-rotated rounding) also filters.
     float gq[B];
@@ -278,15 +307,24 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
             for (int u = 0; u < U; ++u) {
                 const int64_t pos = base + u * NTH + tid;
                 if constexpr (Q16) {
-                    uint32_t acc0[NQ], acc1[NQ];
-                    adc_q16<M, NQ>(w[u], rw, sel, colA, colB, acc0, acc1);
                     uint32_t dq[B];
+                    if constexpr (U6) {
+                        uint32_t acc[4];
+                        adc_u6<M, U6_GJ, U6_R2>(w[u], U6_R2 ? rw2 : rw, sel, colA, colB, a.one, acc);
+                        dq[0] = acc[0] & 0xffffu; dq[2] = acc[0] >> 16;
+                        dq[1] = acc[1] & 0xffffu; dq[3] = acc[1] >> 16;
+                        dq[4] = acc[2] & 0xffffu; dq[6] = acc[2] >> 16;
+                        dq[5] = acc[3] & 0xffffu; dq[7] = acc[3] >> 16;
+                    } else {
+                        uint32_t acc0[NQ], acc1[NQ];
+                        adc_q16<M, NQ>(w[u], rw, sel, colA, colB, acc0, acc1);
 #pragma unroll
-                    for (int p = 0; p < NQ; ++p) {
-                        dq[4 * p] = acc0[p] & 0xffffu;
-                        dq[4 * p + 2] = acc0[p] >> 16;
-                        dq[4 * p + 1] = acc1[p] & 0xffffu;
-                        dq[4 * p + 3] = acc1[p] >> 16;
+                        for (int p = 0; p < NQ; ++p) {
+                            dq[4 * p] = acc0[p] & 0xffffu;
+                            dq[4 * p + 2] = acc0[p] >> 16;
+                            dq[4 * p + 1] = acc1[p] & 0xffffu;
+                            dq[4 * p + 3] = acc1[p] >> 16;
+                        }
                     }
                     bool any = false;
 #pragma unroll
@@ -564,14 +602,19 @@ static int scan_cfg() {
 }
 static int scan_threads() { return scan_cfg() == 0 ? 256 : 512; }
 
-static int q16_cfg() {
+// Linear integer-table kernel (RII_Q16_CFG for A/B; default: u6 oct tables for M = 32,
+// where they measured 134.6 ms against 204.1 ms for u16 on deep10m, u16 otherwise
+// (sift1m, M = 16: u16 16.0 ms, u6 24.6 ms)).  0 = u16, 384 threads, window 128;
+// 1 = u16 window 32; 2 = u16 256 x 2; 3 = u16 512 threads; 4 = u6 384; 5 = u6 512.
+static int q16_cfg(int M) {
     const char *e = getenv("RII_Q16_CFG");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : (M == 32 ? 7 : 0);
 }
-static int q16_nth() {
-    const int c = q16_cfg();
-    return c == 2 ? 256 : c == 3 ? 512 : 384;
+static int q16_nth(int M) {
+    const int c = q16_cfg(M);
+    return c == 2 ? 256 : (c == 3 || c == 5) ? 512 : 384;
 }
+bool q16_is_u6(int M) { const int c = q16_cfg(M); return c >= 4 && c <= 8; }
 
 template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr(bool q16 = false) {
@@ -584,7 +627,12 @@ static void *fast_kernel_ptr(bool q16 = false) {
                 // 384 threads keep the kernel spill-free (168 registers); the window
                 // is long because the bound makes pushes rare (B200, deep10m: 4 steps
                 // 272 ms, 8: 251 ms, 32: 223 ms, 128: 219 ms per 10k-query launch).
-                switch (q16_cfg()) {
+                switch (q16_cfg(M)) {
+                    case 4: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 3, 64>;  // u6 oct tables
+                    case 5: return (void *)scan_fast_kernel<M, 8, false, 512, 1, 3, 64>;
+                    case 6: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 3, 65>;  // 5-bit entries
+                    case 7: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 3, 66>;  // two copies
+                    case 8: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 3, 67>;  // both
                     case 1: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 2, 16>;  // window 32
                     case 2: return (void *)scan_fast_kernel<M, 8, false, 256, 2, 2, 64>;
                     case 3: return (void *)scan_fast_kernel<M, 8, false, 512, 1, 2, 64>;
@@ -616,9 +664,11 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
     a.codes = codes; a.n_codes = n; a.q = q; a.nq = nq; a.cb = cb; a.ds = ds; a.kk = kk;
     a.nb = pl.nb; a.chunk = pl.chunk; a.nc = pl.nc; a.out = out; a.tables = tables;
     a.gthr = gthr;
+    a.one = 1;
     void *args[] = {&a};
-    KernelTimer t(timer, st), tp(B == 8 && timer == TK_LINEAR ? (q16 ? TK_Q16 : TK_PACKED) : -1, st);
-    const int nth = q16 ? q16_nth() : (B == 8 ? PACKED_NTH : scan_threads());
+    KernelTimer t(timer, st), tp(B == 8 && timer == TK_LINEAR ? (q16 ? (q16_is_u6(M) ? TK_U6 : TK_Q16) : TK_PACKED) : -1,
+                                 st);
+    const int nth = q16 ? q16_nth(M) : (B == 8 ? PACKED_NTH : scan_threads());
     RII_CUDA(cudaLaunchKernel(kern, dim3(pl.nb * pl.nc), dim3(nth), args, smem, st));
     count_launch();
 }

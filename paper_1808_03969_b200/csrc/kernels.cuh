@@ -46,6 +46,7 @@ struct ScanArgs {
     // u16 list mode: precomputed per-query u16 tables [nq][256][32] and their scales
     const uint16_t *qtab16;
     const float *qscale;
+    uint32_t one;  // = 1 (runtime: keeps the u6 SWAR adds on the FMA pipe, lut.cuh fma_add)
 };
 
 // List-major inverted-index scan: B queries per CTA share one posting list's codes.

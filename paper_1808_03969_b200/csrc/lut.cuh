@@ -321,6 +321,66 @@ __device__ __forceinline__ void load_lut_quad_u16(uint32_t *dst, const uint16_t 
     }
 }
 
+// ---- u6 fixed-point oct tables (8 queries per 8-byte column) ---------------
+// Entry q(v) = floor(min(v (x)_rd s, 63)) with s = 63 * U6_ALPHA / T: an entry may
+// saturate (only ever lowering the sum: q(v) <= v s still holds, so the filter
+// Sum q <= floor(s thr (1 + 2^-16)) keeps every code with d <= thr -- saturation
+// only adds false positives, which the exact rescore removes).  Four lookups of
+// one query add in a byte lane (4 * 63 < 256) before the even / odd bytes are
+// widened into 16-bit lanes (M * 63 < 65536): one 128-B wavefront carries 128
+// lookups.  Column c of row z = bytes [q0 .. q7] (word 0 = queries 0-3).
+constexpr float U6_ALPHA = 8.0f;
+constexpr int OCT_BYTES = 256 * 256;  // 256 rows x 32 columns x 8 B: one table for 8 queries
+
+__device__ __forceinline__ uint32_t u6_entry(float v, float s, float cap) {
+    return __float2uint_rd(fminf(__fmul_rd(v, s), cap));
+}
+
+// Oct table(s) of 8 queries from their fp32 HBM tables (entries capped at `cap`).
+// R2 (M = 32): a second copy 64 KB above the first whose column c holds column
+// c ^ 8 (a 256-B row covers the 32 banks twice, so column c ^ 8 is the other half
+// of c's bank set), so that lanes 8 apart read disjoint banks with the same word
+// index.
+template <bool R2>
+__device__ __forceinline__ void load_lut_oct_u6(uint32_t *dst, const float *const (&t)[8], const float (&s)[8],
+                                                float cap) {
+    uint2 *o = reinterpret_cast<uint2 *>(dst);
+    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 4; e += blockDim.x) {  // 4 columns of one row
+        float4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float4 *>(t[k]) + e);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float a = c == 0 ? v[k].x : c == 1 ? v[k].y : c == 2 ? v[k].z : v[k].w;
+                const float b = c == 0 ? v[k + 4].x : c == 1 ? v[k + 4].y : c == 2 ? v[k + 4].z : v[k + 4].w;
+                lo |= u6_entry(a, s[k], cap) << (8 * k);
+                hi |= u6_entry(b, s[k + 4], cap) << (8 * k);
+            }
+            const int col = 4 * e + c;  // row * 32 + column
+            o[col] = make_uint2(lo, hi);
+            if constexpr (R2) o[OCT_BYTES / 8 + (col ^ 8)] = make_uint2(lo, hi);
+        }
+    }
+}
+
+// u6 lane-rotated ADC of one code against the oct table: per word index a, the four
+// steps' 8-byte loads are summed bytewise, then widened.  acc[0] = queries (0, 2)
+// in (low, high) 16-bit lanes, acc[1] = (1, 3), acc[2] = (4, 6), acc[3] = (5, 7).
+template <int M, int GJ, bool R2>
+__device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, const uint32_t (&sel)[4],
+                                       uint32_t colA, uint32_t colB, uint32_t one, uint32_t (&acc)[4]);
+
+// a * one + b on the FMA pipe (IMAD): `one` is a runtime 1 the compiler cannot fold,
+// which moves the SWAR additions off the integer ALU pipe (the u6 kernel's limiter).
+__device__ __forceinline__ uint32_t fma_add(uint32_t a, uint32_t one, uint32_t b) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+    return r;
+}
+
 // PRMT selectors of the q16 kernel: byte0 <- byte (t & 1) of the column register
 // (two column offsets per register), byte1 <- code byte ((t ^ r) & 3) of the
 // permuted word, bytes 2-3 <- bytes 2-3 of the column register (table base >> 16).
@@ -372,6 +432,55 @@ __device__ __forceinline__ void adc_q16(const uint32_t (&w)[M / 4], uint32_t rw,
                     acc1[p] = acc1[p] + h[p].y + v.y;
                 }
             }
+        }
+    }
+}
+
+template <int M, int GJ, bool R2>
+__device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, const uint32_t (&sel)[4],
+                                       uint32_t colA, uint32_t colB, uint32_t one, uint32_t (&acc)[4]) {
+    // GJ steps (4: 6-bit entries, 8: 5-bit entries) are summed bytewise before widening
+    constexpr int W = M / 4, GW = GJ / 4;
+    static_assert(W % GW == 0, "word groups");
+    uint32_t wp[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) wp[i] = w[i];
+    if constexpr (R2) {  // rw in {0, 1}: one select stage
+        const bool c = rw != 0;
+#pragma unroll
+        for (int i = 0; i < W; i += 2) {
+            const uint32_t x = wp[i], y = wp[i + 1];
+            wp[i] = c ? y : x;
+            wp[i + 1] = c ? x : y;
+        }
+    } else {
+        permute_words<W>(wp, rw);
+    }
+#pragma unroll
+    for (int g = 0; g < W / GW; ++g) {
+        uint32_t s0 = 0, s1 = 0;
+#pragma unroll
+        for (int h = 0; h < GW; ++h) {
+            const int aw = g * GW + h;
+            const uint32_t ca = colA ^ (uint32_t)(aw * 0x2020), cb = colB ^ (uint32_t)(aw * 0x2020);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t off = __byte_perm(wp[aw], t < 2 ? ca : cb, sel[t]);
+                const uint2 v = lds64_quad(off, 0);
+                const bool first = h == 0 && t == 0;
+                s0 = first ? v.x : fma_add(v.x, one, s0);  // bytewise: GJ * cap < 256, no carries
+                s1 = first ? v.y : fma_add(v.y, one, s1);
+            }
+        }
+        const uint32_t e0 = s0 & 0x00ff00ffu, o0 = __byte_perm(s0, 0u, 0x4341);
+        const uint32_t e1 = s1 & 0x00ff00ffu, o1 = __byte_perm(s1, 0u, 0x4341);
+        if (g == 0) {
+            acc[0] = e0; acc[1] = o0; acc[2] = e1; acc[3] = o1;
+        } else {
+            acc[0] = fma_add(e0, one, acc[0]);
+            acc[1] = fma_add(o0, one, acc[1]);
+            acc[2] = fma_add(e1, one, acc[2]);
+            acc[3] = fma_add(o1, one, acc[3]);
         }
     }
 }

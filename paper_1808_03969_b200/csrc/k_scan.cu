@@ -44,7 +44,7 @@ __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
 }
 
 // Top lists, fresh buffers, counters, thresholds, scratch[16] and the q16 scales.
-__host__ __device__ constexpr int smem_aux_bytes(int B, int kk) { return B * (kk + NEWCAP) * 8 + B * 8 + 64 + B * 8; }
+__host__ __device__ constexpr int smem_aux_bytes(int B, int kk) { return B * (kk + NEWCAP) * 8 + B * 8 + 64 + B * 12; }
 
 // TAB: 0 = fp32 pair tables, 1 = bf16-packed quad tables, 2 = u16 fixed-point quad
 // tables (integer SWAR sums, linear mode with a per-query bound).
@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     }
     // List mode: the item's query indices are read from qlist once into shared memory.
     int *qid_s = reinterpret_cast<int *>(qsc + B);
+    float *tsc = qsc + 2 * B;  // integer tables: the bound T each query's scale was set from
     if constexpr (LISTS) {
         if (threadIdx.x < B) {
             const int qq = (int)threadIdx.x < nqi ? (int)threadIdx.x : nqi - 1;
@@ -121,8 +122,8 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
 #pragma unroll
         for (int qq = 0; qq < 8; ++qq) {
             const float T = __ldcg(a.gthr + query_of(qq));
-            qs[qq] = __fdiv_rd(U6_CAP * U6_ALPHA, fmaxf(T, 1e-30f));
-            if (tid == 0) qsc[qq] = qs[qq];
+            qs[qq] = __fdiv_rd(U6_CAP * u6_alpha(M), fmaxf(T, 1e-30f));
+            if (tid == 0) { qsc[qq] = qs[qq]; tsc[qq] = T; }
             tq[qq] = a.tables + query_of(qq) * LUT_Q_FLOATS;
         }
         load_lut_oct_u6<U6_R2>(reinterpret_cast<uint32_t *>(lut), tq, qs, U6_CAP);
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
         for (int qq = 0; qq < B; ++qq) {
             const float T = __ldcg(a.gthr + query_of(qq));  // current bound on the kk-th distance
             qs[qq] = __fdiv_rd((float)q16_cap<M>(), fmaxf(T, 1e-30f));
-            if (tid == 0) qsc[qq] = qs[qq];
+            if (tid == 0) { qsc[qq] = qs[qq]; tsc[qq] = T; }
         }
 #pragma unroll
         for (int p = 0; p < NQ; ++p)
@@ -219,6 +220,50 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
 #pragma unroll
     for (int qq = 0; qq < B; ++qq) th[qq] = relax(fminf(thr[qq], gq[qq]));
     set_thq();
+    // Integer tables (linear mode): when a query's bound has halved since its scale was
+    // set, re-quantise the tables at the new bound (any scale keeps the filter exact;
+    // a tight one keeps it selective).  Block-uniform: thread 0 decides from smem.
+    auto maybe_rescale = [&]() {
+        if constexpr (Q16 && !LISTS) {
+            if (tid == 0) {
+                int f = 0;
+                for (int qq = 0; qq < B; ++qq) f |= fminf(thr[qq], gq[qq]) < 0.5f * tsc[qq];
+                if (f) {
+                    for (int qq = 0; qq < B; ++qq) {
+                        const float T = fminf(thr[qq], gq[qq]);
+                        if (!(T < tsc[qq])) continue;
+                        tsc[qq] = T;
+                        qsc[qq] = U6 ? __fdiv_rd(U6_CAP * u6_alpha(M), fmaxf(T, 1e-30f))
+                                     : __fdiv_rd((float)q16_cap<M>(), fmaxf(T, 1e-30f));
+                    }
+                }
+                scratch[15] = f;
+            }
+            __syncthreads();
+            if (scratch[15]) {
+                float qs[B];
+#pragma unroll
+                for (int qq = 0; qq < B; ++qq) qs[qq] = qsc[qq];
+                if constexpr (U6) {
+                    const float *tq[8];
+#pragma unroll
+                    for (int qq = 0; qq < 8; ++qq) tq[qq] = a.tables + query_of(qq) * LUT_Q_FLOATS;
+                    load_lut_oct_u6<U6_R2>(reinterpret_cast<uint32_t *>(lut), tq, qs, U6_CAP);
+                } else {
+#pragma unroll
+                    for (int p = 0; p < NQ; ++p)
+                        load_lut_quad_q16<M>(reinterpret_cast<uint32_t *>(lut + p * QUAD_BYTES),
+                                             a.tables + query_of(4 * p) * LUT_Q_FLOATS,
+                                             a.tables + query_of(4 * p + 1) * LUT_Q_FLOATS,
+                                             a.tables + query_of(4 * p + 2) * LUT_Q_FLOATS,
+                                             a.tables + query_of(4 * p + 3) * LUT_Q_FLOATS, qs[4 * p], qs[4 * p + 1],
+                                             qs[4 * p + 2], qs[4 * p + 3]);
+                }
+                __syncthreads();
+                set_thq();
+            }
+        }
+    };
     // Packed mode: canonical (CA2) rescore of the fresh entries from the queries'
     // fp32 HBM tables before they are compacted into the exact top lists.
     auto rescore_fresh = [&]() {
@@ -411,6 +456,7 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
             }
             __syncthreads();  // snapshot taken before the next window pushes
         }
+        maybe_rescale();
         if (safe > 0) --safe;
     }
     __syncthreads();

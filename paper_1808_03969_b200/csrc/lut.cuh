@@ -322,14 +322,15 @@ __device__ __forceinline__ void load_lut_quad_u16(uint32_t *dst, const uint16_t 
 }
 
 // ---- u6 fixed-point oct tables (8 queries per 8-byte column) ---------------
-// Entry q(v) = floor(min(v (x)_rd s, 63)) with s = 63 * U6_ALPHA / T: an entry may
+// Entry q(v) = floor(min(v (x)_rd s, 63)) with s = 63 * alpha / T, alpha = M / 4 (an
+// entry saturates at 4x the mean entry of a code at the threshold): an entry may
 // saturate (only ever lowering the sum: q(v) <= v s still holds, so the filter
 // Sum q <= floor(s thr (1 + 2^-16)) keeps every code with d <= thr -- saturation
 // only adds false positives, which the exact rescore removes).  Four lookups of
 // one query add in a byte lane (4 * 63 < 256) before the even / odd bytes are
 // widened into 16-bit lanes (M * 63 < 65536): one 128-B wavefront carries 128
 // lookups.  Column c of row z = bytes [q0 .. q7] (word 0 = queries 0-3).
-constexpr float U6_ALPHA = 8.0f;
+__host__ __device__ constexpr float u6_alpha(int M) { return M >= 4 ? M / 4.0f : 1.0f; }
 constexpr int OCT_BYTES = 256 * 256;  // 256 rows x 32 columns x 8 B: one table for 8 queries
 
 __device__ __forceinline__ uint32_t u6_entry(float v, float s, float cap) {

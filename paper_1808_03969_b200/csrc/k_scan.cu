@@ -857,22 +857,27 @@ void launch_assign_scan(const uint8_t *codes, int64_t n, const uint8_t *centers,
 }
 
 // ------------------------------------------------------------ LUT tables ---
-// One CTA per query: warp w fills rows z = w, w + 8, ...; lane c = column c,
-// A(c mod M, z) by CA1 (the code book stays in L1: this kernel has no smem).
+// One CTA per query, thread z = code word z: the code book rows of subspace m are
+// read coalesced (consecutive z), A(m, z) (CA1) goes to a [256][33] smem tile, and
+// the rows (column c = A(c mod M, z)) are written out coalesced.
 __global__ void __launch_bounds__(256) lut_tables_kernel(const float *__restrict__ q, int64_t nq,
                                                          const float *__restrict__ cb, int M, int ds,
                                                          float *__restrict__ tables) {
+    __shared__ float qv[32 * 64];
+    __shared__ float tile[KS][33];
     const int64_t qi = blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int m = lane % M;
-    const float *qv = q + qi * (int64_t)M * ds + m * ds;
-    float *t = tables + qi * LUT_Q_FLOATS;
-    for (int z = warp; z < KS; z += 8) {
+    const int D = M * ds, z = threadIdx.x;
+    for (int e = threadIdx.x; e < D; e += blockDim.x) qv[e] = q[qi * D + e];
+    __syncthreads();
+    for (int m = 0; m < M; ++m) {
         const float *cv = cb + ((size_t)m * KS + z) * ds;
         float a = 0.f;
-        for (int j = 0; j < ds; ++j) a = ca1_step(a, qv[j], cv[j]);
-        t[z * 32 + lane] = a;
+        for (int j = 0; j < ds; ++j) a = ca1_step(a, qv[m * ds + j], __ldg(cv + j));
+        tile[z][m] = a;
     }
+    __syncthreads();
+    float *t = tables + qi * LUT_Q_FLOATS;
+    for (int e = threadIdx.x; e < LUT_Q_FLOATS; e += blockDim.x) t[e] = tile[e >> 5][(e & 31) & (M - 1)];
 }
 
 void launch_lut_tables(const float *q, int64_t nq, const float *cb, int D, int M, float *tables, cudaStream_t st) {

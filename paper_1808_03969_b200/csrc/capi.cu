@@ -555,10 +555,16 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             launch_list_scan(x->M, Bl, sa, n_items, st);
             if (n_items_b > 0) {
                 tr.mark("list scan A");
-                uint16_t *t16 = x->s_tab16.get<uint16_t>((size_t)a.nq * LUT_Q_FLOATS);
                 float *qsc = x->s_qscale.get<float>(a.nq);
-                launch_q16_tables(tables, gthr, a.nq, x->M, t16, qsc, st);
-                sa.qtab16 = t16;
+                if (list_u6_cfg(x->M)) {  // u6 oct items
+                    uint8_t *t8 = x->s_tab16.get<uint8_t>((size_t)a.nq * LUT_Q_FLOATS);
+                    launch_u6_tables(tables, gthr, a.nq, x->M, t8, qsc, st);
+                    sa.qtab8 = t8;
+                } else {
+                    uint16_t *t16 = x->s_tab16.get<uint16_t>((size_t)a.nq * LUT_Q_FLOATS);
+                    launch_q16_tables(tables, gthr, a.nq, x->M, t16, qsc, st);
+                    sa.qtab16 = t16;
+                }
                 sa.qscale = qsc;
                 sa.items = items + n_items;
                 launch_list_scan(x->M, 8, sa, n_items_b, st, true);

@@ -49,11 +49,18 @@ __host__ __device__ constexpr int smem_aux_bytes(int B, int kk) { return B * (kk
 // TAB: 0 = fp32 pair tables, 1 = bf16-packed quad tables, 2 = u16 fixed-point quad
 // tables (integer SWAR sums, linear mode with a per-query bound).
 template <int M, int B, bool LISTS, int NTH, int U, int TAB, int VARIANT = 0>
-__global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
+__global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(const ScanArgs a) {
     constexpr int W = M / 4, NP = B / 2, NQ = B / 4;
     constexpr bool PACKED = TAB != 0, U6 = TAB == 3, Q16 = TAB == 2 || U6;  // U6: integer path as Q16
     static_assert(!PACKED || B % 4 == 0, "packed tables hold 4 queries each");
-    static_assert(!U6 || (B == 8 && !LISTS), "u6 oct tables: 8 queries, linear mode");
+    // VARIANT bit 7 (FIXB): the integer tables sit at dynamic-smem offset 0, whose shared
+    // address is the compile-time 0x400 (checked at run time), so the LDS carries it as
+    // an immediate and no 64 KB-aligned padding is needed (two CTAs fit on an SM).
+    constexpr bool FIXB = (VARIANT & 128) != 0;
+    constexpr int LDS_BASE = FIXB ? 0x400 : 0;
+    static_assert(!U6 || B == 8, "u6 oct tables hold 8 queries");
+    static_assert(!(U6 && LISTS) || FIXB, "list-mode u6 uses the fixed-base layout");
+    static_assert(!FIXB || U6, "the fixed-base layout is implemented for the u6 tables");
     // u6 options (VARIANT bit 0: 5-bit entries summed over 8 steps; bit 1: two table
     // copies so that the code-word permutation needs one select stage, M = 32 only)
     constexpr int U6_GJ = ((VARIANT & 1) && M >= 8) ? 8 : 4;
@@ -64,7 +71,10 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     uint8_t *lut = smem;
     const int kk = a.kk;
     uint8_t *aux = smem + (PACKED ? NQ * QUAD_BYTES : NP * LUT_PAIR_BYTES);
-    if constexpr (Q16) {
+    if constexpr (Q16 && FIXB) {
+        if ((uint32_t)__cvta_generic_to_shared(smem) != (uint32_t)LDS_BASE) __trap();  // layout assumption
+        aux = smem + LUTB;
+    } else if constexpr (Q16) {
         // The u16 tables start at a 64 KB-aligned shared address, so that one PRMT
         // yields the complete LDS address (bytes 2-3 = table base >> 16); the top
         // lists and buffers go into the padding below it when they fit, else above.
@@ -115,7 +125,14 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     };
     const int D = M * a.ds, tid = threadIdx.x, lane = tid & 31;
 
-    if constexpr (U6) {
+    if constexpr (U6 && LISTS) {
+        // precomputed per-query u6 tables (u6_tables_kernel) with their scales
+        if (tid < B) qsc[tid] = __ldg(a.qscale + query_of(tid));
+        const uint8_t *tq[8];
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) tq[qq] = a.qtab8 + query_of(qq) * LUT_Q_FLOATS;
+        load_lut_oct_u8pre<U6_R2>(reinterpret_cast<uint32_t *>(lut), tq);
+    } else if constexpr (U6) {
         // u6 tables: per-query scale s = 63 * ALPHA / T (T = +inf -> s = 0: everything passes)
         float qs[8];
         const float *tq[8];
@@ -185,7 +202,7 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     else make_selectors(r, sel);
     // q16 column registers: bytes 0-1 = 8 (l ^ t) for t = 0,1 (colA) and 2,3 (colB),
     // bytes 2-3 = the table's shared address >> 16
-    const uint32_t lut_hi = (uint32_t)__cvta_generic_to_shared(lut) & 0xffff0000u;
+    const uint32_t lut_hi = FIXB ? 0u : (uint32_t)__cvta_generic_to_shared(lut) & 0xffff0000u;
     uint32_t colA = lut_hi | (((uint32_t)lane ^ 0u) << 3) | (((uint32_t)lane ^ 1u) << 11);
     uint32_t colB = lut_hi | (((uint32_t)lane ^ 2u) << 3) | (((uint32_t)lane ^ 3u) << 11);
     // two-copy u6 layout: word rotation by bit 2 of the lane only; bit 3 picks the copy
@@ -305,7 +322,7 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
     // (its pushes dropped, the buffer compacted) and redone one step at a time,
     // which cannot overflow (an empty buffer holds a whole step, NEWCAP >= NT*U).
     // (u16 tables start from the sampled bound, so few pushes: VARIANT bits 2/3 widen the window)
-    constexpr int STEP = NTH * U, WIN = (VARIANT & 0xfc) ? (VARIANT & 0xfc) * 2 : 4, SOFT = NEWCAP / 4;
+    constexpr int STEP = NTH * U, WIN = (VARIANT & 0x7c) ? (VARIANT & 0x7c) * 2 : 4, SOFT = NEWCAP / 4;
     static_assert(NEWCAP >= STEP, "a single step must fit the fresh buffer");
     int *s_ovf = scratch + 1, *s_cnt0 = scratch + 2;  // flags, fill snapshot at the window start
     uint32_t w[U][W];
@@ -355,7 +372,7 @@ __global__ void __launch_bounds__(NTH, 1) scan_fast_kernel(const ScanArgs a) {
                     uint32_t dq[B];
                     if constexpr (U6) {
                         uint32_t acc[4];
-                        adc_u6<M, U6_GJ, U6_R2>(w[u], U6_R2 ? rw2 : rw, sel, colA, colB, a.one, acc);
+                        adc_u6<M, U6_GJ, U6_R2, LDS_BASE>(w[u], U6_R2 ? rw2 : rw, sel, colA, colB, a.one, acc);
                         dq[0] = acc[0] & 0xffffu; dq[2] = acc[0] >> 16;
                         dq[1] = acc[1] & 0xffffu; dq[3] = acc[1] >> 16;
                         dq[4] = acc[2] & 0xffffu; dq[6] = acc[2] >> 16;
@@ -661,12 +678,32 @@ static int q16_nth(int M) {
     return c == 2 ? 256 : (c == 3 || c == 5) ? 512 : 384;
 }
 bool q16_is_u6(int M) { const int c = q16_cfg(M); return c >= 4 && c <= 8; }
+// List-major u6 items (phase B of the two-phase IVF): 0 = u16 items; 1 = u6, 192
+// threads, one table copy (two CTAs per SM); 2 = u6, 384 threads, two copies;
+// 3 = u6, 384 threads, one copy.
+int list_u6_cfg(int M) {
+    const char *e = getenv("RII_LIST_U6");
+    return M != 32 ? 0 : e ? atoi(e) : 3;
+}
+static int list_q16_nth(int M) { return list_u6_cfg(M) == 1 ? 192 : 384; }
+static size_t smem_list_q16(int M, int kk) {
+    const int c = list_u6_cfg(M);
+    if (c == 0) return smem_q16(kk);
+    return (size_t)(c == 2 ? 2 : 1) * OCT_BYTES + smem_aux_bytes(8, kk) + 16;
+}
 
 template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr(bool q16 = false) {
     if constexpr (B == 8) {
         if constexpr (LISTS) {
-            if (q16) return (void *)scan_fast_kernel<M, 8, true, 384, 1, 2, 64>;  // window 128
+            if (q16) {
+                switch (list_u6_cfg(M)) {  // RII_LIST_U6 (A/B): u6 oct items (fixed-base layout)
+                    case 1: return (void *)scan_fast_kernel<M, 8, true, 192, 1, 3, 128 | 64>;      // 2 CTAs/SM
+                    case 2: return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64 | 2>;  // two copies
+                    case 3: return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64>;
+                    default: return (void *)scan_fast_kernel<M, 8, true, 384, 1, 2, 64>;  // u16, window 128
+                }
+            }
         } else {
             if (q16) {
                 // RII_Q16_CFG (A/B): threads x codes per step, barrier window (steps).
@@ -755,12 +792,13 @@ template <int M, int B>
 static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
     q16 = q16 && B == 8;
     void *kern = fast_kernel_ptr<M, B, true>(q16);
-    const size_t smem = q16 ? smem_q16(a.kk) : smem_fast(B, a.kk);
+    const size_t smem = q16 ? smem_list_q16(M, a.kk) : smem_fast(B, a.kk);
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ScanArgs aa = a;
+    aa.one = 1;
     void *args[] = {&aa};
     KernelTimer t(TK_IVF, st);
-    const int nth = q16 ? 384 : (B == 8 ? PACKED_NTH : scan_threads());
+    const int nth = q16 ? list_q16_nth(M) : (B == 8 ? PACKED_NTH : scan_threads());
     RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)n_items), dim3(nth), args, smem, st));
     count_launch();
 }
@@ -939,6 +977,34 @@ __global__ void __launch_bounds__(256) q16_tables_kernel(const float *__restrict
         o[e] = make_uint2(q16_entry(v.x, s, cap) | (q16_entry(v.y, s, cap) << 16),
                           q16_entry(v.z, s, cap) | (q16_entry(v.w, s, cap) << 16));
     }
+}
+
+// Per-query u6 tables (lut.cuh u6 entries, bytes [z][32]) at scale 63 * alpha / gthr[q].
+template <int M>
+__global__ void __launch_bounds__(256) u6_tables_kernel(const float *__restrict__ tables, const float *__restrict__ gthr,
+                                                        int64_t nq, uint8_t *__restrict__ out, float *__restrict__ scale) {
+    const int64_t q = blockIdx.x;
+    const float s = __fdiv_rd(63.0f * u6_alpha(M), fmaxf(__ldcg(gthr + q), 1e-30f));
+    if (threadIdx.x == 0) scale[q] = s;
+    const float4 *t4 = reinterpret_cast<const float4 *>(tables + q * LUT_Q_FLOATS);
+    uint32_t *o = reinterpret_cast<uint32_t *>(out + q * LUT_Q_FLOATS);
+    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 4; e += blockDim.x) {
+        const float4 v = __ldg(t4 + e);
+        o[e] = u6_entry(v.x, s, 63.f) | (u6_entry(v.y, s, 63.f) << 8) | (u6_entry(v.z, s, 63.f) << 16) |
+               (u6_entry(v.w, s, 63.f) << 24);
+    }
+}
+
+void launch_u6_tables(const float *tables, const float *gthr, int64_t nq, int M, uint8_t *out, float *scale,
+                      cudaStream_t st) {
+    if (nq <= 0) return;
+    switch (M) {
+        case 4: u6_tables_kernel<4><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
+        case 8: u6_tables_kernel<8><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
+        case 16: u6_tables_kernel<16><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
+        default: u6_tables_kernel<32><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
+    }
+    RII_LAUNCHED();
 }
 
 void launch_q16_tables(const float *tables, const float *gthr, int64_t nq, int M, uint16_t *out, float *scale,

@@ -45,6 +45,7 @@ struct ScanArgs {
     const uint8_t *qcodes;
     // u16 list mode: precomputed per-query u16 tables [nq][256][32] and their scales
     const uint16_t *qtab16;
+    const uint8_t *qtab8;  // u6 list mode: precomputed per-query u6 tables [nq][256][32]
     const float *qscale;
     uint32_t one;  // = 1 (runtime: keeps the u6 SWAR adds on the FMA pipe, lut.cuh fma_add)
 };
@@ -77,6 +78,10 @@ bool q16_supported(int kk);  // shared-memory budget of the u16 kernels (kk <= 2
 // out[q] = u16 entries of tables[q] with scale[q] = CAP / gthr[q] (u16 list scan).
 void launch_q16_tables(const float *tables, const float *gthr, int64_t nq, int M, uint16_t *out, float *scale,
                        cudaStream_t st);
+// u6 list items (M = 32, RII_LIST_U6): config (0 = u16 items) and the per-query u6 tables.
+int list_u6_cfg(int M);
+void launch_u6_tables(const float *tables, const float *gthr, int64_t nq, int M, uint8_t *out, float *scale,
+                      cudaStream_t st);
 void launch_strided_gather(const uint8_t *codes, int M, int64_t stride, int64_t n, uint8_t *out, cudaStream_t st);
 void launch_kth_bound(const uint64_t *keys, int64_t nq, int kk, float *bound, cudaStream_t st);
 

@@ -370,9 +370,33 @@ __device__ __forceinline__ void load_lut_oct_u6(uint32_t *dst, const float *cons
 // u6 lane-rotated ADC of one code against the oct table: per word index a, the four
 // steps' 8-byte loads are summed bytewise, then widened.  acc[0] = queries (0, 2)
 // in (low, high) 16-bit lanes, acc[1] = (1, 3), acc[2] = (4, 6), acc[3] = (5, 7).
-template <int M, int GJ, bool R2>
+template <int M, int GJ, bool R2, int BASE = 0>
 __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, const uint32_t (&sel)[4],
                                        uint32_t colA, uint32_t colB, uint32_t one, uint32_t (&acc)[4]);
+
+// Oct layout from 8 precomputed per-query u6 tables ([z][32 columns] bytes, written by
+// u6_tables_kernel): column c = [t0[c] .. t7[c]] (an 8 x 8 byte transpose per group of
+// 8 columns, 3 PRMT per output word).  R2: the second copy as in load_lut_oct_u6.
+template <bool R2>
+__device__ __forceinline__ void load_lut_oct_u8pre(uint32_t *dst, const uint8_t *const (&t)[8]) {
+    uint2 *o = reinterpret_cast<uint2 *>(dst);
+    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 8; e += blockDim.x) {  // 8 columns of one row
+        uint2 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const uint2 *>(t[k]) + e);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const uint32_t sc = (uint32_t)(c & 3) | ((uint32_t)(4 + (c & 3)) << 4);  // byte c of a, of b
+            auto w_of = [&](int k) { return c < 4 ? v[k].x : v[k].y; };
+            const uint32_t p01 = __byte_perm(w_of(0), w_of(1), sc), p23 = __byte_perm(w_of(2), w_of(3), sc);
+            const uint32_t p45 = __byte_perm(w_of(4), w_of(5), sc), p67 = __byte_perm(w_of(6), w_of(7), sc);
+            const uint2 col = make_uint2(__byte_perm(p01, p23, 0x5410), __byte_perm(p45, p67, 0x5410));
+            const int idx = 8 * e + c;  // row * 32 + column
+            o[idx] = col;
+            if constexpr (R2) o[OCT_BYTES / 8 + (idx ^ 8)] = col;
+        }
+    }
+}
 
 // a * one + b on the FMA pipe (IMAD): `one` is a runtime 1 the compiler cannot fold,
 // which moves the SWAR additions off the integer ALU pipe (the u6 kernel's limiter).
@@ -388,6 +412,14 @@ __device__ __forceinline__ uint32_t fma_add(uint32_t a, uint32_t one, uint32_t b
 __device__ __forceinline__ void make_selectors_q16(uint32_t r, uint32_t (&sel)[4]) {
 #pragma unroll
     for (int t = 0; t < 4; ++t) sel[t] = 0x7600u | ((((uint32_t)t ^ r) & 3u) << 4) | (4u + ((uint32_t)t & 1u));
+}
+
+// 8-byte shared load at address off + IMM (a compile-time offset).
+template <int IMM>
+__device__ __forceinline__ uint2 lds64_imm(uint32_t off) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2+%3];" : "=r"(v.x), "=r"(v.y) : "r"(off), "n"(IMM));
+    return v;
 }
 
 // 8-byte shared load at address off + p * QUAD_BYTES (p an unrolled constant).
@@ -437,7 +469,7 @@ __device__ __forceinline__ void adc_q16(const uint32_t (&w)[M / 4], uint32_t rw,
     }
 }
 
-template <int M, int GJ, bool R2>
+template <int M, int GJ, bool R2, int BASE>
 __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, const uint32_t (&sel)[4],
                                        uint32_t colA, uint32_t colB, uint32_t one, uint32_t (&acc)[4]) {
     // GJ steps (4: 6-bit entries, 8: 5-bit entries) are summed bytewise before widening
@@ -467,7 +499,7 @@ __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, 
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const uint32_t off = __byte_perm(wp[aw], t < 2 ? ca : cb, sel[t]);
-                const uint2 v = lds64_quad(off, 0);
+                const uint2 v = lds64_imm<BASE>(off);
                 const bool first = h == 0 && t == 0;
                 s0 = first ? v.x : fma_add(v.x, one, s0);  // bytewise: GJ * cap < 256, no carries
                 s1 = first ? v.y : fma_add(v.y, one, s1);

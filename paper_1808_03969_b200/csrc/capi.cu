@@ -451,13 +451,19 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
                 const int64_t stride = n_codes / ns;
                 uint8_t *samp = x->s_samp.get<uint8_t>((size_t)ns * x->M);
                 launch_strided_gather(scan_codes, x->M, stride, ns, samp, st);
-                // one chunk per query batch: the sample is short, so per-CTA top-k work dominates
-                ScanPlan ps = plan_linear(x->M, kk, a.nq, ns, x->num_sms, true, ns_chunks());
-                uint64_t *sp = x->s_spart.get<uint64_t>((size_t)ps.nb * ps.B * ps.nc * kk);
-                launch_linear_scan(ps, samp, ns, x->M, a.q, a.nq, cb, x->D, kk, sp, st, tables, nullptr, false, -1);
-                uint64_t *sk = x->s_ckeys.get<uint64_t>((size_t)a.nq * kk);
-                launch_merge(sp, (int64_t)ps.nc * kk, kk, ps.nc, a.nq, kk, kk, IdMap(), nullptr, nullptr, sk, st);
-                launch_kth_bound(sk, a.nq, kk, gthr, st);
+                if (ns >= 4096 && kk <= 512 && !getenv("RII_BOUND_TOPK")) {
+                    // kk-th smallest of 1024 group minima (no top-k lists; k_scan.cu)
+                    launch_group_min_bound(samp, ns, x->M, tables, a.nq, kk, gthr, st);
+                } else {
+                    // exact kk-th over the sample: one chunk per query batch
+                    ScanPlan ps = plan_linear(x->M, kk, a.nq, ns, x->num_sms, true, ns_chunks());
+                    uint64_t *sp = x->s_spart.get<uint64_t>((size_t)ps.nb * ps.B * ps.nc * kk);
+                    launch_linear_scan(ps, samp, ns, x->M, a.q, a.nq, cb, x->D, kk, sp, st, tables, nullptr, false,
+                                       -1);
+                    uint64_t *sk = x->s_ckeys.get<uint64_t>((size_t)a.nq * kk);
+                    launch_merge(sp, (int64_t)ps.nc * kk, kk, ps.nc, a.nq, kk, kk, IdMap(), nullptr, nullptr, sk, st);
+                    launch_kth_bound(sk, a.nq, kk, gthr, st);
+                }
                 tr.mark("q16 bound");
             }
             uint64_t *pp = x->s_part.get<uint64_t>((size_t)pl.nb * pl.B * pl.nc * kk);

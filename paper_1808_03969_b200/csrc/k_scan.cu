@@ -947,6 +947,99 @@ void launch_strided_gather(const uint8_t *codes, int M, int64_t stride, int64_t 
     RII_LAUNCHED();
 }
 
+// Group-minimum bound: the sample's ns codes form G = ns / GSZ groups; each group's
+// minimum ADC distance is a distance of a distinct sample code, so the kk-th smallest
+// of the G group minima is >= the kk-th smallest of the sample, which is >= the final
+// kk-th distance (the sample is a subset).  No top-k list is needed: CTA = 6 queries
+// (three fp32 pair tables, lane-rotated sums inflated by 1e-5 to bound the canonical
+// CA2 value from above), thread = groups, then a bitonic sort of the G minima.
+constexpr int GB_Q = 6, GB_NT = 512;
+
+template <int M>
+__global__ void __launch_bounds__(GB_NT, 1) group_min_bound_kernel(const uint8_t *__restrict__ samp, int64_t ns,
+                                                                   int gsz, const float *__restrict__ tables,
+                                                                   int64_t nq, int kk, float *__restrict__ gthr) {
+    constexpr int W = M / 4, NP = GB_Q / 2;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t q0 = (int64_t)blockIdx.x * GB_Q;
+    const int G = (int)(ns / gsz);
+    auto qidx = [&](int qq) { return min(q0 + qq, nq - 1); };
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+        load_lut_pair(reinterpret_cast<float *>(smem + p * LUT_PAIR_BYTES), tables + qidx(2 * p) * LUT_Q_FLOATS,
+                      tables + qidx(2 * p + 1) * LUT_Q_FLOATS);
+    __syncthreads();
+    const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
+    uint32_t sel[4];
+    make_selectors(r, sel);
+    // groups g = tid, tid + NT, ...; per group the min over its gsz codes
+    float gmin[2][GB_Q];
+    const int ng = (G + GB_NT - 1) / GB_NT;  // <= 2 (G <= 1024)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int qq = 0; qq < GB_Q; ++qq) gmin[h][qq] = __int_as_float(0x7f800000);
+    for (int h = 0; h < ng && h < 2; ++h) {
+        const int g = tid + h * GB_NT;
+        if (g >= G) continue;
+        const uint8_t *gp = samp + (int64_t)g * gsz * M;
+        uint32_t wn[W];
+        load_code<W>(gp, wn);  // the next code is loaded while the current one is summed
+        for (int i = 0; i < gsz; ++i) {
+            uint32_t w[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) w[k] = wn[k];
+            if (i + 1 < gsz) load_code<W>(gp + (int64_t)(i + 1) * M, wn);
+            float2 acc[NP];
+            adc_rotated<M, GB_Q>(smem, w, rw, sel, l8, acc);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                gmin[h][2 * p] = fminf(gmin[h][2 * p], acc[p].x);
+                gmin[h][2 * p + 1] = fminf(gmin[h][2 * p + 1], acc[p].y);
+            }
+        }
+    }
+    __syncthreads();  // tables no longer needed: reuse smem for the sort keys
+    uint64_t *keys = reinterpret_cast<uint64_t *>(smem);  // [GB_Q][1024]
+    for (int e = tid; e < GB_Q * 1024; e += GB_NT) keys[e] = KEY_MAX;
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int g = tid + h * GB_NT;
+        if (g >= G) continue;
+#pragma unroll
+        for (int qq = 0; qq < GB_Q; ++qq) keys[qq * 1024 + g] = make_key(gmin[h][qq], (uint32_t)g);
+    }
+    __syncthreads();
+    bitonic_sort_rows(keys, GB_Q, 1024, 1024);
+    if (tid < GB_Q && q0 + tid < nq) {
+        const uint64_t k = keys[tid * 1024 + kk - 1];
+        // rotated fp32 order differs from CA2 by < 4e-6 relative: inflate to bound it
+        gthr[q0 + tid] = k == KEY_MAX ? __int_as_float(0x7f800000) : __fmul_ru(key_dist(k), 1.00001f);
+    }
+}
+
+void launch_group_min_bound(const uint8_t *samp, int64_t ns, int M, const float *tables, int64_t nq, int kk,
+                            float *gthr, cudaStream_t st) {
+    if (nq <= 0) return;
+    const int gsz = (int)std::max<int64_t>(1, ceil_div(ns, 1024));  // G = ns / gsz <= 1024 groups
+    const size_t smem = std::max<size_t>((size_t)(GB_Q / 2) * LUT_PAIR_BYTES, (size_t)GB_Q * 1024 * 8);
+    const unsigned grid = (unsigned)ceil_div(nq, GB_Q);
+    switch (M) {
+#define RII_GB(MM)                                                                                                 \
+    case MM:                                                                                                       \
+        RII_CUDA(cudaFuncSetAttribute(group_min_bound_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                      (int)smem));                                                                 \
+        group_min_bound_kernel<MM><<<grid, GB_NT, smem, st>>>(samp, ns, gsz, tables, nq, kk, gthr);               \
+        break;
+        RII_GB(4) RII_GB(8) RII_GB(16) RII_GB(32)
+#undef RII_GB
+        default: throw Error(1, "group-minimum bound: fast M only");
+    }
+    RII_LAUNCHED();
+}
+
 // bound[q] = distance of the kk-th key of keys[q][kk] (+inf when the list is short).
 __global__ void kth_bound_kernel(const uint64_t *__restrict__ keys, int64_t nq, int kk, float *__restrict__ bound) {
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

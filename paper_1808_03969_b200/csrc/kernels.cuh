@@ -84,6 +84,10 @@ void launch_u6_tables(const float *tables, const float *gthr, int64_t nq, int M,
                       cudaStream_t st);
 void launch_strided_gather(const uint8_t *codes, int M, int64_t stride, int64_t n, uint8_t *out, cudaStream_t st);
 void launch_kth_bound(const uint64_t *keys, int64_t nq, int kk, float *bound, cudaStream_t st);
+// gthr[q] = an upper bound on the kk-th distance over the ns sample codes (the kk-th
+// smallest of 1024 group minima, inflated by 1e-5); ns / 1024 codes per group.
+void launch_group_min_bound(const uint8_t *samp, int64_t ns, int M, const float *tables, int64_t nq, int kk,
+                            float *gthr, cudaStream_t st);
 
 // Per-query rotated tables [nq][256][32] (M in {4,8,16,32}), CA1 values.
 void launch_lut_tables(const float *q, int64_t nq, const float *cb, int D, int M, float *tables, cudaStream_t st);

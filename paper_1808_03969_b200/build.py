@@ -22,7 +22,8 @@ OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "librii_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
+         "-split-compile=0"]  # NVVM / ptxas work of a translation unit in parallel (k_scan.cu: 198 s -> 59 s)
 SOURCES = ["capi.cu", "k_scan.cu", "k_ivf.cu", "k_build.cu", "k_opq.cu", "k_large.cu", "comm.cpp", "opq.cpp"]
 
 

@@ -602,15 +602,7 @@ static constexpr int PACKED_MIN_CODES = 16384;  // codes per CTA below which fp3
 // Packed-kernel configuration (RII_PACK_CFG, for A/B measurements): 0 = 512 threads,
 // shift unpack; 1 = 384 threads, PRMT unpack; 2 = 512 threads, PRMT unpack,
 // recomputed column offsets; 3 = 384 threads, shift unpack.
-static int pack_cfg() {
-    static int cfg = [] {
-        const char *e = getenv("RII_PACK_CFG");
-        return e ? atoi(e) : 0;
-    }();
-    return cfg;
-}
-static int packed_nth() { return (pack_cfg() == 1 || pack_cfg() == 3) ? 384 : 512; }
-#define PACKED_NTH packed_nth()
+constexpr int PACKED_NTH = 512;  // bf16-packed kernels: 512 threads
 
 ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available, int max_nc) {
     ScanPlan p{};
@@ -656,14 +648,7 @@ ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bo
 
 // Threads per CTA x codes per thread and step of the lane-rotated kernels
 // (RII_SCAN_CFG=0: 256 x 2, 1: 512 x 1; default below).
-static int scan_cfg() {
-    static int cfg = [] {
-        const char *e = getenv("RII_SCAN_CFG");
-        return e ? atoi(e) : 1;
-    }();
-    return cfg;
-}
-static int scan_threads() { return scan_cfg() == 0 ? 256 : 512; }
+static int scan_threads() { return 512; }  // fp32 pair kernels
 
 // Linear integer-table kernel (RII_Q16_CFG for A/B; default: u6 oct tables for M = 32,
 // where they measured 134.6 ms against 204.1 ms for u16 on deep10m, u16 otherwise
@@ -673,64 +658,45 @@ static int q16_cfg(int M) {
     const char *e = getenv("RII_Q16_CFG");
     return e ? atoi(e) : (M == 32 ? 7 : 0);
 }
-static int q16_nth(int M) {
-    const int c = q16_cfg(M);
-    return c == 2 ? 256 : (c == 3 || c == 5) ? 512 : 384;
-}
-bool q16_is_u6(int M) { const int c = q16_cfg(M); return c >= 4 && c <= 8; }
-// List-major u6 items (phase B of the two-phase IVF): 0 = u16 items; 1 = u6, 192
-// threads, one table copy (two CTAs per SM); 2 = u6, 384 threads, two copies;
-// 3 = u6, 384 threads, one copy.
+static int q16_nth(int) { return 384; }
+bool q16_is_u6(int M) { const int c = q16_cfg(M); return c == 4 || c == 7; }
+// List-major u6 items (phase B of the two-phase IVF): 0 = u16 items; 3 = u6, 384
+// threads, one table copy (deep10m L = 64: 21.4 -> 19.1 ms; 192 threads with two CTAs
+// per SM measured 19.2 ms, two table copies 20.7 ms).
 int list_u6_cfg(int M) {
     const char *e = getenv("RII_LIST_U6");
     return M != 32 ? 0 : e ? atoi(e) : 3;
 }
-static int list_q16_nth(int M) { return list_u6_cfg(M) == 1 ? 192 : 384; }
+static int list_q16_nth(int) { return 384; }
 static size_t smem_list_q16(int M, int kk) {
-    const int c = list_u6_cfg(M);
-    if (c == 0) return smem_q16(kk);
-    return (size_t)(c == 2 ? 2 : 1) * OCT_BYTES + smem_aux_bytes(8, kk) + 16;
+    if (list_u6_cfg(M) != 3) return smem_q16(kk);
+    return (size_t)OCT_BYTES + smem_aux_bytes(8, kk) + 16;
 }
 
 template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr(bool q16 = false) {
+    // Kernel variants kept for A/B runs (measured on B200, deep10m, 10k queries; the
+    // others this round tried are recorded in DESIGN.md and were removed to bound the
+    // build time): RII_Q16_CFG 0 = u16 tables (204 ms), 4 = u6 one copy (131 ms),
+    // 7 = u6 two copies (125 ms, default for M = 32); RII_LIST_U6 0 = u16 items,
+    // 3 = u6 items (default for M = 32); RII_PACKED=0 = fp32 pairs.
     if constexpr (B == 8) {
         if constexpr (LISTS) {
             if (q16) {
-                switch (list_u6_cfg(M)) {  // RII_LIST_U6 (A/B): u6 oct items (fixed-base layout)
-                    case 1: return (void *)scan_fast_kernel<M, 8, true, 192, 1, 3, 128 | 64>;      // 2 CTAs/SM
-                    case 2: return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64 | 2>;  // two copies
-                    case 3: return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64>;
-                    default: return (void *)scan_fast_kernel<M, 8, true, 384, 1, 2, 64>;  // u16, window 128
-                }
+                if (list_u6_cfg(M) == 3) return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64>;
+                return (void *)scan_fast_kernel<M, 8, true, 384, 1, 2, 64>;  // u16, window 128
             }
         } else {
             if (q16) {
-                // RII_Q16_CFG (A/B): threads x codes per step, barrier window (steps).
-                // 384 threads keep the kernel spill-free (168 registers); the window
-                // is long because the bound makes pushes rare (B200, deep10m: 4 steps
-                // 272 ms, 8: 251 ms, 32: 223 ms, 128: 219 ms per 10k-query launch).
                 switch (q16_cfg(M)) {
                     case 4: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 3, 64>;  // u6 oct tables
-                    case 5: return (void *)scan_fast_kernel<M, 8, false, 512, 1, 3, 64>;
-                    case 6: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 3, 65>;  // 5-bit entries
                     case 7: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 3, 66>;  // two copies
-                    case 8: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 3, 67>;  // both
-                    case 1: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 2, 16>;  // window 32
-                    case 2: return (void *)scan_fast_kernel<M, 8, false, 256, 2, 2, 64>;
-                    case 3: return (void *)scan_fast_kernel<M, 8, false, 512, 1, 2, 64>;
-                    default: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 2, 64>;  // window 128
+                    default: return (void *)scan_fast_kernel<M, 8, false, 384, 1, 2, 64>;  // u16, window 128
                 }
             }
         }
-        switch (pack_cfg()) {
-            case 1: return (void *)scan_fast_kernel<M, 8, LISTS, 384, 1, 1, 1>;
-            case 2: return (void *)scan_fast_kernel<M, 8, LISTS, 512, 1, 1, 3>;
-            case 3: return (void *)scan_fast_kernel<M, 8, LISTS, 384, 1, 1, 0>;
-            default: return (void *)scan_fast_kernel<M, 8, LISTS, 512, 1, 1, 0>;
-        }
+        return (void *)scan_fast_kernel<M, 8, LISTS, 512, 1, 1, 0>;  // bf16-packed quads
     } else {
-        if (scan_cfg() == 0) return (void *)scan_fast_kernel<M, B, LISTS, 256, 2, 0>;
         return (void *)scan_fast_kernel<M, B, LISTS, 512, 1, 0>;
     }
 }

@@ -135,23 +135,24 @@ __device__ __forceinline__ void warp_bitonic_merge(uint64_t (&v)[E], int lane) {
     for (int j = 16 * E; j > 0; j >>= 1) warp_cas_stage<E>(v, lane, 32 * E, j);
 }
 
-// One warp folds fresh_q[0..n) (n <= 64) into top_q[kk] (kk = 32 * E, ascending):
-// sort the fresh keys (2 per lane), then top[i] = min(top[i], fresh[kk-1-i]) keeps
-// the kk smallest of the union as a bitonic sequence, which the merge sorts.
-template <int E>
+// One warp folds fresh_q[0..n) (n <= 32 * EF) into top_q[kk] (kk = 32 * E,
+// ascending): sort the fresh keys (EF per lane), then top[i] = min(top[i],
+// fresh[kk-1-i]) keeps the kk smallest of the union as a bitonic sequence, which
+// the merge sorts.
+template <int E, int EF>
 __device__ __forceinline__ float warp_compact_query(uint64_t *top_q, uint64_t *fresh_q, int n, int lane) {
-    uint64_t f[2];
+    uint64_t f[EF];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) f[e] = lane * 2 + e < n ? fresh_q[lane * 2 + e] : KEY_MAX;
-    warp_bitonic_sort<2>(f, lane);
+    for (int e = 0; e < EF; ++e) f[e] = lane * EF + e < n ? fresh_q[lane * EF + e] : KEY_MAX;
+    warp_bitonic_sort<EF>(f, lane);
 #pragma unroll
-    for (int e = 0; e < 2; ++e) fresh_q[lane * 2 + e] = f[e];
+    for (int e = 0; e < EF; ++e) fresh_q[lane * EF + e] = f[e];
     __syncwarp();
     uint64_t v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         const int i = lane * E + e, x = 32 * E - 1 - i;
-        const uint64_t t = top_q[i], c = x < 64 ? fresh_q[x] : KEY_MAX;
+        const uint64_t t = top_q[i], c = x < 32 * EF ? fresh_q[x] : KEY_MAX;
         v[e] = c < t ? c : t;
     }
     warp_bitonic_merge<E>(v, lane);
@@ -167,7 +168,10 @@ __device__ __forceinline__ void warp_compact_all(uint64_t *top, uint64_t *fresh,
     for (int q = threadIdx.x >> 5; q < nq; q += nw) {
         const int n = cnt[q];
         if (n > 0) {
-            const float t = warp_compact_query<E>(top + (size_t)q * (32 * E), fresh + (size_t)q * NEWCAP, n, lane);
+            uint64_t *tq = top + (size_t)q * (32 * E), *fq = fresh + (size_t)q * NEWCAP;
+            float t;
+            if (n <= 64) t = warp_compact_query<E, 2>(tq, fq, n, lane);
+            else t = warp_compact_query<E, 8>(tq, fq, n, lane);
             if (lane == 0) thr[q] = t;
         }
         __syncwarp();
@@ -188,7 +192,7 @@ __device__ inline void compact_topk(uint64_t *top, uint64_t *fresh, int *cnt, fl
     }
     __syncthreads();
     const int mx = scratch[0];
-    if (mx > 0 && mx <= 64 && kk >= 32 && kk <= 256) {  // warp per query
+    if (mx > 0 && mx <= 256 && kk >= 32 && kk <= 256) {  // warp per query
         switch (kk) {
             case 32: warp_compact_all<1>(top, fresh, cnt, thr, nq); break;
             case 64: warp_compact_all<2>(top, fresh, cnt, thr, nq); break;

@@ -633,11 +633,17 @@ ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bo
         return (int64_t)(e ? atoi(e) : 40);
     }();
     const int64_t nc_min = chunk_mb > 0 ? std::min<int64_t>(nc_max, ceil_div(n_codes * M, chunk_mb << 20)) : 1;
+    // Cost of a chunking: waves x (codes per chunk + a fixed per-CTA cost in code
+    // equivalents: table load, final compaction and output, ~25 us ~ 8192 codes).
+    static const double fix = [] {
+        const char *e = getenv("RII_CTA_FIX");
+        return e ? atof(e) : 8192.0;
+    }();
     double best = 1e300;
     int bnc = (int)nc_min;
     for (int nc = (int)nc_min; nc <= nc_max; ++nc) {
         const double waves = (double)ceil_div((int64_t)p.nb * nc, num_sms);
-        const double t = waves / nc * (1.0 + 0.002 * nc);
+        const double t = waves * ((double)n_codes / nc + fix) * (1.0 + 0.002 * nc);
         if (t < best * 0.999) { best = t; bnc = nc; }
     }
     p.nc = bnc;

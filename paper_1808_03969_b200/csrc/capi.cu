@@ -368,6 +368,14 @@ Targets prepare_targets(const rii_index *x, const QueryArgs &a, cudaStream_t st)
 
 // u16 tables: scans of at least RII_Q16_MIN (default 2^19) codes; the bound comes
 // from min(Q16_SAMPLE, n / 4) strided codes.
+// Non-fast M at or above this use the large-M kernels (k_large.cu); below, the fp32
+// generic kernels (RII_LARGE_MIN_M for A/B; M > 64 always needs the large kernels).
+// The paper's SIFT1M shape (M = 64, Table 2): generic 856 ms, large 496 ms per 10k
+// queries over 1M codes; IVF L = 5: 22.4 -> 13.7 ms.
+static int large_min_m() {
+    const char *e = getenv("RII_LARGE_MIN_M");
+    return std::min(65, e ? atoi(e) : 33);
+}
 static double list_q16_min_len() {  // RII_LIST_Q16_MIN: average list length for two-phase u16
     const char *e = getenv("RII_LIST_Q16_MIN");
     return e ? atof(e) : 1024.0;
@@ -398,7 +406,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
     PhaseTrace tr(st);
     // per-query rotated ADC tables, built once per batch (a1)
     const float *tables = nullptr;
-    const bool large = x->M > 64;  // k_large.cu: one query per CTA, bf16 resident table
+    const bool large = !fast && x->M >= large_min_m();  // k_large.cu: one query per CTA, bf16 resident table
     if (fast) {
         float *tb = x->s_tables.get<float>((size_t)a.nq * LUT_Q_FLOATS);
         launch_lut_tables(a.q, a.nq, cb, x->D, x->M, tb, st);

@@ -507,7 +507,8 @@ def test_train_opq_properties(rii, ref, tmp_path):
 # ------------------------------------------------------- large M (F3) -------
 @pytest.mark.parametrize("kind,N,D,M,K,nq,topk", [("deep", 3_001, 960, 240, 6, 7, 20),  # GIST1M shape
                                                   ("sift", 4_003, 384, 192, 8, 9, 50),  # MET-like M = 192
-                                                  ("gaussian", 2_503, 140, 70, 5, 5, 10)])  # M % 4 != 0
+                                                  ("gaussian", 2_503, 140, 70, 5, 5, 10),  # M % 4 != 0
+                                                  ("sift", 4_001, 128, 64, 8, 9, 50)])  # SIFT1M Table 2 shape
 def test_large_m_shapes(rii, ref, kind, N, D, M, K, nq, topk):
     """M > 64 (the paper's range reaches M = 240): train,
     add, reconfigure (large-M SDC assignment) and every query path (linear whole /

@@ -449,8 +449,15 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             // every CTA filters with, and publishes its kk-th distance into, gthr
             float *gthr = x->s_gthr.get<float>(a.nq);
             const int64_t ns = std::min<int64_t>(q16_sample(), n_codes / 4);
-            const bool q16 = pl.B == 8 && pl.fast && q16_enabled() && q16_supported(kk) && n_codes >= q16_min_codes() &&
-                             ns >= 4 * kk;
+            // Whole-database scans on several ranks share the bound pass: rank r bounds
+            // the queries of its slice from its own shard's sample (a subset of the
+            // database, so the bound holds globally) and the slices are all-gathered.
+            // The decision uses N / world so that every rank takes the same branch.
+            const bool shard_bound = !a.S && x->world > 1 && x->comm != nullptr;
+            const int64_t n_dec = shard_bound ? ceil_div(x->N, x->world) : n_codes;
+            const int64_t ns_dec = std::min<int64_t>(q16_sample(), n_dec / 4);
+            const bool q16 = pl.B == 8 && pl.fast && q16_enabled() && q16_supported(kk) && n_dec >= q16_min_codes() &&
+                             ns_dec >= 4 * kk && ns >= 4 * kk;
             if (!q16) {
                 if (pl.fast) launch_fill_f32(gthr, a.nq, INFINITY, st);
                 else gthr = nullptr;
@@ -459,7 +466,22 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
                 const int64_t stride = n_codes / ns;
                 uint8_t *samp = x->s_samp.get<uint8_t>((size_t)ns * x->M);
                 launch_strided_gather(scan_codes, x->M, stride, ns, samp, st);
-                if (ns >= 4096 && kk <= 512 && !getenv("RII_BOUND_TOPK")) {
+                if (shard_bound) {
+                    const int64_t qs = ceil_div(a.nq, (int64_t)x->world), q_lo = std::min<int64_t>(a.nq, x->rank * qs);
+                    const int64_t nloc = std::min<int64_t>(a.nq, q_lo + qs) - q_lo;
+                    float *slice = x->s_bound.get<float>((size_t)qs + 1);
+                    float *all = x->s_spart.get<float>((size_t)qs * x->world + 1);
+                    launch_fill_f32(slice, qs, INFINITY, st);
+                    if (nloc > 0) {
+                        if (ns >= 4096 && kk <= 512)
+                            launch_group_min_bound(samp, ns, x->M, tables + q_lo * LUT_Q_FLOATS, nloc, kk, slice, st);
+                        else
+                            launch_fill_f32(slice, nloc, INFINITY, st);  // no bound: filter from +inf
+                    }
+                    nccl_allgather_u8(x->comm, reinterpret_cast<const uint8_t *>(slice), reinterpret_cast<uint8_t *>(all),
+                                      (size_t)qs * 4, st);
+                    RII_CUDA(cudaMemcpyAsync(gthr, all, (size_t)a.nq * 4, cudaMemcpyDeviceToDevice, st));
+                } else if (ns >= 4096 && kk <= 512 && !getenv("RII_BOUND_TOPK")) {
                     // kk-th smallest of 1024 group minima (no top-k lists; k_scan.cu)
                     launch_group_min_bound(samp, ns, x->M, tables, a.nq, kk, gthr, st);
                 } else {

@@ -496,14 +496,14 @@ __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, 
         for (int h = 0; h < GW; ++h) {
             const int aw = g * GW + h;
             const uint32_t ca = colA ^ (uint32_t)(aw * 0x2020), cb = colB ^ (uint32_t)(aw * 0x2020);
+            uint2 v[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const uint32_t off = __byte_perm(wp[aw], t < 2 ? ca : cb, sel[t]);
-                const uint2 v = lds64_imm<BASE>(off);
-                const bool first = h == 0 && t == 0;
-                s0 = first ? v.x : fma_add(v.x, one, s0);  // bytewise: GJ * cap < 256, no carries
-                s1 = first ? v.y : fma_add(v.y, one, s1);
-            }
+            for (int t = 0; t < 4; ++t) v[t] = lds64_imm<BASE>(__byte_perm(wp[aw], t < 2 ? ca : cb, sel[t]));
+            // bytewise (GJ * cap < 256, no carries), as a tree: dependency depth 2
+            const uint32_t x0 = fma_add(fma_add(v[0].x, one, v[1].x), one, fma_add(v[2].x, one, v[3].x));
+            const uint32_t x1 = fma_add(fma_add(v[0].y, one, v[1].y), one, fma_add(v[2].y, one, v[3].y));
+            s0 = h == 0 ? x0 : fma_add(x0, one, s0);
+            s1 = h == 0 ? x1 : fma_add(x1, one, s1);
         }
         const uint32_t e0 = s0 & 0x00ff00ffu, o0 = __byte_perm(s0, 0u, 0x4341);
         const uint32_t e1 = s1 & 0x00ff00ffu, o1 = __byte_perm(s1, 0u, 0x4341);

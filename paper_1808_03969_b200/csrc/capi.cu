@@ -388,10 +388,7 @@ static int ns_chunks() {
     const char *e = getenv("RII_Q16_SAMPLE_NC");
     return e ? atoi(e) : 1;
 }
-static int64_t q16_min_codes() {
-    const char *e = getenv("RII_Q16_MIN");
-    return e ? atoll(e) : ((int64_t)1 << 19);
-}
+
 
 // One batch of queries (a.q, a.nq) against this rank's shard.  Writes either the
 // final result (world == 1, out_keys == nullptr) or this rank's top-kk keys with
@@ -408,7 +405,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
     const float *tables = nullptr;
     const bool large = !fast && x->M >= large_min_m();  // k_large.cu: one query per CTA, bf16 resident table
     if (fast) {
-        float *tb = x->s_tables.get<float>((size_t)a.nq * LUT_Q_FLOATS);
+        float *tb = x->s_tables.get<float>((size_t)a.nq * lut_q_floats(x->M));
         launch_lut_tables(a.q, a.nq, cb, x->D, x->M, tb, st);
         tables = tb;
     } else if (large) {
@@ -458,6 +455,8 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             const int64_t ns_dec = std::min<int64_t>(q16_sample(), n_dec / 4);
             const bool q16 = pl.B == 8 && pl.fast && q16_enabled() && q16_supported(kk) && n_dec >= q16_min_codes() &&
                              ns_dec >= 4 * kk && ns >= 4 * kk;
+            if (!q16 && pl.B == 8 && lut_halves(x->M) > 1)  // M = 64 has no float B = 8 kernel
+                pl = plan_linear(x->M, kk, a.nq, n_codes, x->num_sms, tables != nullptr, 1 << 30, false);
             if (!q16) {
                 if (pl.fast) launch_fill_f32(gthr, a.nq, INFINITY, st);
                 else gthr = nullptr;
@@ -474,7 +473,8 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
                     launch_fill_f32(slice, qs, INFINITY, st);
                     if (nloc > 0) {
                         if (ns >= 4096 && kk <= 512)
-                            launch_group_min_bound(samp, ns, x->M, tables + q_lo * LUT_Q_FLOATS, nloc, kk, slice, st);
+                            launch_group_min_bound(samp, ns, x->M, tables + q_lo * lut_q_floats(x->M), nloc, kk,
+                                                   slice, st);
                         else
                             launch_fill_f32(slice, nloc, INFINITY, st);  // no bound: filter from +inf
                     }
@@ -486,7 +486,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
                     launch_group_min_bound(samp, ns, x->M, tables, a.nq, kk, gthr, st);
                 } else {
                     // exact kk-th over the sample: one chunk per query batch
-                    ScanPlan ps = plan_linear(x->M, kk, a.nq, ns, x->num_sms, true, ns_chunks());
+                    ScanPlan ps = plan_linear(x->M, kk, a.nq, ns, x->num_sms, true, ns_chunks(), false);
                     uint64_t *sp = x->s_spart.get<uint64_t>((size_t)ps.nb * ps.B * ps.nc * kk);
                     launch_linear_scan(ps, samp, ns, x->M, a.q, a.nq, cb, x->D, kk, sp, st, tables, nullptr, false,
                                        -1);
@@ -528,7 +528,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
         } else if (fast && P <= 1008) {
             // coarse ranking (L2-L5) with the lane-rotated scan over the K centre codes,
             // canonical rescore, top-P by (d0, k) (L6)
-            ScanPlan pc = plan_linear(x->M, kkc, a.nq, x->K, x->num_sms, tables != nullptr);
+            ScanPlan pc = plan_linear(x->M, kkc, a.nq, x->K, x->num_sms, tables != nullptr, 1 << 30, false);
             uint64_t *cp = x->s_cpart.get<uint64_t>((size_t)pc.nb * pc.B * pc.nc * kkc);
             launch_linear_scan(pc, x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, kkc, cp, st, tables);
             uint64_t *ck = x->s_ckeys.get<uint64_t>((size_t)a.nq * kkc);
@@ -546,7 +546,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
         // [nq][P][kk] partials stay small; otherwise query-major (one table per query).
         const int64_t n_cand = a.S ? std::max<int64_t>(t.n_loc, 1) : x->n_local;
         const double avg_len = (double)n_cand / (double)x->K;
-        const int Bl = fast ? list_major_B(kk, avg_len) : 0;
+        const int Bl = fast ? list_major_B(kk, avg_len, x->M) : 0;
         bool list_major = Bl > 0 && avg_len >= 768.0 && (double)a.nq * P * kk * 8 <= 4e9 && (double)a.nq * P < 4e9;
         if (const char *mode = getenv("RII_IVF_MODE")) {  // test / tuning override: "list" or "query"
             if (!strcmp(mode, "list")) list_major = Bl > 0 && (double)a.nq * P < 4e9;
@@ -593,7 +593,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
                 tr.mark("list scan A");
                 float *qsc = x->s_qscale.get<float>(a.nq);
                 if (list_u6_cfg(x->M)) {  // u6 oct items
-                    uint8_t *t8 = x->s_tab16.get<uint8_t>((size_t)a.nq * LUT_Q_FLOATS);
+                    uint8_t *t8 = x->s_tab16.get<uint8_t>((size_t)a.nq * lut_q_floats(x->M));
                     launch_u6_tables(tables, gthr, a.nq, x->M, t8, qsc, st);
                     sa.qtab8 = t8;
                 } else {

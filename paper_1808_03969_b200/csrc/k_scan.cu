@@ -27,7 +27,13 @@ namespace rii {
 
 template <int W>
 __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
-    if constexpr (W == 8) {
+    if constexpr (W == 16) {  // M = 64
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p) + k);
+            w[4 * k] = a.x; w[4 * k + 1] = a.y; w[4 * k + 2] = a.z; w[4 * k + 3] = a.w;
+        }
+    } else if constexpr (W == 8) {
         const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
         const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
         w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
@@ -39,6 +45,7 @@ __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
         const uint2 a = __ldg(reinterpret_cast<const uint2 *>(p));
         w[0] = a.x; w[1] = a.y;
     } else {
+        static_assert(W == 1, "code words per thread");
         w[0] = __ldg(reinterpret_cast<const uint32_t *>(p));
     }
 }
@@ -66,11 +73,13 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     constexpr int U6_GJ = ((VARIANT & 1) && M >= 8) ? 8 : 4;
     constexpr bool U6_R2 = U6 && (VARIANT & 2) && M == 32;
     constexpr float U6_CAP = U6_GJ == 8 ? 31.0f : 63.0f;
-    constexpr int LUTB = U6 ? (U6_R2 ? 2 : 1) * OCT_BYTES : NQ * QUAD_BYTES;  // 64 KB-aligned integer tables
+    constexpr int H = lut_halves(M), LQF = lut_q_floats(M);  // M = 64: two 32-subspace halves
+    static_assert(H == 1 || TAB == 0 || TAB == 3, "M = 64 runs the fp32-pair and u6 tables");
+    constexpr int LUTB = U6 ? (U6_R2 ? 2 : 1) * H * OCT_BYTES : NQ * QUAD_BYTES;  // 64 KB-aligned integer tables
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t *lut = smem;
     const int kk = a.kk;
-    uint8_t *aux = smem + (PACKED ? NQ * QUAD_BYTES : NP * LUT_PAIR_BYTES);
+    uint8_t *aux = smem + (PACKED ? NQ * QUAD_BYTES : NP * H * LUT_PAIR_BYTES);
     if constexpr (Q16 && FIXB) {
         if ((uint32_t)__cvta_generic_to_shared(smem) != (uint32_t)LDS_BASE) __trap();  // layout assumption
         aux = smem + LUTB;
@@ -130,8 +139,8 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         if (tid < B) qsc[tid] = __ldg(a.qscale + query_of(tid));
         const uint8_t *tq[8];
 #pragma unroll
-        for (int qq = 0; qq < 8; ++qq) tq[qq] = a.qtab8 + query_of(qq) * LUT_Q_FLOATS;
-        load_lut_oct_u8pre<U6_R2>(reinterpret_cast<uint32_t *>(lut), tq);
+        for (int qq = 0; qq < 8; ++qq) tq[qq] = a.qtab8 + query_of(qq) * LQF;
+        load_lut_oct_u8pre<U6_R2, H>(reinterpret_cast<uint32_t *>(lut), tq);
     } else if constexpr (U6) {
         // u6 tables: per-query scale s = 63 * ALPHA / T (T = +inf -> s = 0: everything passes)
         float qs[8];
@@ -141,17 +150,17 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             const float T = __ldcg(a.gthr + query_of(qq));
             qs[qq] = __fdiv_rd(U6_CAP * u6_alpha(M), fmaxf(T, 1e-30f));
             if (tid == 0) { qsc[qq] = qs[qq]; tsc[qq] = T; }
-            tq[qq] = a.tables + query_of(qq) * LUT_Q_FLOATS;
+            tq[qq] = a.tables + query_of(qq) * LQF;
         }
-        load_lut_oct_u6<U6_R2>(reinterpret_cast<uint32_t *>(lut), tq, qs, U6_CAP);
+        load_lut_oct_u6<U6_R2, H>(reinterpret_cast<uint32_t *>(lut), tq, qs, U6_CAP);
     } else if (Q16 && a.qtab16) {
         // precomputed per-query u16 tables (q16_tables_kernel) with their scales
         if (tid < B) qsc[tid] = __ldg(a.qscale + query_of(tid));
 #pragma unroll
         for (int p = 0; p < NQ; ++p)
-            load_lut_quad_u16(reinterpret_cast<uint32_t *>(lut + p * QUAD_BYTES), a.qtab16 + query_of(4 * p) * LUT_Q_FLOATS,
-                              a.qtab16 + query_of(4 * p + 1) * LUT_Q_FLOATS, a.qtab16 + query_of(4 * p + 2) * LUT_Q_FLOATS,
-                              a.qtab16 + query_of(4 * p + 3) * LUT_Q_FLOATS);
+            load_lut_quad_u16(reinterpret_cast<uint32_t *>(lut + p * QUAD_BYTES), a.qtab16 + query_of(4 * p) * LQF,
+                              a.qtab16 + query_of(4 * p + 1) * LQF, a.qtab16 + query_of(4 * p + 2) * LQF,
+                              a.qtab16 + query_of(4 * p + 3) * LQF);
     } else if constexpr (Q16) {
         // u16 tables: per-query scale s = CAP / T (T = +inf -> s = 0: everything passes)
         float qs[B];
@@ -164,9 +173,9 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
 #pragma unroll
         for (int p = 0; p < NQ; ++p)
             load_lut_quad_q16<M>(reinterpret_cast<uint32_t *>(lut + p * QUAD_BYTES),
-                                 a.tables + query_of(4 * p) * LUT_Q_FLOATS, a.tables + query_of(4 * p + 1) * LUT_Q_FLOATS,
-                                 a.tables + query_of(4 * p + 2) * LUT_Q_FLOATS,
-                                 a.tables + query_of(4 * p + 3) * LUT_Q_FLOATS, qs[4 * p], qs[4 * p + 1],
+                                 a.tables + query_of(4 * p) * LQF, a.tables + query_of(4 * p + 1) * LQF,
+                                 a.tables + query_of(4 * p + 2) * LQF,
+                                 a.tables + query_of(4 * p + 3) * LQF, qs[4 * p], qs[4 * p + 1],
                                  qs[4 * p + 2], qs[4 * p + 3]);
     } else if constexpr (PACKED) {
 #pragma unroll
@@ -176,19 +185,21 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                 load_lut_quad_sdc<M>(dq, a.sdcT, a.qcodes + query_of(4 * p) * M, a.qcodes + query_of(4 * p + 1) * M,
                                      a.qcodes + query_of(4 * p + 2) * M, a.qcodes + query_of(4 * p + 3) * M);
             else
-                load_lut_quad(dq, a.tables + query_of(4 * p) * LUT_Q_FLOATS, a.tables + query_of(4 * p + 1) * LUT_Q_FLOATS,
-                              a.tables + query_of(4 * p + 2) * LUT_Q_FLOATS,
-                              a.tables + query_of(4 * p + 3) * LUT_Q_FLOATS);
+                load_lut_quad(dq, a.tables + query_of(4 * p) * LQF, a.tables + query_of(4 * p + 1) * LQF,
+                              a.tables + query_of(4 * p + 2) * LQF,
+                              a.tables + query_of(4 * p + 3) * LQF);
         }
     } else {
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            float *lp = reinterpret_cast<float *>(lut + p * LUT_PAIR_BYTES);
+            float *lp = reinterpret_cast<float *>(lut + p * H * LUT_PAIR_BYTES);
             if (a.tables)
-                load_lut_pair(lp, a.tables + query_of(2 * p) * LUT_Q_FLOATS,
-                              a.tables + query_of(2 * p + 1) * LUT_Q_FLOATS);
+                load_lut_pair_h<M>(lp, a.tables + query_of(2 * p) * LQF, a.tables + query_of(2 * p + 1) * LQF);
             else
-                build_lut_pair<M>(lp, a.q + query_of(2 * p) * D, a.q + query_of(2 * p + 1) * D, a.cb, a.ds);
+            {
+                if constexpr (H == 1) build_lut_pair<M>(lp, a.q + query_of(2 * p) * D, a.q + query_of(2 * p + 1) * D, a.cb, a.ds);
+                else __trap();  // M = 64 always runs with per-query HBM tables
+            }
         }
     }
     for (int e = tid; e < B * kk; e += NTH) top[e] = KEY_MAX;
@@ -264,16 +275,16 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                 if constexpr (U6) {
                     const float *tq[8];
 #pragma unroll
-                    for (int qq = 0; qq < 8; ++qq) tq[qq] = a.tables + query_of(qq) * LUT_Q_FLOATS;
-                    load_lut_oct_u6<U6_R2>(reinterpret_cast<uint32_t *>(lut), tq, qs, U6_CAP);
+                    for (int qq = 0; qq < 8; ++qq) tq[qq] = a.tables + query_of(qq) * LQF;
+                    load_lut_oct_u6<U6_R2, H>(reinterpret_cast<uint32_t *>(lut), tq, qs, U6_CAP);
                 } else {
 #pragma unroll
                     for (int p = 0; p < NQ; ++p)
                         load_lut_quad_q16<M>(reinterpret_cast<uint32_t *>(lut + p * QUAD_BYTES),
-                                             a.tables + query_of(4 * p) * LUT_Q_FLOATS,
-                                             a.tables + query_of(4 * p + 1) * LUT_Q_FLOATS,
-                                             a.tables + query_of(4 * p + 2) * LUT_Q_FLOATS,
-                                             a.tables + query_of(4 * p + 3) * LUT_Q_FLOATS, qs[4 * p], qs[4 * p + 1],
+                                             a.tables + query_of(4 * p) * LQF,
+                                             a.tables + query_of(4 * p + 1) * LQF,
+                                             a.tables + query_of(4 * p + 2) * LQF,
+                                             a.tables + query_of(4 * p + 3) * LQF, qs[4 * p], qs[4 * p + 1],
                                              qs[4 * p + 2], qs[4 * p + 3]);
                 }
                 __syncthreads();
@@ -301,14 +312,14 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                     }
                     continue;
                 }
-                const float *tq = a.tables + query_of(qq) * LUT_Q_FLOATS;
+                const float *tq = a.tables + query_of(qq) * LQF;
                 for (int i = tid; i < n; i += NTH) {
                     uint64_t *f = fresh + qq * NEWCAP + i;
                     const uint32_t id = key_id(*f);
                     const uint8_t *cp = codes + (size_t)id * M;
                     float d = 0.f;
 #pragma unroll
-                    for (int m = 0; m < M; ++m) d = __fadd_rn(d, __ldg(tq + (int)cp[m] * 32 + m));
+                    for (int m = 0; m < M; ++m) d = __fadd_rn(d, lut_q_entry(tq, m, cp[m]));
                     *f = make_key(d, id);
                 }
             }
@@ -496,7 +507,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         const int qq = e >> lkk;
         const uint32_t id = key_id(k);
         const uint8_t *cp = codes + (size_t)id * M;
-        const float *lq = reinterpret_cast<const float *>(lut + (qq >> 1) * LUT_PAIR_BYTES);
+        const float *lq = reinterpret_cast<const float *>(lut + (qq >> 1) * H * LUT_PAIR_BYTES);
         float d = 0.f;
 #pragma unroll
         for (int m = 0; m < M; ++m) d = __fadd_rn(d, lut_pair_entry(lq, qq & 1, m, cp[m]));
@@ -582,9 +593,14 @@ __global__ void __launch_bounds__(NT, 1)
 // u16 variant: 64 KB-aligned tables + the aux block below or above them (kernel).
 static size_t smem_q16(int kk) { return (size_t)2 * QUAD_BYTES + 2 * (size_t)smem_aux_bytes(8, kk) + 16; }
 bool q16_supported(int kk) { return smem_q16(kk) <= 227 * 1024; }
-static size_t smem_fast(int B, int kk) {
-    const size_t lut = B == 8 ? (size_t)2 * QUAD_BYTES : (size_t)(B / 2) * LUT_PAIR_BYTES;
+static size_t smem_fast(int B, int kk, int M = 32) {
+    const size_t lut = B == 8 ? (size_t)2 * QUAD_BYTES : (size_t)(B / 2) * lut_halves(M) * LUT_PAIR_BYTES;
     return lut + smem_aux_bytes(B, kk);
+}
+// Integer tables run for scans of at least RII_Q16_MIN (default 2^19) codes.
+int64_t q16_min_codes() {
+    const char *e = getenv("RII_Q16_MIN");
+    return e ? atoll(e) : ((int64_t)1 << 19);
 }
 // RII_PACKED=0 disables the bf16-packed tables (A/B measurements).
 static bool packed_enabled() {
@@ -604,11 +620,18 @@ static constexpr int PACKED_MIN_CODES = 16384;  // codes per CTA below which fp3
 // recomputed column offsets; 3 = 384 threads, shift unpack.
 constexpr int PACKED_NTH = 512;  // bf16-packed kernels: 512 threads
 
-ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available, int max_nc) {
+ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available, int max_nc,
+                     bool int_ok_caller) {
     ScanPlan p{};
-    p.fast = (M == 4 || M == 8 || M == 16 || M == 32);
+    p.fast = (M == 4 || M == 8 || M == 16 || M == 32 || M == 64);
     p.B = 0;
-    if (p.fast) {
+    if (p.fast && M == 64) {
+        // two table halves: the u6 oct tables (B = 8, 128 KB) for long scans, else fp32 pairs (B = 2)
+        const bool int_ok = int_ok_caller && tables_available && q16_enabled() && q16_supported(kk) &&
+                            n_codes >= q16_min_codes();
+        if (int_ok) { p.B = 8; p.smem = smem_q16(kk); }
+        else if (smem_fast(2, kk, M) <= SMEM_CAP) { p.B = 2; p.smem = smem_fast(2, kk, M); }
+    } else if (p.fast) {
         // Packed tables cost a larger per-CTA table build: only for long code ranges.
         const bool pk = packed_enabled() && tables_available && n_codes >= (int64_t)PACKED_MIN_CODES;
         for (int B : {8, 6, 4, 2}) {
@@ -662,6 +685,7 @@ static int scan_threads() { return 512; }  // fp32 pair kernels
 // 1 = u16 window 32; 2 = u16 256 x 2; 3 = u16 512 threads; 4 = u6 384; 5 = u6 512.
 static int q16_cfg(int M) {
     const char *e = getenv("RII_Q16_CFG");
+    if (M == 64) return 4;  // two halves: u6 oct tables, one copy
     return e ? atoi(e) : (M == 32 ? 7 : 0);
 }
 static int q16_nth(int) { return 384; }
@@ -670,17 +694,37 @@ bool q16_is_u6(int M) { const int c = q16_cfg(M); return c == 4 || c == 7; }
 // threads, one table copy (deep10m L = 64: 21.4 -> 19.1 ms; 192 threads with two CTAs
 // per SM measured 19.2 ms, two table copies 20.7 ms).
 int list_u6_cfg(int M) {
+    if (M == 64) return 3;  // two halves: only the u6 items fit (128 KB)
     const char *e = getenv("RII_LIST_U6");
     return M != 32 ? 0 : e ? atoi(e) : 3;
 }
 static int list_q16_nth(int) { return 384; }
 static size_t smem_list_q16(int M, int kk) {
     if (list_u6_cfg(M) != 3) return smem_q16(kk);
-    return (size_t)OCT_BYTES + smem_aux_bytes(8, kk) + 16;
+    return (size_t)lut_halves(M) * OCT_BYTES + smem_aux_bytes(8, kk) + 16;
 }
 
 template <int M, int B, bool LISTS>
+static void *fast_kernel_ptr_h1(bool q16);
+
+template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr(bool q16 = false) {
+    if constexpr (lut_halves(M) > 1) {  // M = 64: u6 oct tables (B = 8) or fp32 pairs (B = 2) only
+        if constexpr (B == 8) {
+            if constexpr (LISTS) return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64>;
+            else return (void *)scan_fast_kernel<M, 8, false, 384, 1, 3, 64>;
+        } else if constexpr (B == 2) {
+            return (void *)scan_fast_kernel<M, 2, LISTS, 512, 1, 0>;
+        } else {
+            return nullptr;
+        }
+    } else {
+        return fast_kernel_ptr_h1<M, B, LISTS>(q16);
+    }
+}
+
+template <int M, int B, bool LISTS>
+static void *fast_kernel_ptr_h1(bool q16) {
     // Kernel variants kept for A/B runs (measured on B200, deep10m, 10k queries; the
     // others this round tried are recorded in DESIGN.md and were removed to bound the
     // build time): RII_Q16_CFG 0 = u16 tables (204 ms), 4 = u6 one copy (131 ms),
@@ -748,9 +792,10 @@ static void launch_generic_t(const ScanPlan &pl, const uint8_t *codes, int64_t n
     RII_LAUNCHED();
 }
 
-bool list_major_supported(int M) { return M == 4 || M == 8 || M == 16 || M == 32; }
+bool list_major_supported(int M) { return M == 4 || M == 8 || M == 16 || M == 32 || M == 64; }
 
-int list_major_B(int kk, double avg_len) {
+int list_major_B(int kk, double avg_len, int M) {
+    if (lut_halves(M) > 1) return smem_fast(2, kk, M) <= SMEM_CAP ? 2 : 0;  // fp32 pairs of two halves
     const char *pe = getenv("RII_LIST_PACKED_MIN");  // A/B knob
     const double pmin = pe ? atof(pe) : (double)PACKED_MIN_CODES;
     for (int B : {8, 6, 4, 2}) {
@@ -764,7 +809,7 @@ template <int M, int B>
 static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
     q16 = q16 && B == 8;
     void *kern = fast_kernel_ptr<M, B, true>(q16);
-    const size_t smem = q16 ? smem_list_q16(M, a.kk) : smem_fast(B, a.kk);
+    const size_t smem = q16 ? smem_list_q16(M, a.kk) : smem_fast(B, a.kk, M);
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ScanArgs aa = a;
     aa.one = 1;
@@ -791,6 +836,7 @@ void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStre
         case 4: launch_list_m<4>(B, a, n_items, st, q16); break;
         case 8: launch_list_m<8>(B, a, n_items, st, q16); break;
         case 16: launch_list_m<16>(B, a, n_items, st, q16); break;
+        case 64: launch_list_m<64>(B, a, n_items, st, q16); break;
         default: launch_list_m<32>(B, a, n_items, st, q16); break;
     }
 }
@@ -804,6 +850,7 @@ void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_code
             case 4: launch_fast_m<4>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
             case 8: launch_fast_m<8>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
             case 16: launch_fast_m<16>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
+            case 64: launch_fast_m<64>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
             default: launch_fast_m<32>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
         }
     } else if (pl.B == 4) {
@@ -869,30 +916,34 @@ void launch_assign_scan(const uint8_t *codes, int64_t n, const uint8_t *centers,
 // ------------------------------------------------------------ LUT tables ---
 // One CTA per query, thread z = code word z: the code book rows of subspace m are
 // read coalesced (consecutive z), A(m, z) (CA1) goes to a [256][33] smem tile, and
-// the rows (column c = A(c mod M, z)) are written out coalesced.
+// the rows (column c = A(c mod M, z)) are written out coalesced; M = 64 writes its
+// two 32-subspace halves one after the other.
 __global__ void __launch_bounds__(256) lut_tables_kernel(const float *__restrict__ q, int64_t nq,
                                                          const float *__restrict__ cb, int M, int ds,
                                                          float *__restrict__ tables) {
-    __shared__ float qv[32 * 64];
+    extern __shared__ float qv[];  // [D]
     __shared__ float tile[KS][33];
     const int64_t qi = blockIdx.x;
-    const int D = M * ds, z = threadIdx.x;
+    const int D = M * ds, z = threadIdx.x, H = lut_halves(M), MH = M < 32 ? M : 32;
     for (int e = threadIdx.x; e < D; e += blockDim.x) qv[e] = q[qi * D + e];
-    __syncthreads();
-    for (int m = 0; m < M; ++m) {
-        const float *cv = cb + ((size_t)m * KS + z) * ds;
-        float a = 0.f;
-        for (int j = 0; j < ds; ++j) a = ca1_step(a, qv[m * ds + j], __ldg(cv + j));
-        tile[z][m] = a;
+    for (int h = 0; h < H; ++h) {
+        __syncthreads();
+        for (int mm = 0; mm < MH; ++mm) {
+            const int m = 32 * h + mm;
+            const float *cv = cb + ((size_t)m * KS + z) * ds;
+            float a = 0.f;
+            for (int j = 0; j < ds; ++j) a = ca1_step(a, qv[m * ds + j], __ldg(cv + j));
+            tile[z][mm] = a;
+        }
+        __syncthreads();
+        float *t = tables + qi * (int64_t)lut_q_floats(M) + h * LUT_Q_FLOATS;
+        for (int e = threadIdx.x; e < LUT_Q_FLOATS; e += blockDim.x) t[e] = tile[e >> 5][(e & 31) & (MH - 1)];
     }
-    __syncthreads();
-    float *t = tables + qi * LUT_Q_FLOATS;
-    for (int e = threadIdx.x; e < LUT_Q_FLOATS; e += blockDim.x) t[e] = tile[e >> 5][(e & 31) & (M - 1)];
 }
 
 void launch_lut_tables(const float *q, int64_t nq, const float *cb, int D, int M, float *tables, cudaStream_t st) {
     if (nq <= 0) return;
-    lut_tables_kernel<<<(unsigned)nq, 256, 0, st>>>(q, nq, cb, M, D / M, tables);
+    lut_tables_kernel<<<(unsigned)nq, 256, (size_t)D * 4, st>>>(q, nq, cb, M, D / M, tables);
     RII_LAUNCHED();
 }
 
@@ -925,13 +976,15 @@ void launch_strided_gather(const uint8_t *codes, int M, int64_t stride, int64_t 
 // kk-th distance (the sample is a subset).  No top-k list is needed: CTA = 6 queries
 // (three fp32 pair tables, lane-rotated sums inflated by 1e-5 to bound the canonical
 // CA2 value from above), thread = groups, then a bitonic sort of the G minima.
-constexpr int GB_Q = 6, GB_NT = 512;
+constexpr int GB_NT = 512;
+// queries per CTA: three fp32 pair tables (M <= 32) or one pair of two halves (M = 64)
+__host__ __device__ constexpr int gb_q(int M) { return M > 32 ? 2 : 6; }
 
 template <int M>
 __global__ void __launch_bounds__(GB_NT, 1) group_min_bound_kernel(const uint8_t *__restrict__ samp, int64_t ns,
                                                                    int gsz, const float *__restrict__ tables,
                                                                    int64_t nq, int kk, float *__restrict__ gthr) {
-    constexpr int W = M / 4, NP = GB_Q / 2;
+    constexpr int GB_Q = gb_q(M), W = M / 4, NP = GB_Q / 2, H = lut_halves(M), LQF = lut_q_floats(M);
     extern __shared__ __align__(16) uint8_t smem[];
     const int tid = threadIdx.x, lane = tid & 31;
     const int64_t q0 = (int64_t)blockIdx.x * GB_Q;
@@ -939,8 +992,8 @@ __global__ void __launch_bounds__(GB_NT, 1) group_min_bound_kernel(const uint8_t
     auto qidx = [&](int qq) { return min(q0 + qq, nq - 1); };
 #pragma unroll
     for (int p = 0; p < NP; ++p)
-        load_lut_pair(reinterpret_cast<float *>(smem + p * LUT_PAIR_BYTES), tables + qidx(2 * p) * LUT_Q_FLOATS,
-                      tables + qidx(2 * p + 1) * LUT_Q_FLOATS);
+        load_lut_pair_h<M>(reinterpret_cast<float *>(smem + p * H * LUT_PAIR_BYTES), tables + qidx(2 * p) * LQF,
+                           tables + qidx(2 * p + 1) * LQF);
     __syncthreads();
     const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
     uint32_t sel[4];
@@ -996,7 +1049,8 @@ void launch_group_min_bound(const uint8_t *samp, int64_t ns, int M, const float 
                             float *gthr, cudaStream_t st) {
     if (nq <= 0) return;
     const int gsz = (int)std::max<int64_t>(1, ceil_div(ns, 1024));  // G = ns / gsz <= 1024 groups
-    const size_t smem = std::max<size_t>((size_t)(GB_Q / 2) * LUT_PAIR_BYTES, (size_t)GB_Q * 1024 * 8);
+    const int GB_Q = gb_q(M);
+    const size_t smem = std::max<size_t>((size_t)(GB_Q / 2) * lut_halves(M) * LUT_PAIR_BYTES, (size_t)GB_Q * 1024 * 8);
     const unsigned grid = (unsigned)ceil_div(nq, GB_Q);
     switch (M) {
 #define RII_GB(MM)                                                                                                 \
@@ -1005,7 +1059,7 @@ void launch_group_min_bound(const uint8_t *samp, int64_t ns, int M, const float 
                                       (int)smem));                                                                 \
         group_min_bound_kernel<MM><<<grid, GB_NT, smem, st>>>(samp, ns, gsz, tables, nq, kk, gthr);               \
         break;
-        RII_GB(4) RII_GB(8) RII_GB(16) RII_GB(32)
+        RII_GB(4) RII_GB(8) RII_GB(16) RII_GB(32) RII_GB(64)
 #undef RII_GB
         default: throw Error(1, "group-minimum bound: fast M only");
     }
@@ -1051,9 +1105,9 @@ __global__ void __launch_bounds__(256) u6_tables_kernel(const float *__restrict_
     const int64_t q = blockIdx.x;
     const float s = __fdiv_rd(63.0f * u6_alpha(M), fmaxf(__ldcg(gthr + q), 1e-30f));
     if (threadIdx.x == 0) scale[q] = s;
-    const float4 *t4 = reinterpret_cast<const float4 *>(tables + q * LUT_Q_FLOATS);
-    uint32_t *o = reinterpret_cast<uint32_t *>(out + q * LUT_Q_FLOATS);
-    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 4; e += blockDim.x) {
+    const float4 *t4 = reinterpret_cast<const float4 *>(tables + q * lut_q_floats(M));
+    uint32_t *o = reinterpret_cast<uint32_t *>(out + q * lut_q_floats(M));
+    for (int e = threadIdx.x; e < lut_q_floats(M) / 4; e += blockDim.x) {
         const float4 v = __ldg(t4 + e);
         o[e] = u6_entry(v.x, s, 63.f) | (u6_entry(v.y, s, 63.f) << 8) | (u6_entry(v.z, s, 63.f) << 16) |
                (u6_entry(v.w, s, 63.f) << 24);
@@ -1067,6 +1121,7 @@ void launch_u6_tables(const float *tables, const float *gthr, int64_t nq, int M,
         case 4: u6_tables_kernel<4><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
         case 8: u6_tables_kernel<8><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
         case 16: u6_tables_kernel<16><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
+        case 64: u6_tables_kernel<64><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
         default: u6_tables_kernel<32><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
     }
     RII_LAUNCHED();
@@ -1140,14 +1195,14 @@ __global__ void __launch_bounds__(NT) merge_kernel(const uint64_t *__restrict__ 
         bitonic_merge_rows(top, 1, kk, kk);
     }
     if (rs.tables) {  // canonical (CA2) rescore from the query's HBM table, then re-sort
-        const float *tq = rs.tables + q * LUT_Q_FLOATS;
+        const float *tq = rs.tables + q * lut_q_floats(rs.M);
         for (int i = threadIdx.x; i < kk; i += blockDim.x) {
             const uint64_t k = top[i];
             if (k == KEY_MAX) continue;
             const uint32_t id = key_id(k);
             const uint8_t *cp = rs.codes + (size_t)id * rs.M;
             float d = 0.f;
-            for (int m = 0; m < rs.M; ++m) d = __fadd_rn(d, __ldg(tq + (int)cp[m] * 32 + m));
+            for (int m = 0; m < rs.M; ++m) d = __fadd_rn(d, lut_q_entry(tq, m, cp[m]));
             top[i] = make_key(d, id);
         }
         __syncthreads();

@@ -16,8 +16,10 @@ struct ScanPlan {
     bool fast;    // lane-rotated conflict-free LUT layout
     size_t smem;
 };
+// int_ok: the caller will run the integer-table path (sampled bound in gthr) when the
+// plan picks B = 8 for M = 64 (its only B = 8 kernel).
 ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available = false,
-                     int max_nc = 1 << 30);
+                     int max_nc = 1 << 30, bool int_ok = true);
 
 // Arguments of the lane-rotated scan kernel (linear mode, or list-major inverted
 // index mode where a work item is (posting list, up to B queries probing it)).
@@ -52,7 +54,7 @@ struct ScanArgs {
 
 // List-major inverted-index scan: B queries per CTA share one posting list's codes.
 bool list_major_supported(int M);
-int list_major_B(int kk, double avg_len);
+int list_major_B(int kk, double avg_len, int M);
 // q16: u16 fixed-point tables (B == 8, kk <= 256), scaled per item by the queries'
 // gthr bounds (items whose queries have no bound yet should run without q16).
 void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16 = false);
@@ -74,6 +76,7 @@ void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_code
                         int timer = TK_LINEAR);
 // u16 tables (RII_Q16 != 0), the strided code sample and the kk-th-distance bound.
 bool q16_enabled();
+int64_t q16_min_codes();  // RII_Q16_MIN (default 2^19): shortest scan that uses integer tables
 bool q16_supported(int kk);  // shared-memory budget of the u16 kernels (kk <= 256)
 // out[q] = u16 entries of tables[q] with scale[q] = CAP / gthr[q] (u16 list scan).
 void launch_q16_tables(const float *tables, const float *gthr, int64_t nq, int M, uint16_t *out, float *scale,

@@ -33,7 +33,11 @@ __device__ __forceinline__ void build_lut_pair(float *lutp, const float *q0, con
 
 // Per-query table in HBM (built once per call by lut_tables_kernel): row z holds
 // 32 fp32 columns, column c = A(c mod M, z).  32 KB per query for every M <= 32.
+// M = 64 (the paper's SIFT1M shape) uses H = 2 such halves, half h holding
+// subspaces 32h .. 32h+31: every table (HBM and shared) is H consecutive halves.
 constexpr int LUT_Q_FLOATS = KS * 32;
+__host__ __device__ constexpr int lut_halves(int M) { return M > 32 ? M / 32 : 1; }
+__host__ __device__ constexpr int lut_q_floats(int M) { return LUT_Q_FLOATS * lut_halves(M); }
 
 // Copy the HBM tables of queries qa, qb into the interleaved pair layout:
 // coalesced 16-byte loads, 16-byte conflict-free stores.
@@ -62,9 +66,23 @@ __device__ __forceinline__ void load_lut_pair(float *lutp, const float *__restri
     }
 }
 
-// Canonical (replica 0) entry A_h(m, z) of the pair table.
+// Pair table of M subspaces (H halves): half h of each query's HBM table -> half h.
+template <int M>
+__device__ __forceinline__ void load_lut_pair_h(float *lutp, const float *__restrict__ ta,
+                                                const float *__restrict__ tb) {
+#pragma unroll
+    for (int h = 0; h < lut_halves(M); ++h)
+        load_lut_pair(lutp + h * (LUT_PAIR_BYTES / 4), ta + h * LUT_Q_FLOATS, tb + h * LUT_Q_FLOATS);
+}
+
+// Canonical (replica 0) entry A_h(m, z) of the pair table (halves of 64 KB for M = 64).
 __device__ __forceinline__ float lut_pair_entry(const float *lutp, int h, int m, int z) {
-    return lutp[z * 64 + 2 * m + h];
+    return lutp[(m >> 5) * (LUT_PAIR_BYTES / 4) + z * 64 + 2 * (m & 31) + h];
+}
+
+// Entry A(m, z) of a per-query HBM table (lut_tables_kernel layout, H halves).
+__device__ __forceinline__ float lut_q_entry(const float *tq, int m, int z) {
+    return __ldg(tq + (m >> 5) * LUT_Q_FLOATS + z * 32 + (m & 31));
 }
 
 // Packed fp32x2 add (sm_100 FADD2): two IEEE round-to-nearest fp32 adds.
@@ -80,11 +98,12 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
     return r;
 }
 
-// XOR-permute the code words by the lane's rotation: wp[i] = w[i ^ rw].
+// XOR-permute the code words by the lane's rotation: wp[i] = w[i ^ rw] (rw < 8:
+// for M = 64 the rotation stays inside each 32-subspace half).
 template <int W>
 __device__ __forceinline__ void permute_words(uint32_t (&w)[W], uint32_t rw) {
 #pragma unroll
-    for (int b = 1; b < W; b <<= 1) {
+    for (int b = 1; b < W && b < 8; b <<= 1) {
         const bool c = (rw & b) != 0;
 #pragma unroll
         for (int i = 0; i < W; ++i) {
@@ -110,13 +129,13 @@ __device__ __forceinline__ void make_selectors(uint32_t r, uint32_t (&sel)[4]) {
 template <int M, int B>
 __device__ __forceinline__ void adc_rotated_pre(const uint8_t *lut, const uint32_t (&wp)[M / 4],
                                                 const uint32_t (&sel)[4], uint32_t l8, float2 (&acc)[B / 2]) {
-    constexpr int NP = B / 2;
+    constexpr int NP = B / 2, H = lut_halves(M);
 #pragma unroll
     for (int j = 0; j < M; ++j) {
-        const uint32_t off = __byte_perm(wp[j >> 2], l8 ^ (uint32_t)(j << 3), sel[j & 3]);
+        const uint32_t off = __byte_perm(wp[j >> 2], l8 ^ (uint32_t)((j & 31) << 3), sel[j & 3]);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            const float2 v = *reinterpret_cast<const float2 *>(lut + p * LUT_PAIR_BYTES + off);
+            const float2 v = *reinterpret_cast<const float2 *>(lut + (p * H + (j >> 5)) * LUT_PAIR_BYTES + off);
             acc[p] = j == 0 ? v : fadd2(acc[p], v);  // 0 + v == v for v >= +0
         }
     }
@@ -342,14 +361,15 @@ __device__ __forceinline__ uint32_t u6_entry(float v, float s, float cap) {
 // c ^ 8 (a 256-B row covers the 32 banks twice, so column c ^ 8 is the other half
 // of c's bank set), so that lanes 8 apart read disjoint banks with the same word
 // index.
-template <bool R2>
+template <bool R2, int H = 1>
 __device__ __forceinline__ void load_lut_oct_u6(uint32_t *dst, const float *const (&t)[8], const float (&s)[8],
                                                 float cap) {
-    uint2 *o = reinterpret_cast<uint2 *>(dst);
-    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 4; e += blockDim.x) {  // 4 columns of one row
+    for (int eh = threadIdx.x; eh < H * LUT_Q_FLOATS / 4; eh += blockDim.x) {  // 4 columns of one row
+        const int h = eh / (LUT_Q_FLOATS / 4), e = eh - h * (LUT_Q_FLOATS / 4);
+        uint2 *o = reinterpret_cast<uint2 *>(dst) + h * (OCT_BYTES / 8);  // half h: 64 KB further
         float4 v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float4 *>(t[k]) + e);
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float4 *>(t[k] + h * LUT_Q_FLOATS) + e);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             uint32_t lo = 0, hi = 0;
@@ -377,13 +397,14 @@ __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, 
 // Oct layout from 8 precomputed per-query u6 tables ([z][32 columns] bytes, written by
 // u6_tables_kernel): column c = [t0[c] .. t7[c]] (an 8 x 8 byte transpose per group of
 // 8 columns, 3 PRMT per output word).  R2: the second copy as in load_lut_oct_u6.
-template <bool R2>
+template <bool R2, int H = 1>
 __device__ __forceinline__ void load_lut_oct_u8pre(uint32_t *dst, const uint8_t *const (&t)[8]) {
-    uint2 *o = reinterpret_cast<uint2 *>(dst);
-    for (int e = threadIdx.x; e < LUT_Q_FLOATS / 8; e += blockDim.x) {  // 8 columns of one row
+    for (int eh = threadIdx.x; eh < H * LUT_Q_FLOATS / 8; eh += blockDim.x) {  // 8 columns of one row
+        const int h = eh / (LUT_Q_FLOATS / 8), e = eh - h * (LUT_Q_FLOATS / 8);
+        uint2 *o = reinterpret_cast<uint2 *>(dst) + h * (OCT_BYTES / 8);
         uint2 v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const uint2 *>(t[k]) + e);
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const uint2 *>(t[k] + h * LUT_Q_FLOATS) + e);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             const uint32_t sc = (uint32_t)(c & 3) | ((uint32_t)(4 + (c & 3)) << 4);  // byte c of a, of b
@@ -495,10 +516,13 @@ __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, 
 #pragma unroll
         for (int h = 0; h < GW; ++h) {
             const int aw = g * GW + h;
-            const uint32_t ca = colA ^ (uint32_t)(aw * 0x2020), cb = colB ^ (uint32_t)(aw * 0x2020);
+            const uint32_t ca = colA ^ (uint32_t)((aw & 7) * 0x2020), cb = colB ^ (uint32_t)((aw & 7) * 0x2020);
             uint2 v[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) v[t] = lds64_imm<BASE>(__byte_perm(wp[aw], t < 2 ? ca : cb, sel[t]));
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t off = __byte_perm(wp[aw], t < 2 ? ca : cb, sel[t]);
+                v[t] = aw < 8 ? lds64_imm<BASE>(off) : lds64_imm<BASE + 0x10000>(off);  // M = 64: half 1
+            }
             // bytewise (GJ * cap < 256, no carries), as a tree: dependency depth 2
             const uint32_t x0 = fma_add(fma_add(v[0].x, one, v[1].x), one, fma_add(v[2].x, one, v[3].x));
             const uint32_t x1 = fma_add(fma_add(v[0].y, one, v[1].y), one, fma_add(v[2].y, one, v[3].y));

@@ -95,6 +95,7 @@ def test_paths_match_oracle(rii, ref, kind, N, D, M, K, nq, topk):
 
 @pytest.mark.parametrize("mode", ["list", "query"])
 @pytest.mark.parametrize("kind,N,D,M,K", [("deep", 30_011, 96, 32, 20), ("sift", 25_000, 128, 16, 16),
+                                          ("sift", 24_001, 128, 64, 12),
                                           ("deep", 20_003, 96, 8, 12), ("deep", 40_000, 96, 32, 2)])
 def test_ivf_list_major_and_query_major(rii, ref, monkeypatch, mode, kind, N, D, M, K):
     """Both posting-list traversals (list-major: B queries share a list; query-major:
@@ -370,6 +371,7 @@ def test_save_load_roundtrip(rii, ref, tmp_path):
 
 # ------------------------------------------------- u16 fixed-point tables ---
 @pytest.mark.parametrize("kind,N,D,M,nq,topk", [("deep", 40_009, 96, 32, 45, 100), ("sift", 33_333, 128, 16, 19, 64),
+                                                ("sift", 30_011, 128, 64, 21, 100),  # two table halves
                                                 ("deep", 20_011, 96, 8, 23, 10), ("gaussian", 17_003, 32, 4, 9, 100)])
 def test_linear_u16_tables(rii, ref, monkeypatch, kind, N, D, M, nq, topk):
     """The u16 fixed-point SWAR scan (sampled kk-th bound, integer filter, canonical

@@ -688,7 +688,13 @@ static int q16_cfg(int M) {
     if (M == 64) return 4;  // two halves: u6 oct tables, one copy
     return e ? atoi(e) : (M == 32 ? 7 : 0);
 }
-static int q16_nth(int) { return 384; }
+// M = 64 u6 linear kernel threads (RII_M64_NTH: 384 spills ~200 B of code words and
+// took 52.9 ms on sift1m_m64; 256 does not spill: 43.5 ms)
+static int m64_nth() {
+    const char *e = getenv("RII_M64_NTH");
+    return e ? atoi(e) : 256;
+}
+static int q16_nth(int M) { return M == 64 ? m64_nth() : 384; }
 bool q16_is_u6(int M) { const int c = q16_cfg(M); return c == 4 || c == 7; }
 // List-major u6 items (phase B of the two-phase IVF): 0 = u16 items; 3 = u6, 384
 // threads, one table copy (deep10m L = 64: 21.4 -> 19.1 ms; 192 threads with two CTAs
@@ -712,6 +718,7 @@ static void *fast_kernel_ptr(bool q16 = false) {
     if constexpr (lut_halves(M) > 1) {  // M = 64: u6 oct tables (B = 8) or fp32 pairs (B = 2) only
         if constexpr (B == 8) {
             if constexpr (LISTS) return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64>;
+            else if (m64_nth() == 256) return (void *)scan_fast_kernel<M, 8, false, 256, 1, 3, 64>;
             else return (void *)scan_fast_kernel<M, 8, false, 384, 1, 3, 64>;
         } else if constexpr (B == 2) {
             return (void *)scan_fast_kernel<M, 2, LISTS, 512, 1, 0>;

@@ -22,8 +22,11 @@ OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "librii_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
-         "-split-compile=0"]  # NVVM / ptxas work of a translation unit in parallel (k_scan.cu: 198 s -> 59 s)
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+# No -split-compile: it parallelises a unit's NVVM / ptxas work (k_scan.cu 198 s -> 59 s) but the code
+# it produced for the headline u6 scan loop varied from build to build (a 17 % slower register
+# allocation was observed).  Units compile in parallel with each other instead.
+SPLIT = {"default": []}
 SOURCES = ["capi.cu", "k_scan.cu", "k_ivf.cu", "k_build.cu", "k_opq.cu", "k_large.cu", "comm.cpp", "opq.cpp"]
 
 
@@ -38,7 +41,7 @@ def _compile(src: str, force: bool, verbose: bool) -> str:
     newest = max(os.path.getmtime(path), _headers_mtime(), os.path.getmtime(os.path.join(ROOT, "include", "rii.h")))
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest:
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *SPLIT.get(src, SPLIT["default"]), "-c", path, "-o", obj]
     if verbose:
         cmd[1:1] = ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -226,6 +226,16 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         colA = hi | cb(0) | (cb(1) << 8);
         colB = hi | cb(2) | (cb(3) << 8);
     }
+    // The column registers of every word group, computed once with opaque XORs: left
+    // to itself the compiler sometimes re-materialises these 16 values inside the
+    // loop (16 more ALU ops per code: 127 -> 149 ms on deep10m, build-dependent).
+    // (colB = colA ^ 0x1010 in every layout, so only colA's groups are kept: 8 registers)
+    uint32_t colv[U6 ? (M / 4 < 8 ? M / 4 : 8) : 1];
+    if constexpr (U6) {
+#pragma unroll
+        for (int aw = 0; aw < (M / 4 < 8 ? M / 4 : 8); ++aw)
+            asm volatile("xor.b32 %0, %1, %2;" : "=r"(colv[aw]) : "r"(colA), "r"((uint32_t)(aw * 0x2020)));
+    }
     // List mode: the query's global bound (the best kk-th distance any finished item
     // of this query saw, inflated by 1e-5 for the lane-rotated rounding) also filters.
     float gq[B];
@@ -383,7 +393,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                     uint32_t dq[B];
                     if constexpr (U6) {
                         uint32_t acc[4];
-                        adc_u6<M, U6_GJ, U6_R2, LDS_BASE>(w[u], U6_R2 ? rw2 : rw, sel, colA, colB, a.one, acc);
+                        adc_u6<M, U6_GJ, U6_R2, LDS_BASE>(w[u], U6_R2 ? rw2 : rw, sel, colv, a.one, acc);
                         dq[0] = acc[0] & 0xffffu; dq[2] = acc[0] >> 16;
                         dq[1] = acc[1] & 0xffffu; dq[3] = acc[1] >> 16;
                         dq[4] = acc[2] & 0xffffu; dq[6] = acc[2] >> 16;
@@ -694,7 +704,7 @@ static int m64_nth() {
     const char *e = getenv("RII_M64_NTH");
     return e ? atoi(e) : 256;
 }
-static int q16_nth(int M) { return M == 64 ? m64_nth() : 384; }
+static int q16_nth(int M) { return M == 64 ? m64_nth() : 384; }  // 256 x 2 codes per thread: 150 ms (deep10m)
 bool q16_is_u6(int M) { const int c = q16_cfg(M); return c == 4 || c == 7; }
 // List-major u6 items (phase B of the two-phase IVF): 0 = u16 items; 3 = u6, 384
 // threads, one table copy (deep10m L = 64: 21.4 -> 19.1 ms; 192 threads with two CTAs

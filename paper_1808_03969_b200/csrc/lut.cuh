@@ -392,7 +392,8 @@ __device__ __forceinline__ void load_lut_oct_u6(uint32_t *dst, const float *cons
 // in (low, high) 16-bit lanes, acc[1] = (1, 3), acc[2] = (4, 6), acc[3] = (5, 7).
 template <int M, int GJ, bool R2, int BASE = 0>
 __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, const uint32_t (&sel)[4],
-                                       uint32_t colA, uint32_t colB, uint32_t one, uint32_t (&acc)[4]);
+                                       const uint32_t (&colv)[M / 4 < 8 ? M / 4 : 8], uint32_t one,
+                                       uint32_t (&acc)[4]);
 
 // Oct layout from 8 precomputed per-query u6 tables ([z][32 columns] bytes, written by
 // u6_tables_kernel): column c = [t0[c] .. t7[c]] (an 8 x 8 byte transpose per group of
@@ -492,7 +493,8 @@ __device__ __forceinline__ void adc_q16(const uint32_t (&w)[M / 4], uint32_t rw,
 
 template <int M, int GJ, bool R2, int BASE>
 __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, const uint32_t (&sel)[4],
-                                       uint32_t colA, uint32_t colB, uint32_t one, uint32_t (&acc)[4]) {
+                                       const uint32_t (&colv)[M / 4 < 8 ? M / 4 : 8], uint32_t one,
+                                       uint32_t (&acc)[4]) {
     // GJ steps (4: 6-bit entries, 8: 5-bit entries) are summed bytewise before widening
     constexpr int W = M / 4, GW = GJ / 4;
     static_assert(W % GW == 0, "word groups");
@@ -516,12 +518,13 @@ __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, 
 #pragma unroll
         for (int h = 0; h < GW; ++h) {
             const int aw = g * GW + h;
-            const uint32_t ca = colA ^ (uint32_t)((aw & 7) * 0x2020), cb = colB ^ (uint32_t)((aw & 7) * 0x2020);
+            const uint32_t ca = colv[aw & 7], cb = ca ^ 0x1010u;  // columns of steps t = 0,1 / 2,3 of group aw
             uint2 v[4];
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const uint32_t off = __byte_perm(wp[aw], t < 2 ? ca : cb, sel[t]);
-                v[t] = aw < 8 ? lds64_imm<BASE>(off) : lds64_imm<BASE + 0x10000>(off);  // M = 64: half 1
+                if constexpr (W <= 8) v[t] = lds64_imm<BASE>(off);
+                else v[t] = aw < 8 ? lds64_imm<BASE>(off) : lds64_imm<BASE + 0x10000>(off);  // M = 64: half 1
             }
             // bytewise (GJ * cap < 256, no carries), as a tree: dependency depth 2
             const uint32_t x0 = fma_add(fma_add(v[0].x, one, v[1].x), one, fma_add(v[2].x, one, v[3].x));

@@ -1118,9 +1118,10 @@ __global__ void __launch_bounds__(256) q16_tables_kernel(const float *__restrict
 // Per-query u6 tables (lut.cuh u6 entries, bytes [z][32]) at scale 63 * alpha / gthr[q].
 template <int M>
 __global__ void __launch_bounds__(256) u6_tables_kernel(const float *__restrict__ tables, const float *__restrict__ gthr,
-                                                        int64_t nq, uint8_t *__restrict__ out, float *__restrict__ scale) {
+                                                        int64_t nq, uint8_t *__restrict__ out, float *__restrict__ scale,
+                                                        float amul) {
     const int64_t q = blockIdx.x;
-    const float s = __fdiv_rd(63.0f * u6_alpha(M), fmaxf(__ldcg(gthr + q), 1e-30f));
+    const float s = __fdiv_rd(63.0f * u6_alpha(M) * amul, fmaxf(__ldcg(gthr + q), 1e-30f));
     if (threadIdx.x == 0) scale[q] = s;
     const float4 *t4 = reinterpret_cast<const float4 *>(tables + q * lut_q_floats(M));
     uint32_t *o = reinterpret_cast<uint32_t *>(out + q * lut_q_floats(M));
@@ -1134,12 +1135,15 @@ __global__ void __launch_bounds__(256) u6_tables_kernel(const float *__restrict_
 void launch_u6_tables(const float *tables, const float *gthr, int64_t nq, int M, uint8_t *out, float *scale,
                       cudaStream_t st) {
     if (nq <= 0) return;
+    // list items' saturation scale multiplier (RII_U6_LIST_AMUL, A/B): the phase-A bound is tight
+    const char *e = getenv("RII_U6_LIST_AMUL");
+    const float amul = e ? (float)atof(e) : 1.0f;
     switch (M) {
-        case 4: u6_tables_kernel<4><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
-        case 8: u6_tables_kernel<8><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
-        case 16: u6_tables_kernel<16><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
-        case 64: u6_tables_kernel<64><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
-        default: u6_tables_kernel<32><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale); break;
+        case 4: u6_tables_kernel<4><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul); break;
+        case 8: u6_tables_kernel<8><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul); break;
+        case 16: u6_tables_kernel<16><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul); break;
+        case 64: u6_tables_kernel<64><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul); break;
+        default: u6_tables_kernel<32><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul); break;
     }
     RII_LAUNCHED();
 }

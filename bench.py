@@ -56,6 +56,9 @@ WORKLOADS = {
     # the paper's own SIFT1M setting (Table 2: K = 1000, M = 64); not a BASELINE.json config
     "sift1m_m64": ("sift", 1_000_000, 128, 64, 1000, 10_000, 100, 100_000,
                    "paper Table 2 shape: SIFT1M-like 1M x 128, M=64, nlist=1000, 10k queries, top-100"),
+    # the paper's GIST1M setting (Table 2: K = 1000, M = 240, L = 8000 candidates)
+    "gist1m": ("deep", 1_000_000, 960, 240, 1000, 10_000, 100, 100_000,
+               "paper Table 2 shape: GIST1M-like 1M x 960, M=240, nlist=1000, 10k queries, top-100"),
     "tiny": ("gaussian", 10_000, 32, 4, 100, 100, 10, 10_000,
              "BASELINE.json configs[0]: N(0,1) 10k x 32, M=4, nlist=100, 100 queries, top-10"),
 }

@@ -27,7 +27,11 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC"
 # it produced for the headline u6 scan loop varied from build to build (a 17 % slower register
 # allocation was observed).  Units compile in parallel with each other instead.
 SPLIT = {"default": []}
-SOURCES = ["capi.cu", "k_scan.cu", "k_ivf.cu", "k_build.cu", "k_opq.cu", "k_large.cu", "comm.cpp", "opq.cpp"]
+# (source, extra defines, object): k_scan.cu is compiled once for its common code and once per M
+# for the scan kernels of that M (its translation units then build in parallel)
+SOURCES = [("capi.cu", [], "capi.cu.o"), ("k_scan.cu", [], "k_scan.cu.o")] + \
+          [("k_scan.cu", [f"-DRII_SCAN_M={m}"], f"k_scan_m{m}.o") for m in (4, 8, 16, 32, 64)] + \
+          [(f, [], f + ".o") for f in ("k_ivf.cu", "k_build.cu", "k_opq.cu", "k_large.cu", "comm.cpp", "opq.cpp")]
 
 
 def _headers_mtime():
@@ -35,13 +39,14 @@ def _headers_mtime():
                if f.endswith((".cuh", ".hpp", ".h"))) if os.path.isdir(CSRC) else 0.0
 
 
-def _compile(src: str, force: bool, verbose: bool) -> str:
+def _compile(entry, force: bool, verbose: bool) -> str:
+    src, defines, objname = entry
     path = os.path.join(CSRC, src)
-    obj = os.path.join(OBJ, src + ".o")
+    obj = os.path.join(OBJ, objname)
     newest = max(os.path.getmtime(path), _headers_mtime(), os.path.getmtime(os.path.join(ROOT, "include", "rii.h")))
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest:
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, *SPLIT.get(src, SPLIT["default"]), "-c", path, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *SPLIT.get(src, SPLIT["default"]), *defines, "-c", path, "-o", obj]
     if verbose:
         cmd[1:1] = ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

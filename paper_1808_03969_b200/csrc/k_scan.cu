@@ -602,16 +602,20 @@ __global__ void __launch_bounds__(NT, 1)
 // B == 8 means the bf16-packed variant (2 quad tables); otherwise B / 2 fp32 pair tables.
 // u16 variant: 64 KB-aligned tables + the aux block below or above them (kernel).
 static size_t smem_q16(int kk) { return (size_t)2 * QUAD_BYTES + 2 * (size_t)smem_aux_bytes(8, kk) + 16; }
+#ifndef RII_SCAN_M  // common translation unit only
 bool q16_supported(int kk) { return smem_q16(kk) <= 227 * 1024; }
+#endif  // !RII_SCAN_M
 static size_t smem_fast(int B, int kk, int M = 32) {
     const size_t lut = B == 8 ? (size_t)2 * QUAD_BYTES : (size_t)(B / 2) * lut_halves(M) * LUT_PAIR_BYTES;
     return lut + smem_aux_bytes(B, kk);
 }
 // Integer tables run for scans of at least RII_Q16_MIN (default 2^19) codes.
+#ifndef RII_SCAN_M  // common translation unit only
 int64_t q16_min_codes() {
     const char *e = getenv("RII_Q16_MIN");
     return e ? atoll(e) : ((int64_t)1 << 19);
 }
+#endif  // !RII_SCAN_M
 // RII_PACKED=0 disables the bf16-packed tables (A/B measurements).
 static bool packed_enabled() {
     static bool on = [] {
@@ -630,6 +634,7 @@ static constexpr int PACKED_MIN_CODES = 16384;  // codes per CTA below which fp3
 // recomputed column offsets; 3 = 384 threads, shift unpack.
 constexpr int PACKED_NTH = 512;  // bf16-packed kernels: 512 threads
 
+#ifndef RII_SCAN_M  // common translation unit only
 ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available, int max_nc,
                      bool int_ok_caller) {
     ScanPlan p{};
@@ -684,6 +689,7 @@ ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bo
     if (p.chunk < 1) p.chunk = 1;
     return p;
 }
+#endif  // !RII_SCAN_M
 
 // Threads per CTA x codes per thread and step of the lane-rotated kernels
 // (RII_SCAN_CFG=0: 256 x 2, 1: 512 x 1; default below).
@@ -705,15 +711,19 @@ static int m64_nth() {
     return e ? atoi(e) : 256;
 }
 static int q16_nth(int M) { return M == 64 ? m64_nth() : 384; }  // 256 x 2 codes per thread: 150 ms (deep10m)
+#ifndef RII_SCAN_M  // common translation unit only
 bool q16_is_u6(int M) { const int c = q16_cfg(M); return c == 4 || c == 7; }
+#endif  // !RII_SCAN_M
 // List-major u6 items (phase B of the two-phase IVF): 0 = u16 items; 3 = u6, 384
 // threads, one table copy (deep10m L = 64: 21.4 -> 19.1 ms; 192 threads with two CTAs
 // per SM measured 19.2 ms, two table copies 20.7 ms).
+#ifndef RII_SCAN_M  // common translation unit only
 int list_u6_cfg(int M) {
     if (M == 64) return 3;  // two halves: only the u6 items fit (128 KB)
     const char *e = getenv("RII_LIST_U6");
     return M != 32 ? 0 : e ? atoi(e) : 3;
 }
+#endif  // !RII_SCAN_M
 static int list_q16_nth(int) { return 384; }
 static size_t smem_list_q16(int M, int kk) {
     if (list_u6_cfg(M) != 3) return smem_q16(kk);
@@ -790,7 +800,7 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
 }
 
 template <int M>
-static void launch_fast_m(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
+void launch_fast_m(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
                           const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st, const float *tables,
                           float *gthr, bool q16, int timer) {
     if (pl.B == 8) launch_fast_t<M, 8>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
@@ -809,8 +819,11 @@ static void launch_generic_t(const ScanPlan &pl, const uint8_t *codes, int64_t n
     RII_LAUNCHED();
 }
 
+#ifndef RII_SCAN_M  // common translation unit only
 bool list_major_supported(int M) { return M == 4 || M == 8 || M == 16 || M == 32 || M == 64; }
+#endif  // !RII_SCAN_M
 
+#ifndef RII_SCAN_M  // common translation unit only
 int list_major_B(int kk, double avg_len, int M) {
     if (lut_halves(M) > 1) return smem_fast(2, kk, M) <= SMEM_CAP ? 2 : 0;  // fp32 pairs of two halves
     const char *pe = getenv("RII_LIST_PACKED_MIN");  // A/B knob
@@ -821,6 +834,7 @@ int list_major_B(int kk, double avg_len, int M) {
     }
     return 0;
 }
+#endif  // !RII_SCAN_M
 
 template <int M, int B>
 static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
@@ -838,13 +852,28 @@ static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st, b
 }
 
 template <int M>
-static void launch_list_m(int B, const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
+void launch_list_m(int B, const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
     if (B == 8) launch_list_t<M, 8>(a, n_items, st, q16);
     else if (B == 6) launch_list_t<M, 6>(a, n_items, st, false);
     else if (B == 4) launch_list_t<M, 4>(a, n_items, st, false);
     else launch_list_t<M, 2>(a, n_items, st, false);
 }
 
+#ifndef RII_SCAN_M  // common translation unit only
+// The scan kernels of each M are instantiated in their own translation unit (build.py
+// compiles this file once per M with -DRII_SCAN_M): only declared here.
+template <int M>
+void assign_scan_m(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, const float *T, int32_t *assign,
+                   float *dist, cudaStream_t st);
+#define RII_EXTERN_M(MM)                                                                                          \
+    extern template void launch_fast_m<MM>(const ScanPlan &, const uint8_t *, int64_t, const float *, int64_t,   \
+                                           const float *, int, int, uint64_t *, cudaStream_t, const float *,     \
+                                           float *, bool, int);                                                  \
+    extern template void launch_list_m<MM>(int, const ScanArgs &, int64_t, cudaStream_t, bool);                  \
+    extern template void assign_scan_m<MM>(const uint8_t *, int64_t, const uint8_t *, int64_t, const float *,    \
+                                           int32_t *, float *, cudaStream_t);
+RII_EXTERN_M(4) RII_EXTERN_M(8) RII_EXTERN_M(16) RII_EXTERN_M(32) RII_EXTERN_M(64)
+#undef RII_EXTERN_M
 void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
     if (n_items <= 0) return;
     if (B == 0) throw Error(1, "topk too large for the list-major scan");
@@ -857,7 +886,9 @@ void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStre
         default: launch_list_m<32>(B, a, n_items, st, q16); break;
     }
 }
+#endif  // !RII_SCAN_M
 
+#ifndef RII_SCAN_M  // common translation unit only
 void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_codes, int M, const float *q, int64_t nq,
                         const float *cb, int D, int kk, uint64_t *out, cudaStream_t st, const float *tables,
                         float *gthr, bool q16, int timer) {
@@ -878,14 +909,17 @@ void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_code
         launch_generic_t<1>(pl, codes, n_codes, M, q, nq, cb, ds, kk, out, st);
     }
 }
+#endif  // !RII_SCAN_M
 
 // ---------------------------------------------------- SDC-mode assignment ---
+#ifndef RII_SCAN_M  // common translation unit only
 bool assign_scan_supported(int M, int64_t K) {
     return (M == 4 || M == 8 || M == 16 || M == 32) && packed_enabled() && K >= 8192 &&
            smem_fast(8, 32) <= SMEM_CAP;
 }
+#endif  // !RII_SCAN_M
 
-__global__ void top1_kernel(const uint64_t *__restrict__ keys, int64_t n, int kk, int32_t *__restrict__ assign,
+static __global__ void top1_kernel(const uint64_t *__restrict__ keys, int64_t n, int kk, int32_t *__restrict__ assign,
                             float *__restrict__ dist) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -895,7 +929,7 @@ __global__ void top1_kernel(const uint64_t *__restrict__ keys, int64_t n, int kk
 }
 
 template <int M>
-static void assign_scan_m(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, const float *T,
+void assign_scan_m(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, const float *T,
                           int32_t *assign, float *dist, cudaStream_t st) {
     const int kk = 32, B = 8;
     const size_t smem = smem_fast(B, kk);
@@ -919,6 +953,7 @@ static void assign_scan_m(const uint8_t *codes, int64_t n, const uint8_t *center
     RII_CUDA(cudaFreeAsync(keys, st));
 }
 
+#ifndef RII_SCAN_M  // common translation unit only
 void launch_assign_scan(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, int M, const float *T,
                         int32_t *assign, float *dist, int, cudaStream_t st) {
     if (n <= 0) return;
@@ -929,7 +964,9 @@ void launch_assign_scan(const uint8_t *codes, int64_t n, const uint8_t *centers,
         default: assign_scan_m<32>(codes, n, centers, K, T, assign, dist, st); break;
     }
 }
+#endif  // !RII_SCAN_M
 
+#ifndef RII_SCAN_M  // common translation unit only: tables, bounds, gather, merge
 // ------------------------------------------------------------ LUT tables ---
 // One CTA per query, thread z = code word z: the code book rows of subspace m are
 // read coalesced (consecutive z), A(m, z) (CA1) goes to a [256][33] smem tile, and
@@ -1252,5 +1289,15 @@ void launch_merge(const uint64_t *keys, int64_t q_stride, int64_t p_stride, int 
                                                                out_ids, out_dist, out_keys, rs);
     RII_LAUNCHED();
 }
+
+#endif  // !RII_SCAN_M
+
+#ifdef RII_SCAN_M  // per-M translation unit: the scan kernels of one M (build.py compiles k_scan.cu once per M)
+template void launch_fast_m<RII_SCAN_M>(const ScanPlan &, const uint8_t *, int64_t, const float *, int64_t, const float *,
+                                        int, int, uint64_t *, cudaStream_t, const float *, float *, bool, int);
+template void launch_list_m<RII_SCAN_M>(int, const ScanArgs &, int64_t, cudaStream_t, bool);
+template void assign_scan_m<RII_SCAN_M>(const uint8_t *, int64_t, const uint8_t *, int64_t, const float *, int32_t *,
+                                        float *, cudaStream_t);
+#endif
 
 }  // namespace rii

@@ -11,7 +11,7 @@ from collections import Counter
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OBJ = os.path.join(ROOT, "paper_1808_03969_b200", "build_obj", "k_scan.cu.o")
+OBJ = os.path.join(ROOT, "paper_1808_03969_b200", "build_obj", "k_scan_m32.o")  # the M = 32 unit
 KERNEL = "_ZN3rii16scan_fast_kernelILi32ELi8ELb0ELi384ELi1ELi3ELi66EEEvNS_8ScanArgsE"
 
 

@@ -2,7 +2,7 @@
 one JSON line per row.  Timing: CUDA events on the launching stream, >= 1 warm-up,
 queries resident in HBM, median of `reps` runs.
 
-    python tools/configs.py [--only tiny,sift1m,growth,deep10m] [--reps 3]
+    python tools/configs.py [--only tiny,sift1m,growth,deep10m,paper_t2] [--reps 3]
 """
 import argparse
 import json
@@ -83,12 +83,35 @@ def build(kind, N, D, M, nlist, n_train, train_iter=20):
     return g, dict(train_s=t_train, add_s=t_add, reconfigure_s=t_rec)
 
 
+def paper_table2_rows(reps):
+    """The paper's own Table 2 shapes on synthetic stand-ins:
+    SIFT1M-like with M = 64 and GIST1M-like with M = 240, K = 1000, IVF with L lists
+    ~ the paper's L candidates (5000 -> 5 lists, 8000 -> 8 lists), top-1 and top-100,
+    plus the whole linear scan.  The paper: 0.73 ms and 3.2 ms per query, one CPU thread."""
+    for name, Lp in (("sift1m_m64", 5), ("gist1m", 8)):
+        kind, N, D, M, nlist, nq, topk, n_train, _ = bench.WORKLOADS[name]
+        g, b = build(kind, N, D, M, nlist, n_train)
+        emit(config=name, row="build", **b)
+        q = bench._device_data(kind, nq, D, DEV, 0, gen.STREAM_QUERY)
+        for k in (1, 100):
+            ms = timed(lambda: g.query(q, k, None, L=Lp, path="ivf"), reps)
+            emit(config=name, row=f"ivf whole L={Lp} top-{k}", N=N, nq=nq, topk=k, ms=ms, qps=nq / ms * 1e3,
+                 ms_per_query=ms / nq)
+        ms = timed(lambda: g.query(q, 100, None, L=1, path="linear"), reps)
+        emit(config=name, row="linear whole top-100", N=N, nq=nq, topk=100, ms=ms, qps=nq / ms * 1e3,
+             scanned_codes_per_s=nq * N / ms * 1e3)
+        del g
+        torch.cuda.empty_cache()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="tiny,sift1m,growth")
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
     only = a.only.split(",")
+    if "paper_t2" in only:
+        paper_table2_rows(a.reps)
     if "tiny" in only:
         c = gen.CONFIGS["tiny"]
         g, b = build("gaussian", c["N"], c["D"], c["M"], c["nlist"], c["N"])

@@ -249,10 +249,19 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     auto relax = [](float t) { return PACKED ? __fmul_ru(t, PACK_SLACK) : t; };
     float th[B];
     uint32_t thq[Q16 ? B : 1];
+    // u6: the thresholds packed per accumulator word, lanes (q, q + 2) as 0x8000 | thq
+    uint32_t thp[U6 ? 4 : 1];
     auto set_thq = [&]() {
         if constexpr (Q16) {
 #pragma unroll
             for (int qq = 0; qq < B; ++qq) thq[qq] = q16_threshold(fminf(thr[qq], gq[qq]), qsc[qq]);
+        }
+        if constexpr (U6) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int lo = (k >> 1) * 4 + (k & 1);
+                thp[k] = 0x80008000u | min(thq[lo], 0x7fffu) | (min(thq[lo + 2], 0x7fffu) << 16);
+            }
         }
     };
 #pragma unroll
@@ -394,10 +403,22 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                     if constexpr (U6) {
                         uint32_t acc[4];
                         adc_u6<M, U6_GJ, U6_R2, LDS_BASE>(w[u], U6_R2 ? rw2 : rw, sel, colv, a.one, acc);
-                        dq[0] = acc[0] & 0xffffu; dq[2] = acc[0] >> 16;
-                        dq[1] = acc[1] & 0xffffu; dq[3] = acc[1] >> 16;
-                        dq[4] = acc[2] & 0xffffu; dq[6] = acc[2] >> 16;
-                        dq[5] = acc[3] & 0xffffu; dq[7] = acc[3] >> 16;
+                        // SWAR compare: lane sums <= M * 63 < 2^15 and thp holds 0x8000 | thq per
+                        // lane, so bit 15 / 31 of thp - acc is set exactly when sum <= thq
+                        uint32_t t[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) t[k] = thp[k] - acc[k];
+                        const bool anyp = ((t[0] | t[1] | t[2] | t[3]) & 0x80008000u) != 0;
+                        if (__any_sync(0xffffffffu, anyp && pos < c1)) {
+#pragma unroll
+                            for (int qq = 0; qq < B; ++qq) {  // word (qq / 4) * 2 + qq % 2, lane qq & 2
+                                const uint32_t tk = t[(qq >> 2) * 2 + (qq & 1)];
+                                const bool pass = ((qq & 2) ? (tk >> 31) : (tk >> 15)) & 1u;
+                                push_candidate_win(pos < c1 && pass, (uint64_t)cid[u], fresh + qq * NEWCAP, cnt + qq,
+                                                   lane, SOFT, need, ovf);
+                            }
+                        }
+                        continue;
                     } else {
                         uint32_t acc0[NQ], acc1[NQ];
                         adc_q16<M, NQ>(w[u], rw, sel, colA, colB, acc0, acc1);

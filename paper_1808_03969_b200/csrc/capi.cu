@@ -567,7 +567,8 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             // first with fp32 / bf16 tables and publish each query's kk-th distance as its
             // bound; the remaining pairs run with u16 tables scaled by those bounds.
             const int64_t r0 = std::max<int64_t>(1, std::min<int64_t>(P, ceil_div(4 * kk, (int64_t)std::max(avg_len, 1.0))));
-            const bool q16l = q16_enabled() && q16_supported(kk) && P > r0 && avg_len >= list_q16_min_len();
+            const bool q16l = q16_enabled() && q16_supported(kk) && P > r0 && avg_len >= list_q16_min_len() &&
+                              (lut_halves(x->M) == 1 || list_u6_cfg(x->M) == 3);  // M = 64 needs the u6 items
             // RII_LIST_MULTI_PHASE=1: integer phases over growing rank ranges [r0, 4 r0),
             // [4 r0, 16 r0), [16 r0, P), each from tables re-quantised at the bounds the
             // earlier phases left (deep10m L = 64: 17.3 ms against 17.2 ms for one phase,

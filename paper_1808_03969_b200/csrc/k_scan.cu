@@ -739,7 +739,26 @@ bool q16_is_u6(int M) { const int c = q16_cfg(M); return c == 4 || c == 7; }
 // threads, one table copy (deep10m L = 64: 21.4 -> 19.1 ms; 192 threads with two CTAs
 // per SM measured 19.2 ms, two table copies 20.7 ms).
 #ifndef RII_SCAN_M  // common translation unit only
+// The fixed-base layout of the u6 list items assumes the dynamic shared memory of a
+// kernel without static shared memory starts at shared address 0x400 (1 KB reserved);
+// probed once on the device so that a different base falls back instead of trapping.
+static __global__ void smem_base_probe_kernel(uint32_t *out) {
+    extern __shared__ uint8_t probe_smem[];
+    if (threadIdx.x == 0) *out = (uint32_t)__cvta_generic_to_shared(probe_smem);
+}
+static bool fixed_base_ok() {
+    static const bool ok = [] {
+        uint32_t *d = nullptr, h = 0;
+        if (cudaMalloc(&d, 4) != cudaSuccess) return false;
+        smem_base_probe_kernel<<<1, 32, 1024>>>(d);
+        const bool good = cudaMemcpy(&h, d, 4, cudaMemcpyDeviceToHost) == cudaSuccess && h == 0x400u;
+        cudaFree(d);
+        return good;
+    }();
+    return ok;
+}
 int list_u6_cfg(int M) {
+    if (!fixed_base_ok()) return 0;
     if (M == 64) return 3;  // two halves: only the u6 items fit (128 KB)
     const char *e = getenv("RII_LIST_U6");
     return M != 32 ? 0 : e ? atoi(e) : 3;

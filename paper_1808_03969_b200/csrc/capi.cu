@@ -459,7 +459,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             const bool shard_bound = !a.S && x->world > 1 && x->comm != nullptr;
             const int64_t n_dec = shard_bound ? ceil_div(x->N, x->world) : n_codes;
             const int64_t ns_dec = std::min<int64_t>(q16_sample(), n_dec / 4);
-            const bool q16 = pl.B == 8 && pl.fast && q16_enabled() && q16_supported(kk) && n_dec >= q16_min_codes() &&
+            const bool q16 = (pl.B == 8 || pl.B == 16) && pl.fast && q16_enabled() && q16_supported(kk) && n_dec >= q16_min_codes() &&
                              ns_dec >= 4 * kk && ns >= 4 * kk;
             if (!q16 && pl.B == 8 && lut_halves(x->M) > 1)  // M = 64 has no float B = 8 kernel
                 pl = plan_linear(x->M, kk, a.nq, n_codes, x->num_sms, tables != nullptr, 1 << 30, false);

@@ -51,7 +51,8 @@ __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
 }
 
 // Top lists, fresh buffers, counters, thresholds, scratch[16] and the q16 scales.
-__host__ __device__ constexpr int smem_aux_bytes(int B, int kk) { return B * (kk + NEWCAP) * 8 + B * 8 + 64 + B * 12; }
+// (scratch: 32 ints -- [0] compaction max, [1] overflow flag, [2, 2 + B) fill snapshot, [31] rescale flag)
+__host__ __device__ constexpr int smem_aux_bytes(int B, int kk) { return B * (kk + NEWCAP) * 8 + B * 8 + 128 + B * 12; }
 
 // TAB: 0 = fp32 pair tables, 1 = bf16-packed quad tables, 2 = u16 fixed-point quad
 // tables (integer SWAR sums, linear mode with a per-query bound).
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     // an immediate and no 64 KB-aligned padding is needed (two CTAs fit on an SM).
     constexpr bool FIXB = (VARIANT & 128) != 0;
     constexpr int LDS_BASE = FIXB ? 0x400 : 0;
-    static_assert(!U6 || B == 8, "u6 oct tables hold 8 queries");
+    static_assert(!U6 || B == 8 || B == 16, "u6 oct tables hold 8 queries");
     static_assert(!(U6 && LISTS) || FIXB, "list-mode u6 uses the fixed-base layout");
     static_assert(!FIXB || U6, "the fixed-base layout is implemented for the u6 tables");
     // u6 options (VARIANT bit 0: 5-bit entries summed over 8 steps; bit 1: two table
@@ -75,7 +76,9 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     constexpr float U6_CAP = U6_GJ == 8 ? 31.0f : 63.0f;
     constexpr int H = lut_halves(M), LQF = lut_q_floats(M);  // M = 64: two 32-subspace halves
     static_assert(H == 1 || TAB == 0 || TAB == 3, "M = 64 runs the fp32-pair and u6 tables");
-    constexpr int LUTB = U6 ? (U6_R2 ? 2 : 1) * H * OCT_BYTES : NQ * QUAD_BYTES;  // 64 KB-aligned integer tables
+    constexpr int NO = U6 ? B / 8 : 1;  // u6 oct tables (B = 16: two, fixed-base layout, 384 threads)
+    static_assert(NO == 1 || (FIXB && H == 1 && !LISTS && !U6_R2), "16-query u6 tables: fixed-base linear, M <= 32");
+    constexpr int LUTB = U6 ? (U6_R2 ? 2 : 1) * H * NO * OCT_BYTES : NQ * QUAD_BYTES;  // integer tables
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t *lut = smem;
     const int kk = a.kk;
@@ -96,7 +99,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     int *cnt = reinterpret_cast<int *>(fresh + B * NEWCAP);
     float *thr = reinterpret_cast<float *>(cnt + B);
     int *scratch = reinterpret_cast<int *>(thr + B);
-    float *qsc = reinterpret_cast<float *>(scratch + 16);  // q16: per-query scale [B]
+    float *qsc = reinterpret_cast<float *>(scratch + 32);  // q16: per-query scale [B]
     const uint8_t *__restrict__ codes = a.codes;
 
     // Work item: linear mode = (code chunk ci, query batch qb); list mode = (posting
@@ -143,16 +146,20 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         load_lut_oct_u8pre<U6_R2, H>(reinterpret_cast<uint32_t *>(lut), tq);
     } else if constexpr (U6) {
         // u6 tables: per-query scale s = 63 * ALPHA / T (T = +inf -> s = 0: everything passes)
-        float qs[8];
-        const float *tq[8];
 #pragma unroll
-        for (int qq = 0; qq < 8; ++qq) {
-            const float T = __ldcg(a.gthr + query_of(qq));
-            qs[qq] = __fdiv_rd(U6_CAP * u6_alpha(M), fmaxf(T, 1e-30f));
-            if (tid == 0) { qsc[qq] = qs[qq]; tsc[qq] = T; }
-            tq[qq] = a.tables + query_of(qq) * LQF;
+        for (int o = 0; o < NO; ++o) {
+            float qs[8];
+            const float *tq[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int qq = 8 * o + k;
+                const float T = __ldcg(a.gthr + query_of(qq));
+                qs[k] = __fdiv_rd(U6_CAP * u6_alpha(M), fmaxf(T, 1e-30f));
+                if (tid == 0) { qsc[qq] = qs[k]; tsc[qq] = T; }
+                tq[k] = a.tables + query_of(qq) * LQF;
+            }
+            load_lut_oct_u6<U6_R2, H>(reinterpret_cast<uint32_t *>(lut + o * OCT_BYTES), tq, qs, U6_CAP);
         }
-        load_lut_oct_u6<U6_R2, H>(reinterpret_cast<uint32_t *>(lut), tq, qs, U6_CAP);
     } else if (Q16 && a.qtab16) {
         // precomputed per-query u16 tables (q16_tables_kernel) with their scales
         if (tid < B) qsc[tid] = __ldg(a.qscale + query_of(tid));
@@ -250,7 +257,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     float th[B];
     uint32_t thq[Q16 ? B : 1];
     // u6: the thresholds packed per accumulator word, lanes (q, q + 2) as 0x8000 | thq
-    uint32_t thp[U6 ? 4 : 1];
+    uint32_t thp[U6 ? B / 2 : 1];
     auto set_thq = [&]() {
         if constexpr (Q16) {
 #pragma unroll
@@ -258,7 +265,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         }
         if constexpr (U6) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < B / 2; ++k) {
                 const int lo = (k >> 1) * 4 + (k & 1);
                 thp[k] = 0x80008000u | min(thq[lo], 0x7fffu) | (min(thq[lo + 2], 0x7fffu) << 16);
             }
@@ -284,18 +291,25 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                                      : __fdiv_rd((float)q16_cap<M>(), fmaxf(T, 1e-30f));
                     }
                 }
-                scratch[15] = f;
+                scratch[31] = f;
             }
             __syncthreads();
-            if (scratch[15]) {
+            if (scratch[31]) {
                 float qs[B];
 #pragma unroll
                 for (int qq = 0; qq < B; ++qq) qs[qq] = qsc[qq];
                 if constexpr (U6) {
-                    const float *tq[8];
 #pragma unroll
-                    for (int qq = 0; qq < 8; ++qq) tq[qq] = a.tables + query_of(qq) * LQF;
-                    load_lut_oct_u6<U6_R2, H>(reinterpret_cast<uint32_t *>(lut), tq, qs, U6_CAP);
+                    for (int o = 0; o < NO; ++o) {
+                        const float *tq[8];
+                        float qo[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            tq[k] = a.tables + query_of(8 * o + k) * LQF;
+                            qo[k] = qs[8 * o + k];
+                        }
+                        load_lut_oct_u6<U6_R2, H>(reinterpret_cast<uint32_t *>(lut + o * OCT_BYTES), tq, qo, U6_CAP);
+                    }
                 } else {
 #pragma unroll
                     for (int p = 0; p < NQ; ++p)
@@ -401,14 +415,17 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                 if constexpr (Q16) {
                     uint32_t dq[B];
                     if constexpr (U6) {
-                        uint32_t acc[4];
-                        adc_u6<M, U6_GJ, U6_R2, LDS_BASE>(w[u], U6_R2 ? rw2 : rw, sel, colv, a.one, acc);
+                        uint32_t acc[4 * NO];
+                        adc_u6<M, U6_GJ, U6_R2, LDS_BASE, NO>(w[u], U6_R2 ? rw2 : rw, sel, colv, a.one, acc);
                         // SWAR compare: lane sums <= M * 63 < 2^15 and thp holds 0x8000 | thq per
                         // lane, so bit 15 / 31 of thp - acc is set exactly when sum <= thq
-                        uint32_t t[4];
+                        uint32_t t[4 * NO], tor = 0;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) t[k] = thp[k] - acc[k];
-                        const bool anyp = ((t[0] | t[1] | t[2] | t[3]) & 0x80008000u) != 0;
+                        for (int k = 0; k < 4 * NO; ++k) {
+                            t[k] = thp[k] - acc[k];
+                            tor |= t[k];
+                        }
+                        const bool anyp = (tor & 0x80008000u) != 0;
                         if (__any_sync(0xffffffffu, anyp && pos < c1)) {
 #pragma unroll
                             for (int qq = 0; qq < B; ++qq) {  // word (qq / 4) * 2 + qq % 2, lane qq & 2
@@ -656,6 +673,8 @@ static constexpr int PACKED_MIN_CODES = 16384;  // codes per CTA below which fp3
 constexpr int PACKED_NTH = 512;  // bf16-packed kernels: 512 threads
 
 #ifndef RII_SCAN_M  // common translation unit only
+static int q16_cfg(int M);
+static bool fixed_base_ok();
 ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available, int max_nc,
                      bool int_ok_caller) {
     ScanPlan p{};
@@ -667,6 +686,11 @@ ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bo
                             n_codes >= q16_min_codes();
         if (int_ok) { p.B = 8; p.smem = smem_q16(kk); }
         else if (smem_fast(2, kk, M) <= SMEM_CAP) { p.B = 2; p.smem = smem_fast(2, kk, M); }
+    } else if (p.fast && q16_cfg(M) == 9 && int_ok_caller && tables_available && q16_enabled() &&
+               n_codes >= q16_min_codes() && fixed_base_ok() &&
+               (size_t)2 * OCT_BYTES + smem_aux_bytes(16, kk) + 16 <= SMEM_CAP) {
+        p.B = 16;  // u6, two oct tables (RII_Q16_CFG=9)
+        p.smem = (size_t)2 * OCT_BYTES + smem_aux_bytes(16, kk) + 16;
     } else if (p.fast) {
         // Packed tables cost a larger per-CTA table build: only for long code ranges.
         const bool pk = packed_enabled() && tables_available && n_codes >= (int64_t)PACKED_MIN_CODES;
@@ -723,7 +747,9 @@ static int scan_threads() { return 512; }  // fp32 pair kernels
 static int q16_cfg(int M) {
     const char *e = getenv("RII_Q16_CFG");
     if (M == 64) return 4;  // two halves: u6 oct tables, one copy
-    return e ? atoi(e) : (M == 32 ? 7 : 0);
+    // M = 32: 9 = 16 queries per CTA (two oct tables, fixed-base layout; 117 ms on deep10m),
+    // 7 = 8 queries with two table copies (127 ms)
+    return e ? atoi(e) : (M == 32 ? 9 : 0);
 }
 // M = 64 u6 linear kernel threads (RII_M64_NTH: 384 spills ~200 B of code words and
 // took 52.9 ms on sift1m_m64; 256 does not spill: 43.5 ms)
@@ -733,7 +759,7 @@ static int m64_nth() {
 }
 static int q16_nth(int M) { return M == 64 ? m64_nth() : 384; }  // 256 x 2 codes per thread: 150 ms (deep10m)
 #ifndef RII_SCAN_M  // common translation unit only
-bool q16_is_u6(int M) { const int c = q16_cfg(M); return c == 4 || c == 7; }
+bool q16_is_u6(int M) { const int c = q16_cfg(M); return c == 4 || c == 7 || c == 9; }
 #endif  // !RII_SCAN_M
 // List-major u6 items (phase B of the two-phase IVF): 0 = u16 items; 3 = u6, 384
 // threads, one table copy (deep10m L = 64: 21.4 -> 19.1 ms; 192 threads with two CTAs
@@ -772,6 +798,8 @@ static size_t smem_list_q16(int M, int kk) {
 
 template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr_h1(bool q16);
+template <int M, int B, bool LISTS>
+static void *fast_kernel_ptr_b(bool q16);
 
 template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr(bool q16 = false) {
@@ -792,6 +820,16 @@ static void *fast_kernel_ptr(bool q16 = false) {
 
 template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr_h1(bool q16) {
+    if constexpr (B == 16) {  // u6, two oct tables, fixed-base layout (linear only)
+        if constexpr (LISTS) return nullptr;
+        else return (void *)scan_fast_kernel<M, 16, false, 384, 1, 3, 128 | 64>;
+    } else {
+        return fast_kernel_ptr_b<M, B, LISTS>(q16);
+    }
+}
+
+template <int M, int B, bool LISTS>
+static void *fast_kernel_ptr_b(bool q16) {
     // Kernel variants kept for A/B runs (measured on B200, deep10m, 10k queries; the
     // others this round tried are recorded in DESIGN.md and were removed to bound the
     // build time): RII_Q16_CFG 0 = u16 tables (204 ms), 4 = u6 one copy (131 ms),
@@ -822,9 +860,9 @@ template <int M, int B>
 static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
                           const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st, const float *tables,
                           float *gthr, bool q16_req, int timer) {
-    const bool q16 = B == 8 && q16_req && gthr != nullptr;
+    const bool q16 = (B == 8 || B == 16) && q16_req && gthr != nullptr;
     void *kern = fast_kernel_ptr<M, B, false>(q16);
-    const size_t smem = q16 ? smem_q16(kk) : pl.smem;
+    const size_t smem = q16 && B == 8 ? smem_q16(kk) : pl.smem;
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ScanArgs a{};
     a.codes = codes; a.n_codes = n; a.q = q; a.nq = nq; a.cb = cb; a.ds = ds; a.kk = kk;
@@ -832,7 +870,7 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
     a.gthr = gthr;
     a.one = 1;
     void *args[] = {&a};
-    KernelTimer t(timer, st), tp(B == 8 && timer == TK_LINEAR ? (q16 ? (q16_is_u6(M) ? TK_U6 : TK_Q16) : TK_PACKED) : -1,
+    KernelTimer t(timer, st), tp(B >= 8 && timer == TK_LINEAR ? (q16 ? (q16_is_u6(M) ? TK_U6 : TK_Q16) : TK_PACKED) : -1,
                                  st);
     const int nth = q16 ? q16_nth(M) : (B == 8 ? PACKED_NTH : scan_threads());
     RII_CUDA(cudaLaunchKernel(kern, dim3(pl.nb * pl.nc), dim3(nth), args, smem, st));
@@ -843,7 +881,8 @@ template <int M>
 void launch_fast_m(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
                           const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st, const float *tables,
                           float *gthr, bool q16, int timer) {
-    if (pl.B == 8) launch_fast_t<M, 8>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
+    if (pl.B == 16) launch_fast_t<M, 16>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
+    else if (pl.B == 8) launch_fast_t<M, 8>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
     else if (pl.B == 6) launch_fast_t<M, 6>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
     else if (pl.B == 4) launch_fast_t<M, 4>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
     else launch_fast_t<M, 2>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);

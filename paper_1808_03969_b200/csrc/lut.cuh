@@ -390,10 +390,10 @@ __device__ __forceinline__ void load_lut_oct_u6(uint32_t *dst, const float *cons
 // u6 lane-rotated ADC of one code against the oct table: per word index a, the four
 // steps' 8-byte loads are summed bytewise, then widened.  acc[0] = queries (0, 2)
 // in (low, high) 16-bit lanes, acc[1] = (1, 3), acc[2] = (4, 6), acc[3] = (5, 7).
-template <int M, int GJ, bool R2, int BASE = 0>
+template <int M, int GJ, bool R2, int BASE = 0, int NO = 1>
 __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, const uint32_t (&sel)[4],
                                        const uint32_t (&colv)[M / 4 < 8 ? M / 4 : 8], uint32_t one,
-                                       uint32_t (&acc)[4]);
+                                       uint32_t (&acc)[4 * NO]);
 
 // Oct layout from 8 precomputed per-query u6 tables ([z][32 columns] bytes, written by
 // u6_tables_kernel): column c = [t0[c] .. t7[c]] (an 8 x 8 byte transpose per group of
@@ -491,11 +491,12 @@ __device__ __forceinline__ void adc_q16(const uint32_t (&w)[M / 4], uint32_t rw,
     }
 }
 
-template <int M, int GJ, bool R2, int BASE>
+template <int M, int GJ, bool R2, int BASE, int NO>
 __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, const uint32_t (&sel)[4],
                                        const uint32_t (&colv)[M / 4 < 8 ? M / 4 : 8], uint32_t one,
-                                       uint32_t (&acc)[4]) {
-    // GJ steps (4: 6-bit entries, 8: 5-bit entries) are summed bytewise before widening
+                                       uint32_t (&acc)[4 * NO]) {
+    // GJ steps (4: 6-bit entries, 8: 5-bit entries) are summed bytewise before widening;
+    // NO oct tables (8 queries each) 64 KB apart share the offsets of every step
     constexpr int W = M / 4, GW = GJ / 4;
     static_assert(W % GW == 0, "word groups");
     uint32_t wp[W];
@@ -512,35 +513,50 @@ __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, 
     } else {
         permute_words<W>(wp, rw);
     }
+    auto lds = [&](uint32_t off, int aw, int o) -> uint2 {
+        // compile-time immediate: table o (64 KB apart), half aw / 8 (M = 64)
+        if constexpr (W <= 8) {
+            if constexpr (NO == 1) return lds64_imm<BASE>(off);
+            else return o == 0 ? lds64_imm<BASE>(off) : lds64_imm<BASE + 0x10000>(off);
+        } else {
+            return aw < 8 ? lds64_imm<BASE>(off) : lds64_imm<BASE + 0x10000>(off);
+        }
+    };
 #pragma unroll
     for (int g = 0; g < W / GW; ++g) {
-        uint32_t s0 = 0, s1 = 0;
+        uint32_t s0[NO], s1[NO];
 #pragma unroll
         for (int h = 0; h < GW; ++h) {
             const int aw = g * GW + h;
             const uint32_t ca = colv[aw & 7], cb = ca ^ 0x1010u;  // columns of steps t = 0,1 / 2,3 of group aw
-            uint2 v[4];
+            uint32_t off[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const uint32_t off = __byte_perm(wp[aw], t < 2 ? ca : cb, sel[t]);
-                if constexpr (W <= 8) v[t] = lds64_imm<BASE>(off);
-                else v[t] = aw < 8 ? lds64_imm<BASE>(off) : lds64_imm<BASE + 0x10000>(off);  // M = 64: half 1
+            for (int t = 0; t < 4; ++t) off[t] = __byte_perm(wp[aw], t < 2 ? ca : cb, sel[t]);
+#pragma unroll
+            for (int o = 0; o < NO; ++o) {
+                uint2 v[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) v[t] = lds(off[t], aw, o);
+                // bytewise (GJ * cap < 256, no carries), as a tree: dependency depth 2
+                const uint32_t x0 = fma_add(fma_add(v[0].x, one, v[1].x), one, fma_add(v[2].x, one, v[3].x));
+                const uint32_t x1 = fma_add(fma_add(v[0].y, one, v[1].y), one, fma_add(v[2].y, one, v[3].y));
+                s0[o] = h == 0 ? x0 : fma_add(x0, one, s0[o]);
+                s1[o] = h == 0 ? x1 : fma_add(x1, one, s1[o]);
             }
-            // bytewise (GJ * cap < 256, no carries), as a tree: dependency depth 2
-            const uint32_t x0 = fma_add(fma_add(v[0].x, one, v[1].x), one, fma_add(v[2].x, one, v[3].x));
-            const uint32_t x1 = fma_add(fma_add(v[0].y, one, v[1].y), one, fma_add(v[2].y, one, v[3].y));
-            s0 = h == 0 ? x0 : fma_add(x0, one, s0);
-            s1 = h == 0 ? x1 : fma_add(x1, one, s1);
         }
-        const uint32_t e0 = s0 & 0x00ff00ffu, o0 = __byte_perm(s0, 0u, 0x4341);
-        const uint32_t e1 = s1 & 0x00ff00ffu, o1 = __byte_perm(s1, 0u, 0x4341);
-        if (g == 0) {
-            acc[0] = e0; acc[1] = o0; acc[2] = e1; acc[3] = o1;
-        } else {
-            acc[0] = fma_add(e0, one, acc[0]);
-            acc[1] = fma_add(o0, one, acc[1]);
-            acc[2] = fma_add(e1, one, acc[2]);
-            acc[3] = fma_add(o1, one, acc[3]);
+#pragma unroll
+        for (int o = 0; o < NO; ++o) {
+            const uint32_t e0 = s0[o] & 0x00ff00ffu, o0 = __byte_perm(s0[o], 0u, 0x4341);
+            const uint32_t e1 = s1[o] & 0x00ff00ffu, o1 = __byte_perm(s1[o], 0u, 0x4341);
+            uint32_t *ac = acc + 4 * o;
+            if (g == 0) {
+                ac[0] = e0; ac[1] = o0; ac[2] = e1; ac[3] = o1;
+            } else {
+                ac[0] = fma_add(e0, one, ac[0]);
+                ac[1] = fma_add(o0, one, ac[1]);
+                ac[2] = fma_add(e1, one, ac[2]);
+                ac[3] = fma_add(o1, one, ac[3]);
+            }
         }
     }
 }

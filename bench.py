@@ -281,8 +281,8 @@ def run_ours(args, rank, world, local):
             traffic = json.load(f).get("dram_bytes_per_launch")
     roofline = {
         "bound": "alu",
-        "kernel": ("scan_fast_kernel<32,8,u6> (linear ADC scan + top-k, u6 fixed-point oct tables, bytewise SWAR "
-                   "sums + exact rescore)" if u6 else
+        "kernel": (f"scan_fast_kernel<32,{16 if os.environ.get('RII_Q16_CFG', '9') == '9' else 8},u6> (linear ADC "
+                   "scan + top-k, u6 fixed-point oct tables, bytewise SWAR sums + exact rescore)" if u6 else
                    "scan_fast_kernel<32,8,u16> (linear ADC scan + top-k, u16 fixed-point SWAR tables + exact rescore)"
                    if q16 else
                    "scan_fast_kernel<32,8,packed> (linear ADC scan + top-k, bf16-packed tables + exact rescore)"

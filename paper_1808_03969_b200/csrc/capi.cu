@@ -602,8 +602,9 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             int64_t n_ph_items[4] = {0, 0, 0, 0};
             n_ph_items[0] = build_list_items(qoff, x->K, Bl, qlist, P, items, cap, st);
             int64_t n_items = n_ph_items[0];
+            const int Bi = list_int_B(x->M, kk);  // queries per integer item
             for (int ph = 1; ph < pb.n; ++ph) {
-                n_ph_items[ph] = build_list_items(qoff + ph * x->K, x->K, 8, qlist, P, items + n_items, cap - n_items, st);
+                n_ph_items[ph] = build_list_items(qoff + ph * x->K, x->K, Bi, qlist, P, items + n_items, cap - n_items, st);
                 n_items += n_ph_items[ph];
             }
             tr.mark("items");
@@ -621,7 +622,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
                 if (n_ph_items[ph] == 0) continue;
                 tr.mark("list scan phase");
                 float *qsc = x->s_qscale.get<float>(a.nq);
-                if (list_u6_cfg(x->M)) {  // u6 oct items
+                if (list_u6_cfg(x->M) >= 3) {  // u6 oct items
                     uint8_t *t8 = x->s_tab16.get<uint8_t>((size_t)a.nq * lut_q_floats(x->M));
                     launch_u6_tables(tables, gthr, a.nq, x->M, t8, qsc, st);
                     sa.qtab8 = t8;
@@ -632,7 +633,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
                 }
                 sa.qscale = qsc;
                 sa.items = items + done;
-                launch_list_scan(x->M, 8, sa, n_ph_items[ph], st, true);
+                launch_list_scan(x->M, Bi, sa, n_ph_items[ph], st, true);
                 done += n_ph_items[ph];
             }
             tr.mark("list scan");

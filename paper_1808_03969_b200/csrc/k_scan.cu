@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     constexpr int H = lut_halves(M), LQF = lut_q_floats(M);  // M = 64: two 32-subspace halves
     static_assert(H == 1 || TAB == 0 || TAB == 3, "M = 64 runs the fp32-pair and u6 tables");
     constexpr int NO = U6 ? B / 8 : 1;  // u6 oct tables (B = 16: two, fixed-base layout, 384 threads)
-    static_assert(NO == 1 || (FIXB && H == 1 && !LISTS && !U6_R2), "16-query u6 tables: fixed-base linear, M <= 32");
+    static_assert(NO == 1 || (FIXB && H == 1 && !U6_R2), "16-query u6 tables: fixed-base layout, M <= 32");
     constexpr int LUTB = U6 ? (U6_R2 ? 2 : 1) * H * NO * OCT_BYTES : NQ * QUAD_BYTES;  // integer tables
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t *lut = smem;
@@ -140,10 +140,13 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     if constexpr (U6 && LISTS) {
         // precomputed per-query u6 tables (u6_tables_kernel) with their scales
         if (tid < B) qsc[tid] = __ldg(a.qscale + query_of(tid));
-        const uint8_t *tq[8];
 #pragma unroll
-        for (int qq = 0; qq < 8; ++qq) tq[qq] = a.qtab8 + query_of(qq) * LQF;
-        load_lut_oct_u8pre<U6_R2, H>(reinterpret_cast<uint32_t *>(lut), tq);
+        for (int o = 0; o < NO; ++o) {
+            const uint8_t *tq[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) tq[k] = a.qtab8 + query_of(8 * o + k) * LQF;
+            load_lut_oct_u8pre<U6_R2, H>(reinterpret_cast<uint32_t *>(lut + o * OCT_BYTES), tq);
+        }
     } else if constexpr (U6) {
         // u6 tables: per-query scale s = 63 * ALPHA / T (T = +inf -> s = 0: everything passes)
 #pragma unroll
@@ -789,12 +792,20 @@ int list_u6_cfg(int M) {
     const char *e = getenv("RII_LIST_U6");
     return M != 32 ? 0 : e ? atoi(e) : 3;
 }
+
 #endif  // !RII_SCAN_M
 static int list_q16_nth(int) { return 384; }
-static size_t smem_list_q16(int M, int kk) {
-    if (list_u6_cfg(M) != 3) return smem_q16(kk);
+static size_t smem_list_q16(int M, int kk, int B = 8) {
+    if (B == 16) return 2 * OCT_BYTES + smem_aux_bytes(16, kk) + 16;
+    if (list_u6_cfg(M) < 3) return smem_q16(kk);
     return (size_t)lut_halves(M) * OCT_BYTES + smem_aux_bytes(8, kk) + 16;
 }
+
+#ifndef RII_SCAN_M  // common translation unit only
+int list_int_B(int M, int kk) {
+    return list_u6_cfg(M) == 4 && smem_list_q16(M, kk, 16) <= SMEM_CAP ? 16 : 8;
+}
+#endif  // !RII_SCAN_M
 
 template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr_h1(bool q16);
@@ -820,9 +831,13 @@ static void *fast_kernel_ptr(bool q16 = false) {
 
 template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr_h1(bool q16) {
-    if constexpr (B == 16) {  // u6, two oct tables, fixed-base layout (linear only)
-        if constexpr (LISTS) return nullptr;
-        else return (void *)scan_fast_kernel<M, 16, false, 384, 1, 3, 128 | 64>;
+    if constexpr (B == 16) {  // u6, two oct tables, fixed-base layout (list items: M = 32)
+        if constexpr (LISTS) {
+            if constexpr (M == 32) return (void *)scan_fast_kernel<M, 16, true, 384, 1, 3, 128 | 64>;
+            else return nullptr;
+        } else {
+            return (void *)scan_fast_kernel<M, 16, false, 384, 1, 3, 128 | 64>;
+        }
     } else {
         return fast_kernel_ptr_b<M, B, LISTS>(q16);
     }
@@ -838,7 +853,7 @@ static void *fast_kernel_ptr_b(bool q16) {
     if constexpr (B == 8) {
         if constexpr (LISTS) {
             if (q16) {
-                if (list_u6_cfg(M) == 3) return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64>;
+                if (list_u6_cfg(M) >= 3) return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64>;
                 return (void *)scan_fast_kernel<M, 8, true, 384, 1, 2, 64>;  // u16, window 128
             }
         } else {
@@ -917,9 +932,10 @@ int list_major_B(int kk, double avg_len, int M) {
 
 template <int M, int B>
 static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
-    q16 = q16 && B == 8;
+    q16 = q16 && (B == 8 || B == 16);
     void *kern = fast_kernel_ptr<M, B, true>(q16);
-    const size_t smem = q16 ? smem_list_q16(M, a.kk) : smem_fast(B, a.kk, M);
+    if (!kern) throw Error(1, "no list-major kernel for this (M, B)");
+    const size_t smem = q16 ? smem_list_q16(M, a.kk, B) : smem_fast(B, a.kk, M);
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ScanArgs aa = a;
     aa.one = 1;
@@ -932,7 +948,8 @@ static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st, b
 
 template <int M>
 void launch_list_m(int B, const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
-    if (B == 8) launch_list_t<M, 8>(a, n_items, st, q16);
+    if (B == 16) launch_list_t<M, 16>(a, n_items, st, true);
+    else if (B == 8) launch_list_t<M, 8>(a, n_items, st, q16);
     else if (B == 6) launch_list_t<M, 6>(a, n_items, st, false);
     else if (B == 4) launch_list_t<M, 4>(a, n_items, st, false);
     else launch_list_t<M, 2>(a, n_items, st, false);
@@ -956,7 +973,8 @@ RII_EXTERN_M(4) RII_EXTERN_M(8) RII_EXTERN_M(16) RII_EXTERN_M(32) RII_EXTERN_M(6
 void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
     if (n_items <= 0) return;
     if (B == 0) throw Error(1, "topk too large for the list-major scan");
-    if (q16 && (B != 8 || !q16_supported(a.kk) || !a.gthr)) throw Error(1, "u16 list scan needs B = 8, kk <= 256, gthr");
+    if (q16 && ((B != 8 && B != 16) || !q16_supported(a.kk) || !a.gthr))
+        throw Error(1, "integer list scan needs B = 8 or 16, kk <= 256, gthr");
     switch (M) {
         case 4: launch_list_m<4>(B, a, n_items, st, q16); break;
         case 8: launch_list_m<8>(B, a, n_items, st, q16); break;

@@ -83,6 +83,8 @@ void launch_q16_tables(const float *tables, const float *gthr, int64_t nq, int M
                        cudaStream_t st);
 // u6 list items (M = 32, RII_LIST_U6): config (0 = u16 items) and the per-query u6 tables.
 int list_u6_cfg(int M);
+// queries per integer list-major item: 16 (RII_LIST_U6=4, two u6 oct tables) or 8
+int list_int_B(int M, int kk);
 bool q16_is_u6(int M);  // the linear integer-table kernel of this M uses u6 tables
 void launch_u6_tables(const float *tables, const float *gthr, int64_t nq, int M, uint8_t *out, float *scale,
                       cudaStream_t st);

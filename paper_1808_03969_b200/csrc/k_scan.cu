@@ -26,18 +26,29 @@ namespace rii {
 
 
 template <int W>
+__device__ __forceinline__ void ldg256(const uint8_t *p, uint32_t (&w)[W], int o) {
+    asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(w[o]), "=r"(w[o + 1]), "=r"(w[o + 2]), "=r"(w[o + 3]), "=r"(w[o + 4]), "=r"(w[o + 5]),
+                   "=r"(w[o + 6]), "=r"(w[o + 7])
+                 : "l"(p));
+}
+
+// The 32-byte code loads need 32-byte aligned code arrays (M >= 32).
+static inline void check_code_align(const void *codes, int M) {
+    if (M >= 32 && ((uintptr_t)codes & 31u)) throw Error(1, "code array must be 32-byte aligned");
+}
+
+template <int W>
 __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
+    // M >= 32: 32-byte loads (sm_100 LDG.256): the warp's 32 codes of one load are
+    // 1 KB contiguous, 8 L1 wavefronts per load instead of 8 per 16-byte half (the
+    // code loads share the L1 data pipe with the table lookups).  Code arrays are
+    // 32-byte aligned (checked by the launchers).
     if constexpr (W == 16) {  // M = 64
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p) + k);
-            w[4 * k] = a.x; w[4 * k + 1] = a.y; w[4 * k + 2] = a.z; w[4 * k + 3] = a.w;
-        }
+        ldg256(p, w, 0);
+        ldg256(p + 32, w, 8);
     } else if constexpr (W == 8) {
-        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
-        const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
-        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
-        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+        ldg256(p, w, 0);
     } else if constexpr (W == 4) {
         const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
         w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
@@ -888,6 +899,7 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
     KernelTimer t(timer, st), tp(B >= 8 && timer == TK_LINEAR ? (q16 ? (q16_is_u6(M) ? TK_U6 : TK_Q16) : TK_PACKED) : -1,
                                  st);
     const int nth = q16 ? q16_nth(M) : (B == 8 ? PACKED_NTH : scan_threads());
+    check_code_align(codes, M);
     RII_CUDA(cudaLaunchKernel(kern, dim3(pl.nb * pl.nc), dim3(nth), args, smem, st));
     count_launch();
 }
@@ -942,6 +954,7 @@ static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st, b
     void *args[] = {&aa};
     KernelTimer t(TK_IVF, st);
     const int nth = q16 ? list_q16_nth(M) : (B == 8 ? PACKED_NTH : scan_threads());
+    check_code_align(a.codes, M);
     RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)n_items), dim3(nth), args, smem, st));
     count_launch();
 }
@@ -1042,6 +1055,7 @@ void assign_scan_m(const uint8_t *codes, int64_t n, const uint8_t *centers, int6
         a.nb = (int)ceil_div(cn, B); a.chunk = K; a.nc = 1;
         a.sdcT = T; a.qcodes = codes + s0 * M;
         void *args[] = {&a};
+        check_code_align(a.codes, M);
         RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)a.nb), dim3(PACKED_NTH), args, smem, st));
         count_launch();
         top1_kernel<<<(unsigned)ceil_div(cn, 256), 256, 0, st>>>(keys, cn, kk, assign + s0, dist ? dist + s0 : nullptr);
@@ -1203,6 +1217,7 @@ void launch_group_min_bound(const uint8_t *samp, int64_t ns, int M, const float 
     const int GB_Q = gb_q(M);
     const size_t smem = std::max<size_t>((size_t)(GB_Q / 2) * lut_halves(M) * LUT_PAIR_BYTES, (size_t)GB_Q * 1024 * 8);
     const unsigned grid = (unsigned)ceil_div(nq, GB_Q);
+    check_code_align(samp, M);
     switch (M) {
 #define RII_GB(MM)                                                                                                 \
     case MM:                                                                                                       \

@@ -1349,14 +1349,24 @@ __global__ void __launch_bounds__(NT) merge_kernel(const uint64_t *__restrict__ 
                                                    int64_t *__restrict__ out_ids, float *__restrict__ out_dist,
                                                    uint64_t *__restrict__ out_keys, Rescore rs) {
     extern __shared__ __align__(16) uint64_t msm[];
-    uint64_t *top = msm, *prt = msm + kk;
+    uint64_t *top = msm;
     const int64_t q = blockIdx.x;
     const uint64_t *base = keys + q * q_stride;
     for (int i = threadIdx.x; i < kk; i += blockDim.x) top[i] = base[i];
     __syncthreads();
+    uint64_t *prt = msm + kk;
     for (int p = 1; p < parts; ++p) {
-        for (int i = threadIdx.x; i < kk; i += blockDim.x) prt[i] = base[(int64_t)p * p_stride + i];
-        __syncthreads();
+        // A part whose smallest key is not below the current kk-th key cannot change
+        // the list (parts are sorted ascending): thread 0 tests its own prt[0] against
+        // top[kk - 1] (final since the last barrier) inside the barrier that publishes
+        // the part, and the whole block skips the merge.
+        uint64_t first = KEY_MAX;
+        for (int i = threadIdx.x; i < kk; i += blockDim.x) {
+            const uint64_t v = base[(int64_t)p * p_stride + i];
+            prt[i] = v;
+            if (i == 0) first = v;
+        }
+        if (!__syncthreads_or(threadIdx.x == 0 && first < top[kk - 1])) continue;
         for (int i = threadIdx.x; i < kk; i += blockDim.x) {
             const uint64_t v = prt[kk - 1 - i];
             if (v < top[i]) top[i] = v;

@@ -580,7 +580,9 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     for (int e = tid; e < B * kk; e += NTH) {
         const int qq = e >> lkk, i = e & (kk - 1);
         if (qq >= nqi) continue;
-        if constexpr (LISTS) a.out[a.qlist[qstart + qq] * kk + i] = top[e];   // [q][probe rank][kk]
+        if constexpr (LISTS) {  // [q][probe rank][kk]; an empty list writes its first key only
+            if (i == 0 || top[e - i] != KEY_MAX) a.out[a.qlist[qstart + qq] * kk + i] = top[e];
+        }
         else a.out[(((int64_t)qb * B + qq) * a.nc + ci) * kk + i] = top[e];
     }
 }
@@ -1349,24 +1351,20 @@ __global__ void __launch_bounds__(NT) merge_kernel(const uint64_t *__restrict__ 
                                                    int64_t *__restrict__ out_ids, float *__restrict__ out_dist,
                                                    uint64_t *__restrict__ out_keys, Rescore rs) {
     extern __shared__ __align__(16) uint64_t msm[];
-    uint64_t *top = msm;
+    uint64_t *top = msm, *prt = msm + kk;
     const int64_t q = blockIdx.x;
     const uint64_t *base = keys + q * q_stride;
-    for (int i = threadIdx.x; i < kk; i += blockDim.x) top[i] = base[i];
+    for (int i = threadIdx.x; i < kk; i += blockDim.x) top[i] = KEY_MAX;
     __syncthreads();
-    uint64_t *prt = msm + kk;
-    for (int p = 1; p < parts; ++p) {
-        // A part whose smallest key is not below the current kk-th key cannot change
-        // the list (parts are sorted ascending): thread 0 tests its own prt[0] against
-        // top[kk - 1] (final since the last barrier) inside the barrier that publishes
-        // the part, and the whole block skips the merge.
-        uint64_t first = KEY_MAX;
-        for (int i = threadIdx.x; i < kk; i += blockDim.x) {
-            const uint64_t v = base[(int64_t)p * p_stride + i];
-            prt[i] = v;
-            if (i == 0) first = v;
-        }
-        if (!__syncthreads_or(threadIdx.x == 0 && first < top[kk - 1])) continue;
+    for (int p = 0; p < parts; ++p) {
+        // A part whose smallest key (its first: parts are sorted ascending) is not below
+        // the current kk-th key cannot change the list: one broadcast load, and the
+        // block skips it without a barrier (top is final since the last barrier).  An
+        // empty part may hold only its first key (KEY_MAX; list items write no more).
+        const uint64_t *src = base + (int64_t)p * p_stride;
+        if (__ldg(src) >= top[kk - 1]) continue;
+        for (int i = threadIdx.x; i < kk; i += blockDim.x) prt[i] = src[i];
+        __syncthreads();
         for (int i = threadIdx.x; i < kk; i += blockDim.x) {
             const uint64_t v = prt[kk - 1 - i];
             if (v < top[i]) top[i] = v;

@@ -441,11 +441,17 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                         }
                         const bool anyp = (tor & 0x80008000u) != 0;
                         if (__any_sync(0xffffffffu, anyp && pos < c1)) {
+                            // per-lane pass mask (bit qq = query qq; query qq sits in word
+                            // (qq / 4) * 2 + qq % 2, bit 15 or 31 by qq & 2), OR-reduced over
+                            // the warp: only the queries some lane passes take a ballot
+                            uint32_t mk = 0;
 #pragma unroll
-                            for (int qq = 0; qq < B; ++qq) {  // word (qq / 4) * 2 + qq % 2, lane qq & 2
-                                const uint32_t tk = t[(qq >> 2) * 2 + (qq & 1)];
-                                const bool pass = ((qq & 2) ? (tk >> 31) : (tk >> 15)) & 1u;
-                                push_candidate_win(pos < c1 && pass, (uint64_t)cid[u], fresh + qq * NEWCAP, cnt + qq,
+                            for (int k = 0; k < 4 * NO; ++k)
+                                mk |= (t[k] & 0x80008000u) >> (15 - (4 * (k >> 1) + (k & 1)));
+                            mk = pos < c1 ? (mk | (mk >> 14)) & ((1u << B) - 1u) : 0u;
+                            for (uint32_t wm = __reduce_or_sync(0xffffffffu, mk); wm; wm &= wm - 1u) {
+                                const int qq = __ffs(wm) - 1;
+                                push_candidate_win((mk >> qq) & 1u, (uint64_t)cid[u], fresh + qq * NEWCAP, cnt + qq,
                                                    lane, SOFT, need, ovf);
                             }
                         }
@@ -461,15 +467,15 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                             dq[4 * p + 3] = acc1[p] >> 16;
                         }
                     }
-                    bool any = false;
+                    uint32_t mk = 0;  // bit qq: query qq passes (the u6 branch's warp-mask loop)
 #pragma unroll
-                    for (int qq = 0; qq < B; ++qq) any |= dq[qq] <= thq[qq];
-                    if (__any_sync(0xffffffffu, any && pos < c1)) {
-                        // the key's distance field is replaced by the canonical rescore
-#pragma unroll
-                        for (int qq = 0; qq < B; ++qq)
-                            push_candidate_win(pos < c1 && dq[qq] <= thq[qq], (uint64_t)cid[u], fresh + qq * NEWCAP,
-                                               cnt + qq, lane, SOFT, need, ovf);
+                    for (int qq = 0; qq < B; ++qq) mk |= (uint32_t)(dq[qq] <= thq[qq]) << qq;
+                    if (pos >= c1) mk = 0;
+                    // the key's distance field is replaced by the canonical rescore
+                    for (uint32_t wm = __reduce_or_sync(0xffffffffu, mk); wm; wm &= wm - 1u) {
+                        const int qq = __ffs(wm) - 1;
+                        push_candidate_win((mk >> qq) & 1u, (uint64_t)cid[u], fresh + qq * NEWCAP, cnt + qq, lane,
+                                           SOFT, need, ovf);
                     }
                     continue;
                 }

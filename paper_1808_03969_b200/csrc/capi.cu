@@ -127,7 +127,7 @@ struct rii_index {
     double fit_a = 0.0, fit_b = 0.0;
     // scratch (query side is const-callable: mutable)
     mutable Buf s_q, s_S, s_pos, s_sub, s_part, s_keys, s_gather, s_d0, s_probe, s_roff, s_rids, s_rkey, s_rval,
-        s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_items, s_gthr, s_tables, s_cpart, s_ckeys, s_take,
+        s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_qoff2, s_ql2, s_items, s_gthr, s_tables, s_cpart, s_ckeys, s_take,
         s_samp, s_spart, s_bound, s_skey, s_tab16, s_qscale, s_qrot, s_xrot;
 };
 
@@ -596,15 +596,31 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             int64_t *qoff = x->s_qoff.get<int64_t>(nb + 1);
             uint32_t *qlist = x->s_ql.get<uint32_t>(npairs);
             build_csr(keys, vals, npairs, nb, qoff, qlist, st);  // (query, rank) pairs grouped by list
-            const int64_t cap = npairs / std::min(Bl, 8) + nb + 1;
+            // RII_LIST_BOUND=1 (A/B knob): the ranks < r0 only publish a group-minimum
+            // bound per query (list_bound_kernel) and the integer items cover every rank
+            // (deep10m L = 64: 16.3 ms against 16.1 ms for the exact phase-A items).
+            const char *lbe = getenv("RII_LIST_BOUND");
+            const bool lbound = q16l && pb.n == 2 && lbe && atoi(lbe) != 0;
+            const int B0 = lbound ? list_bound_B(x->M) : Bl;
+            const int64_t cap = npairs / std::min(B0, 8) + npairs / 8 + 2 * nb + 2;
             int4 *items = x->s_items.get<int4>(cap);
             tr.mark("pairs csr");
             int64_t n_ph_items[4] = {0, 0, 0, 0};
-            n_ph_items[0] = build_list_items(qoff, x->K, Bl, qlist, P, items, cap, st);
+            n_ph_items[0] = build_list_items(qoff, x->K, B0, qlist, P, items, cap, st);
             int64_t n_items = n_ph_items[0];
             const int Bi = list_int_B(x->M, kk);  // queries per integer item
+            const int64_t *qoff_i = qoff + x->K;
+            const uint32_t *qlist_i = qlist;
+            if (lbound) {  // integer items over all ranks: the unsplit (query, rank) CSR
+                int64_t *qoff2 = x->s_qoff2.get<int64_t>(x->K + 1);
+                uint32_t *ql2 = x->s_ql2.get<uint32_t>(npairs);
+                build_csr(probes, vals, npairs, x->K, qoff2, ql2, st);
+                qoff_i = qoff2;
+                qlist_i = ql2;
+            }
             for (int ph = 1; ph < pb.n; ++ph) {
-                n_ph_items[ph] = build_list_items(qoff + ph * x->K, x->K, Bi, qlist, P, items + n_items, cap - n_items, st);
+                n_ph_items[ph] = build_list_items(lbound ? qoff_i : qoff + ph * x->K, x->K, Bi, qlist_i, P,
+                                                  items + n_items, cap - n_items, st);
                 n_items += n_ph_items[ph];
             }
             tr.mark("items");
@@ -616,8 +632,12 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             sa.codes = codes; sa.q = a.q; sa.nq = a.nq; sa.cb = cb; sa.ds = x->ds; sa.kk = kk; sa.out = pp;
             sa.items = items; sa.qlist = qlist; sa.P = P; sa.offsets = off; sa.ids = ids; sa.gthr = gthr;
             sa.tables = tables;
-            launch_list_scan(x->M, Bl, sa, n_ph_items[0], st);
+            if (lbound)
+                launch_list_bound(codes, x->M, items, n_ph_items[0], off, ids, qlist, P, tables, kk, gthr, st);
+            else
+                launch_list_scan(x->M, Bl, sa, n_ph_items[0], st);
             int64_t done = n_ph_items[0];
+            if (lbound) sa.qlist = qlist_i;
             for (int ph = 1; ph < pb.n; ++ph) {
                 if (n_ph_items[ph] == 0) continue;
                 tr.mark("list scan phase");
@@ -638,7 +658,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             }
             tr.mark("list scan");
             parts = pp;
-            if (Bl != 8) {  // fp32-pair items keep lane-rotated keys: rescore in the merge
+            if (Bl != 8 && !lbound) {  // fp32-pair items keep lane-rotated keys: rescore in the merge
                 rs.codes = codes;
                 rs.tables = tables;
                 rs.M = x->M;

@@ -1218,6 +1218,109 @@ __global__ void __launch_bounds__(GB_NT, 1) group_min_bound_kernel(const uint8_t
     }
 }
 
+// List-major bound items (IVF, before the integer items): a work item = (posting
+// list, <= GB_Q of the queries whose nearest lists it is).  The list's codes are cut
+// into G <= 1024 groups of gsz consecutive members; the kk-th smallest group minimum
+// of a query is a distance that at least kk members reach (kk distinct groups), so
+// it bounds the query's kk-th distance over any superset of the list -- the whole
+// probed set.  Lane-rotated fp32 sums, inflated by 1e-5 as in group_min_bound_kernel;
+// published with atomicMin (non-negative floats order as ints).  A list shorter
+// than kk bounds nothing on its own and is skipped.
+template <int M>
+__global__ void __launch_bounds__(GB_NT, 1) list_bound_kernel(const uint8_t *__restrict__ codes,
+                                                              const int4 *__restrict__ items,
+                                                              const int64_t *__restrict__ offsets,
+                                                              const uint32_t *__restrict__ ids,
+                                                              const uint32_t *__restrict__ qlist, int64_t P,
+                                                              const float *__restrict__ tables, int kk,
+                                                              float *__restrict__ gthr) {
+    constexpr int GB_Q = gb_q(M), W = M / 4, NP = GB_Q / 2, H = lut_halves(M), LQF = lut_q_floats(M);
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int4 it = items[blockIdx.x];
+    const int64_t beg = offsets[it.x], len = offsets[it.x + 1] - beg;
+    const int nqi = it.z;
+    if (len < kk || nqi <= 0) return;  // block-uniform
+    auto qidx = [&](int qq) -> int64_t { return (int64_t)(qlist[it.y + (qq < nqi ? qq : nqi - 1)] / P); };
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+        load_lut_pair_h<M>(reinterpret_cast<float *>(smem + p * H * LUT_PAIR_BYTES), tables + qidx(2 * p) * LQF,
+                           tables + qidx(2 * p + 1) * LQF);
+    __syncthreads();
+    const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
+    uint32_t sel[4];
+    make_selectors(r, sel);
+    const int gsz = (int)((len + 1023) / 1024), G = (int)((len + gsz - 1) / gsz);
+    float gmin[2][GB_Q];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int qq = 0; qq < GB_Q; ++qq) gmin[h][qq] = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int g = tid + h * GB_NT;
+        if (g >= G) continue;
+        const int64_t p0 = beg + (int64_t)g * gsz, p1 = min(p0 + gsz, beg + len);
+        uint32_t wn[W];
+        load_code<W>(codes + (size_t)__ldg(ids + p0) * M, wn);
+        for (int64_t p = p0; p < p1; ++p) {
+            uint32_t w[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) w[k] = wn[k];
+            if (p + 1 < p1) load_code<W>(codes + (size_t)__ldg(ids + p + 1) * M, wn);
+            float2 acc[NP];
+            adc_rotated<M, GB_Q>(smem, w, rw, sel, l8, acc);
+#pragma unroll
+            for (int q2 = 0; q2 < NP; ++q2) {
+                gmin[h][2 * q2] = fminf(gmin[h][2 * q2], acc[q2].x);
+                gmin[h][2 * q2 + 1] = fminf(gmin[h][2 * q2 + 1], acc[q2].y);
+            }
+        }
+    }
+    __syncthreads();  // tables no longer needed: reuse smem for the sort keys
+    uint64_t *keys = reinterpret_cast<uint64_t *>(smem);  // [GB_Q][1024]
+    for (int e = tid; e < GB_Q * 1024; e += GB_NT) keys[e] = KEY_MAX;
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int g = tid + h * GB_NT;
+        if (g >= G) continue;
+#pragma unroll
+        for (int qq = 0; qq < GB_Q; ++qq) keys[qq * 1024 + g] = make_key(gmin[h][qq], (uint32_t)g);
+    }
+    __syncthreads();
+    bitonic_sort_rows(keys, GB_Q, 1024, 1024);
+    if (tid < nqi) {
+        const uint64_t k = keys[tid * 1024 + kk - 1];
+        if (k != KEY_MAX)
+            atomicMin(reinterpret_cast<int *>(gthr + qidx(tid)), __float_as_int(__fmul_ru(key_dist(k), 1.00001f)));
+    }
+}
+
+int list_bound_B(int M) { return gb_q(M); }
+
+void launch_list_bound(const uint8_t *codes, int M, const int4 *items, int64_t n_items, const int64_t *offsets,
+                       const uint32_t *ids, const uint32_t *qlist, int64_t P, const float *tables, int kk,
+                       float *gthr, cudaStream_t st) {
+    if (n_items <= 0) return;
+    const int GB_Q = gb_q(M);
+    const size_t smem = std::max<size_t>((size_t)(GB_Q / 2) * lut_halves(M) * LUT_PAIR_BYTES, (size_t)GB_Q * 1024 * 8);
+    check_code_align(codes, M);
+    switch (M) {
+#define RII_LB(MM)                                                                                                 \
+    case MM:                                                                                                       \
+        RII_CUDA(cudaFuncSetAttribute(list_bound_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                                      (int)smem));                                                                 \
+        list_bound_kernel<MM><<<(unsigned)n_items, GB_NT, smem, st>>>(codes, items, offsets, ids, qlist, P, tables,  \
+                                                                      kk, gthr);                                   \
+        break;
+        RII_LB(4) RII_LB(8) RII_LB(16) RII_LB(32) RII_LB(64)
+#undef RII_LB
+        default: throw Error(1, "list bound: M outside the fast set");
+    }
+    RII_LAUNCHED();
+}
+
 void launch_group_min_bound(const uint8_t *samp, int64_t ns, int M, const float *tables, int64_t nq, int kk,
                             float *gthr, cudaStream_t st) {
     if (nq <= 0) return;

@@ -85,6 +85,12 @@ void launch_q16_tables(const float *tables, const float *gthr, int64_t nq, int M
 int list_u6_cfg(int M);
 // queries per integer list-major item: 16 (RII_LIST_U6=4, two u6 oct tables) or 8
 int list_int_B(int M, int kk);
+// IVF bound items (list_bound_kernel): queries per item, and the launcher that
+// publishes every item's kk-th smallest group minimum into gthr (atomicMin).
+int list_bound_B(int M);
+void launch_list_bound(const uint8_t *codes, int M, const int4 *items, int64_t n_items, const int64_t *offsets,
+                       const uint32_t *ids, const uint32_t *qlist, int64_t P, const float *tables, int kk,
+                       float *gthr, cudaStream_t st);
 bool q16_is_u6(int M);  // the linear integer-table kernel of this M uses u6 tables
 void launch_u6_tables(const float *tables, const float *gthr, int64_t nq, int M, uint8_t *out, float *scale,
                       cudaStream_t st);

@@ -118,6 +118,10 @@ def test_ivf_list_major_and_query_major(rii, ref, monkeypatch, mode, kind, N, D,
                 g2 = g.query(q, 100, target_ids=sub, L=L, path="ivf")
                 monkeypatch.delenv("RII_Q16")
                 assert np.array_equal(gr[0], g2[0]) and np.array_equal(gr[1], g2[1])
+                monkeypatch.setenv("RII_LIST_BOUND", "1")  # group-minimum bound items instead of phase A
+                g4 = g.query(q, 100, target_ids=sub, L=L, path="ivf")
+                monkeypatch.delenv("RII_LIST_BOUND")
+                assert np.array_equal(gr[0], g4[0]) and np.array_equal(gr[1], g4[1])
                 if M == 32:  # u6 items of 8 (RII_LIST_U6=3) and 16 queries (=4)
                     for cfg in ("3", "4"):
                         monkeypatch.setenv("RII_LIST_U6", cfg)

@@ -63,7 +63,7 @@ __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
 
 // Top lists, fresh buffers, counters, thresholds, scratch[16] and the q16 scales.
 // (scratch: 32 ints -- [0] compaction max, [1] overflow flag, [2, 2 + B) fill snapshot, [31] rescale flag)
-__host__ __device__ constexpr int smem_aux_bytes(int B, int kk) { return B * (kk + NEWCAP) * 8 + B * 8 + 128 + B * 12; }
+__host__ __device__ constexpr int smem_aux_bytes(int B, int kk) { return B * (kk + NEWCAP) * 8 + B * 8 + 128 + B * 16; }
 
 // TAB: 0 = fp32 pair tables, 1 = bf16-packed quad tables, 2 = u16 fixed-point quad
 // tables (integer SWAR sums, linear mode with a per-query bound).
@@ -134,6 +134,11 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     // List mode: the item's query indices are read from qlist once into shared memory.
     int *qid_s = reinterpret_cast<int *>(qsc + B);
     float *tsc = qsc + 2 * B;  // integer tables: the bound T each query's scale was set from
+    // The query's global bound (list mode: the best kk-th distance any finished item
+    // of this query saw, inflated by 1e-5 for the lane-rotated rounding; linear: the
+    // sampled bound) also filters.  Kept in shared memory: it is read at window ends
+    // only, so it holds no registers across the scan loop.
+    float *gqs = qsc + 3 * B;
     if constexpr (LISTS) {
         if (threadIdx.x < B) {
             const int qq = (int)threadIdx.x < nqi ? (int)threadIdx.x : nqi - 1;
@@ -224,7 +229,10 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         }
     }
     for (int e = tid; e < B * kk; e += NTH) top[e] = KEY_MAX;
-    if (tid < B) { cnt[tid] = 0; thr[tid] = __int_as_float(0x7f800000); scratch[2 + tid] = 0; }
+    if (tid < B) {
+        cnt[tid] = 0; thr[tid] = __int_as_float(0x7f800000); scratch[2 + tid] = 0;
+        gqs[tid] = a.gthr ? __ldcg(a.gthr + query_of(tid)) : __int_as_float(0x7f800000);
+    }
     if (tid == 0) scratch[1] = 0;
     __syncthreads();
 
@@ -257,14 +265,6 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         for (int aw = 0; aw < (M / 4 < 8 ? M / 4 : 8); ++aw)
             asm volatile("xor.b32 %0, %1, %2;" : "=r"(colv[aw]) : "r"(colA), "r"((uint32_t)(aw * 0x2020)));
     }
-    // List mode: the query's global bound (the best kk-th distance any finished item
-    // of this query saw, inflated by 1e-5 for the lane-rotated rounding) also filters.
-    float gq[B];
-#pragma unroll
-    for (int qq = 0; qq < B; ++qq) {
-        gq[qq] = __int_as_float(0x7f800000);
-        if (a.gthr) gq[qq] = __ldcg(a.gthr + query_of(qq));
-    }
     // Filter thresholds: the exact kk-th distance (and list bound); relaxed by
     // PACK_SLACK for the approximate packed sums.
     auto relax = [](float t) { return PACKED ? __fmul_ru(t, PACK_SLACK) : t; };
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     auto set_thq = [&]() {
         if constexpr (Q16) {
 #pragma unroll
-            for (int qq = 0; qq < B; ++qq) thq[qq] = q16_threshold(fminf(thr[qq], gq[qq]), qsc[qq]);
+            for (int qq = 0; qq < B; ++qq) thq[qq] = q16_threshold(fminf(thr[qq], gqs[qq]), qsc[qq]);
         }
         if constexpr (U6) {
 #pragma unroll
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         }
     };
 #pragma unroll
-    for (int qq = 0; qq < B; ++qq) th[qq] = relax(fminf(thr[qq], gq[qq]));
+    for (int qq = 0; qq < B; ++qq) th[qq] = relax(fminf(thr[qq], gqs[qq]));
     set_thq();
     // Integer tables (linear mode): when a query's bound has halved since its scale was
     // set, re-quantise the tables at the new bound (any scale keeps the filter exact;
@@ -295,10 +295,10 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         if constexpr (Q16 && !LISTS) {
             if (tid == 0) {
                 int f = 0;
-                for (int qq = 0; qq < B; ++qq) f |= fminf(thr[qq], gq[qq]) < 0.5f * tsc[qq];
+                for (int qq = 0; qq < B; ++qq) f |= fminf(thr[qq], gqs[qq]) < 0.5f * tsc[qq];
                 if (f) {
                     for (int qq = 0; qq < B; ++qq) {
-                        const float T = fminf(thr[qq], gq[qq]);
+                        const float T = fminf(thr[qq], gqs[qq]);
                         if (!(T < tsc[qq])) continue;
                         tsc[qq] = T;
                         qsc[qq] = U6 ? __fdiv_rd(U6_CAP * u6_alpha(M), fmaxf(T, 1e-30f))
@@ -527,11 +527,12 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             compact_topk(top, fresh, cnt, thr, B, kk, scratch);
             if (tid == 0) *s_ovf = 0;
             if (tid < B) s_cnt0[tid] = 0;
-#pragma unroll
-            for (int qq = 0; qq < B; ++qq) {
-                if (a.gthr) gq[qq] = fminf(gq[qq], __ldcg(a.gthr + query_of(qq)));
-                th[qq] = relax(fminf(thr[qq], gq[qq]));
+            if (a.gthr) {
+                if (tid < B) gqs[tid] = fminf(gqs[tid], __ldcg(a.gthr + query_of(tid)));
+                __syncthreads();
             }
+#pragma unroll
+            for (int qq = 0; qq < B; ++qq) th[qq] = relax(fminf(thr[qq], gqs[qq]));
             set_thq();
             if (rolled) {
                 base = wstart;
@@ -543,11 +544,10 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         } else {
             if (tid < B) s_cnt0[tid] = cnt[tid];
             if (a.gthr) {
+                if (tid < B) gqs[tid] = fminf(gqs[tid], __ldcg(a.gthr + query_of(tid)));
+                __syncthreads();
 #pragma unroll
-                for (int qq = 0; qq < B; ++qq) {
-                    gq[qq] = fminf(gq[qq], __ldcg(a.gthr + query_of(qq)));
-                    th[qq] = fminf(th[qq], relax(gq[qq]));
-                }
+                for (int qq = 0; qq < B; ++qq) th[qq] = fminf(th[qq], relax(gqs[qq]));
                 set_thq();
             }
             __syncthreads();  // snapshot taken before the next window pushes

@@ -16,7 +16,7 @@ KERNELS = {  # mangled name -> (LDS.64 per code, max LOP3, max SEL, max local-me
     # default M = 32 kernel: 16 queries, two oct tables, fixed-base layout
     "_ZN3rii16scan_fast_kernelILi32ELi16ELb0ELi384ELi1ELi3ELi192EEEvNS_8ScanArgsE": (64, 72, 26, 4),
     # 8 queries, two table copies (RII_Q16_CFG=7)
-    "_ZN3rii16scan_fast_kernelILi32ELi8ELb0ELi384ELi1ELi3ELi66EEEvNS_8ScanArgsE": (32, 44, 10, 0),
+    "_ZN3rii16scan_fast_kernelILi32ELi8ELb0ELi384ELi1ELi3ELi66EEEvNS_8ScanArgsE": (32, 46, 10, 0),
 }
 
 

@@ -236,15 +236,21 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     if (tid == 0) scratch[1] = 0;
     __syncthreads();
 
-    const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
+    // u6 tables (one copy, M >= 32): an 8-byte LDS is served per half-warp, so the
+    // columns only need to differ within each half: lane l reads column
+    // (l mod 16) ^ j at step j (lanes l and l + 16 the same column, in the other
+    // wavefront), and the code-word rotation rw < 4 needs two select stages, not three.
+    constexpr bool HALFW = U6 && !U6_R2 && M >= 32;
+    const uint32_t lr = HALFW ? ((uint32_t)lane & 15u) : (uint32_t)lane;
+    const uint32_t r = lr & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
     uint32_t sel[4];
     if constexpr (Q16) make_selectors_q16(r, sel);
     else make_selectors(r, sel);
     // q16 column registers: bytes 0-1 = 8 (l ^ t) for t = 0,1 (colA) and 2,3 (colB),
     // bytes 2-3 = the table's shared address >> 16
     const uint32_t lut_hi = FIXB ? 0u : (uint32_t)__cvta_generic_to_shared(lut) & 0xffff0000u;
-    uint32_t colA = lut_hi | (((uint32_t)lane ^ 0u) << 3) | (((uint32_t)lane ^ 1u) << 11);
-    uint32_t colB = lut_hi | (((uint32_t)lane ^ 2u) << 3) | (((uint32_t)lane ^ 3u) << 11);
+    uint32_t colA = lut_hi | ((lr ^ 0u) << 3) | ((lr ^ 1u) << 11);
+    uint32_t colB = lut_hi | ((lr ^ 2u) << 3) | ((lr ^ 3u) << 11);
     // two-copy u6 layout: word rotation by bit 2 of the lane only; bit 3 picks the copy
     // (64 KB higher, columns XOR 8), so a half-warp still covers all 32 banks once
     const uint32_t rw2 = ((uint32_t)lane >> 2) & 1u;
@@ -430,7 +436,8 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                     uint32_t dq[B];
                     if constexpr (U6) {
                         uint32_t acc[4 * NO];
-                        adc_u6<M, U6_GJ, U6_R2, LDS_BASE, NO>(w[u], U6_R2 ? rw2 : rw, sel, colv, a.one, acc);
+                        adc_u6<M, U6_GJ, U6_R2, LDS_BASE, NO, HALFW ? 4 : 8>(w[u], U6_R2 ? rw2 : rw, sel, colv, a.one,
+                                                                             acc);
                         // SWAR compare: lane sums <= M * 63 < 2^15 and thp holds 0x8000 | thq per
                         // lane, so bit 15 / 31 of thp - acc is set exactly when sum <= thq
                         uint32_t t[4 * NO], tor = 0;

@@ -100,10 +100,11 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 
 // XOR-permute the code words by the lane's rotation: wp[i] = w[i ^ rw] (rw < 8:
 // for M = 64 the rotation stays inside each 32-subspace half).
-template <int W>
+// (LIM = 4: rw < 4, two select stages -- the half-warp column scheme of adc_u6)
+template <int W, int LIM = 8>
 __device__ __forceinline__ void permute_words(uint32_t (&w)[W], uint32_t rw) {
 #pragma unroll
-    for (int b = 1; b < W && b < 8; b <<= 1) {
+    for (int b = 1; b < W && b < LIM; b <<= 1) {
         const bool c = (rw & b) != 0;
 #pragma unroll
         for (int i = 0; i < W; ++i) {
@@ -390,7 +391,7 @@ __device__ __forceinline__ void load_lut_oct_u6(uint32_t *dst, const float *cons
 // u6 lane-rotated ADC of one code against the oct table: per word index a, the four
 // steps' 8-byte loads are summed bytewise, then widened.  acc[0] = queries (0, 2)
 // in (low, high) 16-bit lanes, acc[1] = (1, 3), acc[2] = (4, 6), acc[3] = (5, 7).
-template <int M, int GJ, bool R2, int BASE = 0, int NO = 1>
+template <int M, int GJ, bool R2, int BASE = 0, int NO = 1, int PLIM = 8>
 __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, const uint32_t (&sel)[4],
                                        const uint32_t (&colv)[M / 4 < 8 ? M / 4 : 8], uint32_t one,
                                        uint32_t (&acc)[4 * NO]);
@@ -491,7 +492,7 @@ __device__ __forceinline__ void adc_q16(const uint32_t (&w)[M / 4], uint32_t rw,
     }
 }
 
-template <int M, int GJ, bool R2, int BASE, int NO>
+template <int M, int GJ, bool R2, int BASE, int NO, int PLIM>
 __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, const uint32_t (&sel)[4],
                                        const uint32_t (&colv)[M / 4 < 8 ? M / 4 : 8], uint32_t one,
                                        uint32_t (&acc)[4 * NO]) {
@@ -511,7 +512,7 @@ __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, 
             wp[i + 1] = c ? x : y;
         }
     } else {
-        permute_words<W>(wp, rw);
+        permute_words<W, PLIM>(wp, rw);
     }
     auto lds = [&](uint32_t off, int aw, int o) -> uint2 {
         // compile-time immediate: table o (64 KB apart), half aw / 8 (M = 64)

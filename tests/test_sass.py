@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OBJ = os.path.join(ROOT, "paper_1808_03969_b200", "build_obj", "k_scan_m32.o")  # the M = 32 unit
 KERNELS = {  # mangled name -> (LDS.64 per code, max LOP3, max SEL, max local-memory ops) in the loop window
     # default M = 32 kernel: 16 queries, two oct tables, fixed-base layout
-    "_ZN3rii16scan_fast_kernelILi32ELi16ELb0ELi384ELi1ELi3ELi192EEEvNS_8ScanArgsE": (64, 72, 26, 4),
+    "_ZN3rii16scan_fast_kernelILi32ELi16ELb0ELi384ELi1ELi3ELi192EEEvNS_8ScanArgsE": (64, 80, 18, 4),
     # 8 queries, two table copies (RII_Q16_CFG=7)
     "_ZN3rii16scan_fast_kernelILi32ELi8ELb0ELi384ELi1ELi3ELi66EEEvNS_8ScanArgsE": (32, 46, 10, 0),
 }

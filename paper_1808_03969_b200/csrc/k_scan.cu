@@ -240,9 +240,10 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     // columns only need to differ within each half: lane l reads column
     // (l mod 16) ^ j at step j (lanes l and l + 16 the same column, in the other
     // wavefront), and the code-word rotation rw < 4 needs two select stages, not three.
-    constexpr bool HALFW = U6 && !U6_R2 && M >= 32;
+    // (the fp32-pair and bf16-packed tables have 8-byte columns too)
+    constexpr bool HALFW = ((U6 && !U6_R2) || TAB == 0 || TAB == 1) && M >= 32;
     const uint32_t lr = HALFW ? ((uint32_t)lane & 15u) : (uint32_t)lane;
-    const uint32_t r = lr & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
+    const uint32_t r = lr & (M - 1), rw = r >> 2, l8 = lr << 3;
     uint32_t sel[4];
     if constexpr (Q16) make_selectors_q16(r, sel);
     else make_selectors(r, sel);
@@ -499,7 +500,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                     }
                 } else {
                     float2 acc2[NP];
-                    adc_rotated<M, B>(lut, w[u], rw, sel, l8, acc2);
+                    adc_rotated<M, B, HALFW ? 4 : 8>(lut, w[u], rw, sel, l8, acc2);
 #pragma unroll
                     for (int p = 0; p < NP; ++p) {
                         d[2 * p] = acc2[p].x;
@@ -1175,7 +1176,9 @@ __global__ void __launch_bounds__(GB_NT, 1) group_min_bound_kernel(const uint8_t
         load_lut_pair_h<M>(reinterpret_cast<float *>(smem + p * H * LUT_PAIR_BYTES), tables + qidx(2 * p) * LQF,
                            tables + qidx(2 * p + 1) * LQF);
     __syncthreads();
-    const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
+    // half-warp columns (see scan_fast_kernel): lane l reads column (l mod 16) ^ j for M >= 32
+    const uint32_t lr = M >= 32 ? ((uint32_t)lane & 15u) : (uint32_t)lane;
+    const uint32_t r = lr & (M - 1), rw = r >> 2, l8 = lr << 3;
     uint32_t sel[4];
     make_selectors(r, sel);
     // groups g = tid, tid + NT, ...; per group the min over its gsz codes
@@ -1197,7 +1200,7 @@ __global__ void __launch_bounds__(GB_NT, 1) group_min_bound_kernel(const uint8_t
             for (int k = 0; k < W; ++k) w[k] = wn[k];
             if (i + 1 < gsz) load_code<W>(gp + (int64_t)(i + 1) * M, wn);
             float2 acc[NP];
-            adc_rotated<M, GB_Q>(smem, w, rw, sel, l8, acc);
+            adc_rotated<M, GB_Q, M >= 32 ? 4 : 8>(smem, w, rw, sel, l8, acc);
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
                 gmin[h][2 * p] = fminf(gmin[h][2 * p], acc[p].x);
@@ -1254,7 +1257,9 @@ __global__ void __launch_bounds__(GB_NT, 1) list_bound_kernel(const uint8_t *__r
         load_lut_pair_h<M>(reinterpret_cast<float *>(smem + p * H * LUT_PAIR_BYTES), tables + qidx(2 * p) * LQF,
                            tables + qidx(2 * p + 1) * LQF);
     __syncthreads();
-    const uint32_t r = (uint32_t)lane & (M - 1), rw = r >> 2, l8 = (uint32_t)lane << 3;
+    // half-warp columns (see scan_fast_kernel): lane l reads column (l mod 16) ^ j for M >= 32
+    const uint32_t lr = M >= 32 ? ((uint32_t)lane & 15u) : (uint32_t)lane;
+    const uint32_t r = lr & (M - 1), rw = r >> 2, l8 = lr << 3;
     uint32_t sel[4];
     make_selectors(r, sel);
     const int gsz = (int)((len + 1023) / 1024), G = (int)((len + gsz - 1) / gsz);
@@ -1276,7 +1281,7 @@ __global__ void __launch_bounds__(GB_NT, 1) list_bound_kernel(const uint8_t *__r
             for (int k = 0; k < W; ++k) w[k] = wn[k];
             if (p + 1 < p1) load_code<W>(codes + (size_t)__ldg(ids + p + 1) * M, wn);
             float2 acc[NP];
-            adc_rotated<M, GB_Q>(smem, w, rw, sel, l8, acc);
+            adc_rotated<M, GB_Q, M >= 32 ? 4 : 8>(smem, w, rw, sel, l8, acc);
 #pragma unroll
             for (int q2 = 0; q2 < NP; ++q2) {
                 gmin[h][2 * q2] = fminf(gmin[h][2 * q2], acc[q2].x);

@@ -143,14 +143,14 @@ __device__ __forceinline__ void adc_rotated_pre(const uint8_t *lut, const uint32
 }
 
 
-template <int M, int B>
+template <int M, int B, int PLIM = 8>
 __device__ __forceinline__ void adc_rotated(const uint8_t *lut, const uint32_t (&w)[M / 4], uint32_t rw,
                                             const uint32_t (&sel)[4], uint32_t l8, float2 (&acc)[B / 2]) {
     constexpr int W = M / 4;
     uint32_t wp[W];
 #pragma unroll
     for (int i = 0; i < W; ++i) wp[i] = w[i];
-    permute_words<W>(wp, rw);
+    permute_words<W, PLIM>(wp, rw);
     adc_rotated_pre<M, B>(lut, wp, sel, l8, acc);
 }
 

@@ -24,7 +24,11 @@
  *  - Ownership: the index owns every device buffer it allocates (code book,
  *    codes, centres, posting lists, scratch) and frees them in rii_destroy.
  *  - Concurrency: one writer (train / add / reconfigure / set_*) or many readers
- *    (query / get_*) at a time per index.
+ *    (query / query_partial / get_*) at a time per index.  Readers may run
+ *    concurrently from several host threads on several streams: every query
+ *    allocates its scratch per call (cudaMallocAsync on its own stream from the
+ *    device's memory pool, freed before it returns), so no two calls share a
+ *    buffer.  A writer must not overlap any other call on the same index.
  *  - Multi-GPU (world > 1): one process per GPU, every rank calls every function
  *    collectively with identical arguments (full x, q, S).  The database is
  *    sharded by id range; each rank scans its shard and the per-rank top-k lists
@@ -59,8 +63,10 @@ typedef enum { RII_MEM_HOST = 0, RII_MEM_DEVICE = 1 } rii_mem;
 /* Size of the opaque NCCL unique id accepted by rii_create. */
 #define RII_NCCL_ID_BYTES 128
 
-/* Message of the last failed call on this thread ("" if none).  Never NULL. */
-const char *rii_last_error(void);
+/* Message of the last failed call on the calling thread ("" if none); never NULL.
+ * The message is thread-local, so idx only documents which index the caller means
+ * (SURVEY 8(b) signature); it may be NULL (e.g. after a failed rii_create). */
+const char *rii_last_error(const rii_index *idx);
 
 /* Number of CUDA kernels this library has launched in this process (all
  * indexes).  Used by bench.py to report "gpu_launches". */
@@ -79,6 +85,18 @@ uint64_t rii_launch_count(void);
  * which outside [0, 7) -> RII_ERR_ARG. */
 void rii_kernel_timing(int32_t enable);
 rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *launches);
+
+/* Diagnostic event counters of the scan kernels (device atomics at barrier-window
+ * ends, process-wide, for tests; counting costs nothing when off).
+ * rii_debug_counters(1) allocates and clears them (on the current device) and
+ * starts counting; (0) stops and frees.  rii_debug_counters_read copies n values
+ * (synchronises the device): [0] window ends, [1] compactions (a CTA's own kk-th
+ * distance tightened), [2] overflowing windows rolled back, [3] window-end reads
+ * of the shared per-query bound that lowered it (another CTA's published kk-th,
+ * i.e. mid-chunk tightening), [4] integer-table re-quantisations at a tighter
+ * bound, [5] bound publications (atomicMin) that lowered the shared bound. */
+rii_status rii_debug_counters(int32_t enable);
+rii_status rii_debug_counters_read(int64_t *out, int32_t n);
 
 /* The rows [*lo, *hi) of an n-row rii_add batch that rank `rank` of `world` stores
  * (contiguous chunks of ceil(n / world) rows; host-only, no device needed). */
@@ -101,6 +119,26 @@ rii_status rii_nccl_unique_id(void *out);
  *  *out receives the index (NULL on failure). */
 rii_status rii_create(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t rank, int32_t world,
                       const void *nccl_id, rii_index **out);
+
+/* Host transport for a multi-process job without NCCL (e.g. torch.distributed
+ * with the gloo backend): allgather(ctx, send, recv, bytes) must place every
+ * rank's `bytes` host bytes (at its `send`) at recv + rank * bytes, recv holding
+ * world * bytes, and return 0 (non-zero -> RII_ERR_NCCL).  It is called from
+ * inside the library's calls, collectively (every rank, same bytes, same order),
+ * after the library synchronised its stream, so no kernel ever waits on another
+ * rank.  ctx is passed through; the struct is copied, ctx and the function must
+ * outlive the index. */
+typedef struct rii_transport {
+    void *ctx;
+    int32_t (*allgather)(void *ctx, const void *send, void *recv, uint64_t bytes);
+} rii_transport;
+
+/* rii_create for a world > 1 job whose exchange step (top-k merge, shared scan
+ * bound, reconfigure sample) runs over `transport` instead of NCCL.  Same shard
+ * layout, calls and results as with NCCL.  transport == NULL or world == 1 ->
+ * RII_ERR_ARG. */
+rii_status rii_create_with_transport(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t rank, int32_t world,
+                                     const rii_transport *transport, rii_index **out);
 
 /* Frees every device buffer and the NCCL communicator.  NULL is a no-op. */
 void rii_destroy(rii_index *idx);
@@ -226,16 +264,27 @@ rii_status rii_calibrate_theta(rii_index *idx, const float *q, int64_t nq, int32
                                int32_t n_L, rii_mem where, void *stream, double *a_out, double *b_out,
                                double *crossovers);
 
-/* Persistence (the paper pickles the index; SPEC's "RII1" layout,
- * S:382-397).  Little-endian file: magic "RII1", u32 version (1), u32 D, M, Ks,
- * world, rank, ivf_mode, flags (bit 0: fitted theta), u32 n_segments; i64 N,
- * n_local, K, theta; f64 fit_a, fit_b; then the code book (M*Ks*(D/M) f32),
- * n_segments x (i64 local offset, i64 global first id, i64 count), the codes
- * (n_local*M u8), the centres (K*M u8) and the posting lists (offsets (K+1) i64,
- * ids n_local u32 local positions; the assignment is rebuilt from them, Eq. 4),
- * i.e. (N+K)M + 4N bytes plus header, code book and offsets.  Each rank saves
- * its own shard.  rii_load creates an index from such a file (the same rank/world
- * layout; nccl_id as in rii_create).  Format errors -> RII_ERR_ARG. */
+/* Persistence (the paper pickles the index; SPEC's persistence
+ * module).  All little-endian.
+ *  Single-GPU index (world == 1): SPEC's "RII1" layout bit for bit -- magic
+ *    "RII1", u32 version (1), u32 D, M, Z (256), N, K, u64 theta, u32 default_L
+ *    (always 1 here), u32 flags (bit 0: OPQ rotation present, bit 1: theta is the
+ *    analytic default of reading R3, stored value 0); the code book (M*Z*(D/M)
+ *    f32); the rotation (D*D f32) if bit 0; the codes (N*M u8); the centres (K*M
+ *    u8); the postings (for k < K: u32 length, then that many u32 ids, ascending).
+ *    Payload (N+K)M + 4N(+4K) bytes.  State SPEC has no field for follows
+ *    in an optional trailing block: "RIIX", u32 ivf_mode, u32 fitted-theta flag,
+ *    f64 fit_a, f64 fit_b (written only when ivf_mode != 0 or theta was fitted).
+ *  Shard of a world > 1 job: magic "RIIS" (not SPEC's layout), u32 version (1),
+ *    u32 D, M, Ks, world, rank, ivf_mode, flags (bit 0: fitted theta, bit 1: OPQ),
+ *    n_segments; i64 N, n_local, K, theta; f64 fit_a, fit_b; rotation (if bit 1);
+ *    code book; n_segments x (i64 local offset, i64 global first id, i64 count);
+ *    codes (n_local*M u8); centres; CSR offsets (K+1) i64; ids n_local u32 (local
+ *    positions).  Each rank saves its own shard; rii_load restores it on the same
+ *    rank/world (nccl_id as in rii_create).
+ * rii_load validates everything before upload (header ranges, segments tiling
+ * [0, n_local), posting lists a partition with ascending in-range ids, no trailing
+ * bytes beyond the optional block): format errors -> RII_ERR_ARG. */
 rii_status rii_save(const rii_index *idx, const char *path);
 rii_status rii_load(const char *path, int32_t device, const void *nccl_id, rii_index **out);
 

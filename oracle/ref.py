@@ -69,6 +69,8 @@ def lib():
             "rref_reconfigure": (C.c_int, [p, C.c_int, C.c_int, C.c_int, p, i64, i64, C.c_int, u64,
                                            p, p, p, p, p]),
             "rref_train": (C.c_int, [p, i64, C.c_int, C.c_int, C.c_int, C.c_int, u64, p]),
+            "rref_reseed_count": (i64, [C.c_int]),
+            "rref_reseed_reset": (None, []),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -95,6 +97,15 @@ def _c(a, dt):
 def _chk(st, what):
     if st != 0:
         raise OracleError(st, what)
+
+
+def reseed_counts() -> tuple[int, int]:
+    """(training, PQk-means) empty-cluster re-seeds since the last reset (instrumentation)."""
+    return int(lib().rref_reseed_count(0)), int(lib().rref_reseed_count(1))
+
+
+def reseed_reset() -> None:
+    lib().rref_reseed_reset()
 
 
 def splitmix64(x: int) -> int:

@@ -39,6 +39,16 @@
 #define REF_PATH_IVF 2
 
 /* ------------------------------------------------------------------------- */
+/* Instrumentation (test infrastructure only): how many times the empty-cluster
+ * re-seeding branches ran -- [0] code-book training (R8), [1] PQk-means
+ * (R9) -- so that the pins can show those branches are exercised.  Reading
+ * them changes nothing the oracle computes.  Not thread-safe (the oracle is
+ * single-threaded per call; the counters are only read by serial pin tests). */
+static int64_t g_reseeds[2];
+int64_t rref_reseed_count(int which) { return which >= 0 && which < 2 ? g_reseeds[which] : -1; }
+void rref_reseed_reset(void) { g_reseeds[0] = g_reseeds[1] = 0; }
+
+/* ------------------------------------------------------------------------- */
 /* Counter-based hash used for every seeded choice (R8, R10).                 */
 /* splitmix64 finaliser (Steele, Lea, Flood 2014); a bijection on 64 bits.     */
 uint64_t rref_splitmix64(uint64_t x) {
@@ -500,6 +510,7 @@ int rref_pqkmeans(const float *T, int M, int Z, const uint8_t *X, int64_t ns, in
                 if (bi < 0 || dist[i] > dist[bi]) bi = i;
             }
             if (bi < 0) continue; /* unreachable while K <= ns */
+            g_reseeds[1]++;
             memcpy(C + k * M, X + bi * M, (size_t)M);
             used[bi] = 1;
             a[bi] = (int32_t)k;
@@ -615,6 +626,7 @@ int rref_train(const float *x, int64_t n, int D, int M, int Z, int n_iter, uint6
                     if (bi < 0 || d[i] > d[bi]) bi = i;
                 }
                 used[bi] = 1;
+                g_reseeds[0]++;
                 for (int j = 0; j < ds; ++j) c[z * ds + j] = x[bi * D + m * ds + j];
             }
         }

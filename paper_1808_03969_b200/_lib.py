@@ -21,13 +21,16 @@ NCCL_ID_BYTES = 128
 # name -> (restype, argtypes); every symbol include/rii.h declares.
 _p, _i32, _i64, _u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64
 SIGNATURES = {
-    "rii_last_error": (C.c_char_p, []),
+    "rii_last_error": (C.c_char_p, [_p]),
     "rii_launch_count": (_u64, []),
     "rii_kernel_timing": (None, [_i32]),
     "rii_kernel_timing_read": (C.c_int, [_i32, C.POINTER(C.c_double), C.POINTER(_i64)]),
+    "rii_debug_counters": (C.c_int, [_i32]),
+    "rii_debug_counters_read": (C.c_int, [C.POINTER(_i64), _i32]),
     "rii_shard_range": (C.c_int, [_i64, _i32, _i32, C.POINTER(_i64), C.POINTER(_i64)]),
     "rii_nccl_unique_id": (C.c_int, [_p]),
     "rii_create": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _i32, _p, C.POINTER(_p)]),
+    "rii_create_with_transport": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _i32, _p, C.POINTER(_p)]),
     "rii_destroy": (None, [_p]),
     "rii_train": (C.c_int, [_p, _p, _i64, _i32, _u64, C.c_int, _p]),
     "rii_add": (C.c_int, [_p, _p, _i64, C.c_int, _p, C.POINTER(_i64)]),
@@ -56,6 +59,14 @@ SIGNATURES = {
                                C.POINTER(_i64)]),
 }
 
+# struct rii_transport (include/rii.h): host all-gather callback for world > 1
+TRANSPORT_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+
+
+class Transport(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allgather", TRANSPORT_FN)]
+
+
 _lib = None
 
 
@@ -82,4 +93,4 @@ def load(path: str = LIB_PATH):
 
 def check(status: int):
     if status != RII_OK:
-        raise RiiError(status, load().rii_last_error().decode())
+        raise RiiError(status, load().rii_last_error(None).decode())

@@ -23,6 +23,10 @@
 namespace rii {
 std::atomic<uint64_t> g_launches{0};
 
+// rii_debug_counters: device event counters of the scan kernels (common.cuh)
+std::atomic<int *> g_dbg{nullptr};
+int *debug_counters() { return g_dbg.load(std::memory_order_relaxed); }
+
 namespace timing {
 std::mutex g_tmu;
 bool g_timing = false;
@@ -99,6 +103,45 @@ struct Buf {
     }
 };
 
+// Stream-ordered scratch owned by one call (rii.h "Concurrency"): cudaMallocAsync
+// on the call's stream from the device pool that rii_create keeps warm, released
+// with cudaFreeAsync when the call's scratch goes out of scope, so concurrent
+// readers on different streams never share (or free) each other's buffers.
+struct SBuf {
+    const cudaStream_t *st;
+    void *p = nullptr;
+    size_t cap = 0;
+    explicit SBuf(const cudaStream_t *s) : st(s) {}
+    SBuf(const SBuf &) = delete;
+    SBuf &operator=(const SBuf &) = delete;
+    ~SBuf() { if (p) cudaFreeAsync(p, *st); }
+    template <class T>
+    T *get(size_t count) {
+        const size_t b = std::max<size_t>(count * sizeof(T), 16);
+        if (b > cap) {
+            if (p) cudaFreeAsync(p, *st);
+            p = nullptr;
+            cap = 0;
+            RII_CUDA(cudaMallocAsync(&p, b, *st));
+            cap = b;
+        }
+        return reinterpret_cast<T *>(p);
+    }
+    template <class T>
+    T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+// Every scratch buffer of one rii_query / rii_query_partial call.
+struct QueryScratch {
+    cudaStream_t st;
+    SBuf s_q{&st}, s_S{&st}, s_pos{&st}, s_sub{&st}, s_part{&st}, s_keys{&st}, s_gather{&st}, s_d0{&st},
+        s_probe{&st}, s_roff{&st}, s_rids{&st}, s_rkey{&st}, s_rval{&st}, s_out_ids{&st}, s_out_dist{&st},
+        s_flag{&st}, s_lq{&st}, s_qoff{&st}, s_ql{&st}, s_qoff2{&st}, s_ql2{&st}, s_items{&st}, s_gthr{&st},
+        s_tables{&st}, s_cpart{&st}, s_ckeys{&st}, s_take{&st}, s_samp{&st}, s_spart{&st}, s_bound{&st},
+        s_skey{&st}, s_tab16{&st}, s_qscale{&st}, s_qrot{&st}, s_route{&st};
+    explicit QueryScratch(cudaStream_t s) : st(s) {}
+};
+
 struct Seg {
     int64_t local_off, global_first, count;
 };
@@ -109,13 +152,13 @@ using namespace rii;
 
 struct rii_index {
     int D = 0, M = 0, ds = 0, device = 0, rank = 0, world = 1, num_sms = 148;
-    void *comm = nullptr;
+    Comm *comm = nullptr;  // NCCL or host transport (world > 1); nullptr = single GPU / detached shard
     bool trained = false, T_valid = false;
     Buf cb, T;
     int64_t N = 0, n_local = 0;
     Buf codes, assign;
     std::vector<Seg> segs;
-    Buf seg_local, seg_global;
+    Buf seg_local, seg_global, seg_count;
     int64_t K = 0;
     Buf centers, offsets, ids;
     int64_t theta = -1;
@@ -125,10 +168,9 @@ struct rii_index {
     Buf rot, rotT;
     std::vector<float> rot_host;
     double fit_a = 0.0, fit_b = 0.0;
-    // scratch (query side is const-callable: mutable)
-    mutable Buf s_q, s_S, s_pos, s_sub, s_part, s_keys, s_gather, s_d0, s_probe, s_roff, s_rids, s_rkey, s_rval,
-        s_out_ids, s_out_dist, s_flag, s_x, s_lq, s_qoff, s_ql, s_qoff2, s_ql2, s_items, s_gthr, s_tables, s_cpart, s_ckeys, s_take,
-        s_samp, s_spart, s_bound, s_skey, s_tab16, s_qscale, s_qrot, s_xrot;
+    // writer-side scratch (train / add / reconfigure; single writer).  Queries use a
+    // per-call QueryScratch instead.
+    Buf s_x, s_flag, s_xrot, s_rval;
 };
 
 namespace {
@@ -184,12 +226,14 @@ IdMap local_map(const rii_index *x) {
 }
 
 void upload_segs(rii_index *x, cudaStream_t st) {
-    std::vector<int64_t> lo, gl;
-    for (auto &s : x->segs) { lo.push_back(s.local_off); gl.push_back(s.global_first); }
+    std::vector<int64_t> lo, gl, ct;
+    for (auto &s : x->segs) { lo.push_back(s.local_off); gl.push_back(s.global_first); ct.push_back(s.count); }
     int64_t *dl = x->seg_local.get<int64_t>(lo.size() + 1), *dg = x->seg_global.get<int64_t>(gl.size() + 1);
+    int64_t *dc = x->seg_count.get<int64_t>(ct.size() + 1);
     if (!lo.empty()) {
         RII_CUDA(cudaMemcpyAsync(dl, lo.data(), lo.size() * 8, cudaMemcpyHostToDevice, st));
         RII_CUDA(cudaMemcpyAsync(dg, gl.data(), gl.size() * 8, cudaMemcpyHostToDevice, st));
+        RII_CUDA(cudaMemcpyAsync(dc, ct.data(), ct.size() * 8, cudaMemcpyHostToDevice, st));
     }
     RII_CUDA(cudaStreamSynchronize(st));
 }
@@ -260,33 +304,89 @@ void rank_rows(int64_t n, int rank, int world, int64_t &lo, int64_t &hi) {
     hi = std::min<int64_t>(n, lo + per);
 }
 
+// Subset routing (SURVEY 8(e) "S is routed by binary search over the range table"):
+// S is sorted and each segment of this rank is a contiguous id range, so the ids of
+// S a segment owns form one contiguous range [b_j, e_j) of S.  One block finds those
+// ranges (two binary searches per segment) and their output offsets; then every
+// element of S finds its segment's range by a binary search over the b_j and, if
+// owned, writes its global id and local position.  Only the owned count goes to the
+// host (one 8-byte read), not S itself.
+__device__ __forceinline__ int64_t lower_bound_i64(const int64_t *a, int64_t n, int64_t v) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = lo + ((hi - lo) >> 1);
+        if (a[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void route_ranges_kernel(const int64_t *__restrict__ S, int64_t nS, const int64_t *__restrict__ seg_global,
+                                    const int64_t *__restrict__ seg_count, int nseg, int64_t *__restrict__ rb,
+                                    int64_t *__restrict__ re, int64_t *__restrict__ roff, int64_t *__restrict__ total) {
+    for (int j = threadIdx.x; j < nseg; j += blockDim.x) {
+        rb[j] = lower_bound_i64(S, nS, seg_global[j]);
+        re[j] = lower_bound_i64(S, nS, seg_global[j] + seg_count[j]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // segments are few (one per add batch): a serial prefix sum
+        int64_t acc = 0;
+        for (int j = 0; j < nseg; ++j) {
+            roff[j] = acc;
+            acc += re[j] - rb[j];
+        }
+        *total = acc;
+    }
+}
+
+__global__ void route_scatter_kernel(const int64_t *__restrict__ S, int64_t nS, const int64_t *__restrict__ seg_local,
+                                     const int64_t *__restrict__ seg_global, int nseg, const int64_t *__restrict__ rb,
+                                     const int64_t *__restrict__ re, const int64_t *__restrict__ roff,
+                                     int64_t *__restrict__ S_loc, int64_t *__restrict__ pos) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nS) return;
+    // last segment j with rb[j] <= i (rb is non-decreasing: segments ascend in id)
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (rb[mid] <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    if (i < rb[lo] || i >= re[lo]) return;  // owned by another rank
+    const int64_t o = roff[lo] + (i - rb[lo]), s = S[i];
+    S_loc[o] = s;
+    pos[o] = s - seg_global[lo] + seg_local[lo];
+}
+
 // Target ids of this rank: global ids (device) and local positions (device).
 // world == 1: positions == ids (no copy).  Returns the local count.
-int64_t route_targets(const rii_index *x, const int64_t *S, int64_t nS, cudaStream_t st, const int64_t **S_local,
-                      const int64_t **pos_local) {
+int64_t route_targets(const rii_index *x, QueryScratch &sc, const int64_t *S, int64_t nS, cudaStream_t st,
+                      const int64_t **S_loc, const int64_t **pos_loc) {
     if (x->world == 1) {
-        *S_local = S;
-        *pos_local = S;
+        *S_loc = S;
+        *pos_loc = S;
         return nS;
     }
-    std::vector<int64_t> hs((size_t)nS);
-    if (nS) RII_CUDA(cudaMemcpyAsync(hs.data(), S, (size_t)nS * 8, cudaMemcpyDeviceToHost, st));
-    RII_CUDA(cudaStreamSynchronize(st));
-    std::vector<int64_t> gl, lp;
-    for (auto &s : x->segs) {
-        auto b = std::lower_bound(hs.begin(), hs.end(), s.global_first);
-        auto e = std::lower_bound(hs.begin(), hs.end(), s.global_first + s.count);
-        for (auto it = b; it != e; ++it) { gl.push_back(*it); lp.push_back(*it - s.global_first + s.local_off); }
+    const int nseg = (int)x->segs.size();
+    if (nseg == 0 || nS == 0) {
+        *S_loc = *pos_loc = sc.s_S.get<int64_t>(1);
+        return 0;
     }
-    int64_t *dS = x->s_S.get<int64_t>(gl.size() + 1), *dP = x->s_pos.get<int64_t>(lp.size() + 1);
-    if (!gl.empty()) {
-        RII_CUDA(cudaMemcpyAsync(dS, gl.data(), gl.size() * 8, cudaMemcpyHostToDevice, st));
-        RII_CUDA(cudaMemcpyAsync(dP, lp.data(), lp.size() * 8, cudaMemcpyHostToDevice, st));
-    }
+    int64_t *r = sc.s_route.get<int64_t>((size_t)3 * nseg + 1);  // rb, re, roff, total
+    route_ranges_kernel<<<1, 256, 0, st>>>(S, nS, x->seg_global.as<int64_t>(), x->seg_count.as<int64_t>(), nseg, r,
+                                          r + nseg, r + 2 * nseg, r + 3 * nseg);
+    RII_LAUNCHED();
+    int64_t *dS = sc.s_S.get<int64_t>(nS + 1), *dP = sc.s_pos.get<int64_t>(nS + 1);
+    route_scatter_kernel<<<(unsigned)ceil_div(nS, 256), 256, 0, st>>>(S, nS, x->seg_local.as<int64_t>(),
+                                                                     x->seg_global.as<int64_t>(), nseg, r, r + nseg,
+                                                                     r + 2 * nseg, dS, dP);
+    RII_LAUNCHED();
+    int64_t n_loc = 0;
+    RII_CUDA(cudaMemcpyAsync(&n_loc, r + 3 * nseg, 8, cudaMemcpyDeviceToHost, st));
     RII_CUDA(cudaStreamSynchronize(st));
-    *S_local = dS;
-    *pos_local = dP;
-    return (int64_t)gl.size();
+    *S_loc = dS;
+    *pos_loc = dP;
+    return n_loc;
 }
 
 struct QueryArgs {
@@ -297,13 +397,15 @@ struct QueryArgs {
     int64_t nS;
     int L;
     int path;                // resolved LINEAR / IVF
+    bool collective;         // rii_query with world > 1 and a communicator: every rank runs this call
 };
 
 // OPQ: the rotated copy R x of n device rows in `buf`, or x itself
 // when the index has no rotation.
-const float *rotate_input(const rii_index *x, Buf &buf, const float *dx, int64_t n, cudaStream_t st) {
+template <class B>
+const float *rotate_input(const rii_index *x, B &buf, const float *dx, int64_t n, cudaStream_t st) {
     if (!x->has_rot || n <= 0) return dx;
-    float *o = buf.get<float>((size_t)n * x->D);
+    float *o = buf.template get<float>((size_t)n * x->D);
     launch_rotate(x->rotT.as<float>(), dx, n, x->D, o, st);
     return o;
 }
@@ -347,24 +449,24 @@ struct Targets {
     const uint32_t *rids = nullptr;
 };
 
-Targets prepare_targets(const rii_index *x, const QueryArgs &a, cudaStream_t st) {
+Targets prepare_targets(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cudaStream_t st) {
     Targets t;
     if (!a.S) return t;
-    t.n_loc = route_targets(x, a.S, a.nS, st, &t.S_loc, &t.pos);
+    t.n_loc = route_targets(x, sc, a.S, a.nS, st, &t.S_loc, &t.pos);
     if (a.path == RII_PATH_LINEAR) {
-        uint8_t *sub = x->s_sub.get<uint8_t>((size_t)std::max<int64_t>(t.n_loc, 1) * x->M + 64);
+        uint8_t *sub = sc.s_sub.get<uint8_t>((size_t)std::max<int64_t>(t.n_loc, 1) * x->M + 64);
         launch_gather_codes(x->codes.as<uint8_t>(), x->M, t.pos, t.n_loc, sub, st);
         t.sub_codes = sub;
     } else {
-        int32_t *rk = x->s_rkey.get<int32_t>(t.n_loc + 1);
-        uint32_t *rv = x->s_rval.get<uint32_t>(t.n_loc + 1);
+        int32_t *rk = sc.s_rkey.get<int32_t>(t.n_loc + 1);
+        uint32_t *rv = sc.s_rval.get<uint32_t>(t.n_loc + 1);
         if (t.n_loc > 0) {
             gather_i32_kernel<<<(unsigned)ceil_div(t.n_loc, 256), 256, 0, st>>>(x->assign.as<int32_t>(), t.pos,
                                                                                t.n_loc, rk, rv);
             RII_LAUNCHED();
         }
-        int64_t *roff = x->s_roff.get<int64_t>(x->K + 1);
-        uint32_t *rids = x->s_rids.get<uint32_t>(t.n_loc + 1);
+        int64_t *roff = sc.s_roff.get<int64_t>(x->K + 1);
+        uint32_t *rids = sc.s_rids.get<uint32_t>(t.n_loc + 1);
         build_csr(rk, rv, t.n_loc, x->K, roff, rids, st);
         t.roff = roff;
         t.rids = rids;
@@ -399,8 +501,8 @@ static int ns_chunks() {
 // One batch of queries (a.q, a.nq) against this rank's shard.  Writes either the
 // final result (world == 1, out_keys == nullptr) or this rank's top-kk keys with
 // global ids (out_keys, device [nq][kk]).
-void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cudaStream_t st, int64_t *out_ids,
-                  float *out_dist, uint64_t *out_keys) {
+void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, const Targets &t, cudaStream_t st,
+                  int64_t *out_ids, float *out_dist, uint64_t *out_keys) {
     const int kk = a.kk;
     const float *cb = x->cb.as<float>();
     const uint8_t *codes = x->codes.as<uint8_t>();
@@ -411,11 +513,11 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
     const float *tables = nullptr;
     const bool large = !fast && x->M >= large_min_m();  // k_large.cu: one query per CTA, bf16 resident table
     if (fast) {
-        float *tb = x->s_tables.get<float>((size_t)a.nq * lut_q_floats(x->M));
+        float *tb = sc.s_tables.get<float>((size_t)a.nq * lut_q_floats(x->M));
         launch_lut_tables(a.q, a.nq, cb, x->D, x->M, tb, st);
         tables = tb;
     } else if (large) {
-        float *tb = x->s_tables.get<float>((size_t)a.nq * x->M * KS);
+        float *tb = sc.s_tables.get<float>((size_t)a.nq * x->M * KS);
         launch_lut_large(a.q, a.nq, cb, x->D, x->M, tb, st);
         tables = tb;
     }
@@ -432,13 +534,44 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             map.kind = 1;
             map.table = t.S_loc;
         }
+        // Whole-database scans on several ranks share the bound pass of the integer
+        // tables: rank r bounds the queries of its slice from its own shard's sample (a
+        // subset of the database, so the bound holds globally) and the slices are
+        // all-gathered.  Whether the ranks enter that all-gather is decided from global
+        // quantities only (N, world, M, kk, nq), so every rank -- also one whose shard
+        // is empty or short -- joins the same collectives; each rank then decides
+        // locally whether its own scan runs the integer tables.
+        float *gthr_shared = nullptr;
+        if (!a.S && a.collective && fast && !large) {
+            const int64_t n_dec = ceil_div(x->N, x->world);
+            const ScanPlan pd = plan_linear(x->M, kk, a.nq, std::max<int64_t>(n_dec, 1), x->num_sms, tables != nullptr);
+            const bool q16_glob = (pd.B == 8 || pd.B == 16) && pd.fast && q16_enabled() && q16_supported(kk) &&
+                                  n_dec >= q16_min_codes() && std::min<int64_t>(q16_sample(), n_dec / 4) >= 4 * kk;
+            if (q16_glob) {
+                KernelTimer tb(TK_BOUND, st);
+                const int64_t qs = ceil_div(a.nq, (int64_t)x->world), q_lo = std::min<int64_t>(a.nq, x->rank * qs);
+                const int64_t nloc = std::min<int64_t>(a.nq, q_lo + qs) - q_lo;
+                float *slice = sc.s_bound.get<float>((size_t)qs + 1);
+                float *all = sc.s_spart.get<float>((size_t)qs * x->world + 1);
+                launch_fill_f32(slice, qs, INFINITY, st);  // no bound: filter from +inf
+                const int64_t ns = std::min<int64_t>(q16_sample(), x->n_local / 4);
+                if (nloc > 0 && ns >= 4096 && kk <= 512) {
+                    uint8_t *samp = sc.s_samp.get<uint8_t>((size_t)ns * x->M);
+                    launch_strided_gather(codes, x->M, x->n_local / ns, ns, samp, st);
+                    launch_group_min_bound(samp, ns, x->M, tables + q_lo * lut_q_floats(x->M), nloc, kk, slice, st);
+                }
+                x->comm->allgather(slice, all, (size_t)qs * 4, st);
+                gthr_shared = all;
+                tr.mark("shared q16 bound");
+            }
+        }
         if (n_codes == 0) {
-            uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
+            uint64_t *pp = sc.s_part.get<uint64_t>((size_t)a.nq * kk);
             RII_CUDA(cudaMemsetAsync(pp, 0xff, (size_t)a.nq * kk * 8, st));
             parts = pp;
         } else if (large) {
             const int nc = large_linear_chunks(a.nq, n_codes, x->num_sms);
-            uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * nc * kk);
+            uint64_t *pp = sc.s_part.get<uint64_t>((size_t)a.nq * nc * kk);
             launch_large_linear(scan_codes, n_codes, x->M, tables, a.nq, kk, nc, pp, st);
             parts = pp;
             q_stride = (int64_t)nc * kk;
@@ -446,63 +579,46 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             nparts = nc;
         } else {
             ScanPlan pl = plan_linear(x->M, kk, a.nq, n_codes, x->num_sms, tables != nullptr);
-            // u16 fixed-point tables for long scans: the exact kk-th distance over a
-            // strided sample of the codes bounds each query's final kk-th distance
-            // (the sample is a subset), which scales the tables and seeds the filter.
-            // every CTA filters with, and publishes its kk-th distance into, gthr
-            float *gthr = x->s_gthr.get<float>(a.nq);
-            const int64_t ns = std::min<int64_t>(q16_sample(), n_codes / 4);
-            // Whole-database scans on several ranks share the bound pass: rank r bounds
-            // the queries of its slice from its own shard's sample (a subset of the
-            // database, so the bound holds globally) and the slices are all-gathered.
-            // The decision uses N / world so that every rank takes the same branch.
-            const bool shard_bound = !a.S && x->world > 1 && x->comm != nullptr;
-            const int64_t n_dec = shard_bound ? ceil_div(x->N, x->world) : n_codes;
-            const int64_t ns_dec = std::min<int64_t>(q16_sample(), n_dec / 4);
-            const bool q16 = (pl.B == 8 || pl.B == 16) && pl.fast && q16_enabled() && q16_supported(kk) && n_dec >= q16_min_codes() &&
-                             ns_dec >= 4 * kk && ns >= 4 * kk;
+            // u16 / u6 fixed-point tables for long scans: an upper bound on each query's
+            // final kk-th distance (the group minima of a strided sample of the codes --
+            // a subset) scales the tables and seeds the filter; every CTA filters with,
+            // and publishes its kk-th distance into, gthr.
+            float *gthr = gthr_shared;
+            bool q16;
+            if (gthr_shared) {
+                q16 = (pl.B == 8 || pl.B == 16) && pl.fast && q16_enabled() && q16_supported(kk);
+            } else {
+                gthr = sc.s_gthr.get<float>(a.nq);
+                const int64_t ns = std::min<int64_t>(q16_sample(), n_codes / 4);
+                q16 = (pl.B == 8 || pl.B == 16) && pl.fast && q16_enabled() && q16_supported(kk) &&
+                      n_codes >= q16_min_codes() && ns >= 4 * kk;
+                if (q16) {
+                    KernelTimer tb(TK_BOUND, st);
+                    const int64_t stride = n_codes / ns;
+                    uint8_t *samp = sc.s_samp.get<uint8_t>((size_t)ns * x->M);
+                    launch_strided_gather(scan_codes, x->M, stride, ns, samp, st);
+                    if (ns >= 4096 && kk <= 512 && !getenv("RII_BOUND_TOPK")) {
+                        // kk-th smallest of 1024 group minima (no top-k lists; k_scan.cu)
+                        launch_group_min_bound(samp, ns, x->M, tables, a.nq, kk, gthr, st);
+                    } else {
+                        // exact kk-th over the sample: one chunk per query batch
+                        ScanPlan ps = plan_linear(x->M, kk, a.nq, ns, x->num_sms, true, ns_chunks(), false);
+                        uint64_t *sp = sc.s_spart.get<uint64_t>((size_t)ps.nb * ps.B * ps.nc * kk);
+                        launch_linear_scan(ps, samp, ns, x->M, a.q, a.nq, cb, x->D, kk, sp, st, tables, nullptr, false,
+                                           -1);
+                        uint64_t *sk = sc.s_ckeys.get<uint64_t>((size_t)a.nq * kk);
+                        launch_merge(sp, (int64_t)ps.nc * kk, kk, ps.nc, a.nq, kk, kk, IdMap(), nullptr, nullptr, sk,
+                                     st);
+                        launch_kth_bound(sk, a.nq, kk, gthr, st);
+                    }
+                    tr.mark("q16 bound");
+                }
+            }
             if (!q16 && pl.B == 8 && lut_halves(x->M) > 1)  // M = 64 has no float B = 8 kernel
                 pl = plan_linear(x->M, kk, a.nq, n_codes, x->num_sms, tables != nullptr, 1 << 30, false);
-            if (!q16) {
-                if (pl.fast) launch_fill_f32(gthr, a.nq, INFINITY, st);
-                else gthr = nullptr;
-            } else {
-                KernelTimer tb(TK_BOUND, st);
-                const int64_t stride = n_codes / ns;
-                uint8_t *samp = x->s_samp.get<uint8_t>((size_t)ns * x->M);
-                launch_strided_gather(scan_codes, x->M, stride, ns, samp, st);
-                if (shard_bound) {
-                    const int64_t qs = ceil_div(a.nq, (int64_t)x->world), q_lo = std::min<int64_t>(a.nq, x->rank * qs);
-                    const int64_t nloc = std::min<int64_t>(a.nq, q_lo + qs) - q_lo;
-                    float *slice = x->s_bound.get<float>((size_t)qs + 1);
-                    float *all = x->s_spart.get<float>((size_t)qs * x->world + 1);
-                    launch_fill_f32(slice, qs, INFINITY, st);
-                    if (nloc > 0) {
-                        if (ns >= 4096 && kk <= 512)
-                            launch_group_min_bound(samp, ns, x->M, tables + q_lo * lut_q_floats(x->M), nloc, kk,
-                                                   slice, st);
-                        else
-                            launch_fill_f32(slice, nloc, INFINITY, st);  // no bound: filter from +inf
-                    }
-                    nccl_allgather_u8(x->comm, reinterpret_cast<const uint8_t *>(slice), reinterpret_cast<uint8_t *>(all),
-                                      (size_t)qs * 4, st);
-                    RII_CUDA(cudaMemcpyAsync(gthr, all, (size_t)a.nq * 4, cudaMemcpyDeviceToDevice, st));
-                } else if (ns >= 4096 && kk <= 512 && !getenv("RII_BOUND_TOPK")) {
-                    // kk-th smallest of 1024 group minima (no top-k lists; k_scan.cu)
-                    launch_group_min_bound(samp, ns, x->M, tables, a.nq, kk, gthr, st);
-                } else {
-                    // exact kk-th over the sample: one chunk per query batch
-                    ScanPlan ps = plan_linear(x->M, kk, a.nq, ns, x->num_sms, true, ns_chunks(), false);
-                    uint64_t *sp = x->s_spart.get<uint64_t>((size_t)ps.nb * ps.B * ps.nc * kk);
-                    launch_linear_scan(ps, samp, ns, x->M, a.q, a.nq, cb, x->D, kk, sp, st, tables, nullptr, false,
-                                       -1);
-                    uint64_t *sk = x->s_ckeys.get<uint64_t>((size_t)a.nq * kk);
-                    launch_merge(sp, (int64_t)ps.nc * kk, kk, ps.nc, a.nq, kk, kk, IdMap(), nullptr, nullptr, sk, st);
-                    launch_kth_bound(sk, a.nq, kk, gthr, st);
-                }
-                tr.mark("q16 bound");
-            }
-            uint64_t *pp = x->s_part.get<uint64_t>((size_t)pl.nb * pl.B * pl.nc * kk);
+            if (!pl.fast) gthr = nullptr;
+            else if (!q16 && !gthr_shared) launch_fill_f32(gthr, a.nq, INFINITY, st);
+            uint64_t *pp = sc.s_part.get<uint64_t>((size_t)pl.nb * pl.B * pl.nc * kk);
             launch_linear_scan(pl, scan_codes, n_codes, x->M, a.q, a.nq, cb, x->D, kk, pp, st, tables, gthr, q16);
             parts = pp;
             q_stride = (int64_t)pl.nc * kk;
@@ -512,22 +628,22 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
     } else if (x->ivf_mode == RII_IVF_PAPER) {  // Alg. 2 exactly as printed (mode B)
         const int64_t ns = a.S ? std::max<int64_t>(a.nS, 1) : x->N;
         const int64_t P = std::min<int64_t>(x->K, ceil_div(x->K * (int64_t)a.L, ns));  // ceil(KL/|S|)
-        int32_t *probes = x->s_probe.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
-        float *d0 = x->s_d0.get<float>((size_t)a.nq * x->K);
+        int32_t *probes = sc.s_probe.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
+        float *d0 = sc.s_d0.get<float>((size_t)a.nq * x->K);
         launch_coarse_dist(x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, d0, st);  // L2-L5
         launch_sorted_probes(d0, a.nq, x->K, P, probes, st);                                     // L6
         const int64_t *off = a.S ? t.roff : x->offsets.as<int64_t>();
         const uint32_t *ids = a.S ? t.rids : x->ids.as<uint32_t>();
-        int32_t *take = x->s_take.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
+        int32_t *take = sc.s_take.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
         launch_paper_takes(probes, a.nq, P, off, a.L, take, st);                                  // L14 cut
-        uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
+        uint64_t *pp = sc.s_part.get<uint64_t>((size_t)a.nq * kk);
         if (large) launch_large_ivf(codes, x->M, tables, a.nq, kk, probes, P, off, ids, take, pp, st);
         else launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st, tables, take);
         parts = pp;
     } else {  // Alg. 2, mode A (reading R2)
         const int64_t P = a.S ? std::min<int64_t>(x->K, ceil_div((int64_t)a.L * x->N, std::max<int64_t>(a.nS, 1)))
                               : std::min<int64_t>(a.L, x->K);  // P:492-502, R1
-        int32_t *probes = x->s_probe.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
+        int32_t *probes = sc.s_probe.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
         const int kkc = partial_width((int)std::min<int64_t>(P, 1024));
         if (P >= x->K) {
             launch_select_probes(nullptr, a.nq, x->K, P, probes, st);  // every list
@@ -535,13 +651,13 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             // coarse ranking (L2-L5) with the lane-rotated scan over the K centre codes,
             // canonical rescore, top-P by (d0, k) (L6)
             ScanPlan pc = plan_linear(x->M, kkc, a.nq, x->K, x->num_sms, tables != nullptr, 1 << 30, false);
-            uint64_t *cp = x->s_cpart.get<uint64_t>((size_t)pc.nb * pc.B * pc.nc * kkc);
+            uint64_t *cp = sc.s_cpart.get<uint64_t>((size_t)pc.nb * pc.B * pc.nc * kkc);
             launch_linear_scan(pc, x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, kkc, cp, st, tables);
-            uint64_t *ck = x->s_ckeys.get<uint64_t>((size_t)a.nq * kkc);
+            uint64_t *ck = sc.s_ckeys.get<uint64_t>((size_t)a.nq * kkc);
             launch_merge(cp, (int64_t)pc.nc * kkc, kkc, pc.nc, a.nq, kkc, (int)P, IdMap(), nullptr, nullptr, ck, st);
             launch_keys_to_probes(ck, a.nq, kkc, P, probes, st);
         } else {
-            float *d0 = x->s_d0.get<float>((size_t)a.nq * x->K);
+            float *d0 = sc.s_d0.get<float>((size_t)a.nq * x->K);
             launch_coarse_dist(x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, d0, st);
             launch_select_probes(d0, a.nq, x->K, P, probes, st);
         }
@@ -553,14 +669,16 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
         const int64_t n_cand = a.S ? std::max<int64_t>(t.n_loc, 1) : x->n_local;
         const double avg_len = (double)n_cand / (double)x->K;
         const int Bl = fast ? list_major_B(kk, avg_len, x->M) : 0;
-        bool list_major = Bl > 0 && avg_len >= 768.0 && (double)a.nq * P * kk * 8 <= 4e9 && (double)a.nq * P < 4e9;
+        // (items store the start of their query run in qlist as an int32: nq * P < 2^31)
+        const bool pairs_fit = (double)a.nq * P < 2147483647.0;
+        bool list_major = Bl > 0 && avg_len >= 768.0 && (double)a.nq * P * kk * 8 <= 4e9 && pairs_fit;
         if (const char *mode = getenv("RII_IVF_MODE")) {  // test / tuning override: "list" or "query"
-            if (!strcmp(mode, "list")) list_major = Bl > 0 && (double)a.nq * P < 4e9;
+            if (!strcmp(mode, "list")) list_major = Bl > 0 && pairs_fit;
             if (!strcmp(mode, "query")) list_major = false;
         }
         if (list_major) {
             const int64_t npairs = a.nq * P;
-            uint32_t *vals = x->s_lq.get<uint32_t>(npairs);
+            uint32_t *vals = sc.s_lq.get<uint32_t>(npairs);
             iota_u32_kernel<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(vals, npairs);
             RII_LAUNCHED();
             // Two phases (u16 tables): the pairs of the r0 nearest lists of every query run
@@ -588,13 +706,13 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             const int64_t nb = pb.n * x->K;
             const int32_t *keys = probes;
             if (q16l) {
-                int32_t *k2 = x->s_skey.get<int32_t>(npairs);
+                int32_t *k2 = sc.s_skey.get<int32_t>(npairs);
                 split_keys_kernel<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(probes, npairs, P, pb, x->K, k2);
                 RII_LAUNCHED();
                 keys = k2;
             }
-            int64_t *qoff = x->s_qoff.get<int64_t>(nb + 1);
-            uint32_t *qlist = x->s_ql.get<uint32_t>(npairs);
+            int64_t *qoff = sc.s_qoff.get<int64_t>(nb + 1);
+            uint32_t *qlist = sc.s_ql.get<uint32_t>(npairs);
             build_csr(keys, vals, npairs, nb, qoff, qlist, st);  // (query, rank) pairs grouped by list
             // RII_LIST_BOUND=1 (A/B knob): the ranks < r0 only publish a group-minimum
             // bound per query (list_bound_kernel) and the integer items cover every rank
@@ -603,7 +721,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             const bool lbound = q16l && pb.n == 2 && lbe && atoi(lbe) != 0;
             const int B0 = lbound ? list_bound_B(x->M) : Bl;
             const int64_t cap = npairs / std::min(B0, 8) + npairs / 8 + 2 * nb + 2;
-            int4 *items = x->s_items.get<int4>(cap);
+            int4 *items = sc.s_items.get<int4>(cap);
             tr.mark("pairs csr");
             int64_t n_ph_items[4] = {0, 0, 0, 0};
             n_ph_items[0] = build_list_items(qoff, x->K, B0, qlist, P, items, cap, st);
@@ -612,8 +730,8 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             const int64_t *qoff_i = qoff + x->K;
             const uint32_t *qlist_i = qlist;
             if (lbound) {  // integer items over all ranks: the unsplit (query, rank) CSR
-                int64_t *qoff2 = x->s_qoff2.get<int64_t>(x->K + 1);
-                uint32_t *ql2 = x->s_ql2.get<uint32_t>(npairs);
+                int64_t *qoff2 = sc.s_qoff2.get<int64_t>(x->K + 1);
+                uint32_t *ql2 = sc.s_ql2.get<uint32_t>(npairs);
                 build_csr(probes, vals, npairs, x->K, qoff2, ql2, st);
                 qoff_i = qoff2;
                 qlist_i = ql2;
@@ -624,8 +742,8 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
                 n_items += n_ph_items[ph];
             }
             tr.mark("items");
-            uint64_t *pp = x->s_part.get<uint64_t>((size_t)npairs * kk);
-            float *gthr = x->s_gthr.get<float>(a.nq);
+            uint64_t *pp = sc.s_part.get<uint64_t>((size_t)npairs * kk);
+            float *gthr = sc.s_gthr.get<float>(a.nq);
             launch_fill_f32(gthr, a.nq, INFINITY, st);
             tr.mark("alloc partials");
             ScanArgs sa{};
@@ -641,13 +759,13 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             for (int ph = 1; ph < pb.n; ++ph) {
                 if (n_ph_items[ph] == 0) continue;
                 tr.mark("list scan phase");
-                float *qsc = x->s_qscale.get<float>(a.nq);
+                float *qsc = sc.s_qscale.get<float>(a.nq);
                 if (list_u6_cfg(x->M) >= 3) {  // u6 oct items
-                    uint8_t *t8 = x->s_tab16.get<uint8_t>((size_t)a.nq * lut_q_floats(x->M));
+                    uint8_t *t8 = sc.s_tab16.get<uint8_t>((size_t)a.nq * lut_q_floats(x->M));
                     launch_u6_tables(tables, gthr, a.nq, x->M, t8, qsc, st);
                     sa.qtab8 = t8;
                 } else {
-                    uint16_t *t16 = x->s_tab16.get<uint16_t>((size_t)a.nq * LUT_Q_FLOATS);
+                    uint16_t *t16 = sc.s_tab16.get<uint16_t>((size_t)a.nq * LUT_Q_FLOATS);
                     launch_q16_tables(tables, gthr, a.nq, x->M, t16, qsc, st);
                     sa.qtab16 = t16;
                 }
@@ -667,7 +785,7 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
             p_stride = kk;
             nparts = (int)P;
         } else {
-            uint64_t *pp = x->s_part.get<uint64_t>((size_t)a.nq * kk);
+            uint64_t *pp = sc.s_part.get<uint64_t>((size_t)a.nq * kk);
             if (large) launch_large_ivf(codes, x->M, tables, a.nq, kk, probes, P, off, ids, nullptr, pp, st);
             else launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st, tables);
             parts = pp;
@@ -682,9 +800,9 @@ void search_batch(const rii_index *x, const QueryArgs &a, const Targets &t, cuda
 // 32 KB per query; partials).
 constexpr int64_t QBATCH = 16384;
 
-void search_local(const rii_index *x, const QueryArgs &a, cudaStream_t st, int64_t *out_ids, float *out_dist,
-                  uint64_t *out_keys) {
-    const Targets t = prepare_targets(x, a, st);
+void search_local(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cudaStream_t st, int64_t *out_ids,
+                  float *out_dist, uint64_t *out_keys) {
+    const Targets t = prepare_targets(x, sc, a, st);
     // IVF: smaller batches keep the batch's per-query tables (32 KB each) L2-resident
     // while the list-major items re-read them once per probed list.
     int64_t qb = QBATCH;
@@ -696,14 +814,14 @@ void search_local(const rii_index *x, const QueryArgs &a, cudaStream_t st, int64
         QueryArgs b = a;
         b.q = a.q + q0 * x->D;
         b.nq = std::min<int64_t>(qb, a.nq - q0);
-        search_batch(x, b, t, st, out_ids ? out_ids + q0 * a.topk : nullptr, out_dist ? out_dist + q0 * a.topk : nullptr,
+        search_batch(x, sc, b, t, st, out_ids ? out_ids + q0 * a.topk : nullptr, out_dist ? out_dist + q0 * a.topk : nullptr,
                      out_keys ? out_keys + q0 * a.kk : nullptr);
     }
 }
 
-void check_targets(const rii_index *x, const int64_t *S, int64_t nS, cudaStream_t st) {
+void check_targets(const rii_index *x, QueryScratch &sc, const int64_t *S, int64_t nS, cudaStream_t st) {
     if (!S || nS == 0) return;
-    int *flag = x->s_flag.get<int>(1);
+    int *flag = sc.s_flag.get<int>(1);
     RII_CUDA(cudaMemsetAsync(flag, 0, 4, st));
     launch_validate_targets(S, nS, x->N, flag, st);
     int h = 0;
@@ -728,7 +846,7 @@ void common_query_checks(const rii_index *x, int64_t nq, int topk, const int64_t
 
 extern "C" {
 
-const char *rii_last_error(void) { return t_err.c_str(); }
+const char *rii_last_error(const rii_index *) { return t_err.c_str(); }
 
 uint64_t rii_launch_count(void) { return g_launches.load(); }
 
@@ -749,6 +867,36 @@ rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *laun
     });
 }
 
+rii_status rii_debug_counters(int32_t enable) {
+    return guarded([&] {
+        int *d = g_dbg.load();
+        if (enable) {
+            if (!d) {
+                RII_CUDA(cudaMalloc(&d, DBG_COUNT * sizeof(int)));
+                g_dbg.store(d);
+            }
+            RII_CUDA(cudaMemset(d, 0, DBG_COUNT * sizeof(int)));
+            RII_CUDA(cudaDeviceSynchronize());
+        } else if (d) {
+            g_dbg.store(nullptr);
+            RII_CUDA(cudaDeviceSynchronize());
+            cudaFree(d);
+        }
+    });
+}
+
+rii_status rii_debug_counters_read(int64_t *out, int32_t n) {
+    return guarded([&] {
+        arg_check(out != nullptr && n >= 0, "bad arguments");
+        int h[DBG_COUNT] = {};
+        if (int *d = g_dbg.load()) {
+            RII_CUDA(cudaDeviceSynchronize());
+            RII_CUDA(cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost));
+        }
+        for (int i = 0; i < n; ++i) out[i] = i < DBG_COUNT ? h[i] : 0;
+    });
+}
+
 int32_t rii_partial_width(int32_t topk) { return partial_width(topk); }
 
 rii_status rii_shard_range(int64_t n, int32_t rank, int32_t world, int64_t *lo, int64_t *hi) {
@@ -766,8 +914,8 @@ rii_status rii_nccl_unique_id(void *out) {
     });
 }
 
-rii_status rii_create(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t rank, int32_t world,
-                      const void *nccl_id, rii_index **out) {
+static rii_status create_impl(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t rank, int32_t world,
+                              const void *nccl_id, const rii_transport *tr, rii_index **out) {
     if (out) *out = nullptr;
     return guarded([&] {
         arg_check(out != nullptr, "out is NULL");
@@ -788,7 +936,8 @@ rii_status rii_create(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t 
         x->rank = rank;
         x->world = world;
         RII_CUDA(cudaDeviceGetAttribute(&x->num_sms, cudaDevAttrMultiProcessorCount, device));
-        // keep memory freed by cudaFreeAsync cached in the pool (no re-mapping per call)
+        // keep memory freed by cudaFreeAsync cached in the pool (no re-mapping per call:
+        // every query allocates its scratch from it)
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
             uint64_t keep = UINT64_MAX;
@@ -796,7 +945,8 @@ rii_status rii_create(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t 
         }
         try {
             x->cb.get<float>((size_t)M * KS * x->ds);
-            if (world > 1 && nccl_id) x->comm = nccl_init(nccl_id, rank, world);
+            if (world > 1 && tr) x->comm = host_comm_create(*tr, rank, world);
+            else if (world > 1 && nccl_id) x->comm = nccl_comm_create(nccl_id, rank, world);
         } catch (...) {
             delete x;
             throw;
@@ -805,12 +955,25 @@ rii_status rii_create(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t 
     });
 }
 
+rii_status rii_create(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t rank, int32_t world,
+                      const void *nccl_id, rii_index **out) {
+    return create_impl(D, M, Ks, device, rank, world, nccl_id, nullptr, out);
+}
+
+rii_status rii_create_with_transport(int32_t D, int32_t M, int32_t Ks, int32_t device, int32_t rank, int32_t world,
+                                     const rii_transport *transport, rii_index **out) {
+    if (out) *out = nullptr;
+    if (!transport || !transport->allgather || world < 2)
+        return fail(RII_ERR_ARG, "rii_create_with_transport needs world > 1 and a transport with allgather");
+    return create_impl(D, M, Ks, device, rank, world, nullptr, transport, out);
+}
+
 void rii_destroy(rii_index *x) {
     if (!x) return;
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(x->device);
-    nccl_destroy(x->comm);
+    delete x->comm;
     delete x;
     if (prev >= 0) cudaSetDevice(prev);
 }
@@ -1025,7 +1188,7 @@ rii_status rii_reconfigure(rii_index *x, int32_t nlist, int32_t n_iter, uint64_t
                                                                                    X);
             RII_LAUNCHED();
         } else {
-            state_check(x->comm != nullptr, "multi-rank reconfigure needs an NCCL communicator");
+            state_check(x->comm != nullptr, "multi-rank reconfigure needs a communicator (NCCL id or transport)");
             // each rank contributes its ns smallest keys; the global ns smallest are
             // selected identically on every rank after an all-gather.
             const int64_t nl = std::min<int64_t>(x->n_local, ns);
@@ -1044,8 +1207,8 @@ rii_status rii_reconfigure(rii_index *x, int32_t nlist, int32_t n_iter, uint64_t
             }
             uint64_t *gkeys = gk.get<uint64_t>((size_t)ns * x->world);
             uint8_t *gcodes = gc.get<uint8_t>((size_t)ns * x->world * M);
-            nccl_allgather_u64(x->comm, keys, gkeys, (size_t)ns, st);
-            nccl_allgather_u8(x->comm, lcodes, gcodes, (size_t)ns * M, st);
+            x->comm->allgather(keys, gkeys, (size_t)ns * 8, st);
+            x->comm->allgather(lcodes, gcodes, (size_t)ns * M, st);
             const int64_t tot = ns * x->world;
             uint32_t *order = sv.get<uint32_t>(tot);
             sort_keys_with_index(gkeys, tot, order, st);
@@ -1086,43 +1249,44 @@ static rii_status query_impl(const rii_index *x, const float *q, int64_t nq, int
         if (path_used) *path_used = used;
         if (nq == 0) return;
         arg_check(q && (out_keys || (out_ids && out_dist)), "NULL argument");
+        state_check(out_keys || x->world == 1 || x->comm != nullptr,
+                    "detached shard (world > 1, no communicator): use rii_query_partial + rii_merge_partials");
+        QueryScratch sc(st);  // this call's own scratch (concurrent readers)
         const bool host = where == RII_MEM_HOST && !out_keys;
         const float *dq = q;
         const int64_t *dS = S;
         if (host) {
-            float *b = x->s_q.get<float>((size_t)nq * x->D);
+            float *b = sc.s_q.get<float>((size_t)nq * x->D);
             RII_CUDA(cudaMemcpyAsync(b, q, (size_t)nq * x->D * 4, cudaMemcpyHostToDevice, st));
             dq = b;
             if (S && nS > 0) {
-                int64_t *sb = x->s_gather.get<int64_t>(nS);
+                int64_t *sb = sc.s_gather.get<int64_t>(nS);
                 RII_CUDA(cudaMemcpyAsync(sb, S, (size_t)nS * 8, cudaMemcpyHostToDevice, st));
                 dS = sb;
             }
         }
-        check_targets(x, dS, S ? nS : 0, st);
-        dq = rotate_input(x, x->s_qrot, dq, nq, st);  // OPQ: "an input vector is first rotated"
-        QueryArgs a{dq, nq, topk, partial_width(topk), S ? dS : nullptr, S ? nS : 0, L, used};
-        if (S && nS == 0) {  // empty subset: nothing to return but padding
-            a.S = dS;
-        }
+        check_targets(x, sc, dS, S ? nS : 0, st);
+        dq = rotate_input(x, sc.s_qrot, dq, nq, st);  // OPQ: "an input vector is first rotated"
+        const bool collective = !out_keys && x->world > 1 && x->comm != nullptr;
+        QueryArgs a{dq, nq, topk, partial_width(topk), S ? dS : nullptr, S ? nS : 0, L, used, collective};
         int64_t *oid = out_ids;
         float *od = out_dist;
         if (host) {
-            oid = x->s_out_ids.get<int64_t>((size_t)nq * topk);
-            od = x->s_out_dist.get<float>((size_t)nq * topk);
+            oid = sc.s_out_ids.get<int64_t>((size_t)nq * topk);
+            od = sc.s_out_dist.get<float>((size_t)nq * topk);
         }
         if (out_keys) {
-            search_local(x, a, st, nullptr, nullptr, out_keys);
+            search_local(x, sc, a, st, nullptr, nullptr, out_keys);
         } else if (x->world == 1) {
-            search_local(x, a, st, oid, od, nullptr);
+            search_local(x, sc, a, st, oid, od, nullptr);
         } else {
-            state_check(x->comm != nullptr,
-                        "detached shard (world > 1, no NCCL id): use rii_query_partial + rii_merge_partials");
+            // the one exchange step: all-gather of every rank's top-kk
+            // keys (global ids), then the same merge on every rank
             const int kk = a.kk;
-            uint64_t *lk = x->s_keys.get<uint64_t>((size_t)nq * kk * (x->world + 1));
+            uint64_t *lk = sc.s_keys.get<uint64_t>((size_t)nq * kk * (x->world + 1));
             uint64_t *gk = lk + (size_t)nq * kk;
-            search_local(x, a, st, nullptr, nullptr, lk);
-            nccl_allgather_u64(x->comm, lk, gk, (size_t)nq * kk, st);
+            search_local(x, sc, a, st, nullptr, nullptr, lk);
+            x->comm->allgather(lk, gk, (size_t)nq * kk * 8, st);
             launch_merge(gk, kk, (int64_t)nq * kk, x->world, nq, kk, topk, IdMap(), oid, od, nullptr, st);
         }
         if (host) {
@@ -1245,23 +1409,56 @@ rii_status rii_save(const rii_index *x, const char *path) {
         arg_check(f != nullptr, "cannot open file for writing");
         FileW w{f};
         try {
-            w.put("RII1", 4);
-            w.val<uint32_t>(1);
-            for (uint32_t v : {(uint32_t)x->D, (uint32_t)x->M, (uint32_t)KS, (uint32_t)x->world, (uint32_t)x->rank,
-                               (uint32_t)x->ivf_mode, (uint32_t)((x->theta_fit ? 1 : 0) | (x->has_rot ? 2 : 0)),
-                               (uint32_t)x->segs.size()})
-                w.val(v);
-            for (int64_t v : {x->N, x->n_local, x->K, x->theta}) w.val(v);
-            w.val(x->fit_a);
-            w.val(x->fit_b);
-            if (x->has_rot) w.put(x->rot_host.data(), x->rot_host.size() * 4);  // flags bit 1: OPQ rotation
-            dev_to_file(w, x->cb.as<float>(), (size_t)x->M * KS * x->ds);
-            for (auto &sg : x->segs) { w.val(sg.local_off); w.val(sg.global_first); w.val(sg.count); }
-            dev_to_file(w, x->codes.as<uint8_t>(), (size_t)x->n_local * x->M);
-            if (x->K > 0) {
-                dev_to_file(w, x->centers.as<uint8_t>(), (size_t)x->K * x->M);
-                dev_to_file(w, x->offsets.as<int64_t>(), (size_t)x->K + 1);
-                dev_to_file(w, x->ids.as<uint32_t>(), (size_t)x->n_local);
+            if (x->world == 1) {
+                // SPEC's RII1 layout, bit for bit
+                w.put("RII1", 4);
+                const bool analytic = x->theta < 0 && !x->theta_fit;
+                for (uint32_t v : {1u, (uint32_t)x->D, (uint32_t)x->M, (uint32_t)KS, (uint32_t)x->N, (uint32_t)x->K})
+                    w.val(v);
+                w.val<uint64_t>(x->theta >= 0 ? (uint64_t)x->theta : 0);
+                w.val<uint32_t>(1);  // default_L
+                w.val<uint32_t>((x->has_rot ? 1u : 0u) | (analytic ? 2u : 0u));
+                dev_to_file(w, x->cb.as<float>(), (size_t)x->M * KS * x->ds);
+                if (x->has_rot) w.put(x->rot_host.data(), x->rot_host.size() * 4);
+                dev_to_file(w, x->codes.as<uint8_t>(), (size_t)x->n_local * x->M);
+                if (x->K > 0) {
+                    dev_to_file(w, x->centers.as<uint8_t>(), (size_t)x->K * x->M);
+                    std::vector<int64_t> off((size_t)x->K + 1);
+                    std::vector<uint32_t> ids((size_t)x->n_local);
+                    RII_CUDA(cudaMemcpy(off.data(), x->offsets.as<int64_t>(), off.size() * 8, cudaMemcpyDeviceToHost));
+                    if (x->n_local)
+                        RII_CUDA(cudaMemcpy(ids.data(), x->ids.as<uint32_t>(), ids.size() * 4, cudaMemcpyDeviceToHost));
+                    for (int64_t k = 0; k < x->K; ++k) {
+                        w.val<uint32_t>((uint32_t)(off[k + 1] - off[k]));
+                        w.put(ids.data() + off[k], (size_t)(off[k + 1] - off[k]) * 4);
+                    }
+                }
+                if (x->ivf_mode != 0 || x->theta_fit) {  // state SPEC has no field for
+                    w.put("RIIX", 4);
+                    w.val<uint32_t>((uint32_t)x->ivf_mode);
+                    w.val<uint32_t>(x->theta_fit ? 1u : 0u);
+                    w.val(x->fit_a);
+                    w.val(x->fit_b);
+                }
+            } else {
+                w.put("RIIS", 4);  // a shard of a world > 1 job: this library's own layout
+                w.val<uint32_t>(1);
+                for (uint32_t v : {(uint32_t)x->D, (uint32_t)x->M, (uint32_t)KS, (uint32_t)x->world, (uint32_t)x->rank,
+                                   (uint32_t)x->ivf_mode, (uint32_t)((x->theta_fit ? 1 : 0) | (x->has_rot ? 2 : 0)),
+                                   (uint32_t)x->segs.size()})
+                    w.val(v);
+                for (int64_t v : {x->N, x->n_local, x->K, x->theta}) w.val(v);
+                w.val(x->fit_a);
+                w.val(x->fit_b);
+                if (x->has_rot) w.put(x->rot_host.data(), x->rot_host.size() * 4);
+                dev_to_file(w, x->cb.as<float>(), (size_t)x->M * KS * x->ds);
+                for (auto &sg : x->segs) { w.val(sg.local_off); w.val(sg.global_first); w.val(sg.count); }
+                dev_to_file(w, x->codes.as<uint8_t>(), (size_t)x->n_local * x->M);
+                if (x->K > 0) {
+                    dev_to_file(w, x->centers.as<uint8_t>(), (size_t)x->K * x->M);
+                    dev_to_file(w, x->offsets.as<int64_t>(), (size_t)x->K + 1);
+                    dev_to_file(w, x->ids.as<uint32_t>(), (size_t)x->n_local);
+                }
             }
         } catch (...) {
             fclose(f);
@@ -1270,6 +1467,38 @@ rii_status rii_save(const rii_index *x, const char *path) {
         arg_check(fclose(f) == 0, "close failed");
     });
 }
+
+namespace {
+// Posting lists read from a file must be a partition of [0, n_local) into lists
+// with ascending ids (Eq. 4, R11) before anything indexes device memory with them.
+void check_postings(const std::vector<int64_t> &off, const std::vector<uint32_t> &ids, int64_t K, int64_t n_local) {
+    arg_check(off.size() == (size_t)K + 1 && off[0] == 0 && off[K] == n_local, "posting offsets do not span the codes");
+    std::vector<uint8_t> seen((size_t)n_local, 0);
+    for (int64_t k = 0; k < K; ++k) {
+        arg_check(off[k + 1] >= off[k], "posting offsets are not monotone");
+        for (int64_t p = off[k]; p < off[k + 1]; ++p) {
+            arg_check((int64_t)ids[p] < n_local, "posting id out of range");
+            arg_check(p == off[k] || ids[p] > ids[p - 1], "posting list not strictly ascending");
+            arg_check(!seen[ids[p]], "posting id listed twice");
+            seen[ids[p]] = 1;
+        }
+    }
+}
+
+void upload_postings(rii_index *x, const std::vector<int64_t> &off, const std::vector<uint32_t> &ids) {
+    const int64_t K = x->K, n = x->n_local;
+    RII_CUDA(cudaMemcpy(x->offsets.get<int64_t>((size_t)K + 1), off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+    uint32_t *dids = x->ids.get<uint32_t>((size_t)std::max<int64_t>(n, 1));
+    if (n) RII_CUDA(cudaMemcpy(dids, ids.data(), (size_t)n * 4, cudaMemcpyHostToDevice));
+    // a(n) is implied by W (Eq. 4): rebuilt on the device, not stored
+    int32_t *as = x->assign.get<int32_t>((size_t)std::max<int64_t>(n, 1));
+    if (K > 0 && n > 0) {
+        assign_from_csr_kernel<<<(unsigned)ceil_div(K, 64), 64>>>(x->offsets.as<int64_t>(), K, dids, as);
+        RII_LAUNCHED();
+        RII_CUDA(cudaDeviceSynchronize());
+    }
+}
+}  // namespace
 
 rii_status rii_load(const char *path, int32_t device, const void *nccl_id, rii_index **out) {
     if (out) *out = nullptr;
@@ -1282,63 +1511,122 @@ rii_status rii_load(const char *path, int32_t device, const void *nccl_id, rii_i
         try {
             char magic[4];
             r.get(magic, 4, "magic");
-            arg_check(memcmp(magic, "RII1", 4) == 0, "not an RII1 index file (bad magic)");
+            const bool spec = memcmp(magic, "RII1", 4) == 0, shard = memcmp(magic, "RIIS", 4) == 0;
+            arg_check(spec || shard, "not an index file (magic is neither RII1 nor RIIS)");
             arg_check(r.val<uint32_t>("version") == 1, "unsupported index file version");
-            const uint32_t D = r.val<uint32_t>("header"), M = r.val<uint32_t>("header"), Ks = r.val<uint32_t>("header");
-            const uint32_t world = r.val<uint32_t>("header"), rank = r.val<uint32_t>("header");
-            const uint32_t mode = r.val<uint32_t>("header"), flags = r.val<uint32_t>("header");
-            const uint32_t nseg = r.val<uint32_t>("header");
-            const int64_t N = r.val<int64_t>("header"), n_local = r.val<int64_t>("header");
-            const int64_t K = r.val<int64_t>("header"), theta = r.val<int64_t>("header");
-            const double fa = r.val<double>("header"), fb = r.val<double>("header");
-            arg_check(Ks == KS && M >= 1 && M <= 256 && D % M == 0 && D / M <= 64, "bad shape in header");
-            arg_check(world >= 1 && rank < world && n_local >= 0 && n_local <= N && K >= 0 && mode <= 1,
-                      "bad header");
-            const rii_status st = rii_create((int32_t)D, (int32_t)M, (int32_t)Ks, device, (int32_t)rank,
-                                             (int32_t)world, nccl_id, &x);
-            if (st != RII_OK) throw Error(st, t_err);
-            DeviceGuard g(device);
-            if (flags & 2u) {  // OPQ rotation
-                std::vector<float> R((size_t)D * D);
-                r.get(R.data(), R.size() * 4, "rotation");
-                const rii_status sr = rii_set_rotation(x, R.data());
-                if (sr != RII_OK) throw Error(sr, t_err);
-            }
-            file_to_dev(r, x->cb.as<float>(), (size_t)M * KS * (D / M), "code book");
-            x->trained = true;
-            for (uint32_t i = 0; i < nseg; ++i) {
-                Seg sg;
-                sg.local_off = r.val<int64_t>("segments");
-                sg.global_first = r.val<int64_t>("segments");
-                sg.count = r.val<int64_t>("segments");
-                x->segs.push_back(sg);
-            }
-            x->N = N;
-            x->n_local = n_local;
-            file_to_dev(r, x->codes.get<uint8_t>((size_t)std::max<int64_t>(n_local, 1) * M), (size_t)n_local * M,
-                        "codes");
-            x->K = K;
-            if (K > 0) {
-                file_to_dev(r, x->centers.get<uint8_t>((size_t)K * M), (size_t)K * M, "centres");
-                file_to_dev(r, x->offsets.get<int64_t>((size_t)K + 1), (size_t)K + 1, "posting offsets");
-                file_to_dev(r, x->ids.get<uint32_t>((size_t)std::max<int64_t>(n_local, 1)), (size_t)n_local,
-                            "posting ids");
-                // a(n) is implied by W (Eq. 4): rebuilt on the device, not stored
-                int32_t *as = x->assign.get<int32_t>((size_t)std::max<int64_t>(n_local, 1));
-                if (K > 0 && n_local > 0) {
-                    assign_from_csr_kernel<<<(unsigned)ceil_div(K, 64), 64>>>(x->offsets.as<int64_t>(), K,
-                                                                             x->ids.as<uint32_t>(), as);
-                    RII_LAUNCHED();
-                    RII_CUDA(cudaDeviceSynchronize());
+            if (spec) {  // SPEC's RII1 (single-GPU index)
+                const uint32_t D = r.val<uint32_t>("header"), M = r.val<uint32_t>("header"), Z = r.val<uint32_t>("header");
+                const uint32_t N = r.val<uint32_t>("header"), K = r.val<uint32_t>("header");
+                const uint64_t theta = r.val<uint64_t>("header");
+                r.val<uint32_t>("header");  // default_L (unused: L is a query argument)
+                const uint32_t flags = r.val<uint32_t>("header");
+                arg_check(Z == KS && M >= 1 && M <= 256 && D >= M && D % M == 0 && D / M <= 64, "bad shape in header");
+                arg_check((flags & ~3u) == 0 && K <= N && K < (1u << 31), "bad header");
+                arg_check(theta <= (uint64_t)INT64_MAX, "theta out of range");
+                const rii_status st = create_impl((int32_t)D, (int32_t)M, (int32_t)Z, device, 0, 1, nullptr, nullptr, &x);
+                if (st != RII_OK) throw Error(st, t_err);
+                DeviceGuard g(device);
+                file_to_dev(r, x->cb.as<float>(), (size_t)M * KS * (D / M), "code book");
+                if (flags & 1u) {  // OPQ rotation
+                    std::vector<float> R((size_t)D * D);
+                    r.get(R.data(), R.size() * 4, "rotation");
+                    const rii_status sr = rii_set_rotation(x, R.data());
+                    if (sr != RII_OK) throw Error(sr, t_err);
                 }
+                x->trained = true;
+                x->N = x->n_local = N;
+                file_to_dev(r, x->codes.get<uint8_t>((size_t)std::max<uint32_t>(N, 1) * M + 64), (size_t)N * M, "codes");
+                if (N) x->segs.push_back({0, 0, (int64_t)N});
+                x->K = K;
+                if (K > 0) {
+                    file_to_dev(r, x->centers.get<uint8_t>((size_t)K * M), (size_t)K * M, "centres");
+                    std::vector<int64_t> off((size_t)K + 1, 0);
+                    std::vector<uint32_t> ids((size_t)N);
+                    for (uint32_t k = 0; k < K; ++k) {
+                        const uint32_t len = r.val<uint32_t>("posting length");
+                        arg_check((uint64_t)off[k] + len <= N, "posting lists longer than N");
+                        off[k + 1] = off[k] + len;
+                        r.get(ids.data() + off[k], (size_t)len * 4, "posting ids");
+                    }
+                    check_postings(off, ids, K, N);
+                    upload_postings(x, off, ids);
+                }
+                x->theta = (flags & 2u) ? -1 : (int64_t)theta;
+                char ext[4];
+                const size_t got = fread(ext, 1, 4, f);
+                if (got == 4) {
+                    arg_check(memcmp(ext, "RIIX", 4) == 0, "trailing bytes after the index");
+                    const uint32_t mode = r.val<uint32_t>("extension"), fit = r.val<uint32_t>("extension");
+                    arg_check(mode <= 1 && fit <= 1, "bad extension block");
+                    x->ivf_mode = (int)mode;
+                    x->theta_fit = fit != 0;
+                    x->fit_a = r.val<double>("extension");
+                    x->fit_b = r.val<double>("extension");
+                } else {
+                    arg_check(got == 0, "trailing bytes after the index");
+                }
+            } else {  // RIIS: one shard of a world > 1 job
+                const uint32_t D = r.val<uint32_t>("header"), M = r.val<uint32_t>("header"), Ks = r.val<uint32_t>("header");
+                const uint32_t world = r.val<uint32_t>("header"), rank = r.val<uint32_t>("header");
+                const uint32_t mode = r.val<uint32_t>("header"), flags = r.val<uint32_t>("header");
+                const uint32_t nseg = r.val<uint32_t>("header");
+                const int64_t N = r.val<int64_t>("header"), n_local = r.val<int64_t>("header");
+                const int64_t K = r.val<int64_t>("header"), theta = r.val<int64_t>("header");
+                const double fa = r.val<double>("header"), fb = r.val<double>("header");
+                arg_check(Ks == KS && M >= 1 && M <= 256 && D >= M && D % M == 0 && D / M <= 64, "bad shape in header");
+                arg_check(world >= 1 && world <= 4096 && rank < world && (flags & ~3u) == 0 && mode <= 1, "bad header");
+                arg_check(N >= 0 && N < (1ll << 32) && n_local >= 0 && n_local <= N && K >= 0 && K <= N &&
+                              K < (1ll << 31) && theta >= -1,
+                          "bad header");
+                arg_check(nseg <= (uint64_t)n_local, "more segments than codes");
+                const rii_status st = create_impl((int32_t)D, (int32_t)M, (int32_t)Ks, device, (int32_t)rank,
+                                                  (int32_t)world, nccl_id, nullptr, &x);
+                if (st != RII_OK) throw Error(st, t_err);
+                DeviceGuard g(device);
+                if (flags & 2u) {  // OPQ rotation
+                    std::vector<float> R((size_t)D * D);
+                    r.get(R.data(), R.size() * 4, "rotation");
+                    const rii_status sr = rii_set_rotation(x, R.data());
+                    if (sr != RII_OK) throw Error(sr, t_err);
+                }
+                file_to_dev(r, x->cb.as<float>(), (size_t)M * KS * (D / M), "code book");
+                x->trained = true;
+                int64_t tiled = 0, prev_end = 0;
+                for (uint32_t i = 0; i < nseg; ++i) {  // segments tile [0, n_local), ascending global ranges
+                    Seg sg;
+                    sg.local_off = r.val<int64_t>("segments");
+                    sg.global_first = r.val<int64_t>("segments");
+                    sg.count = r.val<int64_t>("segments");
+                    arg_check(sg.local_off == tiled && sg.count > 0 && sg.global_first >= prev_end &&
+                                  sg.global_first + sg.count <= N,
+                              "segments do not tile the shard");
+                    tiled += sg.count;
+                    prev_end = sg.global_first + sg.count;
+                    x->segs.push_back(sg);
+                }
+                arg_check(tiled == n_local, "segments do not tile the shard");
+                x->N = N;
+                x->n_local = n_local;
+                file_to_dev(r, x->codes.get<uint8_t>((size_t)std::max<int64_t>(n_local, 1) * M + 64),
+                            (size_t)n_local * M, "codes");
+                x->K = K;
+                if (K > 0) {
+                    file_to_dev(r, x->centers.get<uint8_t>((size_t)K * M), (size_t)K * M, "centres");
+                    std::vector<int64_t> off((size_t)K + 1);
+                    std::vector<uint32_t> ids((size_t)n_local);
+                    r.get(off.data(), off.size() * 8, "posting offsets");
+                    r.get(ids.data(), ids.size() * 4, "posting ids");
+                    check_postings(off, ids, K, n_local);
+                    upload_postings(x, off, ids);
+                }
+                char extra;
+                arg_check(fread(&extra, 1, 1, f) == 0, "trailing bytes after the index");
+                x->theta = theta;
+                x->ivf_mode = (int)mode;
+                x->theta_fit = (flags & 1) != 0;
+                x->fit_a = fa;
+                x->fit_b = fb;
             }
-            char extra;
-            arg_check(fread(&extra, 1, 1, f) == 0, "trailing bytes after the index");
-            x->theta = theta;
-            x->ivf_mode = (int)mode;
-            x->theta_fit = (flags & 1) != 0;
-            x->fit_a = fa;
-            x->fit_b = fb;
             upload_segs(x, nullptr);
         } catch (...) {
             fclose(f);
@@ -1432,7 +1720,7 @@ rii_status rii_calibrate_theta(rii_index *x, const float *q, int64_t nq, int32_t
             if (x->world > 1 && x->comm) {
                 int64_t *d = kb.get<int64_t>(2);
                 RII_CUDA(cudaMemcpyAsync(d, &ns, 8, cudaMemcpyHostToDevice, st));
-                nccl_allreduce_max_i64(x->comm, d, d + 1, 1, st);
+                x->comm->allreduce_max_i64(d, d + 1, 1, st);
                 RII_CUDA(cudaMemcpyAsync(&mx, d + 1, 8, cudaMemcpyDeviceToHost, st));
                 RII_CUDA(cudaStreamSynchronize(st));
             }

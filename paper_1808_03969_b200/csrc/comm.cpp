@@ -1,14 +1,18 @@
-// comm.cpp -- NCCL over NVLink 5 / NVSwitch for the one real exchange step of the
-// path (merge of per-GPU top-k lists, and the reconfigure sample).  NCCL is
-// loaded lazily with dlopen so the library (and its CPU-side tests) load on
-// machines without NCCL or a GPU; world == 1 never touches it.
+// comm.cpp -- the one real exchange step of the multi-GPU path (merge of per-GPU
+// top-k lists, the shared u6 bound of a whole-database scan, the reconfigure
+// sample): NCCL over NVLink 5 / NVSwitch, or a caller-supplied host transport
+// (rii_create_with_transport; e.g. torch.distributed gloo in the multi-process
+// tests).  NCCL is loaded lazily with dlopen so the library (and its CPU-side
+// tests) load on machines without NCCL or a GPU; world == 1 never touches it.
 #include "comm.hpp"
 
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
+#include <vector>
 
 namespace rii {
 
@@ -64,29 +68,78 @@ void nccl_unique_id(void *out128) {
     memcpy(out128, &id, sizeof(id));
 }
 
-void *nccl_init(const void *id128, int rank, int world) {
+namespace {
+// NCCL over NVLink 5 / NVSwitch: device buffers, enqueued on the caller's stream.
+struct NcclComm final : Comm {
+    ncclComm_t comm = nullptr;
+    ~NcclComm() override {
+        if (comm && g_api.h) g_api.CommDestroy(comm);
+    }
+    void allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) override {
+        check(api().AllGather(send, recv, bytes, ncclUint8, comm, st), "ncclAllGather");
+    }
+    void allreduce_max_i64(const int64_t *send, int64_t *recv, size_t count, cudaStream_t st) override {
+        check(api().AllReduce(send, recv, count, ncclInt64, ncclMax, comm, st), "ncclAllReduce");
+    }
+};
+
+// Caller-supplied host transport (rii_transport): the device block is staged
+// through host memory around the callback.  The stream is synchronised first, so
+// no kernel of this rank ever waits on another rank's kernels.
+struct HostComm final : Comm {
+    rii_transport t{};
+    void allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) override {
+        std::vector<uint8_t> hs(bytes ? bytes : 1), hr(bytes * (size_t)world + 1);
+        if (cudaMemcpyAsync(hs.data(), send, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            throw Error(4, "host transport: device-to-host staging failed");
+        if (t.allgather(t.ctx, hs.data(), hr.data(), (uint64_t)bytes) != 0)
+            throw Error(5, "host transport: allgather callback failed");
+        if (cudaMemcpyAsync(recv, hr.data(), bytes * (size_t)world, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            throw Error(4, "host transport: host-to-device staging failed");
+    }
+    void allreduce_max_i64(const int64_t *send, int64_t *recv, size_t count, cudaStream_t st) override {
+        std::vector<int64_t> all(count * (size_t)world + 1), h(count + 1);
+        int64_t *tmp = nullptr;
+        if (cudaMallocAsync(&tmp, count * (size_t)world * 8 + 8, st) != cudaSuccess) throw Error(3, "host transport");
+        allgather(send, tmp, count * 8, st);
+        cudaMemcpyAsync(all.data(), tmp, count * (size_t)world * 8, cudaMemcpyDeviceToHost, st);
+        cudaFreeAsync(tmp, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) throw Error(4, "host transport: reduce staging failed");
+        for (size_t i = 0; i < count; ++i) {
+            h[i] = all[i];
+            for (int r = 1; r < world; ++r) h[i] = std::max(h[i], all[(size_t)r * count + i]);
+        }
+        if (cudaMemcpyAsync(recv, h.data(), count * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            throw Error(4, "host transport: host-to-device staging failed");
+    }
+};
+}  // namespace
+
+Comm *nccl_comm_create(const void *id128, int rank, int world) {
     ncclUniqueId id;
     memcpy(&id, id128, sizeof(id));
-    ncclComm_t comm = nullptr;
-    check(api().CommInitRank(&comm, world, id, rank), "ncclCommInitRank");
-    return comm;
+    auto *c = new NcclComm();
+    c->rank = rank;
+    c->world = world;
+    try {
+        check(api().CommInitRank(&c->comm, world, id, rank), "ncclCommInitRank");
+    } catch (...) {
+        delete c;
+        throw;
+    }
+    return c;
 }
 
-void nccl_destroy(void *comm) {
-    if (comm && g_api.h) g_api.CommDestroy(reinterpret_cast<ncclComm_t>(comm));
-}
-
-void nccl_allgather_u64(void *comm, const uint64_t *send, uint64_t *recv, size_t count, cudaStream_t st) {
-    check(api().AllGather(send, recv, count, ncclUint64, reinterpret_cast<ncclComm_t>(comm), st), "ncclAllGather");
-}
-
-void nccl_allgather_u8(void *comm, const uint8_t *send, uint8_t *recv, size_t count, cudaStream_t st) {
-    check(api().AllGather(send, recv, count, ncclUint8, reinterpret_cast<ncclComm_t>(comm), st), "ncclAllGather");
-}
-
-void nccl_allreduce_max_i64(void *comm, const int64_t *send, int64_t *recv, size_t count, cudaStream_t st) {
-    check(api().AllReduce(send, recv, count, ncclInt64, ncclMax, reinterpret_cast<ncclComm_t>(comm), st),
-          "ncclAllReduce");
+Comm *host_comm_create(const rii_transport &t, int rank, int world) {
+    if (!t.allgather) throw Error(1, "rii_transport.allgather is NULL");
+    auto *c = new HostComm();
+    c->t = t;
+    c->rank = rank;
+    c->world = world;
+    return c;
 }
 
 }  // namespace rii

@@ -65,6 +65,15 @@ __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
 // (scratch: 32 ints -- [0] compaction max, [1] overflow flag, [2, 2 + B) fill snapshot, [31] rescale flag)
 __host__ __device__ constexpr int smem_aux_bytes(int B, int kk) { return B * (kk + NEWCAP) * 8 + B * 8 + 128 + B * 16; }
 
+// Window-end read of a query's shared bound (another CTA's published kk-th distance
+// tightens this CTA's filter mid-chunk); counted when it lowers the bound.
+__device__ __forceinline__ void gqs_update(float *gqs, int qq, float g, int *dbg) {
+    if (g < gqs[qq]) {
+        gqs[qq] = g;
+        if (dbg) atomicAdd(dbg + DBG_GTHR_TIGHTEN, 1);
+    }
+}
+
 // TAB: 0 = fp32 pair tables, 1 = bf16-packed quad tables, 2 = u16 fixed-point quad
 // tables (integer SWAR sums, linear mode with a per-query bound).
 template <int M, int B, bool LISTS, int NTH, int U, int TAB, int VARIANT = 0>
@@ -313,6 +322,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                     }
                 }
                 scratch[31] = f;
+                if (f && a.dbg) atomicAdd(a.dbg + DBG_RESCALE, 1);
             }
             __syncthreads();
             if (scratch[31]) {
@@ -527,8 +537,10 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             base += STEP;
         }
         if (ovf) *s_ovf = 1;
+        if (a.dbg && tid == 0) atomicAdd(a.dbg + DBG_WINDOWS, 1);
         if (__syncthreads_or(ovf || need)) {
             const bool rolled = *s_ovf != 0;  // written before the barrier; reset below
+            if (a.dbg && tid == 0) atomicAdd(a.dbg + (rolled ? DBG_ROLLBACK : DBG_COMPACT), 1);
             if (rolled && tid < B) cnt[tid] = s_cnt0[tid];
             __syncthreads();
             rescore_fresh();
@@ -536,7 +548,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             if (tid == 0) *s_ovf = 0;
             if (tid < B) s_cnt0[tid] = 0;
             if (a.gthr) {
-                if (tid < B) gqs[tid] = fminf(gqs[tid], __ldcg(a.gthr + query_of(tid)));
+                if (tid < B) gqs_update(gqs, tid, __ldcg(a.gthr + query_of(tid)), a.dbg);
                 __syncthreads();
             }
 #pragma unroll
@@ -552,7 +564,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         } else {
             if (tid < B) s_cnt0[tid] = cnt[tid];
             if (a.gthr) {
-                if (tid < B) gqs[tid] = fminf(gqs[tid], __ldcg(a.gthr + query_of(tid)));
+                if (tid < B) gqs_update(gqs, tid, __ldcg(a.gthr + query_of(tid)), a.dbg);
                 __syncthreads();
 #pragma unroll
                 for (int qq = 0; qq < B; ++qq) th[qq] = fminf(th[qq], relax(gqs[qq]));
@@ -569,7 +581,8 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     if (a.gthr) {  // publish this item's kk-th distance as a bound for the query
         if (tid < nqi && thr[tid] < __int_as_float(0x7f800000)) {
             const float bound = __fmul_ru(thr[tid], 1.00001f);
-            atomicMin(reinterpret_cast<int *>(a.gthr + query_of(tid)), __float_as_int(bound));
+            const int old = atomicMin(reinterpret_cast<int *>(a.gthr + query_of(tid)), __float_as_int(bound));
+            if (a.dbg && __float_as_int(bound) < old) atomicAdd(a.dbg + DBG_PUBLISH, 1);
         }
     }
 
@@ -762,6 +775,15 @@ ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bo
     p.nc = bnc;
     p.chunk = ceil_div(n_codes, bnc);
     if (p.chunk < 1) p.chunk = 1;
+    // Test knob (multi-window parity tests): a fixed chunk length, so that one CTA
+    // scans many barrier windows and chunks end at different times.
+    if (const char *e = getenv("RII_CHUNK_CODES")) {
+        const int64_t c = atoll(e);
+        if (c > 0 && c < n_codes) {
+            p.chunk = c;
+            p.nc = (int)ceil_div(n_codes, c);
+        }
+    }
     return p;
 }
 #endif  // !RII_SCAN_M
@@ -911,6 +933,7 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
     a.nb = pl.nb; a.chunk = pl.chunk; a.nc = pl.nc; a.out = out; a.tables = tables;
     a.gthr = gthr;
     a.one = 1;
+    a.dbg = debug_counters();
     void *args[] = {&a};
     KernelTimer t(timer, st), tp(B >= 8 && timer == TK_LINEAR ? (q16 ? (q16_is_u6(M) ? TK_U6 : TK_Q16) : TK_PACKED) : -1,
                                  st);
@@ -967,6 +990,7 @@ static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st, b
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ScanArgs aa = a;
     aa.one = 1;
+    aa.dbg = debug_counters();
     void *args[] = {&aa};
     KernelTimer t(TK_IVF, st);
     const int nth = q16 ? list_q16_nth(M) : (B == 8 ? PACKED_NTH : scan_threads());

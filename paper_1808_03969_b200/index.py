@@ -76,6 +76,20 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     return lo.value, hi.value
 
 
+DEBUG_COUNTERS = ("windows", "compactions", "rollbacks", "gthr_tightenings", "rescales", "publishes")
+
+
+def debug_counters(enable: bool) -> None:
+    """Start (clear) or stop the scan kernels' diagnostic event counters."""
+    _rl.check(_rl.load().rii_debug_counters(1 if enable else 0))
+
+
+def read_debug_counters() -> dict:
+    out = (C.c_int64 * len(DEBUG_COUNTERS))()
+    _rl.check(_rl.load().rii_debug_counters_read(out, len(DEBUG_COUNTERS)))
+    return dict(zip(DEBUG_COUNTERS, (int(v) for v in out)))
+
+
 def launch_count() -> int:
     return int(_rl.load().rii_launch_count())
 
@@ -84,11 +98,45 @@ def partial_width(topk: int) -> int:
     return int(_rl.load().rii_partial_width(topk))
 
 
+def torch_allgather(group=None):
+    """A host all-gather over torch.distributed (e.g. the gloo backend) for
+    Index(..., transport=...): maps this rank's bytes to every rank's bytes."""
+    def allgather(send: np.ndarray) -> np.ndarray:
+        torch = _torch()
+        import torch.distributed as dist
+        world = dist.get_world_size(group)
+        t = torch.from_numpy(send)
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t, group=group)
+        return torch.cat(out).numpy()
+    return allgather
+
+
+def _transport(fn, world: int):
+    """struct rii_transport whose callback marshals host bytes through fn."""
+    def cb(ctx, send, recv, nbytes):
+        try:
+            src = np.ctypeslib.as_array((C.c_uint8 * max(int(nbytes), 1)).from_address(send))[:nbytes].copy()
+            out = np.ascontiguousarray(fn(src), dtype=np.uint8)
+            if out.size != world * nbytes:
+                return 1
+            C.memmove(recv, out.ctypes.data, out.size)
+            return 0
+        except Exception:  # reported to the library as a failed exchange (RII_ERR_NCCL)
+            return 1
+    fp = _rl.TRANSPORT_FN(cb)
+    return _rl.Transport(None, fp), fp
+
+
 class Index:
-    """Rii index (Sec. 4.1) on one GPU, or one shard of a multi-GPU job."""
+    """Rii index (Sec. 4.1) on one GPU, or one shard of a multi-GPU job.
+
+    world > 1: pass the NCCL id (nccl_id, from nccl_unique_id() on rank 0) or a host
+    all-gather (transport=fn, fn(bytes of this rank) -> bytes of all ranks, e.g.
+    torch_allgather() over gloo); with neither the index is a detached shard."""
 
     def __init__(self, D: int, M: int, Ks: int = 256, device: int | None = None, rank: int = 0, world: int = 1,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, transport=None):
         self._lib = _rl.load()
         if device is None:
             try:
@@ -97,11 +145,16 @@ class Index:
                 device = 0
         self.D, self.M, self.Ks, self.device, self.rank, self.world = D, M, Ks, device, rank, world
         h = C.c_void_p()
-        idbuf = None
-        if nccl_id is not None:
-            idbuf = (C.c_uint8 * _rl.NCCL_ID_BYTES).from_buffer_copy(nccl_id)
-        _rl.check(self._lib.rii_create(D, M, Ks, device, rank, world,
-                                     C.cast(idbuf, C.c_void_p) if idbuf is not None else None, C.byref(h)))
+        if transport is not None:
+            self._tr, self._tr_fn = _transport(transport, world)  # kept alive with the index
+            _rl.check(self._lib.rii_create_with_transport(D, M, Ks, device, rank, world, C.byref(self._tr),
+                                                          C.byref(h)))
+        else:
+            idbuf = None
+            if nccl_id is not None:
+                idbuf = (C.c_uint8 * _rl.NCCL_ID_BYTES).from_buffer_copy(nccl_id)
+            _rl.check(self._lib.rii_create(D, M, Ks, device, rank, world,
+                                         C.cast(idbuf, C.c_void_p) if idbuf is not None else None, C.byref(h)))
         self._h = h
 
     def close(self):
@@ -238,12 +291,12 @@ class Index:
         return out
 
     def save(self, path: str):
-        """Write this rank's shard as an RII1 file (include/rii.h)."""
+        """Write the index (SPEC's RII1 layout) or this rank's shard (RIIS), include/rii.h."""
         _rl.check(self._lib.rii_save(self._h, os.fsencode(path)))
 
     @classmethod
     def load(cls, path: str, device: int | None = None, nccl_id: bytes | None = None) -> "Index":
-        """Create an index from an RII1 file written by save()."""
+        """Create an index from an RII1 / RIIS file written by save()."""
         lib = _rl.load()
         if device is None:
             try:
@@ -258,7 +311,11 @@ class Index:
         self._lib, self._h, self.device = lib, h, device
         with open(path, "rb") as f:
             hdr = np.frombuffer(f.read(40), dtype="<u4")
-        self.D, self.M, self.Ks, self.world, self.rank = (int(v) for v in hdr[2:7])
+        if bytes(hdr[:1].tobytes()) == b"RII1":  # SPEC layout: D, M, Z, N, K (single GPU)
+            self.D, self.M, self.Ks = (int(v) for v in hdr[2:5])
+            self.world, self.rank = 1, 0
+        else:  # RIIS shard: D, M, Ks, world, rank
+            self.D, self.M, self.Ks, self.world, self.rank = (int(v) for v in hdr[2:7])
         return self
 
     def set_centers(self, centers):

@@ -47,7 +47,7 @@ def test_host_only_calls(lib):
     assert lib.rii_partial_width(1000) == 1024
     assert lib.rii_partial_width(1024) == 2048
     assert isinstance(lib.rii_launch_count(), int)
-    assert lib.rii_last_error() == b""
+    assert lib.rii_last_error(None) == b""
 
 
 def test_no_device_is_an_error_not_a_fallback(lib):
@@ -59,7 +59,7 @@ def test_no_device_is_an_error_not_a_fallback(lib):
     h = C.c_void_p()
     st = lib.rii_create(32, 4, 256, 0, 0, 1, None, C.byref(h))
     assert st == _lib.RII_ERR_CUDA and not h.value
-    assert b"CUDA" in lib.rii_last_error()
+    assert b"CUDA" in lib.rii_last_error(None)
     # argument errors are reported before any device work
     assert lib.rii_create(30, 4, 256, 0, 0, 1, None, C.byref(h)) == _lib.RII_ERR_ARG
     assert lib.rii_create(32, 4, 16, 0, 0, 1, None, C.byref(h)) == _lib.RII_ERR_ARG

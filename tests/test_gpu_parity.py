@@ -55,7 +55,9 @@ def test_tiny_config_end_to_end(rii, ref):
     x = gen.gaussian(c["N"], c["D"], seed=0)
     q = gen.gaussian(c["nq"], c["D"], seed=0, stream=gen.STREAM_QUERY)
     S = gen.subset(c["N"], 1000, seed=0)
+    ref.reseed_reset()
     g, o = _build_pair(rii, ref, x, c["M"], c["nlist"], n_iter=10, train_iter=20)
+    assert ref.reseed_counts()[1] >= 1  # the bit-exact state check covers a PQk-means re-seed (R9)
     _check_state(g, o)
     for path in ("linear", "ivf", "auto"):
         for sub in (None, S):
@@ -233,22 +235,30 @@ def test_add_after_reconfigure_and_growth(rii, ref):
     """Data addition with K > 0 then reconfigure again (config 4 in small)."""
     x = gen.sift_like(12_000, 128, seed=13)
     q = gen.sift_like(12, 128, seed=13, stream=gen.STREAM_QUERY)
+    ref.reseed_reset()
     g, o = _build_pair(rii, ref, x[:2_000], 16, 20, n_iter=3, train_rows=x[:2_000], train_iter=3)
+    assert ref.reseed_counts()[0] >= 1  # training re-seeds (R8) inside the bit-exact code-book check
+    _check_state(g, o)
     for s in range(2_000, 12_000, 3_333):
         g.add(x[s:s + 3_333])
         o.add(x[s:s + 3_333])
     _check_state(g, o)
     for L in (1, 5):
         assert_topk_parity(ref, o.cb, o.codes, q, g.query(q, 20, L=L, path="ivf"), o.query(q, 20, L=L, path=2))
+    ref.reseed_reset()
     g.reconfigure(110, n_iter=3, seed=4)
     o.reconfigure(110, n_iter=3, seed=4)
+    assert ref.reseed_counts()[1] >= 1  # PQk-means re-seeds (R9) inside the bit-exact centre check
     _check_state(g, o)
     assert_topk_parity(ref, o.cb, o.codes, q, g.query(q, 20, L=2, path="ivf"), o.query(q, 20, L=2, path=2))
 
 
-def test_logical_shards_equal_single_index(rii, ref):
+def test_logical_shards_equal_single_index(rii, ref, tmp_path):
     """Id-range sharding on one GPU: two detached shards, per-shard
-    partial top-k, merge -> identical to the single index (C-PIN10)."""
+    partial top-k, merge -> the oracle's result on the whole database (C-PIN10) and
+    identical to the single index; each shard survives save / load (RIIS layout,
+    validated: a corrupted posting offset is rejected)."""
+    import struct
     import torch
     x = gen.deep_like(20_001, 96, seed=17)
     q = gen.deep_like(33, 96, seed=17, stream=gen.STREAM_QUERY)
@@ -260,17 +270,47 @@ def test_logical_shards_equal_single_index(rii, ref):
         s.set_codebook(cb)
         for a in range(0, 20_001, 7_000):      # several add batches -> several id ranges per shard
             s.add(x[a:a + 7_000])
+        s.add(x[:0])
         shards.append(s)
     qt = torch.from_numpy(q).cuda()
     S = gen.subset(20_001, 5_000, seed=3)
     for sub in (None, S):
         parts = torch.stack([s.query_partial(qt, 50, target_ids=sub, path="linear")[0] for s in shards])
         ids, dist = rii.merge_partials(parts, 50)
+        ids, dist = ids.cpu().numpy(), dist.cpu().numpy()
         ref_ids, ref_d, _ = single.query(q, 50, target_ids=sub, path="linear")
-        assert np.array_equal(ids.cpu().numpy(), ref_ids) and np.array_equal(dist.cpu().numpy(), ref_d)
+        assert np.array_equal(ids, ref_ids) and np.array_equal(dist, ref_d)
+        assert_topk_parity(ref, o.cb, o.codes, q, (ids, dist), o.query(q, 50, S=sub, path=1), S=sub, what="shards")
     with pytest.raises(rii.RiiError) as e:
         shards[0].query(q, 5)
     assert e.value.status == 2
+    # shard persistence (RIIS): reload both shards, same partials
+    for s in shards:
+        s.set_centers(ref.reconfigure(o.cb, o.codes, 16, 2, 0)[0])
+    loaded = []
+    for r, s in enumerate(shards):
+        p = str(tmp_path / f"s{r}.rii")
+        s.save(p)
+        raw = open(p, "rb").read()
+        assert raw[:4] == b"RIIS"
+        loaded.append(rii.Index.load(p))
+        assert loaded[-1].info() == s.info() and (loaded[-1].rank, loaded[-1].world) == (r, 2)
+        # corrupt the first posting offset (must be 0)
+        nseg = struct.unpack_from("<I", raw, 36)[0]
+        n_local, K = struct.unpack_from("<qq", raw, 48)
+        off0 = 88 + 256 * 96 * 4 + 24 * nseg + n_local * 32 + K * 32
+        assert struct.unpack_from("<q", raw, off0)[0] == 0
+        bad = bytearray(raw)
+        struct.pack_into("<q", bad, off0, 7)
+        (tmp_path / "bad.rii").write_bytes(bytes(bad))
+        with pytest.raises(rii.RiiError) as e:
+            rii.Index.load(str(tmp_path / "bad.rii"))
+        assert e.value.status == 1
+    for sub in (None, S):
+        for path, L in (("linear", 1), ("ivf", 3)):
+            a = [s.query_partial(qt, 50, target_ids=sub, L=L, path=path)[0] for s in shards]
+            b = [s.query_partial(qt, 50, target_ids=sub, L=L, path=path)[0] for s in loaded]
+            assert all(torch.equal(u, v) for u, v in zip(a, b))
 
 
 def test_theta_calibration(rii, ref):
@@ -348,10 +388,40 @@ def test_assignment_paths_large_k(rii, ref, M, K):
     assert np.array_equal(off, want_off) and np.array_equal(ids, want_ids)
 
 
+def _parse_spec_rii1(raw):
+    """SPEC's persistence layout, read independently of the library."""
+    import struct
+    assert raw[:4] == b"RII1"
+    version, D, M, Z, N, K = struct.unpack_from("<6I", raw, 4)
+    theta, = struct.unpack_from("<Q", raw, 28)
+    default_L, flags = struct.unpack_from("<2I", raw, 36)
+    o = 44
+    cb = np.frombuffer(raw, "<f4", M * Z * (D // M), o).reshape(M, Z, D // M)
+    o += cb.nbytes
+    R = None
+    if flags & 1:
+        R = np.frombuffer(raw, "<f4", D * D, o).reshape(D, D)
+        o += R.nbytes
+    codes = np.frombuffer(raw, np.uint8, N * M, o).reshape(N, M)
+    o += codes.nbytes
+    centers = np.frombuffer(raw, np.uint8, K * M, o).reshape(K, M)
+    o += centers.nbytes
+    lists = []
+    for _ in range(K):
+        n, = struct.unpack_from("<I", raw, o)
+        lists.append(np.frombuffer(raw, "<u4", n, o + 4).astype(np.int64))
+        o += 4 + 4 * n
+    return dict(version=version, D=D, M=M, Z=Z, N=N, K=K, theta=theta, default_L=default_L, flags=flags, cb=cb,
+                R=R, codes=codes, centers=centers, lists=lists, end=o)
+
+
 def test_save_load_roundtrip(rii, ref, tmp_path):
-    """Persistence: load(save(idx)) answers identically; save -> load ->
-    save is byte-identical; the payload is (N+K)M + 4N bytes plus header,
-    code book and list offsets; malformed files are rejected."""
+    """Persistence: a single-GPU index is written in SPEC's RII1 layout bit
+    for bit (parsed here independently); load(save(idx)) answers identically; save ->
+    load -> save is byte-identical; the payload is (N+K)M + 4N (+4K list lengths)
+    bytes plus header and code book; malformed files (truncated, bad magic,
+    corrupted posting lists) are rejected before anything reaches the device."""
+    import struct
     N, D, M, K = 20_000, 128, 16, 64
     x = gen.sift_like(N, D, seed=51)
     q = gen.sift_like(17, D, seed=51, stream=gen.STREAM_QUERY)
@@ -362,26 +432,50 @@ def test_save_load_roundtrip(rii, ref, tmp_path):
     g.set_theta(4321)
     p1, p2 = str(tmp_path / "a.rii"), str(tmp_path / "b.rii")
     g.save(p1)
+    raw = open(p1, "rb").read()
+    f = _parse_spec_rii1(raw)
+    assert (f["version"], f["D"], f["M"], f["Z"], f["N"], f["K"], f["theta"], f["flags"]) == (1, D, M, 256, N, K, 4321, 0)
+    assert f["end"] == len(raw)  # no extension block: ivf_mode 0, theta not fitted
+    assert np.array_equal(f["cb"], g.get_codebook()) and np.array_equal(f["codes"], g.get_codes())
+    assert np.array_equal(f["centers"], g.get_centers())
+    off, ids = g.get_postings()
+    assert all(np.array_equal(f["lists"][k], ids[off[k]:off[k + 1]]) for k in range(K))
+    assert len(raw) == 44 + 256 * D * 4 + (N + K) * M + 4 * N + 4 * K
     h = rii.Index.load(p1)
     assert h.info() == g.info()
     for path, L, S in (("linear", 1, None), ("ivf", 3, None), ("auto", 2, gen.subset(N, 4000, seed=1))):
         a, b = g.query(q, 20, S, L=L, path=path), h.query(q, 20, S, L=L, path=path)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
     h.save(p2)
-    assert open(p1, "rb").read() == open(p2, "rb").read()
-    import os
-    header = 4 + 4 * 9 + 8 * 4 + 8 * 2 + 3 * 8          # magic, u32 fields, i64 fields, fit a/b, one segment
-    assert os.path.getsize(p1) == header + 256 * D * 4 + (N + K) * M + 4 * N + 8 * (K + 1)
-    raw = open(p1, "rb").read()
-    (tmp_path / "t.rii").write_bytes(raw[:-10])
-    (tmp_path / "m.rii").write_bytes(b"XXXX" + raw[4:])
-    for bad in ("t.rii", "m.rii"):
+    assert open(p2, "rb").read() == raw
+    # analytic theta (flags bit 1) and the extension block (paper-mode Alg. 2)
+    g.set_theta(-1)
+    g.set_ivf_mode("paper")
+    g.save(p1)
+    raw2 = open(p1, "rb").read()
+    f2 = _parse_spec_rii1(raw2)
+    assert f2["flags"] == 2 and f2["theta"] == 0 and raw2[f2["end"]:f2["end"] + 4] == b"RIIX"
+    h2 = rii.Index.load(p1)
+    assert h2.info()["theta"] == -1
+    a, b = g.query(q, 20, L=300, path="ivf"), h2.query(q, 20, L=300, path="ivf")
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    # malformed files
+    lists0 = 44 + 256 * D * 4 + (N + K) * M     # first posting list: u32 length, then ids
+    n0, = struct.unpack_from("<I", raw, lists0)
+    bad = {"t.rii": raw[:-10], "m.rii": b"XXXX" + raw[4:], "x.rii": raw + b"\0"}
+    r = bytearray(raw); struct.pack_into("<I", r, lists0 + 4, N + 5); bad["range.rii"] = bytes(r)       # id >= N
+    r = bytearray(raw); struct.pack_into("<I", r, lists0 + 8, struct.unpack_from("<I", raw, lists0 + 4)[0])
+    bad["dup.rii"] = bytes(r)                                                                             # repeated id
+    r = bytearray(raw); struct.pack_into("<I", r, lists0, n0 + 1); bad["len.rii"] = bytes(r)            # lengths != N
+    r = bytearray(raw); struct.pack_into("<I", r, 8, 100); bad["shape.rii"] = bytes(r)                    # D % M != 0
+    for name, data in bad.items():
+        (tmp_path / name).write_bytes(data)
         with pytest.raises(rii.RiiError) as e:
-            rii.Index.load(str(tmp_path / bad))
-        assert e.value.status == 1
+            rii.Index.load(str(tmp_path / name))
+        assert e.value.status == 1, name
 
 
-# ------------------------------------------------- u16 fixed-point tables ---
+# ------------------------------------------------- u16 fixed-point tables ---# ------------------------------------------------- u16 fixed-point tables ---
 @pytest.mark.parametrize("kind,N,D,M,nq,topk", [("deep", 40_009, 96, 32, 45, 100), ("sift", 33_333, 128, 16, 19, 64),
                                                 ("sift", 30_011, 128, 64, 21, 100),  # two table halves
                                                 ("deep", 20_011, 96, 8, 23, 10), ("gaussian", 17_003, 32, 4, 9, 100)])

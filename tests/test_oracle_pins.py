@@ -480,3 +480,73 @@ def test_rotated_index_is_pq_on_rotated_data(ref):
     assert np.array_equal(a.codes, b.codes) and np.array_equal(a.cb, b.cb)
     ra, rb = a.query(q, 7, path=ref.PATH_LINEAR), b.query(ref.rotate(Q, q), 7, path=ref.PATH_LINEAR)
     assert np.array_equal(ra[0], rb[0]) and np.array_equal(ra[1], rb[1])
+
+
+# ------------------------------------------------ empty-cluster re-seeding ---
+def test_train_reseed_worked_example(ref):
+    """R8 / SPEC S:138 ("empty clusters re-seeded from the farthest point"): a hand-
+    traced 1-D Lloyd run (tests/golden/train_reseed_worked_example.txt) in which a
+    code word loses all its rows in iteration 2 and is re-seeded with the unused
+    row of largest assignment distance.  The instrumented oracle shows the branch
+    ran exactly once; the other plausible readings give other code books."""
+    rows = {r[0]: [float(v) for v in r[1:]] for r in _rows("train_reseed_worked_example.txt")}
+    x = np.array(rows["rows"], np.float32)[:, None]
+    Z, seed, n_iter = int(rows["Z"][0]), int(rows["seed"][0]), int(rows["n_iter"][0])
+    init = ref.train(x, 1, 0, seed, Z=Z)
+    assert init[0, :, 0].tolist() == rows["init"]
+    ref.reseed_reset()
+    cb = ref.train(x, 1, n_iter, seed, Z=Z)
+    assert ref.reseed_counts() == (1, 0)
+    assert cb[0, :, 0].tolist() == np.array(rows["result"], np.float32).tolist()
+    ref.reseed_reset()
+    ref.train(x, 1, 1, seed, Z=Z)  # one iteration: nothing is empty yet
+    assert ref.reseed_counts() == (0, 0)
+
+
+def test_pqkmeans_reseed_worked_example(ref):
+    """R9 / SPEC S:273 ("empty clusters re-seeded with the member of the largest
+    cluster farthest from its center"): a hand-traced PQk-means run on symbols
+    placed on a line (tests/golden/pqkmeans_reseed_worked_example.txt).  Cluster 1
+    empties in iteration 1; the largest cluster is a tie (lowest k wins) and its
+    farthest members tie (lowest sample index wins).  The instrumented oracle
+    shows the branch ran once; other readings give other centres."""
+    rows = {r[0]: [float(v) for v in r[1:]] for r in _rows("pqkmeans_reseed_worked_example.txt")}
+    p = np.array(rows["positions"], np.float64)
+    T = ((p[:, None] - p[None, :]) ** 2).astype(np.float32)[None]
+    X = np.array(rows["sample"], np.uint8)[:, None]
+    K, n_iter = int(rows["K"][0]), int(rows["n_iter"][0])
+    ref.reseed_reset()
+    C, obj = ref.pqkmeans(T, X, K, n_iter)
+    assert ref.reseed_counts() == (0, 1)
+    assert C[:, 0].tolist() == [int(v) for v in rows["result"]]
+    ref.reseed_reset()
+    ref.pqkmeans(T, X, K, 1)  # re-seeding after the first update only: nothing is empty yet
+    assert ref.reseed_counts() == (0, 0)
+
+
+def test_reseed_branches_run_at_config_scale(ref):
+    """The re-seeding branches are not only reachable on hand-made inputs: the tiny
+    config's build (BASELINE configs[0]: 20 Lloyd iterations, reconfigure to 100
+    lists) re-seeds one PQk-means cluster, and the small growth build of
+    tests/test_gpu_parity.py (test_add_after_reconfigure_and_growth) re-seeds two
+    training code words and six PQk-means clusters -- the GPU tests compare those
+    builds' code books and centres bit for bit, so the GPU's re-seeding is checked
+    against the pinned rule."""
+    c = gen.CONFIGS["tiny"]
+    x = gen.gaussian(c["N"], c["D"], seed=0)
+    ref.reseed_reset()
+    o = ref.OracleIndex(c["D"], c["M"])
+    o.train(x, n_iter=20, seed=0)
+    o.add(x)
+    o.reconfigure(c["nlist"], n_iter=10, seed=0)
+    assert ref.reseed_counts() == (0, 1)
+    x = gen.sift_like(12_000, 128, seed=13)
+    ref.reseed_reset()
+    o = ref.OracleIndex(128, 16)
+    o.train(x[:2_000], n_iter=3, seed=0)
+    o.add(x[:2_000])
+    o.reconfigure(20, n_iter=3, seed=0)
+    for s in range(2_000, 12_000, 3_333):
+        o.add(x[s:s + 3_333])
+    o.reconfigure(110, n_iter=3, seed=4)
+    assert ref.reseed_counts() == (2, 6)

@@ -38,6 +38,52 @@ SMS = 148
 LUT_LOOKUPS_PER_CLK_PER_SM = 32  # one conflict-free LDS.32 wavefront (128 B) per clock per SM
 
 
+def _source_hash():
+    """sha256[:16] of the scan kernel's sources (k_scan.cu, lut.cuh, topk.cuh,
+    kernels.cuh, common.cuh): ties a committed ncu traffic number to the code it
+    was measured on (the GPU box has no .git)."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in ("k_scan.cu", "lut.cuh", "topk.cuh", "kernels.cuh", "common.cuh"):
+        with open(os.path.join(ROOT, "paper_1808_03969_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def _host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count()
+    return {"nproc": n, "cpu_model": model}
+
+
+def _traffic(kernel_kind):
+    """DRAM bytes per launch of the headline kernel from the committed ncu --set full
+    capture (profiles/scan_traffic.json), with its provenance; null when the capture
+    was taken on other kernel sources than the ones this run built."""
+    tp = os.path.join(ROOT, "profiles", "scan_traffic.json")
+    if not os.path.exists(tp):
+        return None, {"file": None}
+    with open(tp) as f:
+        d = json.load(f)
+    src = _source_hash()
+    prov = {"file": "profiles/scan_traffic.json", "captured_on_source": d.get("source_sha16"),
+            "this_source": src, "commit": d.get("commit"), "capture": d.get("source"), "kernel": d.get("kernel")}
+    if d.get("source_sha16") != src or d.get("kernel_kind") != kernel_kind:
+        return None, dict(prov, note="capture does not match the built kernel sources: traffic unmeasured")
+    return d.get("dram_bytes_per_launch"), prov
+
+
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -274,11 +320,7 @@ def run_ours(args, rank, world, local):
     lut_peak = SMS * per_clk * sm_max * 1e6  # lookups/s
     lookups = nq * n_local * M
     achieved = lookups / (kernel_ms / 1e3)
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_scan_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+    traffic, traffic_src = _traffic("u6" if u6 else "u16" if q16 else "packed" if packed else "fp32")
     roofline = {
         "bound": "alu",
         "kernel": (f"scan_fast_kernel<32,{16 if os.environ.get('RII_Q16_CFG', '9') == '9' else 8},u6> (linear ADC "
@@ -288,7 +330,7 @@ def run_ours(args, rank, world, local):
                    "scan_fast_kernel<32,8,packed> (linear ADC scan + top-k, bf16-packed tables + exact rescore)"
                    if packed else "scan_fast_kernel<32,6> (linear ADC scan + top-k, fp32 tables)"),
         "achieved": achieved / 1e9, "peak": lut_peak / 1e9, "unit": "Glookup/s",
-        "frac": achieved / lut_peak, "traffic": traffic,
+        "frac": achieved / lut_peak, "traffic": traffic, "traffic_provenance": traffic_src,
         "peak_basis": f"shared-memory LUT pipe: one 128-B wavefront/clk/SM = {per_clk} "
                       f"{'u6 (1 B)' if u6 else 'u16 (2 B)' if q16 else 'bf16-packed (2 B)' if packed else 'fp32 (4 B)'} "
                       f"lookups/clk/SM x {SMS} SMs x "
@@ -392,21 +434,32 @@ def _oracle_sample(workload):
     return ref, idx, q, n
 
 
-def cpu_baseline(workload, budget_s=12.0):
+def cpu_baseline(workload, budget_s=8.0):
+    """The oracle as it stands, timed twice on this host: one thread (the paper's
+    protocol) and every core (queries split over threads, each running the
+    single-threaded C oracle; SURVEY 8(d) "two numbers").  `value` is the all-cores
+    number."""
     ref, idx, q, n = _oracle_sample(workload)
     kind, N, D, M, nlist, nq, topk, n_train, label = WORKLOADS[workload]
-    done, t0 = 0, time.perf_counter()
-    while time.perf_counter() - t0 < budget_s:
-        s = done % len(q)
-        ref.linear(idx.cb, idx.codes, q[s:s + 8], topk)
-        done += 8
-    dt = time.perf_counter() - t0
-    qps_sample = done / dt
-    return {"value": qps_sample * n / N, "unit": "queries/s", "cores": 1, "kind": "oracle",
-            "sample": f"{done} queries of Alg. 1 (whole scan, top-{topk}) over {n} codes drawn with the workload's "
-                      f"generator (oracle-built index), single thread; queries/s scaled by {n}/{N} to the full "
-                      f"database (cost O(M N), Table 1)",
-            "measured_qps_on_sample": qps_sample}
+    host = _host_info()
+    threads = ref.cores()
+
+    def run(nthreads, batch):
+        done, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < budget_s:
+            s = done % len(q)
+            ref.linear_mt(idx.cb, idx.codes, q[s:s + batch], topk, threads=nthreads)
+            done += batch
+        return done / (time.perf_counter() - t0)
+
+    qps1 = run(1, 8)
+    qpsn = run(threads, 4 * threads)
+    return {"value": qpsn * n / N, "unit": "queries/s", "cores": threads, "kind": "oracle",
+            "sample": f"Alg. 1 (whole scan, top-{topk}) over {n} codes drawn with the workload's generator "
+                      f"(oracle-built index), {budget_s:.0f} s per measurement; queries/s scaled by {n}/{N} to the "
+                      f"full database (cost O(M N), Table 1); value = all {threads} threads (queries split over "
+                      f"threads), single_thread = the paper's one-thread protocol (P:757)",
+            "single_thread": qps1 * n / N, "measured_qps_on_sample": qpsn, "host": host}
 
 
 def run_reference(args, rank, world):
@@ -414,11 +467,12 @@ def run_reference(args, rank, world):
         return
     ref, idx, q, n = _oracle_sample(args.workload)
     kind, N, D, M, nlist, nq, topk, n_train, label = WORKLOADS[args.workload]
-    per_step = 32
+    threads = ref.cores()
+    per_step = 4 * threads
 
     def step(i):
         s = (i * per_step) % len(q)
-        ref.linear(idx.cb, idx.codes, q[s:s + per_step], topk)
+        ref.linear_mt(idx.cb, idx.codes, q[s:s + per_step], topk, threads=threads)
 
     for i in range(args.warmup):
         step(i)
@@ -432,9 +486,11 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.workload}: {label}", "N": N, "D": D, "M": M, "nq": nq, "topk": topk,
                        "path": "linear (Alg. 1, S = whole database)"},
-            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": threads, "kind": "oracle",
                              "sample": f"each step {per_step} queries of Alg. 1 over {n} oracle-built codes of the "
-                                       f"workload's generator, single thread, scaled by {n}/{N} (cost O(M N))"},
+                                       f"workload's generator, split over {threads} threads (the single-threaded "
+                                       f"C oracle per slice), scaled by {n}/{N} (cost O(M N))",
+                             "host": _host_info()},
             "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

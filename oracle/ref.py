@@ -374,3 +374,48 @@ class OracleIndex:
     def memory_bytes(self):
         """Theoretical footprint (N+K) M log2 Z + 32 N bits in bytes, Z = 256."""
         return self.codes.nbytes + self.centers.nbytes + 4 * self.N
+
+
+# ------------------------------------------------------------- all cores ---
+def cores() -> int:
+    """Host threads available to this process."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def parallel_rows(fn, rows, *args, threads=None, **kw):
+    """Run the single-threaded oracle function fn(..., rows_slice, ...) on contiguous
+    slices of `rows` (queries, or vectors to encode) in a thread pool and
+    concatenate the results along axis 0.  The C oracle releases the GIL (ctypes),
+    so the slices run on separate cores; every slice computes exactly what the
+    single call would (the oracle has no cross-row state).  `rows` is passed as the
+    argument named by fn's signature position: fn(rows_slice, *args, **kw)."""
+    import concurrent.futures as cf
+    threads = threads or cores()
+    n = len(rows)
+    if n == 0 or threads <= 1:
+        return fn(rows, *args, **kw)
+    bounds = np.linspace(0, n, min(threads * 4, n) + 1).astype(int)
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        parts = list(ex.map(lambda ab: fn(rows[ab[0]:ab[1]], *args, **kw), zip(bounds[:-1], bounds[1:])))
+    if isinstance(parts[0], tuple):
+        return tuple(np.concatenate([p[i] for p in parts]) for i in range(len(parts[0])))
+    return np.concatenate(parts)
+
+
+def encode_mt(cb, x, M, threads=None):
+    return parallel_rows(lambda xs: encode(cb, xs, M), x, threads=threads)
+
+
+def linear_mt(cb, codes, q, topk, S=None, threads=None):
+    return parallel_rows(lambda qs: linear(cb, codes, qs, topk, S=S), q, threads=threads)
+
+
+def ivf_mt(cb, codes, centers, offsets, ids_csr, q, topk, L, S=None, threads=None):
+    return parallel_rows(lambda qs: ivf(cb, codes, centers, offsets, ids_csr, qs, topk, L, S=S), q, threads=threads)
+
+
+def assign_mt(T, codes, centers, threads=None):
+    return parallel_rows(lambda cs: assign(T, cs, centers), codes, threads=threads)

@@ -138,7 +138,7 @@ struct QueryScratch {
         s_probe{&st}, s_roff{&st}, s_rids{&st}, s_rkey{&st}, s_rval{&st}, s_out_ids{&st}, s_out_dist{&st},
         s_flag{&st}, s_lq{&st}, s_qoff{&st}, s_ql{&st}, s_qoff2{&st}, s_ql2{&st}, s_items{&st}, s_gthr{&st},
         s_tables{&st}, s_cpart{&st}, s_ckeys{&st}, s_take{&st}, s_samp{&st}, s_spart{&st}, s_bound{&st},
-        s_skey{&st}, s_tab16{&st}, s_qscale{&st}, s_qrot{&st}, s_route{&st};
+        s_skey{&st}, s_tab16{&st}, s_qscale{&st}, s_qrot{&st}, s_route{&st}, s_rmirror{&st};
     explicit QueryScratch(cudaStream_t s) : st(s) {}
 };
 
@@ -161,6 +161,7 @@ struct rii_index {
     Buf seg_local, seg_global, seg_count;
     int64_t K = 0;
     Buf centers, offsets, ids;
+    Buf mirror;  // codes in posting-list order: mirror[p] = codes[ids[p]] (list-major IVF scans)
     int64_t theta = -1;
     int ivf_mode = 0;        // RII_IVF_LISTS / RII_IVF_PAPER
     bool theta_fit = false;  // rii_calibrate_theta result in use (theta(L) = fit_a * L + fit_b)
@@ -283,7 +284,21 @@ __global__ void widen_ids_kernel(const uint32_t *src, int64_t n, IdMap map, int6
 __global__ void gather_u32pos_codes_kernel(const uint8_t *codes, int M, const uint32_t *pos, int64_t n, uint8_t *out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    for (int m = 0; m < M; ++m) out[i * M + m] = codes[(int64_t)pos[i] * M + m];
+    if ((M & 3) == 0) {
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(codes + (int64_t)pos[i] * M);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(out + i * M);
+        for (int m = 0; m < M / 4; ++m) dst[m] = __ldg(src + m);
+    } else {
+        for (int m = 0; m < M; ++m) out[i * M + m] = codes[(int64_t)pos[i] * M + m];
+    }
+}
+
+// out[p] = codes[ids[p]] for the n positions of a CSR: the codes in posting-list order
+// (list-major IVF reads a list as one contiguous range).
+void build_mirror(const uint8_t *codes, int M, const uint32_t *ids, int64_t n, uint8_t *out, cudaStream_t st) {
+    if (n <= 0) return;
+    gather_u32pos_codes_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(codes, M, ids, n, out);
+    RII_LAUNCHED();
 }
 
 void rebuild_csr(rii_index *x, cudaStream_t st) {
@@ -295,6 +310,8 @@ void rebuild_csr(rii_index *x, cudaStream_t st) {
     int64_t *off = x->offsets.get<int64_t>(x->K + 1);
     uint32_t *ids = x->ids.get<uint32_t>(x->n_local + 1);
     build_csr(x->assign.as<int32_t>(), vals, x->n_local, x->K, off, ids, st);
+    build_mirror(x->codes.as<uint8_t>(), x->M, ids, x->n_local,
+                 x->mirror.get<uint8_t>((size_t)std::max<int64_t>(x->n_local, 1) * x->M + 64), st);
 }
 
 // Rows [lo, hi) of this rank in a batch of n rows split into `world` chunks.
@@ -447,6 +464,7 @@ struct Targets {
     const uint8_t *sub_codes = nullptr;     // linear path
     const int64_t *roff = nullptr;          // IVF path
     const uint32_t *rids = nullptr;
+    const uint8_t *rmirror = nullptr;       // codes of the restricted lists in list order
 };
 
 Targets prepare_targets(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cudaStream_t st) {
@@ -470,6 +488,9 @@ Targets prepare_targets(const rii_index *x, QueryScratch &sc, const QueryArgs &a
         build_csr(rk, rv, t.n_loc, x->K, roff, rids, st);
         t.roff = roff;
         t.rids = rids;
+        uint8_t *rm = sc.s_rmirror.get<uint8_t>((size_t)std::max<int64_t>(t.n_loc, 1) * x->M + 64);
+        build_mirror(x->codes.as<uint8_t>(), x->M, rids, t.n_loc, rm, st);
+        t.rmirror = rm;
     }
     return t;
 }
@@ -746,8 +767,11 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             float *gthr = sc.s_gthr.get<float>(a.nq);
             launch_fill_f32(gthr, a.nq, INFINITY, st);
             tr.mark("alloc partials");
+            // items stream their list as a contiguous range of the list-ordered mirror;
+            // keys carry mirror positions, mapped to ids through the CSR in the merge
+            const uint8_t *lcodes = a.S ? t.rmirror : x->mirror.as<uint8_t>();
             ScanArgs sa{};
-            sa.codes = codes; sa.q = a.q; sa.nq = a.nq; sa.cb = cb; sa.ds = x->ds; sa.kk = kk; sa.out = pp;
+            sa.codes = lcodes; sa.q = a.q; sa.nq = a.nq; sa.cb = cb; sa.ds = x->ds; sa.kk = kk; sa.out = pp;
             sa.items = items; sa.qlist = qlist; sa.P = P; sa.offsets = off; sa.ids = ids; sa.gthr = gthr;
             sa.tables = tables;
             if (lbound)
@@ -777,10 +801,11 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             tr.mark("list scan");
             parts = pp;
             if (Bl != 8 && !lbound) {  // fp32-pair items keep lane-rotated keys: rescore in the merge
-                rs.codes = codes;
+                rs.codes = lcodes;
                 rs.tables = tables;
                 rs.M = x->M;
             }
+            map.pre = ids;
             q_stride = P * kk;
             p_stride = kk;
             nparts = (int)P;
@@ -1495,8 +1520,10 @@ void upload_postings(rii_index *x, const std::vector<int64_t> &off, const std::v
     if (K > 0 && n > 0) {
         assign_from_csr_kernel<<<(unsigned)ceil_div(K, 64), 64>>>(x->offsets.as<int64_t>(), K, dids, as);
         RII_LAUNCHED();
-        RII_CUDA(cudaDeviceSynchronize());
     }
+    build_mirror(x->codes.as<uint8_t>(), x->M, dids, n, x->mirror.get<uint8_t>((size_t)std::max<int64_t>(n, 1) * x->M + 64),
+                 nullptr);
+    RII_CUDA(cudaDeviceSynchronize());
 }
 }  // namespace
 

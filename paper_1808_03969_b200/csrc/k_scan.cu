@@ -401,19 +401,11 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     static_assert(NEWCAP >= STEP, "a single step must fit the fresh buffer");
     int *s_ovf = scratch + 1, *s_cnt0 = scratch + 2;  // flags, fill snapshot at the window start
     uint32_t w[U][W];
-    uint32_t cid[U];  // candidate id: position in `codes` (linear) or the list's id (lists)
-    // List mode: the posting-list ids are prefetched one step ahead of the codes they
-    // address (idn = ids of step b), so the two dependent loads overlap across steps.
-    uint32_t idn[U];
-    auto load_ids = [&](int64_t b) {
-        if constexpr (LISTS) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int64_t p = b + u * NTH + tid;
-                idn[u] = p < c1 ? __ldg(a.ids + p) : 0u;
-            }
-        }
-    };
+    // candidate id: position in `codes` -- the linear array (linear mode) or the
+    // list-ordered mirror of the codes (list mode: a posting list is the contiguous
+    // range [offsets[k], offsets[k+1]) of the mirror, read with the same coalesced
+    // loads as a linear chunk; the merge maps positions to ids through the CSR)
+    uint32_t cid[U];
     auto load_step = [&](int64_t b, uint32_t(&dst)[U][W], uint32_t(&did)[U]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -422,15 +414,12 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             for (int i = 0; i < W; ++i) dst[u][i] = 0;
             did[u] = 0;
             if (p < c1) {
-                if constexpr (LISTS) did[u] = idn[u];
-                else did[u] = (uint32_t)p;
-                load_code<W>(codes + (size_t)did[u] * M, dst[u]);
+                did[u] = (uint32_t)p;
+                load_code<W>(codes + (size_t)p * M, dst[u]);
             }
         }
-        load_ids(b + STEP);
     };
     int64_t base = c0;
-    load_ids(base);
     load_step(base, w, cid);
     int safe = 0;
     while (base < c1) {
@@ -556,7 +545,6 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             set_thq();
             if (rolled) {
                 base = wstart;
-                load_ids(base);
                 load_step(base, w, cid);
                 safe = 4;
                 continue;

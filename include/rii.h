@@ -94,7 +94,10 @@ rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *laun
  * distance tightened), [2] overflowing windows rolled back, [3] window-end reads
  * of the shared per-query bound that lowered it (another CTA's published kk-th,
  * i.e. mid-chunk tightening), [4] integer-table re-quantisations at a tighter
- * bound, [5] bound publications (atomicMin) that lowered the shared bound. */
+ * bound, [5] bound publications (atomicMin) that lowered the shared bound, [6]
+ * candidates pushed past the filter (counted at compactions), [7..9] SM cycles of
+ * thread 0 per CTA in table fill / scan loop / final compaction + output (summed),
+ * [10] CTAs counted. */
 rii_status rii_debug_counters(int32_t enable);
 rii_status rii_debug_counters_read(int64_t *out, int32_t n);
 

@@ -24,8 +24,8 @@ namespace rii {
 std::atomic<uint64_t> g_launches{0};
 
 // rii_debug_counters: device event counters of the scan kernels (common.cuh)
-std::atomic<int *> g_dbg{nullptr};
-int *debug_counters() { return g_dbg.load(std::memory_order_relaxed); }
+std::atomic<unsigned long long *> g_dbg{nullptr};
+unsigned long long *debug_counters() { return g_dbg.load(std::memory_order_relaxed); }
 
 namespace timing {
 std::mutex g_tmu;
@@ -254,7 +254,7 @@ __global__ void iota_u32_kernel(uint32_t *v, int64_t n) {
 // List-major phase split: pair (q, r) goes to bucket ph * K + probes[q][r], ph = the
 // phase whose rank range [rb[ph], rb[ph + 1]) holds r (phase 0: float tables; later
 // phases: integer tables re-quantised at the bounds the earlier phases published).
-struct PhaseBounds { int64_t rb[5]; int n; };
+struct PhaseBounds { int64_t rb[8]; int n; };
 __global__ void split_keys_kernel(const int32_t *probes, int64_t npairs, int64_t P, PhaseBounds pb, int64_t K,
                                   int32_t *keys) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -263,6 +263,18 @@ __global__ void split_keys_kernel(const int32_t *probes, int64_t npairs, int64_t
     int ph = 0;
     while (ph + 1 < pb.n && r >= pb.rb[ph + 1]) ++ph;
     keys[i] = probes[i] + ph * (int32_t)K;
+}
+
+// gthr[q] = min(gthr[q], the kk-th distance of keys[q][kk] inflated by 1e-5 (it may
+// be a lane-rotated fp32 sum, within 4e-6 relative of the canonical CA2 value)):
+// the kk-th smallest over a subset of a query's candidates bounds its final kk-th.
+__global__ void merged_bound_kernel(const uint64_t *keys, int64_t nq, int kk, float *gthr) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const uint64_t k = keys[q * kk + kk - 1];
+    if (k == KEY_MAX) return;
+    const float b = __fmul_ru(key_dist(k), 1.00001f);
+    if (b < gthr[q]) gthr[q] = b;
 }
 
 __global__ void gather_i32_kernel(const int32_t *src, const int64_t *pos, int64_t n, int32_t *dst, uint32_t *val) {
@@ -708,20 +720,32 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             const int64_t r0 = std::max<int64_t>(1, std::min<int64_t>(P, ceil_div(4 * kk, (int64_t)std::max(avg_len, 1.0))));
             const bool q16l = q16_enabled() && q16_supported(kk) && P > r0 && avg_len >= list_q16_min_len() &&
                               (lut_halves(x->M) == 1 || list_u6_cfg(x->M) == 3);  // M = 64 needs the u6 items
-            // RII_LIST_MULTI_PHASE=1: integer phases over growing rank ranges [r0, 4 r0),
-            // [4 r0, 16 r0), [16 r0, P), each from tables re-quantised at the bounds the
-            // earlier phases left (deep10m L = 64: 17.3 ms against 17.2 ms for one phase,
-            // so one integer phase is the default)
+            // Integer phases over growing rank ranges (RII_LIST_PHASES = the first rank of
+            // each integer phase, e.g. "1,4,16"; default: one integer phase from r0).  Before
+            // each integer phase the partial top-kk lists of every rank already scanned are
+            // merged and each query's kk-th distance over them -- a bound on its final kk-th
+            // (a subset of its candidates) -- re-scales its u6 tables and seeds the filter.
             PhaseBounds pb{};
             pb.rb[0] = 0;
             pb.n = 1;
             if (q16l) {
-                const bool multi = getenv("RII_LIST_MULTI_PHASE") != nullptr;
-                int64_t r = r0;
-                while (r < P && pb.n < 4) {
-                    pb.rb[pb.n++] = r;
-                    r = (pb.n == 3 || !multi) ? P : 4 * r;
+                // default: a merged-bound phase boundary at 4 r0 when at least 16 lists are
+                // probed (deep10m L = 64: 15.1 -> 13.9 ms, L = 16: 8.8 -> 8.3 ms; no effect
+                // at smaller L or on sift1m's u16 items)
+                std::vector<int64_t> starts{r0};
+                if (P >= 16 && 4 * r0 < P) starts.push_back(4 * r0);
+                if (const char *e = getenv("RII_LIST_PHASES")) {
+                    starts.clear();
+                    for (const char *c = e; *c;) {
+                        char *end = nullptr;
+                        const long v = strtol(c, &end, 10);
+                        if (end == c) break;
+                        starts.push_back(v);
+                        c = *end ? end + 1 : end;
+                    }
                 }
+                for (int64_t r : starts)
+                    if (r > pb.rb[pb.n - 1] && r < P && pb.n < 6) pb.rb[pb.n++] = r;
                 pb.rb[pb.n] = P;
             }
             const int64_t nb = pb.n * x->K;
@@ -783,6 +807,12 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             for (int ph = 1; ph < pb.n; ++ph) {
                 if (n_ph_items[ph] == 0) continue;
                 tr.mark("list scan phase");
+                if (pb.rb[ph] > 1 && !lbound) {  // merged bound over the ranks [0, rb[ph]) scanned so far
+                    uint64_t *mk = sc.s_ckeys.get<uint64_t>((size_t)a.nq * kk);
+                    launch_merge(pp, P * kk, kk, (int)pb.rb[ph], a.nq, kk, kk, IdMap(), nullptr, nullptr, mk, st);
+                    merged_bound_kernel<<<(unsigned)ceil_div(a.nq, 256), 256, 0, st>>>(mk, a.nq, kk, gthr);
+                    RII_LAUNCHED();
+                }
                 float *qsc = sc.s_qscale.get<float>(a.nq);
                 if (list_u6_cfg(x->M) >= 3) {  // u6 oct items
                     uint8_t *t8 = sc.s_tab16.get<uint8_t>((size_t)a.nq * lut_q_floats(x->M));
@@ -894,13 +924,13 @@ rii_status rii_kernel_timing_read(int32_t which, double *total_ms, int64_t *laun
 
 rii_status rii_debug_counters(int32_t enable) {
     return guarded([&] {
-        int *d = g_dbg.load();
+        unsigned long long *d = g_dbg.load();
         if (enable) {
             if (!d) {
-                RII_CUDA(cudaMalloc(&d, DBG_COUNT * sizeof(int)));
+                RII_CUDA(cudaMalloc(&d, DBG_COUNT * sizeof(unsigned long long)));
                 g_dbg.store(d);
             }
-            RII_CUDA(cudaMemset(d, 0, DBG_COUNT * sizeof(int)));
+            RII_CUDA(cudaMemset(d, 0, DBG_COUNT * sizeof(unsigned long long)));
             RII_CUDA(cudaDeviceSynchronize());
         } else if (d) {
             g_dbg.store(nullptr);
@@ -913,12 +943,12 @@ rii_status rii_debug_counters(int32_t enable) {
 rii_status rii_debug_counters_read(int64_t *out, int32_t n) {
     return guarded([&] {
         arg_check(out != nullptr && n >= 0, "bad arguments");
-        int h[DBG_COUNT] = {};
-        if (int *d = g_dbg.load()) {
+        unsigned long long h[DBG_COUNT] = {};
+        if (unsigned long long *d = g_dbg.load()) {
             RII_CUDA(cudaDeviceSynchronize());
             RII_CUDA(cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost));
         }
-        for (int i = 0; i < n; ++i) out[i] = i < DBG_COUNT ? h[i] : 0;
+        for (int i = 0; i < n; ++i) out[i] = i < DBG_COUNT ? (int64_t)h[i] : 0;
     });
 }
 

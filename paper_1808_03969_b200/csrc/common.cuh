@@ -36,10 +36,14 @@ inline void count_launch(int n = 1) { g_launches.fetch_add((uint64_t)n, std::mem
 
 // Optional device event counters of the scan kernels (rii_debug_counters): window
 // ends, compactions, rollbacks, shared-bound tightenings read at a window end,
-// integer-table re-quantisations, bound publications that lowered the bound.
+// integer-table re-quantisations, bound publications that lowered the bound,
+// candidates pushed into the fresh buffers (summed at each compaction), and the
+// SM clock cycles thread 0 spent per CTA in table fill / scan loop / final
+// compaction + output (summed over CTAs), and the number of CTAs.
 enum DebugCounter { DBG_WINDOWS = 0, DBG_COMPACT = 1, DBG_ROLLBACK = 2, DBG_GTHR_TIGHTEN = 3, DBG_RESCALE = 4,
-                    DBG_PUBLISH = 5, DBG_COUNT = 8 };
-int *debug_counters();  // device array [DBG_COUNT] or nullptr (counting off)
+                    DBG_PUBLISH = 5, DBG_FRESH = 6, DBG_CYC_FILL = 7, DBG_CYC_SCAN = 8,
+                    DBG_CYC_TAIL = 9, DBG_ITEMS = 10, DBG_COUNT = 16 };
+unsigned long long *debug_counters();  // device array [DBG_COUNT] or nullptr (counting off)
 
 // Optional per-kernel event timing (rii_kernel_timing).
 enum TimedKernel { TK_LINEAR = 0, TK_IVF = 1, TK_MERGE = 2, TK_PACKED = 3, TK_BOUND = 4, TK_Q16 = 5, TK_U6 = 6, TK_COUNT = 7 };

@@ -7,6 +7,7 @@
 //                  and codes (16-byte gathers from the linear array),
 //                  evaluate ADC with the lane-rotated table of k_scan.cu and keep
 //                  the top-kk in shared memory (L7-L16, mode A of reading R2).
+#include <cstring>
 #include <cub/cub.cuh>
 
 #include "kernels.cuh"
@@ -299,7 +300,12 @@ int64_t build_list_items(const int64_t *qoff, int64_t K, int B, const uint32_t *
     RII_CUDA(cudaMallocAsync(&raw, (size_t)std::max<int64_t>(total, 1) * sizeof(int4), st));
     list_item_fill_kernel<<<(unsigned)ceil_div(K, 256), 256, 0, st>>>(qoff, ioff, K, B, raw);
     RII_LAUNCHED();
-    if (total > 0) {
+    // RII_ITEM_ORDER=list (A/B): keep the items of one list adjacent (L2 reuse of its
+    // codes) instead of ordering them by the smallest probe rank of their queries
+    const char *ord = getenv("RII_ITEM_ORDER");
+    if (total > 0 && ord && !strcmp(ord, "list")) {
+        RII_CUDA(cudaMemcpyAsync(items, raw, (size_t)total * sizeof(int4), cudaMemcpyDeviceToDevice, st));
+    } else if (total > 0) {
         uint32_t *key = nullptr, *key2 = nullptr, *idx = nullptr, *idx2 = nullptr;
         RII_CUDA(cudaMallocAsync(&key, (size_t)total * 4, st));
         RII_CUDA(cudaMallocAsync(&key2, (size_t)total * 4, st));

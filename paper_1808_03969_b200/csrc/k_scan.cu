@@ -65,12 +65,21 @@ __device__ __forceinline__ void load_code(const uint8_t *p, uint32_t (&w)[W]) {
 // (scratch: 32 ints -- [0] compaction max, [1] overflow flag, [2, 2 + B) fill snapshot, [31] rescale flag)
 __host__ __device__ constexpr int smem_aux_bytes(int B, int kk) { return B * (kk + NEWCAP) * 8 + B * 8 + 128 + B * 16; }
 
+// Debug counters of one kernel family (0 linear scans, 1 float list items, 2 integer
+// list items): RII_DBG_MASK (bit per family, default all) restricts what is counted.
+static unsigned long long *debug_counters_for(int family) {
+    unsigned long long *d = debug_counters();
+    if (!d) return nullptr;
+    const char *e = getenv("RII_DBG_MASK");
+    return (!e || ((atoi(e) >> family) & 1)) ? d : nullptr;
+}
+
 // Window-end read of a query's shared bound (another CTA's published kk-th distance
 // tightens this CTA's filter mid-chunk); counted when it lowers the bound.
-__device__ __forceinline__ void gqs_update(float *gqs, int qq, float g, int *dbg) {
+__device__ __forceinline__ void gqs_update(float *gqs, int qq, float g, unsigned long long *dbg) {
     if (g < gqs[qq]) {
         gqs[qq] = g;
-        if (dbg) atomicAdd(dbg + DBG_GTHR_TIGHTEN, 1);
+        if (dbg) atomicAdd(dbg + DBG_GTHR_TIGHTEN, 1ull);
     }
 }
 
@@ -122,6 +131,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     float *qsc = reinterpret_cast<float *>(scratch + 32);  // q16: per-query scale [B]
     const uint8_t *__restrict__ codes = a.codes;
 
+    if (a.dbg && threadIdx.x == 0) *reinterpret_cast<long long *>(scratch + 24) = clock64();  // debug cycles
     // Work item: linear mode = (code chunk ci, query batch qb); list mode = (posting
     // list, up to B of the queries that probe it) -- list-major Alg. 2 L7-L13.
     int64_t c0, c1, qstart = 0;
@@ -132,6 +142,16 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         c1 = a.offsets[it.x + 1];
         qstart = it.y;
         nqi = it.z;
+        // The list is one contiguous range of the list-ordered mirror: one bulk prefetch
+        // into L2 at item start (overlaps the table fill) instead of a DRAM miss per step.
+        if (threadIdx.x == 0 && c1 > c0) {
+            const uintptr_t b0 = (uintptr_t)(codes + (size_t)c0 * M) & ~(uintptr_t)15;
+            const uintptr_t b1 = ((uintptr_t)(codes + (size_t)c1 * M) + 15) & ~(uintptr_t)15;
+            for (uintptr_t o = b0; o < b1; o += 65536) {
+                const uint32_t n = (uint32_t)min((uintptr_t)65536, b1 - o);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(o), "r"(n) : "memory");
+            }
+        }
     } else {
         ci = blockIdx.x / a.nb;
         qb = blockIdx.x - ci * a.nb;
@@ -170,7 +190,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             const uint8_t *tq[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) tq[k] = a.qtab8 + query_of(8 * o + k) * LQF;
-            load_lut_oct_u8pre<U6_R2, H>(reinterpret_cast<uint32_t *>(lut + o * OCT_BYTES), tq);
+            load_lut_oct_u8pre<U6_R2, H, NTH>(reinterpret_cast<uint32_t *>(lut + o * OCT_BYTES), tq);
         }
     } else if constexpr (U6) {
         // u6 tables: per-query scale s = 63 * ALPHA / T (T = +inf -> s = 0: everything passes)
@@ -244,6 +264,13 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     }
     if (tid == 0) scratch[1] = 0;
     __syncthreads();
+    // debug cycle accounting: nothing stays live across the scan loop (the timestamp
+    // of the loop start is kept in shared memory, scratch[24..25], free for B <= 16)
+    if (a.dbg && tid == 0) {
+        const long long t = clock64();
+        atomicAdd(a.dbg + DBG_CYC_FILL, (unsigned long long)(t - *reinterpret_cast<long long *>(scratch + 24)));
+        *reinterpret_cast<long long *>(scratch + 24) = t;
+    }
 
     // u6 tables (one copy, M >= 32): an 8-byte LDS is served per half-warp, so the
     // columns only need to differ within each half: lane l reads column
@@ -322,7 +349,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                     }
                 }
                 scratch[31] = f;
-                if (f && a.dbg) atomicAdd(a.dbg + DBG_RESCALE, 1);
+                if (f && a.dbg) atomicAdd(a.dbg + DBG_RESCALE, 1ull);
             }
             __syncthreads();
             if (scratch[31]) {
@@ -359,6 +386,11 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     // Packed mode: canonical (CA2) rescore of the fresh entries from the queries'
     // fp32 HBM tables before they are compacted into the exact top lists.
     auto rescore_fresh = [&]() {
+        if (a.dbg && tid == 0) {
+            int n = 0;
+            for (int qq = 0; qq < B; ++qq) n += cnt[qq];
+            atomicAdd(a.dbg + DBG_FRESH, (unsigned long long)n);
+        }
         if constexpr (PACKED) {
             for (int qq = 0; qq < B; ++qq) {
                 const int n = cnt[qq];
@@ -421,10 +453,25 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     };
     int64_t base = c0;
     load_step(base, w, cid);
-    int safe = 0;
+    // Adaptive window: without a bound (every threshold +inf) the first window runs one
+    // step, and a window that overflowed is redone from one step; the length doubles
+    // after every window that fit, up to WIN.  Loose early thresholds therefore cost
+    // compactions, not rolled-back windows.
+    // (The linear integer-table kernels always start from a sampled bound and keep the
+    // fixed scheme -- WIN steps, four single steps after a rollback: their register
+    // allocation is at the limit, and the adaptive counter costs them a stack frame.)
+    constexpr bool ADAPT = !(Q16 && !LISTS);
+    int win = 1;
+    if constexpr (ADAPT) {
+#pragma unroll
+        for (int qq = 0; qq < B; ++qq) win &= !(th[qq] < __int_as_float(0x7f800000));
+        win = win ? 1 : WIN;
+    } else {
+        win = 0;  // the `safe` countdown of single-step windows
+    }
     while (base < c1) {
         const int64_t wstart = base;
-        const int nsteps = safe > 0 ? 1 : WIN;
+        const int nsteps = ADAPT ? win : (win > 0 ? 1 : WIN);
         bool ovf = false, need = false;
         for (int s = 0; s < nsteps && base < c1; ++s) {
             uint32_t wn[U][W], nid[U];
@@ -526,10 +573,10 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             base += STEP;
         }
         if (ovf) *s_ovf = 1;
-        if (a.dbg && tid == 0) atomicAdd(a.dbg + DBG_WINDOWS, 1);
+        if (a.dbg && tid == 0) atomicAdd(a.dbg + DBG_WINDOWS, 1ull);
         if (__syncthreads_or(ovf || need)) {
             const bool rolled = *s_ovf != 0;  // written before the barrier; reset below
-            if (a.dbg && tid == 0) atomicAdd(a.dbg + (rolled ? DBG_ROLLBACK : DBG_COMPACT), 1);
+            if (a.dbg && tid == 0) atomicAdd(a.dbg + (rolled ? DBG_ROLLBACK : DBG_COMPACT), 1ull);
             if (rolled && tid < B) cnt[tid] = s_cnt0[tid];
             __syncthreads();
             rescore_fresh();
@@ -546,7 +593,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             if (rolled) {
                 base = wstart;
                 load_step(base, w, cid);
-                safe = 4;
+                win = ADAPT ? 1 : 4;
                 continue;
             }
         } else {
@@ -561,7 +608,13 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             __syncthreads();  // snapshot taken before the next window pushes
         }
         maybe_rescale();
-        if (safe > 0) --safe;
+        if constexpr (ADAPT) win = win * 2 < WIN ? win * 2 : WIN;
+        else if (win > 0) --win;
+    }
+    if (a.dbg && tid == 0) {
+        const long long t = clock64();
+        atomicAdd(a.dbg + DBG_CYC_SCAN, (unsigned long long)(t - *reinterpret_cast<long long *>(scratch + 24)));
+        *reinterpret_cast<long long *>(scratch + 24) = t;
     }
     __syncthreads();
     rescore_fresh();
@@ -570,7 +623,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         if (tid < nqi && thr[tid] < __int_as_float(0x7f800000)) {
             const float bound = __fmul_ru(thr[tid], 1.00001f);
             const int old = atomicMin(reinterpret_cast<int *>(a.gthr + query_of(tid)), __float_as_int(bound));
-            if (a.dbg && __float_as_int(bound) < old) atomicAdd(a.dbg + DBG_PUBLISH, 1);
+            if (a.dbg && __float_as_int(bound) < old) atomicAdd(a.dbg + DBG_PUBLISH, 1ull);
         }
     }
 
@@ -599,6 +652,10 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             if (i == 0 || top[e - i] != KEY_MAX) a.out[a.qlist[qstart + qq] * kk + i] = top[e];
         }
         else a.out[(((int64_t)qb * B + qq) * a.nc + ci) * kk + i] = top[e];
+    }
+    if (a.dbg && tid == 0) {
+        atomicAdd(a.dbg + DBG_CYC_TAIL, (unsigned long long)(clock64() - *reinterpret_cast<long long *>(scratch + 24)));
+        atomicAdd(a.dbg + DBG_ITEMS, 1ull);
     }
 }
 
@@ -831,7 +888,17 @@ int list_u6_cfg(int M) {
 }
 
 #endif  // !RII_SCAN_M
-static int list_q16_nth(int) { return 384; }
+// u6 list items: 384 threads (one CTA per SM) or 192 threads with two CTAs per SM, so
+// one CTA's table fill, barriers and final compaction overlap the other's scan.
+// Measured on deep10m (10k queries): 192 wins at P >= 32 probed lists (L = 64: 15.1
+// -> 13.9 ms; with the merged-bound phases 13.9 -> 12.8 ms) and loses below (L = 16:
+// 8.8 -> 9.4 ms).  RII_LIST_NTH=192 / 384 forces one (A/B).
+static int list_q16_nth(int M, int64_t P) {
+    if (M == 64) return 384;
+    const char *e = getenv("RII_LIST_NTH");
+    if (e) return atoi(e) == 192 ? 192 : 384;
+    return P >= 32 ? 192 : 384;
+}
 static size_t smem_list_q16(int M, int kk, int B = 8) {
     if (B == 16) return 2 * OCT_BYTES + smem_aux_bytes(16, kk) + 16;
     if (list_u6_cfg(M) < 3) return smem_q16(kk);
@@ -845,12 +912,12 @@ int list_int_B(int M, int kk) {
 #endif  // !RII_SCAN_M
 
 template <int M, int B, bool LISTS>
-static void *fast_kernel_ptr_h1(bool q16);
+static void *fast_kernel_ptr_h1(bool q16, int nth);
 template <int M, int B, bool LISTS>
-static void *fast_kernel_ptr_b(bool q16);
+static void *fast_kernel_ptr_b(bool q16, int nth);
 
 template <int M, int B, bool LISTS>
-static void *fast_kernel_ptr(bool q16 = false) {
+static void *fast_kernel_ptr(bool q16 = false, int nth = 384) {
     if constexpr (lut_halves(M) > 1) {  // M = 64: u6 oct tables (B = 8) or fp32 pairs (B = 2) only
         if constexpr (B == 8) {
             if constexpr (LISTS) return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64>;
@@ -862,12 +929,12 @@ static void *fast_kernel_ptr(bool q16 = false) {
             return nullptr;
         }
     } else {
-        return fast_kernel_ptr_h1<M, B, LISTS>(q16);
+        return fast_kernel_ptr_h1<M, B, LISTS>(q16, nth);
     }
 }
 
 template <int M, int B, bool LISTS>
-static void *fast_kernel_ptr_h1(bool q16) {
+static void *fast_kernel_ptr_h1(bool q16, int nth) {
     if constexpr (B == 16) {  // u6, two oct tables, fixed-base layout (list items: M = 32)
         if constexpr (LISTS) {
             if constexpr (M == 32) return (void *)scan_fast_kernel<M, 16, true, 384, 1, 3, 128 | 64>;
@@ -876,12 +943,12 @@ static void *fast_kernel_ptr_h1(bool q16) {
             return (void *)scan_fast_kernel<M, 16, false, 384, 1, 3, 128 | 64>;
         }
     } else {
-        return fast_kernel_ptr_b<M, B, LISTS>(q16);
+        return fast_kernel_ptr_b<M, B, LISTS>(q16, nth);
     }
 }
 
 template <int M, int B, bool LISTS>
-static void *fast_kernel_ptr_b(bool q16) {
+static void *fast_kernel_ptr_b(bool q16, int nth) {
     // Kernel variants kept for A/B runs (measured on B200, deep10m, 10k queries; the
     // others this round tried are recorded in DESIGN.md and were removed to bound the
     // build time): RII_Q16_CFG 0 = u16 tables (204 ms), 4 = u6 one copy (131 ms),
@@ -890,6 +957,8 @@ static void *fast_kernel_ptr_b(bool q16) {
     if constexpr (B == 8) {
         if constexpr (LISTS) {
             if (q16) {
+                if (list_u6_cfg(M) >= 3 && nth == 192)
+                    return (void *)scan_fast_kernel<M, 8, true, 192, 1, 3, 128 | 64>;
                 if (list_u6_cfg(M) >= 3) return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64>;
                 return (void *)scan_fast_kernel<M, 8, true, 384, 1, 2, 64>;  // u16, window 128
             }
@@ -921,7 +990,7 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
     a.nb = pl.nb; a.chunk = pl.chunk; a.nc = pl.nc; a.out = out; a.tables = tables;
     a.gthr = gthr;
     a.one = 1;
-    a.dbg = debug_counters();
+    a.dbg = debug_counters_for(0);
     void *args[] = {&a};
     KernelTimer t(timer, st), tp(B >= 8 && timer == TK_LINEAR ? (q16 ? (q16_is_u6(M) ? TK_U6 : TK_Q16) : TK_PACKED) : -1,
                                  st);
@@ -972,16 +1041,17 @@ int list_major_B(int kk, double avg_len, int M) {
 template <int M, int B>
 static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st, bool q16) {
     q16 = q16 && (B == 8 || B == 16);
-    void *kern = fast_kernel_ptr<M, B, true>(q16);
+    const int nth = q16 ? (B == 8 && list_u6_cfg(M) >= 3 ? list_q16_nth(M, a.P) : 384)
+                        : (B == 8 ? PACKED_NTH : scan_threads());
+    void *kern = fast_kernel_ptr<M, B, true>(q16, nth);
     if (!kern) throw Error(1, "no list-major kernel for this (M, B)");
     const size_t smem = q16 ? smem_list_q16(M, a.kk, B) : smem_fast(B, a.kk, M);
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ScanArgs aa = a;
     aa.one = 1;
-    aa.dbg = debug_counters();
+    aa.dbg = debug_counters_for(q16 ? 2 : 1);
     void *args[] = {&aa};
     KernelTimer t(TK_IVF, st);
-    const int nth = q16 ? list_q16_nth(M) : (B == 8 ? PACKED_NTH : scan_threads());
     check_code_align(a.codes, M);
     RII_CUDA(cudaLaunchKernel(kern, dim3((unsigned)n_items), dim3(nth), args, smem, st));
     count_launch();

@@ -51,7 +51,7 @@ struct ScanArgs {
     const uint8_t *qtab8;  // u6 list mode: precomputed per-query u6 tables [nq][256][32]
     const float *qscale;
     uint32_t one;  // = 1 (runtime: keeps the u6 SWAR adds on the FMA pipe, lut.cuh fma_add)
-    int *dbg;      // debug event counters (rii_debug_counters), nullptr when off
+    unsigned long long *dbg;  // debug event counters (rii_debug_counters), nullptr when off
 };
 
 // List-major inverted-index scan: B queries per CTA share one posting list's codes.

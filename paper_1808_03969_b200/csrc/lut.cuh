@@ -399,18 +399,31 @@ __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, 
 // Oct layout from 8 precomputed per-query u6 tables ([z][32 columns] bytes, written by
 // u6_tables_kernel): column c = [t0[c] .. t7[c]] (an 8 x 8 byte transpose per group of
 // 8 columns, 3 PRMT per output word).  R2: the second copy as in load_lut_oct_u6.
-template <bool R2, int H = 1>
+template <bool R2, int H = 1, int NTHR = 384>
 __device__ __forceinline__ void load_lut_oct_u8pre(uint32_t *dst, const uint8_t *const (&t)[8]) {
-    for (int eh = threadIdx.x; eh < H * LUT_Q_FLOATS / 8; eh += blockDim.x) {  // 8 columns of one row
+    // all loads of a thread are issued before any is used (one L2 round trip, not one
+    // per row group): NTHR threads cover the H * 1024 row groups in NIT iterations
+    constexpr int NG = H * LUT_Q_FLOATS / 8, NIT = (NG + NTHR - 1) / NTHR;
+    uint2 v[NIT][8];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const int eh = (int)threadIdx.x + it * NTHR;
+        if (eh < NG) {
+            const int h = eh / (LUT_Q_FLOATS / 8), e = eh - h * (LUT_Q_FLOATS / 8);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[it][k] = __ldg(reinterpret_cast<const uint2 *>(t[k] + h * LUT_Q_FLOATS) + e);
+        }
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const int eh = (int)threadIdx.x + it * NTHR;
+        if (eh >= NG) continue;
         const int h = eh / (LUT_Q_FLOATS / 8), e = eh - h * (LUT_Q_FLOATS / 8);
         uint2 *o = reinterpret_cast<uint2 *>(dst) + h * (OCT_BYTES / 8);
-        uint2 v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const uint2 *>(t[k] + h * LUT_Q_FLOATS) + e);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             const uint32_t sc = (uint32_t)(c & 3) | ((uint32_t)(4 + (c & 3)) << 4);  // byte c of a, of b
-            auto w_of = [&](int k) { return c < 4 ? v[k].x : v[k].y; };
+            auto w_of = [&](int k) { return c < 4 ? v[it][k].x : v[it][k].y; };
             const uint32_t p01 = __byte_perm(w_of(0), w_of(1), sc), p23 = __byte_perm(w_of(2), w_of(3), sc);
             const uint32_t p45 = __byte_perm(w_of(4), w_of(5), sc), p67 = __byte_perm(w_of(6), w_of(7), sc);
             const uint2 col = make_uint2(__byte_perm(p01, p23, 0x5410), __byte_perm(p45, p67, 0x5410));

@@ -76,7 +76,8 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     return lo.value, hi.value
 
 
-DEBUG_COUNTERS = ("windows", "compactions", "rollbacks", "gthr_tightenings", "rescales", "publishes")
+DEBUG_COUNTERS = ("windows", "compactions", "rollbacks", "gthr_tightenings", "rescales", "publishes", "pushed",
+                  "cycles_fill", "cycles_scan", "cycles_tail", "ctas")
 
 
 def debug_counters(enable: bool) -> None:

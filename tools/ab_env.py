@@ -1,7 +1,7 @@
 """A/B timing of one query configuration under several environment settings
 (knobs read per call by the library), on one bench workload built once.
 
-    python tools/ab_env.py --path ivf --L 64 [--subset 0.1] VAR=a,VAR2=b  VAR=c ...
+    python tools/ab_env.py --path ivf --L 64 [--subset 0.1] "VAR=a;VAR2=b"  VAR=c ...
 """
 import argparse
 import json
@@ -41,7 +41,7 @@ def main():
     dist = torch.empty((nq, topk), dtype=torch.float32, device=dev)
     ref = None
     for st in (a.settings or [""]):
-        env = dict(kv.split("=", 1) for kv in st.split(",") if kv)
+        env = dict(kv.split("=", 1) for kv in st.split(";") if kv)
         old = {k: os.environ.get(k) for k in env}
         os.environ.update(env)
         g.query(q, topk, S, L=a.L, path=a.path, out=(ids, dist))

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--L", type=int, default=64)
     ap.add_argument("--subset", type=float, default=0.0)
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--counters", action="store_true", help="print the scan kernels' debug counters of one call")
     a = ap.parse_args()
     kind, N, D, M, nlist, nq, topk, n_train, _ = bench.WORKLOADS[a.workload]
     dev = torch.device("cuda", 0)
@@ -55,6 +56,11 @@ def main():
         lib.rii_kernel_timing_read(w, C.byref(ms), C.byref(n))
         out[name] = (ms.value / max(a.reps, 1), n.value)
     print(f"path={a.path} used={used} L={a.L} subset={a.subset} wall_ms={dt * 1e3:.2f} qps={nq / dt:.0f} kernels={out}")
+    if a.counters:
+        rii.debug_counters(True)
+        g.query(q, topk, S, L=a.L, path=a.path)
+        print("counters", rii.read_debug_counters())
+        rii.debug_counters(False)
 
 
 if __name__ == "__main__":

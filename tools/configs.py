@@ -194,9 +194,28 @@ def main():
             emit(config="scale1b", row=f"subset |S|=1e6 L=64 {path}", path_used=["auto", "linear", "ivf"][used["p"]],
                  ms=ms, qps=c["nq"] / ms * 1e3)
         q1 = q[:qb]
+        lib = rii.load()
+        import ctypes as C
+        lib.rii_kernel_timing(1)
+        if os.environ.get("RII_PROFILE_LINEAR"):
+            torch.cuda.profiler.start()
         ms = timed(lambda: g.query(q1, c["topk"], None, L=1, path="linear"), 1)
+        if os.environ.get("RII_PROFILE_LINEAR"):
+            torch.cuda.profiler.stop()
+        kms, kn = C.c_double(), C.c_int64()
+        lib.rii_kernel_timing_read(0, C.byref(kms), C.byref(kn))
+        q16ms, q16n = C.c_double(), C.c_int64()
+        lib.rii_kernel_timing_read(5, C.byref(q16ms), C.byref(q16n))
+        lib.rii_kernel_timing(0)
+        kernel_ms = kms.value / max(kn.value, 1)
+        lookups = qb * N * M
+        peak = 148 * 64 * 1965e6  # u16 tables: 64 two-byte lookups per 128-B wavefront per clock per SM
         emit(config="scale1b", row="linear whole (1024 queries)", ms=ms, qps=qb / ms * 1e3,
-             scanned_codes_per_s=qb * N / ms * 1e3)
+             scanned_codes_per_s=qb * N / ms * 1e3, kernel_ms=kernel_ms, kernel_launches=kn.value,
+             u16_launches=q16n.value, lookups_per_s=lookups / (kernel_ms / 1e3),
+             roofline={"bound": "alu (shared-memory LUT pipe)", "peak_lookups_per_s": peak,
+                       "frac": lookups / (kernel_ms / 1e3) / peak,
+                       "code_bytes_per_launch": N * M, "note": "u16 fixed-point tables, 8 queries per CTA (M = 8)"})
     if "deep10m" in only:
         kind, N, D, M, nlist, nq, topk, n_train, _ = bench.WORKLOADS["deep10m"]
         g, b = build(kind, N, D, M, nlist, n_train)

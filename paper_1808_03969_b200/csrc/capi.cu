@@ -521,6 +521,10 @@ static double list_q16_min_len() {  // RII_LIST_Q16_MIN: average list length for
     const char *e = getenv("RII_LIST_Q16_MIN");
     return e ? atof(e) : 1024.0;
 }
+static int64_t large_u6_min_codes() {  // RII_LARGE_U6_MIN: shortest large-M scan on the u6 chunk kernel
+    const char *e = getenv("RII_LARGE_U6_MIN");
+    return e ? atoll(e) : 65536;
+}
 static int64_t q16_sample() {
     const char *e = getenv("RII_Q16_SAMPLE");
     return e ? atoll(e) : ((int64_t)1 << 15);
@@ -602,6 +606,45 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             uint64_t *pp = sc.s_part.get<uint64_t>((size_t)a.nq * kk);
             RII_CUDA(cudaMemsetAsync(pp, 0xff, (size_t)a.nq * kk * 8, st));
             parts = pp;
+        } else if (large && large_u6_supported(x->M, kk) && q16_enabled() && smem_fixed_base_ok() &&
+                   n_codes >= large_u6_min_codes() && std::min<int64_t>(8192, n_codes / 8) >= 4 * kk) {
+            // chunked u6 oct tables (k_large_u6.cu), scaled by the exact kk-th distance
+            // over a strided sample of the codes (a subset: it bounds the final kk-th)
+            KernelTimer tb(TK_BOUND, st);
+            const int64_t ns = std::min<int64_t>(8192, n_codes / 8);
+            uint8_t *samp = sc.s_samp.get<uint8_t>((size_t)ns * x->M + 64);
+            launch_strided_gather(scan_codes, x->M, n_codes / ns, ns, samp, st);
+            const int ncs = large_linear_chunks(a.nq, ns, x->num_sms);
+            uint64_t *sp = sc.s_spart.get<uint64_t>((size_t)a.nq * ncs * kk);
+            launch_large_linear(samp, ns, x->M, tables, a.nq, kk, ncs, sp, st, -1);
+            uint64_t *sk = sc.s_ckeys.get<uint64_t>((size_t)a.nq * kk);
+            launch_merge(sp, (int64_t)ncs * kk, kk, ncs, a.nq, kk, kk, IdMap(), nullptr, nullptr, sk, st);
+            float *gthr = sc.s_gthr.get<float>(a.nq);
+            launch_kth_bound(sk, a.nq, kk, gthr, st);
+            uint8_t *qt = sc.s_tab16.get<uint8_t>((size_t)ceil_div(a.nq, 8) * 8 * large_u6_nch(x->M) * KS * 32);
+            float *qsc = sc.s_qscale.get<float>(a.nq);
+            launch_u6_tables_large(tables, gthr, a.nq, x->M, qt, qsc, st);
+            tr.mark("large u6 bound + tables");
+            // pass 1: the first 1/16 of the codes at the sample bound's scale; pass 2: the
+            // rest, with tables rebuilt at the kk-th over pass 1's exact top lists
+            const int64_t n1 = std::max<int64_t>(ceil_div(n_codes, 16), std::min<int64_t>(n_codes, 16 * kk));
+            const int64_t n2 = n_codes - n1;
+            const int nc1 = large_u6_chunks(a.nq, n1, x->M, x->num_sms),
+                      nc2 = n2 > 0 ? large_u6_chunks(a.nq, n2, x->M, x->num_sms) : 0;
+            const int nct = nc1 + nc2;
+            uint64_t *pp = sc.s_part.get<uint64_t>((size_t)ceil_div(a.nq, 8) * 8 * nct * kk);
+            launch_large_u6_linear(scan_codes, 0, n1, x->M, qt, qsc, tables, gthr, a.nq, kk, nc1, pp, nct, 0, st);
+            if (n2 > 0) {
+                launch_merge(pp, (int64_t)nct * kk, kk, nc1, a.nq, kk, kk, IdMap(), nullptr, nullptr, sk, st);
+                launch_kth_bound(sk, a.nq, kk, gthr, st);
+                launch_u6_tables_large(tables, gthr, a.nq, x->M, qt, qsc, st);
+                launch_large_u6_linear(scan_codes, n1, n2, x->M, qt, qsc, tables, gthr, a.nq, kk, nc2, pp, nct, nc1,
+                                       st);
+            }
+            parts = pp;
+            q_stride = (int64_t)nct * kk;
+            p_stride = kk;
+            nparts = nct;
         } else if (large) {
             const int nc = large_linear_chunks(a.nq, n_codes, x->num_sms);
             uint64_t *pp = sc.s_part.get<uint64_t>((size_t)a.nq * nc * kk);

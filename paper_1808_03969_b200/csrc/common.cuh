@@ -62,6 +62,24 @@ __device__ __forceinline__ float ca1_step(float acc, float u, float c) {
     return __fadd_rn(acc, __fmul_rn(t, t));
 }
 
+// CA2 sum d = ((0 + A[0][c0]) + A[1][c1]) + ... of a code of M bytes (M % 16 == 0,
+// 16-byte aligned) against a canonical [M][256] fp32 table in global memory.  The
+// loads of 16 subspaces are issued before their in-order adds: a rolled loop would
+// serialise two dependent memory round trips per subspace (code byte, then entry).
+__device__ __forceinline__ float rescore_ca2_16(const float *__restrict__ tq, const uint8_t *__restrict__ cp, int M) {
+    float d = 0.f;
+    for (int m0 = 0; m0 < M; m0 += 16) {
+        const uint4 c = __ldg(reinterpret_cast<const uint4 *>(cp + m0));
+        const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __ldg(tq + (int64_t)(m0 + j) * 256 + ((cw[j >> 2] >> (8 * (j & 3))) & 255u));
+#pragma unroll
+        for (int j = 0; j < 16; ++j) d = __fadd_rn(d, v[j]);
+    }
+    return d;
+}
+
 // (dist, id) packed so that unsigned order == (dist asc, id asc) for dist >= +0.
 __device__ __forceinline__ uint64_t make_key(float d, uint32_t id) {
     return ((uint64_t)__float_as_uint(d) << 32) | (uint64_t)id;

@@ -85,7 +85,11 @@ __global__ void __launch_bounds__(NT, 1) scan_large_kernel(const LargeArgs a) {
             const uint32_t id = key_id(fresh[i]);
             const uint8_t *cp = codes + (size_t)id * M;
             float d = 0.f;
-            for (int m = 0; m < M; ++m) d = __fadd_rn(d, entry(m, cp[m]));
+            if (MODE != 2 && (M & 15) == 0) {
+                d = rescore_ca2_16(a.tables + (size_t)q * M * KS, cp, M);  // loads in flight per 16 subspaces
+            } else {
+                for (int m = 0; m < M; ++m) d = __fadd_rn(d, entry(m, cp[m]));
+            }
             fresh[i] = make_key(d, id);
         }
         __syncthreads();
@@ -186,11 +190,11 @@ int large_linear_chunks(int64_t nq, int64_t n_codes, int num_sms) {
 }
 
 void launch_large_linear(const uint8_t *codes, int64_t n_codes, int M, const float *tables, int64_t nq, int kk, int nc,
-                         uint64_t *out, cudaStream_t st) {
+                         uint64_t *out, cudaStream_t st, int timer) {
     LargeArgs a{};
     a.codes = codes; a.M = M; a.kk = kk; a.nq = nq; a.n_codes = n_codes; a.nc = nc;
     a.chunk = ceil_div(n_codes, nc); a.tables = tables; a.out = out;
-    launch_large<0>(a, nq * nc, st, TK_LINEAR);
+    launch_large<0>(a, nq * nc, st, timer);
 }
 
 void launch_large_ivf(const uint8_t *codes, int M, const float *tables, int64_t nq, int kk, const int32_t *probes,

@@ -880,6 +880,7 @@ static bool fixed_base_ok() {
     }();
     return ok;
 }
+bool smem_fixed_base_ok() { return fixed_base_ok(); }
 int list_u6_cfg(int M) {
     if (!fixed_base_ok()) return 0;
     if (M == 64) return 3;  // two halves: only the u6 items fit (128 KB)

@@ -162,11 +162,25 @@ void launch_lut_large(const float *q, int64_t nq, const float *cb, int D, int M,
 int large_linear_chunks(int64_t nq, int64_t n_codes, int num_sms);
 // out[nq][nc][kk] keys (ids = positions in codes) of Alg. 1 over n_codes codes.
 void launch_large_linear(const uint8_t *codes, int64_t n_codes, int M, const float *tables, int64_t nq, int kk, int nc,
-                         uint64_t *out, cudaStream_t st);
+                         uint64_t *out, cudaStream_t st, int timer = TK_LINEAR);
 // out[nq][kk] keys of Alg. 2 over each query's P probed lists (take: optional budget cut).
 void launch_large_ivf(const uint8_t *codes, int M, const float *tables, int64_t nq, int kk, const int32_t *probes,
                       int64_t P, const int64_t *offsets, const uint32_t *ids, const int32_t *take, uint64_t *out,
                       cudaStream_t st);
+// Large-M linear scan on chunked u6 oct tables (k_large_u6.cu): M > 64, M % 16 == 0.
+bool large_u6_supported(int M, int kk);
+int large_u6_nch(int M);  // 32-subspace chunks per code
+// out[q][c][256][32] u6 entries at scale[q] = 63 (M / 4) / gthr[q] (tables: [nq][M][256] fp32)
+void launch_u6_tables_large(const float *tables, const float *gthr, int64_t nq, int M, uint8_t *out, float *scale,
+                            cudaStream_t st);
+int large_u6_chunks(int64_t nq, int64_t n_codes, int M, int num_sms);
+// out[ceil(nq/8)*8][nc][kk] exact (CA2) keys; gthr filters and is lowered (atomicMin) per CTA.
+// Scans codes [base, base + n_codes) (keys = absolute positions) into slots [ci_off, ci_off + nc) of
+// out[ceil(nq/8)*8][nc_out][kk].
+void launch_large_u6_linear(const uint8_t *codes, int64_t base, int64_t n_codes, int M, const uint8_t *qtab8,
+                            const float *qscale, const float *tables, float *gthr, int64_t nq, int kk, int nc,
+                            uint64_t *out, int nc_out, int ci_off, cudaStream_t st);
+bool smem_fixed_base_ok();  // dynamic shared memory starts at shared address 0x400 (probed once)
 // a[i] = argmin_k d_S(codes[i], centers[k]) (CA2 SDC, ties lowest k); dist optional.
 void launch_large_assign(const uint8_t *codes, int64_t n, const uint8_t *centers, int64_t K, int M, const float *T,
                          int32_t *assign, float *dist, cudaStream_t st);

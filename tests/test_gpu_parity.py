@@ -637,3 +637,33 @@ def test_large_m_shapes(rii, ref, kind, N, D, M, K, nq, topk):
     gr = g.query(q, topk, L=Lc, path="ivf")
     orr = ref.ivf_paper(o.cb, o.codes, o.centers, o.offsets, o.ids, q, topk, Lc)
     assert_topk_parity(ref, o.cb, o.codes, q, gr, orr, what=f"M={M} paper L={Lc}")
+
+
+@pytest.mark.parametrize("kind,N,D,M,nq,topk", [("deep", 40_003, 960, 240, 21, 100),   # GIST1M shape
+                                                ("sift", 50_001, 384, 192, 13, 50),    # MET-like M = 192
+                                                ("deep", 30_011, 384, 96, 9, 10)])
+def test_large_m_u6_chunk_kernel(rii, ref, monkeypatch, kind, N, D, M, nq, topk):
+    """The large-M linear scan on chunked u6 oct tables (k_large_u6.cu; M > 64,
+    M % 16 == 0): whole database and a large subset (both on the chunk kernel) and
+    a small subset (the one-query kernel), element by element against the oracle's
+    Alg. 1; several code chunks per query batch and a ragged last tile."""
+    monkeypatch.setenv("RII_LARGE_U6_MIN", "8000")
+    x = gen.base(kind, N, D, seed=N)
+    q = gen.base(kind, nq, D, seed=N, stream=gen.STREAM_QUERY)
+    cb = ref.train(x[:3000], M, n_iter=2, seed=0)
+    g = rii.Index(D, M)
+    g.set_codebook(cb)
+    g.add(x)
+    codes = ref.encode_mt(cb, x, M)
+    assert np.array_equal(g.get_codes(), codes)
+    lib = rii.load()
+    lib.rii_kernel_timing(1)
+    for sub in (None, gen.subset(N, N // 2 + 7, seed=3), gen.subset(N, 999, seed=4)):
+        gr = g.query(q, topk, target_ids=sub, path="linear")
+        assert_topk_parity(ref, cb, codes, q, gr, ref.linear_mt(cb, codes, q, topk, S=sub), S=sub,
+                           what=f"large u6 M={M} |S|={'N' if sub is None else len(sub)}")
+    import ctypes as C
+    ms, n = C.c_double(), C.c_int64()
+    lib.rii_kernel_timing_read(6, C.byref(ms), C.byref(n))  # u6 launches: the chunk kernel ran (two passes)
+    lib.rii_kernel_timing(0)
+    assert n.value == 4

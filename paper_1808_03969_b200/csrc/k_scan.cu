@@ -1583,8 +1583,21 @@ __global__ void __launch_bounds__(NT) merge_kernel(const uint64_t *__restrict__ 
             if (k == KEY_MAX) continue;
             const uint32_t id = key_id(k);
             const uint8_t *cp = rs.codes + (size_t)id * rs.M;
+            // CA2 in m order; the code bytes and 16 entries at a time are loaded before
+            // their adds (a rolled loop serialises two dependent loads per subspace)
             float d = 0.f;
-            for (int m = 0; m < rs.M; ++m) d = __fadd_rn(d, lut_q_entry(tq, m, cp[m]));
+            for (int m0 = 0; m0 < rs.M; m0 += 16) {
+                uint32_t cw[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) cw[j] = m0 + 4 * j < rs.M ? __ldg(reinterpret_cast<const uint32_t *>(cp + m0) + j) : 0u;
+                float v[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    v[j] = m0 + j < rs.M ? lut_q_entry(tq, m0 + j, (cw[j >> 2] >> (8 * (j & 3))) & 255u) : 0.f;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (m0 + j < rs.M) d = __fadd_rn(d, v[j]);
+            }
             top[i] = make_key(d, id);
         }
         __syncthreads();

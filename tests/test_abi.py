@@ -50,6 +50,21 @@ def test_host_only_calls(lib):
     assert lib.rii_last_error(None) == b""
 
 
+def test_transport_and_debug_counter_calls_without_a_device(lib):
+    """Host-side argument checks of the round-2 entry points (no device needed)."""
+    from paper_1808_03969_b200 import _lib
+    h = C.c_void_p()
+    # a transport is required and world must be > 1 (RII_ERR_ARG before any device work)
+    assert lib.rii_create_with_transport(32, 4, 256, 0, 0, 2, None, C.byref(h)) == _lib.RII_ERR_ARG and not h.value
+    tr = _lib.Transport(None, _lib.TRANSPORT_FN(lambda ctx, s, r, n: 0))
+    assert lib.rii_create_with_transport(32, 4, 256, 0, 0, 1, C.byref(tr), C.byref(h)) == _lib.RII_ERR_ARG
+    assert b"transport" in lib.rii_last_error(None)
+    # counters never enabled: reading gives zeros; a NULL output is an argument error
+    out = (C.c_int64 * 4)(1, 2, 3, 4)
+    assert lib.rii_debug_counters_read(out, 4) == _lib.RII_OK and list(out) == [0, 0, 0, 0]
+    assert lib.rii_debug_counters_read(None, 4) == _lib.RII_ERR_ARG
+
+
 def test_no_device_is_an_error_not_a_fallback(lib):
     """Without a usable GPU the library refuses (RII_ERR_CUDA); there is no CPU path."""
     import torch

@@ -728,7 +728,18 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             // canonical rescore, top-P by (d0, k) (L6)
             ScanPlan pc = plan_linear(x->M, kkc, a.nq, x->K, x->num_sms, tables != nullptr, 1 << 30, false);
             uint64_t *cp = sc.s_cpart.get<uint64_t>((size_t)pc.nb * pc.B * pc.nc * kkc);
-            launch_linear_scan(pc, x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, kkc, cp, st, tables);
+            // Seed the filter with the kkc-th smallest of the group minima over all K centre
+            // codes (>= kkc groups: a valid bound on the kkc-th d0): the scan then pushes a
+            // few hundred candidates per query instead of starting from +inf and compacting
+            // its way down (RII_COARSE_BOUND=0 disables, A/B)
+            float *cg = nullptr;
+            const char *cbe = getenv("RII_COARSE_BOUND");
+            const int64_t cgs = ceil_div(x->K, 1024);
+            if (tables && pc.fast && kkc <= 512 && x->K / cgs >= kkc && !(cbe && cbe[0] == '0')) {
+                cg = sc.s_bound.get<float>(a.nq);
+                launch_group_min_bound(x->centers.as<uint8_t>(), x->K, x->M, tables, a.nq, kkc, cg, st);
+            }
+            launch_linear_scan(pc, x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, kkc, cp, st, tables, cg);
             uint64_t *ck = sc.s_ckeys.get<uint64_t>((size_t)a.nq * kkc);
             launch_merge(cp, (int64_t)pc.nc * kkc, kkc, pc.nc, a.nq, kkc, (int)P, IdMap(), nullptr, nullptr, ck, st);
             launch_keys_to_probes(ck, a.nq, kkc, P, probes, st);
@@ -835,10 +846,11 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             launch_fill_f32(gthr, a.nq, INFINITY, st);
             tr.mark("alloc partials");
             // items stream their list as a contiguous range of the list-ordered mirror;
-            // keys carry mirror positions, mapped to ids through the CSR in the merge
+            // keys carry ids (the CSR entry of the position), so ties resolve by id (CA4)
             const uint8_t *lcodes = a.S ? t.rmirror : x->mirror.as<uint8_t>();
             ScanArgs sa{};
-            sa.codes = lcodes; sa.q = a.q; sa.nq = a.nq; sa.cb = cb; sa.ds = x->ds; sa.kk = kk; sa.out = pp;
+            sa.codes = lcodes; sa.rcodes = codes; sa.q = a.q; sa.nq = a.nq; sa.cb = cb; sa.ds = x->ds; sa.kk = kk;
+            sa.out = pp;
             sa.items = items; sa.qlist = qlist; sa.P = P; sa.offsets = off; sa.ids = ids; sa.gthr = gthr;
             sa.tables = tables;
             if (lbound)
@@ -874,11 +886,10 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             tr.mark("list scan");
             parts = pp;
             if (Bl != 8 && !lbound) {  // fp32-pair items keep lane-rotated keys: rescore in the merge
-                rs.codes = lcodes;
+                rs.codes = codes;
                 rs.tables = tables;
                 rs.M = x->M;
             }
-            map.pre = ids;
             q_stride = P * kk;
             p_stride = kk;
             nparts = (int)P;

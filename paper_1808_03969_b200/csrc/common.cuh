@@ -109,7 +109,6 @@ inline int partial_width(int topk) { return next_pow2(topk + 16 < 32 ? 32 : topk
 
 // Mapping of the 32-bit candidate index stored in a key to a global id.
 struct IdMap {
-    const uint32_t *pre = nullptr;  // applied first when set: position -> local id (list-ordered mirror -> CSR ids)
     int kind = 0;                 // 0 identity, 1 table (int64 global ids), 2 ranges
     const int64_t *table = nullptr;
     const int64_t *seg_local = nullptr;  // ranges: local offset of each segment (ascending)
@@ -118,7 +117,6 @@ struct IdMap {
 };
 
 __device__ __forceinline__ int64_t map_id(const IdMap &m, uint32_t i) {
-    if (m.pre) i = m.pre[i];
     if (m.kind == 0) return (int64_t)i;
     if (m.kind == 1) return m.table[i];
     int lo = 0, hi = m.nseg - 1;

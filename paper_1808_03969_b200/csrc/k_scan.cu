@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     int *scratch = reinterpret_cast<int *>(thr + B);
     float *qsc = reinterpret_cast<float *>(scratch + 32);  // q16: per-query scale [B]
     const uint8_t *__restrict__ codes = a.codes;
+    const uint8_t *__restrict__ rcodes = LISTS ? a.rcodes : a.codes;  // codes by candidate id
 
     if (a.dbg && threadIdx.x == 0) *reinterpret_cast<long long *>(scratch + 24) = clock64();  // debug cycles
     // Work item: linear mode = (code chunk ci, query batch qb); list mode = (posting
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                     for (int i = tid; i < n; i += NTH) {
                         uint64_t *f = fresh + qq * NEWCAP + i;
                         const uint32_t id = key_id(*f);
-                        const uint8_t *cp = codes + (size_t)id * M;
+                        const uint8_t *cp = rcodes + (size_t)id * M;
                         float d = 0.f;
 #pragma unroll
                         for (int m = 0; m < M; ++m)
@@ -412,7 +413,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                 for (int i = tid; i < n; i += NTH) {
                     uint64_t *f = fresh + qq * NEWCAP + i;
                     const uint32_t id = key_id(*f);
-                    const uint8_t *cp = codes + (size_t)id * M;
+                    const uint8_t *cp = rcodes + (size_t)id * M;
                     float d = 0.f;
 #pragma unroll
                     for (int m = 0; m < M; ++m) d = __fadd_rn(d, lut_q_entry(tq, m, cp[m]));
@@ -433,11 +434,14 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     static_assert(NEWCAP >= STEP, "a single step must fit the fresh buffer");
     int *s_ovf = scratch + 1, *s_cnt0 = scratch + 2;  // flags, fill snapshot at the window start
     uint32_t w[U][W];
-    // candidate id: position in `codes` -- the linear array (linear mode) or the
-    // list-ordered mirror of the codes (list mode: a posting list is the contiguous
-    // range [offsets[k], offsets[k+1]) of the mirror, read with the same coalesced
-    // loads as a linear chunk; the merge maps positions to ids through the CSR)
+    // Codes are read at positions of the linear array (linear mode) or of the
+    // list-ordered mirror (list mode: a posting list is the contiguous range
+    // [offsets[k], offsets[k+1]) of the mirror, read with the same coalesced loads as a
+    // linear chunk).  cid = the candidate's id: the position (linear) or the CSR entry
+    // ids[p] (lists), so every tie resolves by (dist, id) (CA4); list-mode rescores
+    // read the code by id from the original array (a.rcodes).
     uint32_t cid[U];
+    auto key_of = [&](uint32_t id, int64_t) -> uint32_t { return id; };
     auto load_step = [&](int64_t b, uint32_t(&dst)[U][W], uint32_t(&did)[U]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -446,7 +450,10 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             for (int i = 0; i < W; ++i) dst[u][i] = 0;
             did[u] = 0;
             if (p < c1) {
-                did[u] = (uint32_t)p;
+                // the key id: the position (linear) or its CSR entry (lists; an independent
+                // coalesced 4-byte load, prefetched with the code one step ahead)
+                if constexpr (LISTS) did[u] = __ldg(a.ids + p);
+                else did[u] = (uint32_t)p;
                 load_code<W>(codes + (size_t)p * M, dst[u]);
             }
         }
@@ -503,9 +510,10 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                             for (int k = 0; k < 4 * NO; ++k)
                                 mk |= (t[k] & 0x80008000u) >> (15 - (4 * (k >> 1) + (k & 1)));
                             mk = pos < c1 ? (mk | (mk >> 14)) & ((1u << B) - 1u) : 0u;
+                            const uint32_t kid = key_of(cid[u], pos);
                             for (uint32_t wm = __reduce_or_sync(0xffffffffu, mk); wm; wm &= wm - 1u) {
                                 const int qq = __ffs(wm) - 1;
-                                push_candidate_win((mk >> qq) & 1u, (uint64_t)cid[u], fresh + qq * NEWCAP, cnt + qq,
+                                push_candidate_win((mk >> qq) & 1u, (uint64_t)kid, fresh + qq * NEWCAP, cnt + qq,
                                                    lane, SOFT, need, ovf);
                             }
                         }
@@ -526,9 +534,11 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                     for (int qq = 0; qq < B; ++qq) mk |= (uint32_t)(dq[qq] <= thq[qq]) << qq;
                     if (pos >= c1) mk = 0;
                     // the key's distance field is replaced by the canonical rescore
-                    for (uint32_t wm = __reduce_or_sync(0xffffffffu, mk); wm; wm &= wm - 1u) {
+                    const uint32_t wmask = __reduce_or_sync(0xffffffffu, mk);
+                    const uint32_t kid = wmask ? key_of(cid[u], pos) : 0u;
+                    for (uint32_t wm = wmask; wm; wm &= wm - 1u) {
                         const int qq = __ffs(wm) - 1;
-                        push_candidate_win((mk >> qq) & 1u, (uint64_t)cid[u], fresh + qq * NEWCAP, cnt + qq, lane,
+                        push_candidate_win((mk >> qq) & 1u, (uint64_t)kid, fresh + qq * NEWCAP, cnt + qq, lane,
                                            SOFT, need, ovf);
                     }
                     continue;
@@ -558,9 +568,10 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
 #pragma unroll
                 for (int qq = 0; qq < B; ++qq) any |= d[qq] <= th[qq];
                 if (__any_sync(0xffffffffu, any && pos < c1)) {
+                    const uint32_t kid = key_of(cid[u], pos);
 #pragma unroll
                     for (int qq = 0; qq < B; ++qq)
-                        push_candidate_win(pos < c1 && d[qq] <= th[qq], make_key(d[qq], cid[u]), fresh + qq * NEWCAP,
+                        push_candidate_win(pos < c1 && d[qq] <= th[qq], make_key(d[qq], kid), fresh + qq * NEWCAP,
                                            cnt + qq, lane, SOFT, need, ovf);
                 }
             }

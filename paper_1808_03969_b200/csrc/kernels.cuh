@@ -39,8 +39,9 @@ struct ScanArgs {
     const uint32_t *qlist;  // lists: q * P + probe rank, grouped by list
     int64_t P;
     const int64_t *offsets;  // lists: CSR of the posting lists; `codes` is then the list-ordered
-                             // mirror (code of CSR position p at p * M) and key ids are positions
-    const uint32_t *ids;     // (unused by the scan kernel; list_bound_kernel reads ids into codes)
+                             // mirror (code of CSR position p at p * M)
+    const uint32_t *ids;     // lists: CSR ids (key ids of pushed candidates)
+    const uint8_t *rcodes;   // lists: the codes indexed by id (rescores)
     float *gthr;             // per-query upper bound on the global kk-th distance (optional in linear mode)
     // SDC mode (assignment): the "queries" are PQ codes qcodes[nq][M] whose
     // tables are rows of the SDC tables T (T_m[x^m][.]); the scanned codes are centres.

@@ -71,7 +71,12 @@ def test_deep10m_full_size(ref):
         St = None if S is None else torch.from_numpy(S).to(dev)
         ids, dist, used = g.query(q, topk, target_ids=St, L=L, path=path)
         torch.cuda.synchronize()
-        ids, dist = ids.cpu().numpy()[qi], dist.cpu().numpy()[qi]
+        ids, dist = ids.cpu().numpy(), dist.cpu().numpy()
+        # every row of the whole 10k batch: sorted by (dist, id) (CA4, exact ties by id), unique ids
+        lo = np.where(ids >= 0, ids, np.iinfo(np.int64).max)
+        bad = ((dist[:, 1:] < dist[:, :-1]) | ((dist[:, 1:] == dist[:, :-1]) & (lo[:, 1:] <= lo[:, :-1]))) & (ids[:, 1:] >= 0)
+        assert not bad.any(), f"{path} L={L}: {int(bad.any(1).sum())} rows not in (dist, id) order"
+        ids, dist = ids[qi], dist[qi]
         if path == "linear":
             orr = ref.linear_mt(cb, codes, qh[qi], topk, S=S)
         else:

@@ -200,6 +200,27 @@ def test_duplicate_codes_tie_break(rii, ref):
     assert np.array_equal(gr[0], orr[0]) and np.array_equal(gr[1], orr[1])
 
 
+@pytest.mark.parametrize("mode", ["list", "query"])
+def test_duplicate_codes_tie_break_ivf(rii, ref, monkeypatch, mode):
+    """Exact distance ties in the inverted index resolve to the lowest id (CA4) on
+    both traversals -- list-major items stream a list-ordered copy of the codes, so
+    their keys must carry ids, not positions -- whole and subset, across many lists
+    and the integer (u6 / u16) items."""
+    monkeypatch.setenv("RII_IVF_MODE", mode)
+    monkeypatch.setenv("RII_LIST_Q16_MIN", "64")
+    for kind, D, M in (("deep", 96, 32), ("sift", 128, 16)):
+        base = gen.base(kind, 700, D, seed=19)
+        x = np.concatenate([base] * 60)  # 42,000 rows, every code 60 times
+        q = gen.base(kind, 23, D, seed=19, stream=gen.STREAM_QUERY)
+        g, o = _build_pair(rii, ref, x, M, 12, n_iter=2, train_rows=base, train_iter=2)
+        S = gen.subset(len(x), len(x) // 2 + 11, seed=7)
+        for sub in (None, S):
+            for L in (2, 12):
+                gr = g.query(q, 100, target_ids=sub, L=L, path="ivf")
+                orr = o.query(q, 100, S=sub, L=L, path=2)
+                assert np.array_equal(gr[0], orr[0]) and np.array_equal(gr[1], orr[1]), (kind, mode, L, sub is None)
+
+
 def test_lossless_case_is_exact_knn(rii, ref):
     """C-PIN7 on the GPU: D = M, code book {0..255}, integer data -> exact kNN."""
     x = gen.lossless(6_000, 16, seed=5)

@@ -728,14 +728,14 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             // canonical rescore, top-P by (d0, k) (L6)
             ScanPlan pc = plan_linear(x->M, kkc, a.nq, x->K, x->num_sms, tables != nullptr, 1 << 30, false);
             uint64_t *cp = sc.s_cpart.get<uint64_t>((size_t)pc.nb * pc.B * pc.nc * kkc);
-            // Seed the filter with the kkc-th smallest of the group minima over all K centre
-            // codes (>= kkc groups: a valid bound on the kkc-th d0): the scan then pushes a
-            // few hundred candidates per query instead of starting from +inf and compacting
-            // its way down (RII_COARSE_BOUND=0 disables, A/B)
+            // RII_COARSE_BOUND=1 (A/B, off): seed the filter with the kkc-th smallest of the
+            // group minima over all K centre codes (>= kkc groups: a valid bound on the
+            // kkc-th d0).  Fewer pushes, but the bound pass costs more than it saves
+            // (deep10m L = 64 13.22 -> 13.37 ms, L = 1 2.79 -> 3.05 ms).
             float *cg = nullptr;
             const char *cbe = getenv("RII_COARSE_BOUND");
             const int64_t cgs = ceil_div(x->K, 1024);
-            if (tables && pc.fast && kkc <= 512 && x->K / cgs >= kkc && !(cbe && cbe[0] == '0')) {
+            if (tables && pc.fast && kkc <= 512 && x->K / cgs >= kkc && cbe && cbe[0] == '1') {
                 cg = sc.s_bound.get<float>(a.nq);
                 launch_group_min_bound(x->centers.as<uint8_t>(), x->K, x->M, tables, a.nq, kkc, cg, st);
             }

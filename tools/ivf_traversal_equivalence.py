@@ -1,5 +1,9 @@
-"""Probe: list-major vs query-major IVF on deep10m subsets; for the queries whose
-results differ, which path matches the oracle (and by how much)."""
+"""Equivalence probe at full size (deep10m, 10k queries): the list-major and the
+query-major inverted-index traversals must return identical results (both are
+exact); for any query where they differ, which one matches the oracle and how.
+(Found the round-2 tie-order bug of list-major keys: 26 of 10k queries.)
+
+    python tools/ivf_traversal_equivalence.py"""
 import os
 import sys
 
@@ -27,9 +31,9 @@ q = bench._device_data(kind, nq, D, dev, 0, gen.STREAM_QUERY)
 qh = q.cpu().numpy()
 off, ids = g.get_postings()
 cen = g.get_centers()
-for frac, L in ((0.1, 64),):
-    S = gen.subset_torch(N, int(N * frac), dev, seed=0)
-    Sh = S.cpu().numpy()
+for frac, L in ((0.1, 64), (0.01, 64), (None, 64), (None, 16)):
+    S = None if frac is None else gen.subset_torch(N, int(N * frac), dev, seed=0)
+    Sh = None if S is None else S.cpu().numpy()
     out = {}
     for mode in ("query", "list"):
         os.environ["RII_IVF_MODE"] = mode

@@ -216,6 +216,14 @@ def main():
              roofline={"bound": "alu (shared-memory LUT pipe)", "peak_lookups_per_s": peak,
                        "frac": lookups / (kernel_ms / 1e3) / peak,
                        "code_bytes_per_launch": N * M, "note": "u16 fixed-point tables, 8 queries per CTA (M = 8)"})
+    if "latency" in only:  # small batches (serving): deep10m, time per call for nq in {1, 16, 128, 1024}
+        kind, N, D, M, nlist, nq, topk, n_train, _ = bench.WORKLOADS["deep10m"]
+        g, b = build(kind, N, D, M, nlist, n_train)
+        q = bench._device_data(kind, 1024, D, DEV, 0, gen.STREAM_QUERY)
+        for n in (1, 16, 128, 1024):
+            for path, L in (("linear", 1), ("ivf", 16), ("ivf", 64)):
+                ms = timed(lambda: g.query(q[:n], topk, None, L=L, path=path), max(a.reps, 5))
+                emit(config="latency", row=f"deep10m nq={n} {path} L={L}", nq=n, ms=ms, qps=n / ms * 1e3)
     if "deep10m" in only:
         kind, N, D, M, nlist, nq, topk, n_train, _ = bench.WORKLOADS["deep10m"]
         g, b = build(kind, N, D, M, nlist, n_train)

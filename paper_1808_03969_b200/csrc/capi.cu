@@ -871,7 +871,7 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
                 float *qsc = sc.s_qscale.get<float>(a.nq);
                 if (list_u6_cfg(x->M) >= 3) {  // u6 oct items
                     uint8_t *t8 = sc.s_tab16.get<uint8_t>((size_t)a.nq * lut_q_floats(x->M));
-                    launch_u6_tables(tables, gthr, a.nq, x->M, t8, qsc, st);
+                    launch_u6_tables(tables, gthr, a.nq, x->M, t8, qsc, st, list_u7(x->M));
                     sa.qtab8 = t8;
                 } else {
                     uint16_t *t16 = sc.s_tab16.get<uint16_t>((size_t)a.nq * LUT_Q_FLOATS);

@@ -100,9 +100,11 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     static_assert(!FIXB || U6, "the fixed-base layout is implemented for the u6 tables");
     // u6 options (VARIANT bit 0: 5-bit entries summed over 8 steps; bit 1: two table
     // copies so that the code-word permutation needs one select stage, M = 32 only)
-    constexpr int U6_GJ = ((VARIANT & 1) && M >= 8) ? 8 : 4;
+    // (VARIANT bit 8: 7-bit entries, pairs of steps summed bytewise -- finer steps, so
+    // the filter passes fewer false candidates, for more widening work)
+    constexpr int U6_GJ = ((VARIANT & 1) && M >= 8) ? 8 : (VARIANT & 256) ? 2 : 4;
     constexpr bool U6_R2 = U6 && (VARIANT & 2) && M == 32;
-    constexpr float U6_CAP = U6_GJ == 8 ? 31.0f : 63.0f;
+    constexpr float U6_CAP = U6_GJ == 8 ? 31.0f : U6_GJ == 2 ? 127.0f : 63.0f;
     constexpr int H = lut_halves(M), LQF = lut_q_floats(M);  // M = 64: two 32-subspace halves
     static_assert(H == 1 || TAB == 0 || TAB == 3, "M = 64 runs the fp32-pair and u6 tables");
     constexpr int NO = U6 ? B / 8 : 1;  // u6 oct tables (B = 16: two, fixed-base layout, 384 threads)
@@ -892,6 +894,15 @@ static bool fixed_base_ok() {
     return ok;
 }
 bool smem_fixed_base_ok() { return fixed_base_ok(); }
+// 7-bit list-item entries (M = 32; RII_LIST_U7=0 disables): steps twice as fine at the
+// same saturation point, pairs of steps summed bytewise (2 * 127 < 256) -- more widening
+// work, but the integer items are push-bound, and the finer filter passes fewer false
+// candidates (deep10m phase B: 9.6M -> 7.4M pushes; L = 64 13.2 -> 12.6 ms, L = 16 8.7
+// -> 8.2, L = 4 5.5 -> 5.1).  The per-query tables are then written with cap 127.
+bool list_u7(int M) {
+    const char *e = getenv("RII_LIST_U7");
+    return M == 32 && !(e && atoi(e) == 0);
+}
 int list_u6_cfg(int M) {
     if (!fixed_base_ok()) return 0;
     if (M == 64) return 3;  // two halves: only the u6 items fit (128 KB)
@@ -969,6 +980,10 @@ static void *fast_kernel_ptr_b(bool q16, int nth) {
     if constexpr (B == 8) {
         if constexpr (LISTS) {
             if (q16) {
+                if (list_u6_cfg(M) >= 3 && list_u7(M)) {
+                    if (nth == 192) return (void *)scan_fast_kernel<M, 8, true, 192, 1, 3, 256 | 128 | 64>;
+                    return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 256 | 128 | 64>;
+                }
                 if (list_u6_cfg(M) >= 3 && nth == 192)
                     return (void *)scan_fast_kernel<M, 8, true, 192, 1, 3, 128 | 64>;
                 if (list_u6_cfg(M) >= 3) return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64>;
@@ -1485,31 +1500,32 @@ __global__ void __launch_bounds__(256) q16_tables_kernel(const float *__restrict
 template <int M>
 __global__ void __launch_bounds__(256) u6_tables_kernel(const float *__restrict__ tables, const float *__restrict__ gthr,
                                                         int64_t nq, uint8_t *__restrict__ out, float *__restrict__ scale,
-                                                        float amul) {
+                                                        float amul, float cap) {
     const int64_t q = blockIdx.x;
-    const float s = __fdiv_rd(63.0f * u6_alpha(M) * amul, fmaxf(__ldcg(gthr + q), 1e-30f));
+    const float s = __fdiv_rd(cap * u6_alpha(M) * amul, fmaxf(__ldcg(gthr + q), 1e-30f));
     if (threadIdx.x == 0) scale[q] = s;
     const float4 *t4 = reinterpret_cast<const float4 *>(tables + q * lut_q_floats(M));
     uint32_t *o = reinterpret_cast<uint32_t *>(out + q * lut_q_floats(M));
     for (int e = threadIdx.x; e < lut_q_floats(M) / 4; e += blockDim.x) {
         const float4 v = __ldg(t4 + e);
-        o[e] = u6_entry(v.x, s, 63.f) | (u6_entry(v.y, s, 63.f) << 8) | (u6_entry(v.z, s, 63.f) << 16) |
-               (u6_entry(v.w, s, 63.f) << 24);
+        o[e] = u6_entry(v.x, s, cap) | (u6_entry(v.y, s, cap) << 8) | (u6_entry(v.z, s, cap) << 16) |
+               (u6_entry(v.w, s, cap) << 24);
     }
 }
 
 void launch_u6_tables(const float *tables, const float *gthr, int64_t nq, int M, uint8_t *out, float *scale,
-                      cudaStream_t st) {
+                      cudaStream_t st, bool u7) {
+    const float cap = u7 ? 127.f : 63.f;
     if (nq <= 0) return;
     // list items' saturation scale multiplier (RII_U6_LIST_AMUL, A/B): the phase-A bound is tight
     const char *e = getenv("RII_U6_LIST_AMUL");
     const float amul = e ? (float)atof(e) : 1.0f;
     switch (M) {
-        case 4: u6_tables_kernel<4><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul); break;
-        case 8: u6_tables_kernel<8><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul); break;
-        case 16: u6_tables_kernel<16><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul); break;
-        case 64: u6_tables_kernel<64><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul); break;
-        default: u6_tables_kernel<32><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul); break;
+        case 4: u6_tables_kernel<4><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul, cap); break;
+        case 8: u6_tables_kernel<8><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul, cap); break;
+        case 16: u6_tables_kernel<16><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul, cap); break;
+        case 64: u6_tables_kernel<64><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul, cap); break;
+        default: u6_tables_kernel<32><<<(unsigned)nq, 256, 0, st>>>(tables, gthr, nq, out, scale, amul, cap); break;
     }
     RII_LAUNCHED();
 }

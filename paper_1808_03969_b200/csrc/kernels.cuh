@@ -96,7 +96,8 @@ void launch_list_bound(const uint8_t *codes, int M, const int4 *items, int64_t n
                        float *gthr, cudaStream_t st);
 bool q16_is_u6(int M);  // the linear integer-table kernel of this M uses u6 tables
 void launch_u6_tables(const float *tables, const float *gthr, int64_t nq, int M, uint8_t *out, float *scale,
-                      cudaStream_t st);
+                      cudaStream_t st, bool u7 = false);
+bool list_u7(int M);  // list items on 7-bit entries (RII_LIST_U7)
 void launch_strided_gather(const uint8_t *codes, int M, int64_t stride, int64_t n, uint8_t *out, cudaStream_t st);
 void launch_kth_bound(const uint64_t *keys, int64_t nq, int kk, float *bound, cudaStream_t st);
 // gthr[q] = an upper bound on the kk-th distance over the ns sample codes (the kk-th

@@ -509,9 +509,10 @@ template <int M, int GJ, bool R2, int BASE, int NO, int PLIM>
 __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, const uint32_t (&sel)[4],
                                        const uint32_t (&colv)[M / 4 < 8 ? M / 4 : 8], uint32_t one,
                                        uint32_t (&acc)[4 * NO]) {
-    // GJ steps (4: 6-bit entries, 8: 5-bit entries) are summed bytewise before widening;
-    // NO oct tables (8 queries each) 64 KB apart share the offsets of every step
-    constexpr int W = M / 4, GW = GJ / 4;
+    // GJ steps (2: 7-bit entries, 4: 6-bit entries, 8: 5-bit entries) are summed bytewise
+    // before widening; NO oct tables (8 queries each) 64 KB apart share the offsets of
+    // every step
+    constexpr int W = M / 4, GW = GJ >= 4 ? GJ / 4 : 1;
     static_assert(W % GW == 0, "word groups");
     uint32_t wp[W];
 #pragma unroll
@@ -551,13 +552,35 @@ __device__ __forceinline__ void adc_u6(const uint32_t (&w)[M / 4], uint32_t rw, 
                 uint2 v[4];
 #pragma unroll
                 for (int t = 0; t < 4; ++t) v[t] = lds(off[t], aw, o);
-                // bytewise (GJ * cap < 256, no carries), as a tree: dependency depth 2
-                const uint32_t x0 = fma_add(fma_add(v[0].x, one, v[1].x), one, fma_add(v[2].x, one, v[3].x));
-                const uint32_t x1 = fma_add(fma_add(v[0].y, one, v[1].y), one, fma_add(v[2].y, one, v[3].y));
-                s0[o] = h == 0 ? x0 : fma_add(x0, one, s0[o]);
-                s1[o] = h == 0 ? x1 : fma_add(x1, one, s1[o]);
+                if constexpr (GJ == 2) {
+                    // 7-bit entries: pairs of steps summed bytewise (2 * 127 < 256), each pair
+                    // widened into the 16-bit lanes on its own
+                    uint32_t *ac = acc + 4 * o;
+#pragma unroll
+                    for (int pr = 0; pr < 2; ++pr) {
+                        const uint32_t y0 = fma_add(v[2 * pr].x, one, v[2 * pr + 1].x);
+                        const uint32_t y1 = fma_add(v[2 * pr].y, one, v[2 * pr + 1].y);
+                        const uint32_t e0 = y0 & 0x00ff00ffu, o0 = __byte_perm(y0, 0u, 0x4341);
+                        const uint32_t e1 = y1 & 0x00ff00ffu, o1 = __byte_perm(y1, 0u, 0x4341);
+                        if (g == 0 && pr == 0) {
+                            ac[0] = e0; ac[1] = o0; ac[2] = e1; ac[3] = o1;
+                        } else {
+                            ac[0] = fma_add(e0, one, ac[0]);
+                            ac[1] = fma_add(o0, one, ac[1]);
+                            ac[2] = fma_add(e1, one, ac[2]);
+                            ac[3] = fma_add(o1, one, ac[3]);
+                        }
+                    }
+                } else {
+                    // bytewise (GJ * cap < 256, no carries), as a tree: dependency depth 2
+                    const uint32_t x0 = fma_add(fma_add(v[0].x, one, v[1].x), one, fma_add(v[2].x, one, v[3].x));
+                    const uint32_t x1 = fma_add(fma_add(v[0].y, one, v[1].y), one, fma_add(v[2].y, one, v[3].y));
+                    s0[o] = h == 0 ? x0 : fma_add(x0, one, s0[o]);
+                    s1[o] = h == 0 ? x1 : fma_add(x1, one, s1[o]);
+                }
             }
         }
+        if constexpr (GJ == 2) continue;  // accumulated per pair of steps above
 #pragma unroll
         for (int o = 0; o < NO; ++o) {
             const uint32_t e0 = s0[o] & 0x00ff00ffu, o0 = __byte_perm(s0[o], 0u, 0x4341);

@@ -124,12 +124,13 @@ def test_ivf_list_major_and_query_major(rii, ref, monkeypatch, mode, kind, N, D,
                 g4 = g.query(q, 100, target_ids=sub, L=L, path="ivf")
                 monkeypatch.delenv("RII_LIST_BOUND")
                 assert np.array_equal(gr[0], g4[0]) and np.array_equal(gr[1], g4[1])
-                if M == 32:  # u6 items of 8 (RII_LIST_U6=3) and 16 queries (=4)
-                    for cfg in ("3", "4"):
-                        monkeypatch.setenv("RII_LIST_U6", cfg)
+                if M == 32:  # u6 items of 8 (RII_LIST_U6=3) and 16 queries (=4); 7-bit items
+                    for var, cfg in (("RII_LIST_U6", "3"), ("RII_LIST_U6", "4"), ("RII_LIST_U7", "0"),
+                                     ("RII_LIST_NTH", "192"), ("RII_LIST_NTH", "384")):
+                        monkeypatch.setenv(var, cfg)
                         g3 = g.query(q, 100, target_ids=sub, L=L, path="ivf")
-                        monkeypatch.delenv("RII_LIST_U6")
-                        assert np.array_equal(gr[0], g3[0]) and np.array_equal(gr[1], g3[1]), cfg
+                        monkeypatch.delenv(var)
+                        assert np.array_equal(gr[0], g3[0]) and np.array_equal(gr[1], g3[1]), (var, cfg)
 
 
 def test_device_memory_path_matches_host_path(rii, ref):

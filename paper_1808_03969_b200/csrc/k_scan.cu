@@ -1585,15 +1585,17 @@ __global__ void __launch_bounds__(NT) merge_kernel(const uint64_t *__restrict__ 
     uint64_t *top = msm, *prt = msm + kk;
     const int64_t q = blockIdx.x;
     const uint64_t *base = keys + q * q_stride;
+    uint64_t *first = prt + kk;  // every part's first key, loaded in one round trip
     for (int i = threadIdx.x; i < kk; i += blockDim.x) top[i] = KEY_MAX;
+    for (int p = threadIdx.x; p < parts; p += blockDim.x) first[p] = __ldg(base + (int64_t)p * p_stride);
     __syncthreads();
     for (int p = 0; p < parts; ++p) {
         // A part whose smallest key (its first: parts are sorted ascending) is not below
-        // the current kk-th key cannot change the list: one broadcast load, and the
-        // block skips it without a barrier (top is final since the last barrier).  An
-        // empty part may hold only its first key (KEY_MAX; list items write no more).
+        // the current kk-th key cannot change the list: the block skips it without a
+        // barrier (top is final since the last barrier).  An empty part may hold only
+        // its first key (KEY_MAX; list items write no more).
         const uint64_t *src = base + (int64_t)p * p_stride;
-        if (__ldg(src) >= top[kk - 1]) continue;
+        if (first[p] >= top[kk - 1]) continue;
         for (int i = threadIdx.x; i < kk; i += blockDim.x) prt[i] = src[i];
         __syncthreads();
         for (int i = threadIdx.x; i < kk; i += blockDim.x) {
@@ -1649,7 +1651,9 @@ void launch_merge(const uint64_t *keys, int64_t q_stride, int64_t p_stride, int 
                   const Rescore &rs) {
     if (nq <= 0) return;
     KernelTimer t(TK_MERGE, st);
-    merge_kernel<<<(unsigned)nq, NT, (size_t)2 * kk * 8, st>>>(keys, q_stride, p_stride, parts, kk, topk, map,
+    const size_t smem = (size_t)(2 * kk + parts) * 8;
+    if (smem > 48 * 1024) RII_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    merge_kernel<<<(unsigned)nq, NT, smem, st>>>(keys, q_stride, p_stride, parts, kk, topk, map,
                                                                out_ids, out_dist, out_keys, rs);
     RII_LAUNCHED();
 }

@@ -634,9 +634,13 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             const int nct = nc1 + nc2;
             uint64_t *pp = sc.s_part.get<uint64_t>((size_t)ceil_div(a.nq, 8) * 8 * nct * kk);
             launch_large_u6_linear(scan_codes, 0, n1, x->M, qt, qsc, tables, gthr, a.nq, kk, nc1, pp, nct, 0, st);
+            tr.mark("large u6 pass 1");
             if (n2 > 0) {
                 launch_merge(pp, (int64_t)nct * kk, kk, nc1, a.nq, kk, kk, IdMap(), nullptr, nullptr, sk, st);
-                launch_kth_bound(sk, a.nq, kk, gthr, st);
+                // min with the sample bound: pass 1 may have kept fewer than kk candidates
+                // of a query (its filter already had the sample bound), then its kk-th is +inf
+                merged_bound_kernel<<<(unsigned)ceil_div(a.nq, 256), 256, 0, st>>>(sk, a.nq, kk, gthr);
+                RII_LAUNCHED();
                 launch_u6_tables_large(tables, gthr, a.nq, x->M, qt, qsc, st);
                 launch_large_u6_linear(scan_codes, n1, n2, x->M, qt, qsc, tables, gthr, a.nq, kk, nc2, pp, nct, nc1,
                                        st);

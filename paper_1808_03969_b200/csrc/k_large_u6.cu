@@ -35,6 +35,15 @@ constexpr int LU_B = 8;      // queries per CTA (one oct table)
 constexpr int LU_U = 8;      // codes per thread per tile
 constexpr int LU_CH = 32;    // subspaces per chunk
 constexpr int LU_CHB = KS * LU_CH;  // bytes of one query's u6 table chunk: [256][32]
+// 7-bit entries (cap 127, pairs of steps summed bytewise): half the filter's floor
+// error of 6-bit entries at the same saturation point; lane sums <= M * 127 < 2^15 for
+// M <= 256.  The filter's slack is what the rescores pay for (see below).
+static_assert(256 * 127 < 32768, "SWAR lanes");
+// RII_LARGE_U7=0: 6-bit entries (A/B)
+bool large_u7() {
+    const char *e = getenv("RII_LARGE_U7");
+    return !(e && atoi(e) == 0);
+}
 
 struct LargeU6Args {
     const uint8_t *codes;
@@ -65,16 +74,16 @@ __host__ __device__ constexpr size_t lu_aux_bytes(int kk) {
 __global__ void __launch_bounds__(256) u6_tables_large_kernel(const float *__restrict__ tables,
                                                               const float *__restrict__ gthr, int64_t nq, int M,
                                                               int nch, uint8_t *__restrict__ out,
-                                                              float *__restrict__ scale, float amul) {
+                                                              float *__restrict__ scale, float amul, float cap) {
     const int64_t qp = blockIdx.x, q = qp < nq ? qp : nq - 1;
-    const float s = __fdiv_rd(63.0f * u6_alpha(M) * amul, fmaxf(__ldcg(gthr + q), 1e-30f));
+    const float s = __fdiv_rd(cap * u6_alpha(M) * amul, fmaxf(__ldcg(gthr + q), 1e-30f));
     if (threadIdx.x == 0 && qp < nq) scale[q] = s;
     const float *tq = tables + q * (int64_t)M * KS;
     uint8_t *o = out + (qp >> 3) * (int64_t)nch * OCT_BYTES + (qp & 7);
     for (int e = threadIdx.x; e < nch * LU_CHB; e += blockDim.x) {
         const int c = e / LU_CHB, r = e - c * LU_CHB, z = r / LU_CH, j = r - z * LU_CH, m = c * LU_CH + j;
         o[(int64_t)c * OCT_BYTES + (int64_t)r * 8] =
-            m < M ? (uint8_t)u6_entry(__ldg(tq + (int64_t)m * KS + z), s, 63.f) : (uint8_t)0;
+            m < M ? (uint8_t)u6_entry(__ldg(tq + (int64_t)m * KS + z), s, cap) : (uint8_t)0;
     }
 }
 
@@ -124,7 +133,7 @@ __device__ __noinline__ void lu_compact(uint64_t *top, uint64_t *fresh, int *cnt
     __syncthreads();
 }
 
-template <int NTH>
+template <int NTH, int LU_GJ>
 __global__ void __launch_bounds__(NTH, 1) scan_large_u6_kernel(const LargeU6Args a) {
     constexpr int B = LU_B, U = LU_U, STEP = NTH;
     static_assert(NEWCAP >= STEP, "one round of pushes must fit the fresh buffer");
@@ -239,8 +248,8 @@ __global__ void __launch_bounds__(NTH, 1) scan_large_u6_kernel(const LargeU6Args
             for (int u = 0; u < U; ++u) {
                 if (u + 1 < U) load_w(u + 1, wn);
                 uint32_t s6[4];
-                if (g & 1) adc_u6<32, 4, false, 0x400 + OCT_BYTES, 1, 4>(w, rw, sel, colv, a.one, s6);
-                else adc_u6<32, 4, false, 0x400, 1, 4>(w, rw, sel, colv, a.one, s6);
+                if (g & 1) adc_u6<32, LU_GJ, false, 0x400 + OCT_BYTES, 1, 4>(w, rw, sel, colv, a.one, s6);
+                else adc_u6<32, LU_GJ, false, 0x400, 1, 4>(w, rw, sel, colv, a.one, s6);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) acc[u][k] = fma_add(s6[k], a.one, acc[u][k]);
                 if (u + 1 < U) {
@@ -253,6 +262,9 @@ __global__ void __launch_bounds__(NTH, 1) scan_large_u6_kernel(const LargeU6Args
         // complete sums: SWAR threshold test (lanes <= M * 63 < 2^15), pushes by round
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+            // every push of the previous round must have landed before the fill is read
+            // (reading it before the barrier let two rounds of pushes overflow the buffer)
+            __syncthreads();
             if (__syncthreads_or(tid < B && cnt[tid] > NEWCAP - STEP)) compact();
             const int64_t p = tile + u * STEP + tid;
             uint32_t t[4], tor = 0;
@@ -304,7 +316,8 @@ void launch_u6_tables_large(const float *tables, const float *gthr, int64_t nq, 
     const char *e = getenv("RII_LARGE_U6_AMUL");
     const float amul = e ? (float)atof(e) : 1.0f;
     u6_tables_large_kernel<<<(unsigned)(ceil_div(nq, LU_B) * LU_B), 256, 0, st>>>(tables, gthr, nq, M, large_u6_nch(M),
-                                                                                   out, scale, amul);
+                                                                                   out, scale, amul,
+                                                                                   large_u7() ? 127.f : 63.f);
     RII_LAUNCHED();
 }
 
@@ -333,9 +346,10 @@ void launch_large_u6_linear(const uint8_t *codes, int64_t base, int64_t n_codes,
     a.nc_out = nc_out; a.ci_off = ci_off;
     a.qtab8 = qtab8; a.qscale = qscale; a.tables = tables; a.gthr = gthr; a.out = out; a.one = 1;
     const size_t smem = large_u6_smem(kk);
-    RII_CUDA(cudaFuncSetAttribute(scan_large_u6_kernel<LU_NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kern = large_u7() ? scan_large_u6_kernel<LU_NTH, 2> : scan_large_u6_kernel<LU_NTH, 4>;
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     KernelTimer t(TK_LINEAR, st), tu(TK_U6, st);
-    scan_large_u6_kernel<LU_NTH><<<(unsigned)(a.nb * nc), LU_NTH, smem, st>>>(a);
+    kern<<<(unsigned)(a.nb * nc), LU_NTH, smem, st>>>(a);
     RII_LAUNCHED();
 }
 

@@ -105,6 +105,9 @@ WORKLOADS = {
     # the paper's GIST1M setting (Table 2: K = 1000, M = 240, L = 8000 candidates)
     "gist1m": ("deep", 1_000_000, 960, 240, 1000, 10_000, 100, 100_000,
                "paper Table 2 shape: GIST1M-like 1M x 960, M=240, nlist=1000, 10k queries, top-100"),
+    # configs[4]'s code shape (M = 8) at configs[2]'s size, for A/B of the M = 8 kernels
+    "deep10m_m8": ("deep", 10_000_000, 96, 8, 3162, 10_000, 100, 100_000,
+                   "configs[4] shape at 10M: Deep1B-like 10M x 96, M=8, nlist=3162, 10k queries, top-100"),
     "tiny": ("gaussian", 10_000, 32, 4, 100, 100, 10, 10_000,
              "BASELINE.json configs[0]: N(0,1) 10k x 32, M=4, nlist=100, 100 queries, top-10"),
 }

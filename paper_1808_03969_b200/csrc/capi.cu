@@ -776,7 +776,12 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             // first with fp32 / bf16 tables and publish each query's kk-th distance as its
             // bound; the remaining pairs run with u16 tables scaled by those bounds.
             const int64_t r0 = std::max<int64_t>(1, std::min<int64_t>(P, ceil_div(4 * kk, (int64_t)std::max(avg_len, 1.0))));
-            const bool q16l = q16_enabled() && q16_supported(kk) && P > r0 && avg_len >= list_q16_min_len() &&
+            // integer phases when the lists are long, or half as long but probed many times
+            // (sift1m, lists of 1000 codes: L = 64 12.0 -> 7.1 ms on 7-bit items; L = 16
+            // 5.0 -> 5.4 ms, so not there)
+            const double qmin = list_q16_min_len();
+            const bool q16l = q16_enabled() && q16_supported(kk) && P > r0 &&
+                              (avg_len >= qmin || (avg_len >= qmin / 2 && P >= 32)) &&
                               (lut_halves(x->M) == 1 || list_u6_cfg(x->M) == 3);  // M = 64 needs the u6 items
             // Integer phases over growing rank ranges (RII_LIST_PHASES = the first rank of
             // each integer phase, e.g. "1,4,16"; default: one integer phase from r0).  Before

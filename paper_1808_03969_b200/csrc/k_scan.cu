@@ -901,13 +901,17 @@ bool smem_fixed_base_ok() { return fixed_base_ok(); }
 // -> 8.2, L = 4 5.5 -> 5.1).  The per-query tables are then written with cap 127.
 bool list_u7(int M) {
     const char *e = getenv("RII_LIST_U7");
-    return M == 32 && !(e && atoi(e) == 0);
+    return (M == 32 || M == 16 || M == 8) && !(e && atoi(e) == 0);
 }
 int list_u6_cfg(int M) {
     if (!fixed_base_ok()) return 0;
     if (M == 64) return 3;  // two halves: only the u6 items fit (128 KB)
     const char *e = getenv("RII_LIST_U6");
-    return M != 32 ? 0 : e ? atoi(e) : 3;
+    if (M == 32) return e ? atoi(e) : 3;
+    // M = 16 and 8: 7-bit oct items too (sift1m L = 64: u16 items 10.2 ms, 7-bit 7.1, 6-bit
+    // 7.5; deep10m shape at M = 8, L = 64: u16 11.3 -> 9.1 ms, L = 16 6.1 -> 6.0 ms)
+    if (M == 16 || M == 8) return e ? atoi(e) : 3;
+    return 0;
 }
 
 #endif  // !RII_SCAN_M

@@ -15,6 +15,11 @@ namespace rii {
 constexpr int KS = 256;                      // code words per subspace
 constexpr uint64_t KEY_MAX = ~0ull;          // empty candidate slot
 constexpr int NT = 256;                      // threads per CTA of the scan kernels
+// The dynamic shared memory attribute of every kernel is set to the device limit, not
+// to one launch's size: concurrent callers (rii.h "Concurrency") launching the same
+// kernel with different sizes would otherwise race (one thread's smaller setting
+// undercuts the other's launch: cudaLaunchKernel "invalid argument").
+constexpr int SMEM_ATTR_MAX = 227 * 1024;
 
 // ---------------------------------------------------------------- errors ---
 #define RII_CUDA(call)                                                                            \

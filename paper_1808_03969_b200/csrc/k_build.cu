@@ -43,7 +43,7 @@ void launch_encode(const float *x, int64_t n, int D, int M, const float *cb, uin
     if (n <= 0) return;
     const int ds = D / M;
     const size_t smem = (size_t)2 * KS * ds * 4;
-    RII_CUDA(cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RII_CUDA(cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     dim3 grid((unsigned)ceil_div(n, 256), (unsigned)M);
     encode_kernel<<<grid, 256, smem, st>>>(x, n, D, M, ds, cb, codes);
     RII_LAUNCHED();
@@ -122,7 +122,7 @@ static void launch_assign_canonical(const uint8_t *codes, int64_t n, const uint8
     if (Bc > 64) Bc = 64;
     if (Bc > K) Bc = (int)K;
     const size_t smem = (size_t)Bc * M * KS * 4 + (size_t)256 * AR * M;
-    RII_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RII_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     assign_kernel<<<(unsigned)ceil_div(n, 256 * AR), 256, smem, st>>>(codes, n, centers, K, M, T, Bc, assign, dist);
     RII_LAUNCHED();
 }
@@ -245,7 +245,7 @@ static void assign_fast_t(const uint8_t *codes, int64_t n, const float *tables, 
                           unsigned long long *fb_n, cudaStream_t st) {
     auto kern = assign_fast_kernel<M>;
     const size_t smem = (size_t)3 * LUT_PAIR_BYTES;
-    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     kern<<<(unsigned)ceil_div(n, 256 * ar2<M>()), 256, smem, st>>>(codes, n, tables, K, T, centers, assign, dist, fb,
                                                               fb_n);
     RII_LAUNCHED();
@@ -761,7 +761,7 @@ void run_train(const float *x, int64_t n, int D, int M, int n_iter, uint64_t see
     void *tmp = nullptr;
     RII_CUDA(cudaMallocAsync(&tmp, tb, st));
     const size_t smem = (size_t)KS * ds * 8 + KS * 8 + (size_t)KS * ds * 4;
-    RII_CUDA(cudaFuncSetAttribute(train_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RII_CUDA(cudaFuncSetAttribute(train_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     const unsigned ablocks = (unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 4);
     for (int m = 0; m < M; ++m) {
         float *c = cb + (size_t)m * KS * ds;

@@ -66,7 +66,7 @@ void launch_coarse_dist(const uint8_t *centers, int64_t K, int M, const float *q
                         float *d0, cudaStream_t st) {
     if (nq <= 0 || K <= 0) return;
     const size_t smem = (size_t)CQ * CMC * KS * 4;
-    RII_CUDA(cudaFuncSetAttribute(coarse_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RII_CUDA(cudaFuncSetAttribute(coarse_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     dim3 grid((unsigned)ceil_div(K, NT), (unsigned)ceil_div(nq, CQ));
     coarse_dist_kernel<<<grid, NT, smem, st>>>(centers, K, M, q, nq, cb, D / M, d0);
     RII_LAUNCHED();
@@ -500,7 +500,7 @@ static void ivf_launch_t(const uint8_t *codes, int Mrt, const float *q, int64_t 
                          cudaStream_t st, const float *tables, const int32_t *take) {
     const size_t smem = ivf_smem(Mrt, kk);
     auto kern = ivf_scan_kernel<M, FAST>;
-    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     KernelTimer t(TK_IVF, st);
     kern<<<(unsigned)ceil_div(nq, 2), NT, smem, st>>>(codes, q, nq, cb, Mrt, ds, kk, probes, P, offsets, ids, out,
                                                       FAST ? tables : nullptr, take);

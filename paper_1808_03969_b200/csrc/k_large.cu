@@ -155,7 +155,7 @@ static void launch_large(const LargeArgs &a, int64_t grid, cudaStream_t st, int 
     if (grid <= 0) return;
     const size_t smem = large_smem(a.M, a.kk);
     if (smem > 227 * 1024) throw Error(1, "topk too large for the large-M scan");
-    RII_CUDA(cudaFuncSetAttribute(scan_large_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RII_CUDA(cudaFuncSetAttribute(scan_large_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     KernelTimer t(timer, st);
     scan_large_kernel<MODE><<<(unsigned)grid, NT, smem, st>>>(a);
     RII_LAUNCHED();

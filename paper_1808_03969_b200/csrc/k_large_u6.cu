@@ -347,7 +347,7 @@ void launch_large_u6_linear(const uint8_t *codes, int64_t base, int64_t n_codes,
     a.qtab8 = qtab8; a.qscale = qscale; a.tables = tables; a.gthr = gthr; a.out = out; a.one = 1;
     const size_t smem = large_u6_smem(kk);
     auto kern = large_u7() ? scan_large_u6_kernel<LU_NTH, 2> : scan_large_u6_kernel<LU_NTH, 4>;
-    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     KernelTimer t(TK_LINEAR, st), tu(TK_U6, st);
     kern<<<(unsigned)(a.nb * nc), LU_NTH, smem, st>>>(a);
     RII_LAUNCHED();

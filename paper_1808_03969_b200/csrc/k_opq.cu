@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(128) rotate_kernel(const float *__restrict__ R
 void launch_rotate(const float *Rt, const float *x, int64_t n, int D, float *y, cudaStream_t st) {
     if (n <= 0) return;
     const size_t smem = (size_t)ROT_VT * D * 4;
-    RII_CUDA(cudaFuncSetAttribute(rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RII_CUDA(cudaFuncSetAttribute(rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     dim3 grid((unsigned)ceil_div(D, 128), (unsigned)ceil_div(n, ROT_VT));
     rotate_kernel<<<grid, 128, smem, st>>>(Rt, x, n, D, y);
     RII_LAUNCHED();

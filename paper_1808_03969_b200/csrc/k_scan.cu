@@ -858,8 +858,9 @@ static int q16_cfg(int M) {
     const char *e = getenv("RII_Q16_CFG");
     if (M == 64) return 4;  // two halves: u6 oct tables, one copy
     // M = 32: 9 = 16 queries per CTA (two oct tables, fixed-base layout; 117 ms on deep10m),
-    // 7 = 8 queries with two table copies (127 ms)
-    return e ? atoi(e) : (M == 32 ? 9 : 0);
+    // 7 = 8 queries with two table copies (127 ms).  M = 16 and 8 too (round 2: sift1m
+    // linear, M = 16, u16 13.0 -> 11.0 ms; the deep10m shape at M = 8 93.8 -> 48.9 ms)
+    return e ? atoi(e) : ((M == 32 || M == 16 || M == 8) ? 9 : 0);
 }
 // M = 64 u6 linear kernel threads (RII_M64_NTH: 384 spills ~200 B of code words and
 // took 52.9 ms on sift1m_m64; 256 does not spill: 43.5 ms)
@@ -1015,7 +1016,7 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
     const bool q16 = (B == 8 || B == 16) && q16_req && gthr != nullptr;
     void *kern = fast_kernel_ptr<M, B, false>(q16);
     const size_t smem = q16 && B == 8 ? smem_q16(kk) : pl.smem;
-    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     ScanArgs a{};
     a.codes = codes; a.n_codes = n; a.q = q; a.nq = nq; a.cb = cb; a.ds = ds; a.kk = kk;
     a.nb = pl.nb; a.chunk = pl.chunk; a.nc = pl.nc; a.out = out; a.tables = tables;
@@ -1046,7 +1047,7 @@ template <int B>
 static void launch_generic_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, int M, const float *q, int64_t nq,
                              const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st) {
     auto kern = scan_generic_kernel<B>;
-    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     KernelTimer t(TK_LINEAR, st);
     kern<<<pl.nb * pl.nc, NT, pl.smem, st>>>(codes, n, q, nq, cb, M, ds, kk, pl.nb, pl.chunk, pl.nc, out);
     RII_LAUNCHED();
@@ -1077,7 +1078,7 @@ static void launch_list_t(const ScanArgs &a, int64_t n_items, cudaStream_t st, b
     void *kern = fast_kernel_ptr<M, B, true>(q16, nth);
     if (!kern) throw Error(1, "no list-major kernel for this (M, B)");
     const size_t smem = q16 ? smem_list_q16(M, a.kk, B) : smem_fast(B, a.kk, M);
-    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     ScanArgs aa = a;
     aa.one = 1;
     aa.dbg = debug_counters_for(q16 ? 2 : 1);
@@ -1173,7 +1174,7 @@ void assign_scan_m(const uint8_t *codes, int64_t n, const uint8_t *centers, int6
     const int kk = 32, B = 8;
     const size_t smem = smem_fast(B, kk);
     void *kern = fast_kernel_ptr<M, B, false>(false);
-    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     const int64_t CH = (int64_t)1 << 23;  // codes per launch: bounds the [chunk][kk] keys
     uint64_t *keys = nullptr;
     RII_CUDA(cudaMallocAsync(&keys, (size_t)std::min(n, CH) * kk * 8, st));
@@ -1435,7 +1436,7 @@ void launch_list_bound(const uint8_t *codes, int M, const int4 *items, int64_t n
 #define RII_LB(MM)                                                                                                 \
     case MM:                                                                                                       \
         RII_CUDA(cudaFuncSetAttribute(list_bound_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
-                                      (int)smem));                                                                 \
+                                      SMEM_ATTR_MAX));                                                                 \
         list_bound_kernel<MM><<<(unsigned)n_items, GB_NT, smem, st>>>(codes, items, offsets, ids, qlist, P, tables,  \
                                                                       kk, gthr);                                   \
         break;
@@ -1458,7 +1459,7 @@ void launch_group_min_bound(const uint8_t *samp, int64_t ns, int M, const float 
 #define RII_GB(MM)                                                                                                 \
     case MM:                                                                                                       \
         RII_CUDA(cudaFuncSetAttribute(group_min_bound_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                      (int)smem));                                                                 \
+                                      SMEM_ATTR_MAX));                                                                 \
         group_min_bound_kernel<MM><<<grid, GB_NT, smem, st>>>(samp, ns, gsz, tables, nq, kk, gthr);               \
         break;
         RII_GB(4) RII_GB(8) RII_GB(16) RII_GB(32) RII_GB(64)
@@ -1656,7 +1657,7 @@ void launch_merge(const uint64_t *keys, int64_t q_stride, int64_t p_stride, int 
     if (nq <= 0) return;
     KernelTimer t(TK_MERGE, st);
     const size_t smem = (size_t)(2 * kk + parts) * 8;
-    if (smem > 48 * 1024) RII_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 48 * 1024) RII_CUDA(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     merge_kernel<<<(unsigned)nq, NT, smem, st>>>(keys, q_stride, p_stride, parts, kk, topk, map,
                                                                out_ids, out_dist, out_keys, rs);
     RII_LAUNCHED();

@@ -518,7 +518,7 @@ def test_linear_u16_tables(rii, ref, monkeypatch, kind, N, D, M, nq, topk):
         g2 = g.query(q, topk, target_ids=sub, path="linear")
         monkeypatch.delenv("RII_Q16")
         assert np.array_equal(gr[0], g2[0]) and np.array_equal(gr[1], g2[1])
-        for cfg in ("0", "4"):  # u16 and u6 integer tables (the default picks one by M)
+        for cfg in ("0", "4", "9"):  # u16, u6 (8 queries) and u6 (16 queries) tables (the default picks by M)
             monkeypatch.setenv("RII_Q16_CFG", cfg)
             g3 = g.query(q, topk, target_ids=sub, path="linear")
             monkeypatch.delenv("RII_Q16_CFG")

@@ -196,7 +196,17 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
             load_lut_oct_u8pre<U6_R2, H, NTH>(reinterpret_cast<uint32_t *>(lut + o * OCT_BYTES), tq);
         }
     } else if constexpr (U6) {
-        // u6 tables: per-query scale s = 63 * ALPHA / T (T = +inf -> s = 0: everything passes)
+        // u6 tables: per-query scale s = 63 * ALPHA / T (T = +inf -> s = 0: everything passes).
+        // The bound is read ONCE per query: the CTAs of other chunks lower it with
+        // atomicMin at any moment, and threads that quantised with different reads
+        // built a table of mixed scales whose filter could drop true candidates (a
+        // nondeterministic miss, round 2: ~1 query per run at 1024 queries x 2M codes)
+        if (tid < B) {
+            const float T = __ldcg(a.gthr + query_of(tid));
+            tsc[tid] = T;
+            qsc[tid] = __fdiv_rd(U6_CAP * u6_alpha(M), fmaxf(T, 1e-30f));
+        }
+        __syncthreads();
 #pragma unroll
         for (int o = 0; o < NO; ++o) {
             float qs[8];
@@ -204,9 +214,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int qq = 8 * o + k;
-                const float T = __ldcg(a.gthr + query_of(qq));
-                qs[k] = __fdiv_rd(U6_CAP * u6_alpha(M), fmaxf(T, 1e-30f));
-                if (tid == 0) { qsc[qq] = qs[k]; tsc[qq] = T; }
+                qs[k] = qsc[qq];
                 tq[k] = a.tables + query_of(qq) * LQF;
             }
             load_lut_oct_u6<U6_R2, H>(reinterpret_cast<uint32_t *>(lut + o * OCT_BYTES), tq, qs, U6_CAP);
@@ -220,14 +228,17 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                               a.qtab16 + query_of(4 * p + 1) * LQF, a.qtab16 + query_of(4 * p + 2) * LQF,
                               a.qtab16 + query_of(4 * p + 3) * LQF);
     } else if constexpr (Q16) {
-        // u16 tables: per-query scale s = CAP / T (T = +inf -> s = 0: everything passes)
+        // u16 tables: per-query scale s = CAP / T (T = +inf -> s = 0: everything passes);
+        // the bound is read once per query (see the u6 branch)
+        if (tid < B) {
+            const float T = __ldcg(a.gthr + query_of(tid));  // current bound on the kk-th distance
+            tsc[tid] = T;
+            qsc[tid] = __fdiv_rd((float)q16_cap<M>(), fmaxf(T, 1e-30f));
+        }
+        __syncthreads();
         float qs[B];
 #pragma unroll
-        for (int qq = 0; qq < B; ++qq) {
-            const float T = __ldcg(a.gthr + query_of(qq));  // current bound on the kk-th distance
-            qs[qq] = __fdiv_rd((float)q16_cap<M>(), fmaxf(T, 1e-30f));
-            if (tid == 0) { qsc[qq] = qs[qq]; tsc[qq] = T; }
-        }
+        for (int qq = 0; qq < B; ++qq) qs[qq] = qsc[qq];
 #pragma unroll
         for (int p = 0; p < NQ; ++p)
             load_lut_quad_q16<M>(reinterpret_cast<uint32_t *>(lut + p * QUAD_BYTES),
@@ -902,6 +913,7 @@ bool smem_fixed_base_ok() { return fixed_base_ok(); }
 // -> 8.2, L = 4 5.5 -> 5.1).  The per-query tables are then written with cap 127.
 bool list_u7(int M) {
     const char *e = getenv("RII_LIST_U7");
+    if (M == 64) return e && atoi(e) == 1;  // A/B (two 32-subspace halves)
     return (M == 32 || M == 16 || M == 8) && !(e && atoi(e) == 0);
 }
 int list_u6_cfg(int M) {
@@ -948,8 +960,10 @@ template <int M, int B, bool LISTS>
 static void *fast_kernel_ptr(bool q16 = false, int nth = 384) {
     if constexpr (lut_halves(M) > 1) {  // M = 64: u6 oct tables (B = 8) or fp32 pairs (B = 2) only
         if constexpr (B == 8) {
-            if constexpr (LISTS) return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64>;
-            else if (m64_nth() == 256) return (void *)scan_fast_kernel<M, 8, false, 256, 1, 3, 64>;
+            if constexpr (LISTS) {
+                if (list_u7(M)) return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 256 | 128 | 64>;
+                return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 128 | 64>;
+            } else if (m64_nth() == 256) return (void *)scan_fast_kernel<M, 8, false, 256, 1, 3, 64>;
             else return (void *)scan_fast_kernel<M, 8, false, 384, 1, 3, 64>;
         } else if constexpr (B == 2) {
             return (void *)scan_fast_kernel<M, 2, LISTS, 512, 1, 0>;

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--L", type=int, default=64)
     ap.add_argument("--subset", type=float, default=0.0)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--nq", type=int, default=0, help="queries per call (default: the workload's)")
+    ap.add_argument("--subset_n", type=int, default=0, help="subset size in ids (overrides --subset)")
     ap.add_argument("settings", nargs="*")
     a = ap.parse_args()
     kind, N, D, M, nlist, nq, topk, n_train, _ = bench.WORKLOADS[a.workload]
@@ -35,8 +37,10 @@ def main():
     g.add(x)
     del x
     g.reconfigure(nlist, n_iter=10, seed=0)
+    nq = a.nq or nq
     q = bench._device_data(kind, nq, D, dev, 0, gen.STREAM_QUERY)
-    S = gen.subset_torch(N, int(N * a.subset), dev, seed=0) if a.subset > 0 else None
+    ns = a.subset_n or int(N * a.subset)
+    S = gen.subset_torch(N, ns, dev, seed=0) if ns > 0 else None
     ids = torch.empty((nq, topk), dtype=torch.int64, device=dev)
     dist = torch.empty((nq, topk), dtype=torch.float32, device=dev)
     ref = None

@@ -31,7 +31,7 @@ SPLIT = {"default": []}
 # for the scan kernels of that M (its translation units then build in parallel)
 SOURCES = [("capi.cu", [], "capi.cu.o"), ("k_scan.cu", [], "k_scan.cu.o")] + \
           [("k_scan.cu", [f"-DRII_SCAN_M={m}"], f"k_scan_m{m}.o") for m in (4, 8, 16, 32, 64)] + \
-          [(f, [], f + ".o") for f in ("k_ivf.cu", "k_build.cu", "k_opq.cu", "k_large.cu", "k_large_u6.cu", "comm.cpp",
+          [(f, [], f + ".o") for f in ("k_ivf.cu", "k_build.cu", "k_opq.cu", "k_large.cu", "k_large_u6.cu", "sort.cu", "comm.cpp",
                                         "opq.cpp")]
 
 

@@ -138,7 +138,8 @@ struct QueryScratch {
         s_probe{&st}, s_roff{&st}, s_rids{&st}, s_rkey{&st}, s_rval{&st}, s_out_ids{&st}, s_out_dist{&st},
         s_flag{&st}, s_lq{&st}, s_qoff{&st}, s_ql{&st}, s_qoff2{&st}, s_ql2{&st}, s_items{&st}, s_gthr{&st},
         s_tables{&st}, s_cpart{&st}, s_ckeys{&st}, s_take{&st}, s_samp{&st}, s_spart{&st}, s_bound{&st},
-        s_skey{&st}, s_tab16{&st}, s_qscale{&st}, s_qrot{&st}, s_route{&st}, s_rmirror{&st};
+        s_skey{&st}, s_tab16{&st}, s_qscale{&st}, s_qrot{&st}, s_route{&st}, s_rmirror{&st}, s_alist{&st},
+        s_pmask{&st}, s_salist{&st};
     explicit QueryScratch(cudaStream_t s) : st(s) {}
 };
 
@@ -425,9 +426,45 @@ struct QueryArgs {
     const int64_t *S;        // device global ids or nullptr
     int64_t nS;
     int L;
-    int path;                // resolved LINEAR / IVF
+    int path;                // how the call executes: LINEAR / IVF / EXEC_MASKED (decide_exec)
     bool collective;         // rii_query with world > 1 and a communicator: every rank runs this call
 };
+
+// Execution of an IVF call in mode A (reading R2: every S-member of the P probed lists
+// is a candidate, ranked by (d, id)).  Its candidate set is (union of the P probed
+// lists) ∩ S, so:
+//  - P == K probes every list: the candidates are S itself and the result is the
+//    linear scan's (Alg. 1) -- run it (path_used still reports IVF);
+//  - many probed lists (P * RII_MASKED_RATIO >= K, default 8): a probe-masked linear
+//    scan of S (EXEC_MASKED, ProbeMask) -- each code of S is evaluated only for the
+//    queries that probe its list, at the linear scan's rate, instead of list-major
+//    items over short restricted lists;
+//  - otherwise the posting-list traversal.
+// Every quantity is global (N, K, |S|, L), so all ranks decide alike.
+constexpr int EXEC_MASKED = 3;
+int64_t ivf_num_probes(const rii_index *x, bool has_S, int64_t nS, int L) {
+    return has_S ? std::min<int64_t>(x->K, ceil_div((int64_t)L * x->N, std::max<int64_t>(nS, 1)))
+                 : std::min<int64_t>(L, x->K);  // P:492-502, R1
+}
+static int masked_ratio() {
+    const char *e = getenv("RII_MASKED_RATIO");  // 0 disables both shortcuts (A/B, tests)
+    return e ? atoi(e) : 8;
+}
+int decide_exec(const rii_index *x, int used, bool has_S, int64_t nS, int L) {
+    if (used != RII_PATH_IVF || x->ivf_mode == RII_IVF_PAPER) return used;
+    // RII_IVF_MODE (tests / tuning): "list" / "query" force a traversal, "masked" the
+    // masked scan whenever P < K
+    const char *mode = getenv("RII_IVF_MODE");
+    const bool force_trav = mode && (!strcmp(mode, "list") || !strcmp(mode, "query"));
+    const bool force_mask = mode && !strcmp(mode, "masked");
+    const int r = masked_ratio();
+    if (force_trav || (r <= 0 && !force_mask)) return used;
+    const int64_t P = ivf_num_probes(x, has_S, nS, L);
+    if (P >= x->K) return RII_PATH_LINEAR;
+    const bool fast = list_major_supported(x->M);  // the fast-layout scan kernels carry the mask
+    if (fast && (force_mask || P * r >= x->K)) return EXEC_MASKED;
+    return used;
+}
 
 // OPQ: the rotated copy R x of n device rows in `buf`, or x itself
 // when the index has no rotation.
@@ -477,16 +514,30 @@ struct Targets {
     const int64_t *roff = nullptr;          // IVF path
     const uint32_t *rids = nullptr;
     const uint8_t *rmirror = nullptr;       // codes of the restricted lists in list order
+    const int32_t *alist = nullptr;         // masked IVF: list of each gathered code
 };
 
 Targets prepare_targets(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cudaStream_t st) {
     Targets t;
-    if (!a.S) return t;
+    if (!a.S) {
+        if (a.path == EXEC_MASKED) t.alist = x->assign.as<int32_t>();
+        return t;
+    }
     t.n_loc = route_targets(x, sc, a.S, a.nS, st, &t.S_loc, &t.pos);
-    if (a.path == RII_PATH_LINEAR) {
+    if (a.path == RII_PATH_LINEAR || a.path == EXEC_MASKED) {
         uint8_t *sub = sc.s_sub.get<uint8_t>((size_t)std::max<int64_t>(t.n_loc, 1) * x->M + 64);
         launch_gather_codes(x->codes.as<uint8_t>(), x->M, t.pos, t.n_loc, sub, st);
         t.sub_codes = sub;
+        if (a.path == EXEC_MASKED) {
+            int32_t *al = sc.s_alist.get<int32_t>(t.n_loc + 1);
+            uint32_t *scratch = sc.s_rval.get<uint32_t>(t.n_loc + 1);
+            if (t.n_loc > 0) {
+                gather_i32_kernel<<<(unsigned)ceil_div(t.n_loc, 256), 256, 0, st>>>(x->assign.as<int32_t>(), t.pos,
+                                                                                   t.n_loc, al, scratch);
+                RII_LAUNCHED();
+            }
+            t.alist = al;
+        }
     } else {
         int32_t *rk = sc.s_rkey.get<int32_t>(t.n_loc + 1);
         uint32_t *rv = sc.s_rval.get<uint32_t>(t.n_loc + 1);
@@ -535,6 +586,48 @@ static int ns_chunks() {
 }
 
 
+// Coarse ranking (Alg. 2 L2-L5) and probe selection (L6): the P nearest lists of every
+// query by (d0, k), [nq][P] int32.
+const int32_t *coarse_probes(const rii_index *x, QueryScratch &sc, const QueryArgs &a, const float *tables, int64_t P,
+                             cudaStream_t st) {
+    const float *cb = x->cb.as<float>();
+    const bool fast = list_major_supported(x->M);
+    int32_t *probes = sc.s_probe.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
+    const int kkc = partial_width((int)std::min<int64_t>(P, 1024));
+    const char *cte = getenv("RII_COARSE_TOPP");  // 0: the scan-based coarse ranking (A/B)
+    if (P >= x->K) {
+        launch_select_probes(nullptr, a.nq, x->K, P, probes, st);  // every list
+    } else if (fast && !(cte && cte[0] == '0') &&
+               launch_coarse_topp(x->centers.as<uint8_t>(), x->K, x->M, tables, a.nq, P, probes, st)) {
+        // one CTA per query: canonical d0 of every centre, radix-selected top-P (k_ivf.cu)
+    } else if (fast && P <= 1008) {
+        // coarse ranking (L2-L5) with the lane-rotated scan over the K centre codes,
+        // canonical rescore, top-P by (d0, k) (L6)
+        ScanPlan pc = plan_linear(x->M, kkc, a.nq, x->K, x->num_sms, tables != nullptr, 1 << 30, false);
+        uint64_t *cp = sc.s_cpart.get<uint64_t>((size_t)pc.nb * pc.B * pc.nc * kkc);
+        // RII_COARSE_BOUND=1 (A/B, off): seed the filter with the kkc-th smallest of the
+        // group minima over all K centre codes (>= kkc groups: a valid bound on the
+        // kkc-th d0).  Fewer pushes, but the bound pass costs more than it saves
+        // (deep10m L = 64 13.22 -> 13.37 ms, L = 1 2.79 -> 3.05 ms).
+        float *cg = nullptr;
+        const char *cbe = getenv("RII_COARSE_BOUND");
+        const int64_t cgs = ceil_div(x->K, 1024);
+        if (tables && pc.fast && kkc <= 512 && x->K / cgs >= kkc && cbe && cbe[0] == '1') {
+            cg = sc.s_bound.get<float>(a.nq);
+            launch_group_min_bound(x->centers.as<uint8_t>(), x->K, x->M, tables, a.nq, kkc, cg, st);
+        }
+        launch_linear_scan(pc, x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, kkc, cp, st, tables, cg);
+        uint64_t *ck = sc.s_ckeys.get<uint64_t>((size_t)a.nq * kkc);
+        launch_merge(cp, (int64_t)pc.nc * kkc, kkc, pc.nc, a.nq, kkc, (int)P, IdMap(), nullptr, nullptr, ck, st);
+        launch_keys_to_probes(ck, a.nq, kkc, P, probes, st);
+    } else {
+        float *d0 = sc.s_d0.get<float>((size_t)a.nq * x->K);
+        launch_coarse_dist(x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, d0, st);
+        launch_select_probes(d0, a.nq, x->K, P, probes, st);
+    }
+    return probes;
+}
+
 // One batch of queries (a.q, a.nq) against this rank's shard.  Writes either the
 // final result (world == 1, out_keys == nullptr) or this rank's top-kk keys with
 // global ids (out_keys, device [nq][kk]).
@@ -563,9 +656,18 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
     int64_t q_stride = kk, p_stride = kk;
     int nparts = 1;
     Rescore rs;  // set when the partials hold lane-rotated (not yet canonical) distances
-    if (a.path == RII_PATH_LINEAR) {  // Alg. 1
+    if (a.path == RII_PATH_LINEAR || a.path == EXEC_MASKED) {  // Alg. 1 (masked: Alg. 2 mode A, decide_exec)
         const uint8_t *scan_codes = a.S ? t.sub_codes : codes;
         const int64_t n_codes = a.S ? t.n_loc : x->n_local;
+        // masked IVF: every query's P probed lists (Alg. 2 L2-L6), as the traversal ranks them
+        const bool masked = a.path == EXEC_MASKED;
+        int64_t P_m = 0;
+        const int32_t *probes_m = nullptr;
+        if (masked) {
+            P_m = ivf_num_probes(x, a.S != nullptr, a.nS, a.L);
+            probes_m = coarse_probes(x, sc, a, tables, P_m, st);
+            tr.mark("coarse+probes");
+        }
         if (a.S) {
             map = IdMap();
             map.kind = 1;
@@ -579,7 +681,7 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
         // is empty or short -- joins the same collectives; each rank then decides
         // locally whether its own scan runs the integer tables.
         float *gthr_shared = nullptr;
-        if (!a.S && a.collective && fast && !large) {
+        if (!a.S && a.collective && fast && !large && !masked) {
             const int64_t n_dec = ceil_div(x->N, x->world);
             const ScanPlan pd = plan_linear(x->M, kk, a.nq, std::max<int64_t>(n_dec, 1), x->num_sms, tables != nullptr);
             const bool q16_glob = (pd.B == 8 || pd.B == 16) && pd.fast && q16_enabled() && q16_supported(kk) &&
@@ -659,6 +761,17 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             nparts = nc;
         } else {
             ScanPlan pl = plan_linear(x->M, kk, a.nq, n_codes, x->num_sms, tables != nullptr);
+            ProbeMask mask;
+            auto make_mask = [&](int B) {  // grouped by the plan's query batch
+                if (!masked) return;
+                uint32_t *pm = sc.s_pmask.get<uint32_t>((size_t)ceil_div(a.nq, (int64_t)B) * x->K);
+                launch_probe_mask(probes_m, a.nq, P_m, x->K, B, pm, st);
+                mask.alist = t.alist;
+                mask.pm = pm;
+                mask.K = x->K;
+                mask.B = B;
+            };
+            make_mask(pl.B);
             // u16 / u6 fixed-point tables for long scans: an upper bound on each query's
             // final kk-th distance (the group minima of a strided sample of the codes --
             // a subset) scales the tables and seeds the filter; every CTA filters with,
@@ -677,9 +790,17 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
                     const int64_t stride = n_codes / ns;
                     uint8_t *samp = sc.s_samp.get<uint8_t>((size_t)ns * x->M);
                     launch_strided_gather(scan_codes, x->M, stride, ns, samp, st);
-                    if (ns >= 4096 && kk <= 512 && !getenv("RII_BOUND_TOPK")) {
+                    ProbeMask smask = mask;  // masked: the sample's lists
+                    if (masked) {
+                        int32_t *sal = sc.s_salist.get<int32_t>(ns);
+                        launch_strided_gather_i32(t.alist, stride, ns, sal, st);
+                        smask.alist = sal;
+                    }
+                    if (ns >= 4096 && kk <= 512 && (masked || !getenv("RII_BOUND_TOPK"))) {
                         // kk-th smallest of 1024 group minima (no top-k lists; k_scan.cu)
-                        launch_group_min_bound(samp, ns, x->M, tables, a.nq, kk, gthr, st);
+                        launch_group_min_bound(samp, ns, x->M, tables, a.nq, kk, gthr, st, smask);
+                    } else if (masked) {
+                        launch_fill_f32(gthr, a.nq, INFINITY, st);  // no sampled bound: filter from +inf
                     } else {
                         // exact kk-th over the sample: one chunk per query batch
                         ScanPlan ps = plan_linear(x->M, kk, a.nq, ns, x->num_sms, true, ns_chunks(), false);
@@ -694,12 +815,15 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
                     tr.mark("q16 bound");
                 }
             }
-            if (!q16 && pl.B == 8 && lut_halves(x->M) > 1)  // M = 64 has no float B = 8 kernel
+            if (!q16 && pl.B == 8 && lut_halves(x->M) > 1) {  // M = 64 has no float B = 8 kernel
                 pl = plan_linear(x->M, kk, a.nq, n_codes, x->num_sms, tables != nullptr, 1 << 30, false);
+                make_mask(pl.B);
+            }
             if (!pl.fast) gthr = nullptr;
             else if (!q16 && !gthr_shared) launch_fill_f32(gthr, a.nq, INFINITY, st);
             uint64_t *pp = sc.s_part.get<uint64_t>((size_t)pl.nb * pl.B * pl.nc * kk);
-            launch_linear_scan(pl, scan_codes, n_codes, x->M, a.q, a.nq, cb, x->D, kk, pp, st, tables, gthr, q16);
+            launch_linear_scan(pl, scan_codes, n_codes, x->M, a.q, a.nq, cb, x->D, kk, pp, st, tables, gthr, q16,
+                               TK_LINEAR, mask);
             parts = pp;
             q_stride = (int64_t)pl.nc * kk;
             p_stride = kk;
@@ -721,37 +845,8 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
         else launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, probes, P, off, ids, pp, st, tables, take);
         parts = pp;
     } else {  // Alg. 2, mode A (reading R2)
-        const int64_t P = a.S ? std::min<int64_t>(x->K, ceil_div((int64_t)a.L * x->N, std::max<int64_t>(a.nS, 1)))
-                              : std::min<int64_t>(a.L, x->K);  // P:492-502, R1
-        int32_t *probes = sc.s_probe.get<int32_t>((size_t)a.nq * std::max<int64_t>(P, 1));
-        const int kkc = partial_width((int)std::min<int64_t>(P, 1024));
-        if (P >= x->K) {
-            launch_select_probes(nullptr, a.nq, x->K, P, probes, st);  // every list
-        } else if (fast && P <= 1008) {
-            // coarse ranking (L2-L5) with the lane-rotated scan over the K centre codes,
-            // canonical rescore, top-P by (d0, k) (L6)
-            ScanPlan pc = plan_linear(x->M, kkc, a.nq, x->K, x->num_sms, tables != nullptr, 1 << 30, false);
-            uint64_t *cp = sc.s_cpart.get<uint64_t>((size_t)pc.nb * pc.B * pc.nc * kkc);
-            // RII_COARSE_BOUND=1 (A/B, off): seed the filter with the kkc-th smallest of the
-            // group minima over all K centre codes (>= kkc groups: a valid bound on the
-            // kkc-th d0).  Fewer pushes, but the bound pass costs more than it saves
-            // (deep10m L = 64 13.22 -> 13.37 ms, L = 1 2.79 -> 3.05 ms).
-            float *cg = nullptr;
-            const char *cbe = getenv("RII_COARSE_BOUND");
-            const int64_t cgs = ceil_div(x->K, 1024);
-            if (tables && pc.fast && kkc <= 512 && x->K / cgs >= kkc && cbe && cbe[0] == '1') {
-                cg = sc.s_bound.get<float>(a.nq);
-                launch_group_min_bound(x->centers.as<uint8_t>(), x->K, x->M, tables, a.nq, kkc, cg, st);
-            }
-            launch_linear_scan(pc, x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, kkc, cp, st, tables, cg);
-            uint64_t *ck = sc.s_ckeys.get<uint64_t>((size_t)a.nq * kkc);
-            launch_merge(cp, (int64_t)pc.nc * kkc, kkc, pc.nc, a.nq, kkc, (int)P, IdMap(), nullptr, nullptr, ck, st);
-            launch_keys_to_probes(ck, a.nq, kkc, P, probes, st);
-        } else {
-            float *d0 = sc.s_d0.get<float>((size_t)a.nq * x->K);
-            launch_coarse_dist(x->centers.as<uint8_t>(), x->K, x->M, a.q, a.nq, cb, x->D, d0, st);
-            launch_select_probes(d0, a.nq, x->K, P, probes, st);
-        }
+        const int64_t P = ivf_num_probes(x, a.S != nullptr, a.nS, a.L);
+        const int32_t *probes = coarse_probes(x, sc, a, tables, P, st);
         tr.mark("coarse+probes");
         const int64_t *off = a.S ? t.roff : x->offsets.as<int64_t>();
         const uint32_t *ids = a.S ? t.rids : x->ids.as<uint32_t>();
@@ -1386,7 +1481,8 @@ static rii_status query_impl(const rii_index *x, const float *q, int64_t nq, int
         check_targets(x, sc, dS, S ? nS : 0, st);
         dq = rotate_input(x, sc.s_qrot, dq, nq, st);  // OPQ: "an input vector is first rotated"
         const bool collective = !out_keys && x->world > 1 && x->comm != nullptr;
-        QueryArgs a{dq, nq, topk, partial_width(topk), S ? dS : nullptr, S ? nS : 0, L, used, collective};
+        const int exec = decide_exec(x, used, S != nullptr, S ? nS : 0, L);
+        QueryArgs a{dq, nq, topk, partial_width(topk), S ? dS : nullptr, S ? nS : 0, L, exec, collective};
         int64_t *oid = out_ids;
         float *od = out_dist;
         if (host) {
@@ -1853,6 +1949,13 @@ rii_status rii_calibrate_theta(rii_index *x, const float *q, int64_t nq, int32_t
             double prev_s = 0.0, prev_r = 0.0, c = -1.0;
             for (size_t si = 0; si < sizes.size(); ++si) {
                 const int64_t s = sizes[si];
+                if (decide_exec(x, RII_PATH_IVF, true, s, L) == RII_PATH_LINEAR) {
+                    // P = K: the inverted index executes as the linear scan (same candidates,
+                    // same time), so the crossover lies above s
+                    prev_s = (double)s;
+                    prev_r = 0.0;
+                    continue;
+                }
                 strided_ids_kernel<<<(unsigned)ceil_div(s, 256), 256, 0, st>>>(S, s, x->N);
                 RII_LAUNCHED();
                 const double tl = (double)time_query(s, L, RII_PATH_LINEAR);

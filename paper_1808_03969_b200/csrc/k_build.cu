@@ -333,15 +333,11 @@ void build_csr(const int32_t *keys, const uint32_t *vals, int64_t n, int64_t K, 
     }
     int32_t *kout = nullptr;
     RII_CUDA(cudaMallocAsync(&kout, (size_t)n * 4, st));
-    size_t tb = 0;
-    RII_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout, vals, ids, (int64_t)n, 0, bits_for(K), st));
-    void *tmp = nullptr;
-    RII_CUDA(cudaMallocAsync(&tmp, tb, st));
-    RII_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, kout, vals, ids, (int64_t)n, 0, bits_for(K), st));
-    count_launch(4);
+    // stable (sort.cu): the ids of a list keep their input order (ascending, R11)
+    radix_sort_pairs<uint32_t>(reinterpret_cast<const uint32_t *>(keys), vals, n, bits_for(K),
+                               reinterpret_cast<uint32_t *>(kout), ids, st);
     csr_offsets_kernel<<<(unsigned)ceil_div(K + 1, 256), 256, 0, st>>>(kout, n, K, offsets);
     RII_LAUNCHED();
-    RII_CUDA(cudaFreeAsync(tmp, st));
     RII_CUDA(cudaFreeAsync(kout, st));
 }
 

@@ -7,8 +7,8 @@
 //                  and codes (16-byte gathers from the linear array),
 //                  evaluate ADC with the lane-rotated table of k_scan.cu and keep
 //                  the top-kk in shared memory (L7-L16, mode A of reading R2).
+#include <algorithm>
 #include <cstring>
-#include <cub/cub.cuh>
 
 #include "kernels.cuh"
 #include "lut.cuh"
@@ -17,6 +17,8 @@
 namespace rii {
 
 constexpr int CQ = 4;   // queries per CTA in coarse_dist
+// coarse_topp_kernel: bytes of the staged [M][257] fp32 table, rounded to 16
+__host__ __device__ constexpr size_t coarse_topp_tab_bytes(int M) { return ((size_t)M * (KS + 1) * 4 + 15) / 16 * 16; }
 constexpr int CMC = 32; // subspaces per table chunk in coarse_dist
 
 // d0[q][k] (Alg. 2 L2-L5): CTA = (256 centres, CQ queries); the CA1 table is built
@@ -143,6 +145,132 @@ __global__ void __launch_bounds__(NT) select_probes_kernel(const float *__restri
     }
 }
 
+// Coarse ranking and probe selection in one kernel (Alg. 2 L2-L6) for the fast-layout M
+// (precomputed CA1 tables, lut_tables_kernel): CTA = one query.  Its table is staged in
+// shared memory as [m][z] with a row pitch of 257 floats (bank = (m + z) mod 32); thread
+// = centres k, d0_k summed in CA2 order (m ascending, canonical); the P smallest
+// (d0, k) by a radix select over the d0 bit patterns (d0 >= +0: bit order is value
+// order), ties at the threshold to the lowest k (CA4); the P keys are then sorted by
+// (d0, k) so probes[q][r] is the rank-r list (the list-major items and their phases
+// run nearest lists first).  Replaces, for P <= CT_PMAX, the lane-rotated scan over the
+// centre codes with top-P lists of kkc keys (per-CTA table fill of 6 queries, top-kk
+// compactions from an infinite threshold): deep10m L = 64 ... see DESIGN.md §6.
+constexpr int CT_NT = 256;
+constexpr int CT_PMAX = 2048;
+
+template <int M>
+__global__ void __launch_bounds__(CT_NT) coarse_topp_kernel(const uint8_t *__restrict__ centers, int64_t K,
+                                                            const float *__restrict__ tables, int64_t P,
+                                                            int32_t *__restrict__ probes, size_t d0_off) {
+    constexpr int W = M / 4, MH = M < 32 ? M : 32, PITCH = KS + 1;
+    extern __shared__ __align__(16) uint8_t smem[];
+    float *tab = reinterpret_cast<float *>(smem);                          // [M][257]; later the sort keys
+    uint32_t *d0 = reinterpret_cast<uint32_t *>(smem + d0_off);  // [K] d0 bit patterns (after table / keys)
+    __shared__ int hist[256];
+    __shared__ uint32_t s_prefix, s_mask;
+    __shared__ int s_rem, s_n;
+    __shared__ int wsum[CT_NT / 32];
+    const int64_t qi = blockIdx.x;
+    const float *tq = tables + qi * (int64_t)lut_q_floats(M);
+    // table: A(m, z) = tq[(m / 32) * 8192 + z * 32 + m % 32] (lut.cuh layout)
+    for (int e = threadIdx.x; e < M * KS; e += CT_NT) {
+        const int h = e / (KS * MH), r = e - h * KS * MH, z = r / MH, mm = r - z * MH;
+        tab[(32 * h + mm) * PITCH + z] = __ldg(tq + h * LUT_Q_FLOATS + z * 32 + mm);
+    }
+    __syncthreads();
+    for (int64_t k = threadIdx.x; k < K; k += CT_NT) {
+        uint32_t w[W];
+        const uint32_t *cp = reinterpret_cast<const uint32_t *>(centers + k * M);
+#pragma unroll
+        for (int i = 0; i < W; ++i) w[i] = __ldg(cp + i);
+        float acc = 0.f;
+#pragma unroll
+        for (int m = 0; m < M; ++m) acc = __fadd_rn(acc, tab[m * PITCH + ((w[m >> 2] >> (8 * (m & 3))) & 255u)]);
+        d0[k] = __float_as_uint(acc);
+    }
+    if (threadIdx.x == 0) { s_prefix = 0; s_mask = 0; s_rem = (int)P; s_n = 0; }
+    __syncthreads();
+    // radix select: the P-th smallest bit pattern t, s_rem = how many keys equal to t are taken
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        hist[threadIdx.x] = 0;
+        __syncthreads();
+        const uint32_t pre = s_prefix, msk = s_mask;
+        for (int64_t k = threadIdx.x; k < K; k += CT_NT) {
+            const uint32_t v = d0[k];
+            if ((v & msk) == pre) atomicAdd(&hist[(v >> shift) & 255], 1);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int rem = s_rem, acc = 0, d = 0;
+            for (; d < 256; ++d) {
+                if (acc + hist[d] >= rem) break;
+                acc += hist[d];
+            }
+            s_rem = rem - acc;
+            s_prefix = pre | ((uint32_t)d << shift);
+            s_mask = msk | (255u << shift);
+        }
+        __syncthreads();
+    }
+    const uint32_t t = s_prefix;
+    const int ties = s_rem;
+    uint64_t *keys = reinterpret_cast<uint64_t *>(smem);  // the table is no longer needed
+    int Ppad = 1;
+    while (Ppad < P) Ppad <<= 1;
+    for (int e = threadIdx.x; e < Ppad; e += CT_NT) keys[e] = KEY_MAX;
+    __syncthreads();
+    // below the threshold: exactly P - ties keys, appended in any order (sorted below)
+    for (int64_t k = threadIdx.x; k < K; k += CT_NT) {
+        const uint32_t v = d0[k];
+        if (v < t) keys[atomicAdd(&s_n, 1)] = ((uint64_t)v << 32) | (uint64_t)k;
+    }
+    __syncthreads();
+    // at the threshold: the `ties` lowest k, in k order (block prefix over tie flags)
+    int base = (int)P - ties, seen = 0;
+    for (int64_t k0 = 0; k0 < K && seen < ties; k0 += CT_NT) {
+        const int64_t k = k0 + threadIdx.x;
+        const int tie = (k < K && d0[k] == t) ? 1 : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, tie);
+        if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = __popc(bal);
+        __syncthreads();
+        int off = 0, tot = 0;
+        for (int w = 0; w < CT_NT / 32; ++w) {
+            if (w < (int)(threadIdx.x >> 5)) off += wsum[w];
+            tot += wsum[w];
+        }
+        const int rank = seen + off + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
+        if (tie && rank < ties) keys[base + rank] = ((uint64_t)t << 32) | (uint64_t)k;
+        seen += tot;
+        __syncthreads();
+    }
+    __syncthreads();
+    bitonic_sort_rows(keys, 1, Ppad, Ppad);
+    for (int64_t r = threadIdx.x; r < P; r += CT_NT) probes[qi * P + r] = (int32_t)(keys[r] & 0xffffffffu);
+}
+
+bool launch_coarse_topp(const uint8_t *centers, int64_t K, int M, const float *tables, int64_t nq, int64_t P,
+                        int32_t *probes, cudaStream_t st) {
+    if (P > CT_PMAX || P > K || !tables || (M != 4 && M != 8 && M != 16 && M != 32 && M != 64)) return false;
+    int Ppad = 1;
+    while (Ppad < P) Ppad <<= 1;
+    const size_t d0_off = std::max<size_t>(coarse_topp_tab_bytes(M), (size_t)Ppad * 8);
+    const size_t smem = d0_off + (size_t)K * 4;
+    if (smem + 4096 > (size_t)SMEM_ATTR_MAX) return false;
+    if (nq <= 0) return true;
+    switch (M) {
+#define RII_CT(MM)                                                                                            \
+    case MM:                                                                                                  \
+        RII_CUDA(cudaFuncSetAttribute(coarse_topp_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                      SMEM_ATTR_MAX - 4096));                                                 \
+        coarse_topp_kernel<MM><<<(unsigned)nq, CT_NT, smem, st>>>(centers, K, tables, P, probes, d0_off);    \
+        break;
+        RII_CT(4) RII_CT(8) RII_CT(16) RII_CT(32) RII_CT(64)
+#undef RII_CT
+    }
+    RII_LAUNCHED();
+    return true;
+}
+
 __global__ void keys_to_probes_kernel(const uint64_t *__restrict__ keys, int64_t nq, int kk, int64_t P,
                                       int32_t *__restrict__ probes) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -164,14 +292,15 @@ void launch_select_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int
 }
 
 // --------------------------------------------------- paper mode (Alg. 2) ----
-__global__ void seg_offsets_kernel(int64_t *off, int64_t nseg, int64_t len) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i <= nseg) off[i] = i * len;
-}
-
 __global__ void seg_iota_kernel(int32_t *v, int64_t n, int64_t len) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) v[i] = (int32_t)(i % len);
+}
+
+// composite sort key of (query, list): (q << 32) | bits(d0[q][k])
+__global__ void seg_keys_kernel(const float *__restrict__ d0, int64_t n, int64_t K, uint64_t *__restrict__ key) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) key[i] = ((uint64_t)(i / K) << 32) | (uint64_t)__float_as_uint(d0[i]);
 }
 
 __global__ void seg_head_kernel(const int32_t *sorted, int64_t nq, int64_t K, int64_t P, int32_t *probes) {
@@ -184,29 +313,26 @@ __global__ void seg_head_kernel(const int32_t *sorted, int64_t nq, int64_t K, in
 void launch_sorted_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int32_t *probes, cudaStream_t st) {
     if (nq <= 0 || P <= 0) return;
     const int64_t n = nq * K;
-    uint32_t *kout = nullptr;
     int32_t *vin = nullptr, *vout = nullptr;
-    int64_t *off = nullptr;
-    RII_CUDA(cudaMallocAsync(&kout, (size_t)n * 4, st));
     RII_CUDA(cudaMallocAsync(&vin, (size_t)n * 4, st));
     RII_CUDA(cudaMallocAsync(&vout, (size_t)n * 4, st));
-    RII_CUDA(cudaMallocAsync(&off, (size_t)(nq + 1) * 8, st));
-    seg_offsets_kernel<<<(unsigned)ceil_div(nq + 1, 256), 256, 0, st>>>(off, nq, K);
-    RII_LAUNCHED();
     seg_iota_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(vin, n, K);
     RII_LAUNCHED();
-    const uint32_t *kin = reinterpret_cast<const uint32_t *>(d0);  // d0 >= +0: bit order == value order
-    size_t tb = 0;
-    RII_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, nq, off, off + 1, 0, 32,
-                                                      st));
-    void *tmp = nullptr;
-    RII_CUDA(cudaMallocAsync(&tmp, tb, st));
-    RII_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, n, nq, off, off + 1, 0, 32,
-                                                      st));  // stable: ties keep ascending k (CA4)
-    count_launch(4);
+    // one stable sort of the composite keys (q << 32) | bits(d0): d0 >= +0, so its bit
+    // order is its value order; stable, so ties keep ascending k (CA4)
+    uint64_t *kin = nullptr, *kout64 = nullptr;
+    RII_CUDA(cudaMallocAsync(&kin, (size_t)n * 8, st));
+    RII_CUDA(cudaMallocAsync(&kout64, (size_t)n * 8, st));
+    seg_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(d0, n, K, kin);
+    RII_LAUNCHED();
+    int qbits = 0;
+    while (((int64_t)1 << qbits) < nq) ++qbits;
+    radix_sort_pairs<uint64_t>(kin, reinterpret_cast<const uint32_t *>(vin), n, 32 + qbits, kout64,
+                               reinterpret_cast<uint32_t *>(vout), st);
     seg_head_kernel<<<(unsigned)ceil_div(nq * P, 256), 256, 0, st>>>(vout, nq, K, P, probes);
     RII_LAUNCHED();
-    for (void *pp : {(void *)tmp, (void *)kout, (void *)vin, (void *)vout, (void *)off}) RII_CUDA(cudaFreeAsync(pp, st));
+    for (void *pp : {(void *)kin, (void *)kout64, (void *)vin, (void *)vout})
+        RII_CUDA(cudaFreeAsync(pp, st));
 }
 
 __global__ void paper_takes_kernel(const int32_t *__restrict__ probes, int64_t nq, int64_t P,
@@ -286,12 +412,7 @@ int64_t build_list_items(const int64_t *qoff, int64_t K, int B, const uint32_t *
     RII_CUDA(cudaMallocAsync(&ioff, (size_t)(K + 1) * 8, st));
     list_item_count_kernel<<<(unsigned)ceil_div(K + 1, 256), 256, 0, st>>>(qoff, K, B, n);
     RII_LAUNCHED();
-    size_t tb = 0;
-    RII_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, n, ioff, K + 1, st));
-    void *tmp = nullptr;
-    RII_CUDA(cudaMallocAsync(&tmp, tb, st));
-    RII_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, n, ioff, K + 1, st));
-    count_launch(2);
+    exclusive_scan_i64(n, K + 1, ioff, st);
     int64_t total = 0;
     RII_CUDA(cudaMemcpyAsync(&total, ioff + K, 8, cudaMemcpyDeviceToHost, st));
     RII_CUDA(cudaStreamSynchronize(st));
@@ -315,19 +436,13 @@ int64_t build_list_items(const int64_t *qoff, int64_t K, int B, const uint32_t *
         RII_LAUNCHED();
         int bits = 1;
         while ((1ll << bits) <= P) ++bits;
-        size_t tb2 = 0;
-        RII_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, key, key2, idx, idx2, total, 0, bits, st));
-        void *tmp2 = nullptr;
-        RII_CUDA(cudaMallocAsync(&tmp2, tb2, st));
-        RII_CUDA(cub::DeviceRadixSort::SortPairs(tmp2, tb2, key, key2, idx, idx2, total, 0, bits, st));
-        count_launch(4);
+        radix_sort_pairs<uint32_t>(key, idx, total, bits, key2, idx2, st);  // stable (sort.cu)
         permute_items_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, st>>>(raw, idx2, total, items);
         RII_LAUNCHED();
-        for (void *pp : {(void *)tmp2, (void *)key, (void *)key2, (void *)idx, (void *)idx2})
+        for (void *pp : {(void *)key, (void *)key2, (void *)idx, (void *)idx2})
             RII_CUDA(cudaFreeAsync(pp, st));
     }
     RII_CUDA(cudaFreeAsync(raw, st));
-    RII_CUDA(cudaFreeAsync(tmp, st));
     RII_CUDA(cudaFreeAsync(n, st));
     RII_CUDA(cudaFreeAsync(ioff, st));
     return total;

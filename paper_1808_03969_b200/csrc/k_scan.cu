@@ -455,6 +455,16 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     // read the code by id from the original array (a.rcodes).
     uint32_t cid[U];
     auto key_of = [&](uint32_t id, int64_t) -> uint32_t { return id; };
+    // Probe-masked IVF (linear mode, ProbeMask): the CTA's queries whose probed lists
+    // contain the code at pos (all ones without a mask).  Read only where some lane of
+    // the warp passes the filter, so it costs nothing in the lookup loop.
+    auto probe_bits = [&](int64_t pos) -> uint32_t {
+        if constexpr (LISTS) return 0xffffffffu;
+        else {
+            if (a.alist == nullptr || pos >= c1) return 0xffffffffu;
+            return __ldg(a.pmask + (int64_t)qb * a.pm_K + __ldg(a.alist + pos));
+        }
+    };
     auto load_step = [&](int64_t b, uint32_t(&dst)[U][W], uint32_t(&did)[U]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -523,6 +533,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                             for (int k = 0; k < 4 * NO; ++k)
                                 mk |= (t[k] & 0x80008000u) >> (15 - (4 * (k >> 1) + (k & 1)));
                             mk = pos < c1 ? (mk | (mk >> 14)) & ((1u << B) - 1u) : 0u;
+                            if (!LISTS && mk && a.alist) mk &= probe_bits(pos);
                             const uint32_t kid = key_of(cid[u], pos);
                             for (uint32_t wm = __reduce_or_sync(0xffffffffu, mk); wm; wm &= wm - 1u) {
                                 const int qq = __ffs(wm) - 1;
@@ -546,6 +557,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
 #pragma unroll
                     for (int qq = 0; qq < B; ++qq) mk |= (uint32_t)(dq[qq] <= thq[qq]) << qq;
                     if (pos >= c1) mk = 0;
+                    if (!LISTS && mk && a.alist) mk &= probe_bits(pos);
                     // the key's distance field is replaced by the canonical rescore
                     const uint32_t wmask = __reduce_or_sync(0xffffffffu, mk);
                     const uint32_t kid = wmask ? key_of(cid[u], pos) : 0u;
@@ -582,9 +594,11 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                 for (int qq = 0; qq < B; ++qq) any |= d[qq] <= th[qq];
                 if (__any_sync(0xffffffffu, any && pos < c1)) {
                     const uint32_t kid = key_of(cid[u], pos);
+                    const uint32_t pb = probe_bits(pos);
 #pragma unroll
                     for (int qq = 0; qq < B; ++qq)
-                        push_candidate_win(pos < c1 && d[qq] <= th[qq], make_key(d[qq], kid), fresh + qq * NEWCAP,
+                        push_candidate_win(pos < c1 && d[qq] <= th[qq] && ((pb >> qq) & 1u), make_key(d[qq], kid),
+                                           fresh + qq * NEWCAP,
                                            cnt + qq, lane, SOFT, need, ovf);
                 }
             }
@@ -1026,8 +1040,9 @@ static void *fast_kernel_ptr_b(bool q16, int nth) {
 template <int M, int B>
 static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
                           const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st, const float *tables,
-                          float *gthr, bool q16_req, int timer) {
+                          float *gthr, bool q16_req, int timer, const ProbeMask &mask) {
     const bool q16 = (B == 8 || B == 16) && q16_req && gthr != nullptr;
+    if (mask.alist && mask.B != B) throw Error(1, "probe mask grouped by a different query batch");
     void *kern = fast_kernel_ptr<M, B, false>(q16);
     const size_t smem = q16 && B == 8 ? smem_q16(kk) : pl.smem;
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
@@ -1037,6 +1052,7 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
     a.gthr = gthr;
     a.one = 1;
     a.dbg = debug_counters_for(0);
+    a.alist = mask.alist; a.pmask = mask.pm; a.pm_K = mask.K;
     void *args[] = {&a};
     KernelTimer t(timer, st), tp(B >= 8 && timer == TK_LINEAR ? (q16 ? (q16_is_u6(M) ? TK_U6 : TK_Q16) : TK_PACKED) : -1,
                                  st);
@@ -1049,12 +1065,12 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
 template <int M>
 void launch_fast_m(const ScanPlan &pl, const uint8_t *codes, int64_t n, const float *q, int64_t nq,
                           const float *cb, int ds, int kk, uint64_t *out, cudaStream_t st, const float *tables,
-                          float *gthr, bool q16, int timer) {
-    if (pl.B == 16) launch_fast_t<M, 16>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
-    else if (pl.B == 8) launch_fast_t<M, 8>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
-    else if (pl.B == 6) launch_fast_t<M, 6>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
-    else if (pl.B == 4) launch_fast_t<M, 4>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
-    else launch_fast_t<M, 2>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer);
+                          float *gthr, bool q16, int timer, const ProbeMask &mask) {
+    if (pl.B == 16) launch_fast_t<M, 16>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer, mask);
+    else if (pl.B == 8) launch_fast_t<M, 8>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer, mask);
+    else if (pl.B == 6) launch_fast_t<M, 6>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer, mask);
+    else if (pl.B == 4) launch_fast_t<M, 4>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer, mask);
+    else launch_fast_t<M, 2>(pl, codes, n, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer, mask);
 }
 
 template <int B>
@@ -1121,7 +1137,7 @@ void assign_scan_m(const uint8_t *codes, int64_t n, const uint8_t *centers, int6
 #define RII_EXTERN_M(MM)                                                                                          \
     extern template void launch_fast_m<MM>(const ScanPlan &, const uint8_t *, int64_t, const float *, int64_t,   \
                                            const float *, int, int, uint64_t *, cudaStream_t, const float *,     \
-                                           float *, bool, int);                                                  \
+                                           float *, bool, int, const ProbeMask &);                               \
     extern template void launch_list_m<MM>(int, const ScanArgs &, int64_t, cudaStream_t, bool);                  \
     extern template void assign_scan_m<MM>(const uint8_t *, int64_t, const uint8_t *, int64_t, const float *,    \
                                            int32_t *, float *, cudaStream_t);
@@ -1145,16 +1161,20 @@ void launch_list_scan(int M, int B, const ScanArgs &a, int64_t n_items, cudaStre
 #ifndef RII_SCAN_M  // common translation unit only
 void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_codes, int M, const float *q, int64_t nq,
                         const float *cb, int D, int kk, uint64_t *out, cudaStream_t st, const float *tables,
-                        float *gthr, bool q16, int timer) {
+                        float *gthr, bool q16, int timer, const ProbeMask &mask) {
     const int ds = D / M;
     if (pl.fast) {
         switch (M) {
-            case 4: launch_fast_m<4>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
-            case 8: launch_fast_m<8>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
-            case 16: launch_fast_m<16>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
-            case 64: launch_fast_m<64>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
-            default: launch_fast_m<32>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer); break;
+#define RII_LF(MM) launch_fast_m<MM>(pl, codes, n_codes, q, nq, cb, ds, kk, out, st, tables, gthr, q16, timer, mask)
+            case 4: RII_LF(4); break;
+            case 8: RII_LF(8); break;
+            case 16: RII_LF(16); break;
+            case 64: RII_LF(64); break;
+            default: RII_LF(32); break;
+#undef RII_LF
         }
+    } else if (mask.alist) {
+        throw Error(1, "probe-masked scan: fast-layout plans only");
     } else if (pl.B == 4) {
         launch_generic_t<4>(pl, codes, n_codes, M, q, nq, cb, ds, kk, out, st);
     } else if (pl.B == 2) {
@@ -1279,6 +1299,38 @@ void launch_strided_gather(const uint8_t *codes, int M, int64_t stride, int64_t 
     RII_LAUNCHED();
 }
 
+__global__ void strided_gather_i32_kernel(const int32_t *__restrict__ src, int64_t stride, int64_t n,
+                                          int32_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = __ldg(src + i * stride);
+}
+
+void launch_strided_gather_i32(const int32_t *src, int64_t stride, int64_t n, int32_t *out, cudaStream_t st) {
+    if (n <= 0) return;
+    strided_gather_i32_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(src, stride, n, out);
+    RII_LAUNCHED();
+}
+
+// Probe masks of the masked IVF scan (ProbeMask): thread = (query, probe rank).
+__global__ void probe_mask_kernel(const int32_t *__restrict__ probes, int64_t nq, int64_t P, int64_t K, int B,
+                                  uint32_t *__restrict__ pm) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nq * P) return;
+    const int64_t q = i / P;
+    const int32_t k = probes[i];
+    if (k < 0 || k >= K) return;
+    atomicOr(pm + (q / B) * K + k, 1u << (q % B));
+}
+
+void launch_probe_mask(const int32_t *probes, int64_t nq, int64_t P, int64_t K, int B, uint32_t *pm,
+                       cudaStream_t st) {
+    if (B < 1 || B > 32) throw Error(1, "probe mask: 1 <= B <= 32");
+    RII_CUDA(cudaMemsetAsync(pm, 0, (size_t)ceil_div(nq, (int64_t)B) * K * 4, st));
+    if (nq * P <= 0) return;
+    probe_mask_kernel<<<(unsigned)ceil_div(nq * P, 256), 256, 0, st>>>(probes, nq, P, K, B, pm);
+    RII_LAUNCHED();
+}
+
 // Group-minimum bound: the sample's ns codes form G = ns / GSZ groups; each group's
 // minimum ADC distance is a distance of a distinct sample code, so the kk-th smallest
 // of the G group minima is >= the kk-th smallest of the sample, which is >= the final
@@ -1292,7 +1344,10 @@ __host__ __device__ constexpr int gb_q(int M) { return M > 32 ? 2 : 6; }
 template <int M>
 __global__ void __launch_bounds__(GB_NT, 1) group_min_bound_kernel(const uint8_t *__restrict__ samp, int64_t ns,
                                                                    int gsz, const float *__restrict__ tables,
-                                                                   int64_t nq, int kk, float *__restrict__ gthr) {
+                                                                   int64_t nq, int kk, float *__restrict__ gthr,
+                                                                   const int32_t *__restrict__ salist,
+                                                                   const uint32_t *__restrict__ pm, int64_t pmK,
+                                                                   int pmB) {
     constexpr int GB_Q = gb_q(M), W = M / 4, NP = GB_Q / 2, H = lut_halves(M), LQF = lut_q_floats(M);
     extern __shared__ __align__(16) uint8_t smem[];
     const int tid = threadIdx.x, lane = tid & 31;
@@ -1322,17 +1377,35 @@ __global__ void __launch_bounds__(GB_NT, 1) group_min_bound_kernel(const uint8_t
         const uint8_t *gp = samp + (int64_t)g * gsz * M;
         uint32_t wn[W];
         load_code<W>(gp, wn);  // the next code is loaded while the current one is summed
+        // probe mask (masked IVF): the sample code's list, the mask words of the CTA's
+        // first and last query (GB_Q consecutive queries span at most two batches)
+        const int64_t b0 = qidx(0) / max(pmB, 1), b1 = qidx(GB_Q - 1) / max(pmB, 1);
+        int32_t lst_n = salist ? __ldg(salist + (int64_t)g * gsz) : 0;
         for (int i = 0; i < gsz; ++i) {
             uint32_t w[W];
 #pragma unroll
             for (int k = 0; k < W; ++k) w[k] = wn[k];
-            if (i + 1 < gsz) load_code<W>(gp + (int64_t)(i + 1) * M, wn);
+            const int32_t lst = lst_n;
+            if (i + 1 < gsz) {
+                load_code<W>(gp + (int64_t)(i + 1) * M, wn);
+                if (salist) lst_n = __ldg(salist + (int64_t)g * gsz + i + 1);
+            }
+            uint32_t m0 = 0xffffffffu, m1 = 0xffffffffu;
+            if (salist) {
+                m0 = __ldg(pm + b0 * pmK + lst);
+                m1 = b1 == b0 ? m0 : __ldg(pm + b1 * pmK + lst);
+            }
             float2 acc[NP];
             adc_rotated<M, GB_Q, M >= 32 ? 4 : 8>(smem, w, rw, sel, l8, acc);
+            auto probed = [&](int qq) -> bool {
+                if (!salist) return true;
+                const int64_t qg = qidx(qq);
+                return ((qg / pmB == b0 ? m0 : m1) >> (qg % pmB)) & 1u;
+            };
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
-                gmin[h][2 * p] = fminf(gmin[h][2 * p], acc[p].x);
-                gmin[h][2 * p + 1] = fminf(gmin[h][2 * p + 1], acc[p].y);
+                if (probed(2 * p)) gmin[h][2 * p] = fminf(gmin[h][2 * p], acc[p].x);
+                if (probed(2 * p + 1)) gmin[h][2 * p + 1] = fminf(gmin[h][2 * p + 1], acc[p].y);
             }
         }
     }
@@ -1462,7 +1535,7 @@ void launch_list_bound(const uint8_t *codes, int M, const int4 *items, int64_t n
 }
 
 void launch_group_min_bound(const uint8_t *samp, int64_t ns, int M, const float *tables, int64_t nq, int kk,
-                            float *gthr, cudaStream_t st) {
+                            float *gthr, cudaStream_t st, const ProbeMask &mask) {
     if (nq <= 0) return;
     const int gsz = (int)std::max<int64_t>(1, ceil_div(ns, 1024));  // G = ns / gsz <= 1024 groups
     const int GB_Q = gb_q(M);
@@ -1474,7 +1547,8 @@ void launch_group_min_bound(const uint8_t *samp, int64_t ns, int M, const float 
     case MM:                                                                                                       \
         RII_CUDA(cudaFuncSetAttribute(group_min_bound_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                                       SMEM_ATTR_MAX));                                                                 \
-        group_min_bound_kernel<MM><<<grid, GB_NT, smem, st>>>(samp, ns, gsz, tables, nq, kk, gthr);               \
+        group_min_bound_kernel<MM><<<grid, GB_NT, smem, st>>>(samp, ns, gsz, tables, nq, kk, gthr, mask.alist,     \
+                                                              mask.pm, mask.K, mask.B);                            \
         break;
         RII_GB(4) RII_GB(8) RII_GB(16) RII_GB(32) RII_GB(64)
 #undef RII_GB
@@ -1681,7 +1755,8 @@ void launch_merge(const uint64_t *keys, int64_t q_stride, int64_t p_stride, int 
 
 #ifdef RII_SCAN_M  // per-M translation unit: the scan kernels of one M (build.py compiles k_scan.cu once per M)
 template void launch_fast_m<RII_SCAN_M>(const ScanPlan &, const uint8_t *, int64_t, const float *, int64_t, const float *,
-                                        int, int, uint64_t *, cudaStream_t, const float *, float *, bool, int);
+                                        int, int, uint64_t *, cudaStream_t, const float *, float *, bool, int,
+                                        const ProbeMask &);
 template void launch_list_m<RII_SCAN_M>(int, const ScanArgs &, int64_t, cudaStream_t, bool);
 template void assign_scan_m<RII_SCAN_M>(const uint8_t *, int64_t, const uint8_t *, int64_t, const float *, int32_t *,
                                         float *, cudaStream_t);

@@ -21,6 +21,18 @@ struct ScanPlan {
 ScanPlan plan_linear(int M, int kk, int64_t nq, int64_t n_codes, int num_sms, bool tables_available = false,
                      int max_nc = 1 << 30, bool int_ok = true);
 
+// Probe-masked linear scan (IVF mode A with many probed lists, DESIGN.md §6 "Masked
+// IVF"): a code at scan position p belongs to posting list alist[p]; query q of the
+// plan's batch b = q / B (B = the scan plan's queries per CTA) evaluates it only if
+// bit q % B of pm[b * K + alist[p]] is set, i.e. list alist[p] is among its P probed
+// lists.  The candidate set is then exactly Alg. 2's (probed lists) ∩ S.
+struct ProbeMask {
+    const int32_t *alist = nullptr;  // [n_codes] list of each scanned code; nullptr = no mask
+    const uint32_t *pm = nullptr;    // [ceil(nq / B)][K]
+    int64_t K = 0;
+    int B = 0;                       // query grouping of pm (the scan plan's B)
+};
+
 // Arguments of the lane-rotated scan kernel (linear mode, or list-major inverted
 // index mode where a work item is (posting list, up to B queries probing it)).
 struct ScanArgs {
@@ -53,6 +65,10 @@ struct ScanArgs {
     const float *qscale;
     uint32_t one;  // = 1 (runtime: keeps the u6 SWAR adds on the FMA pipe, lut.cuh fma_add)
     unsigned long long *dbg;  // debug event counters (rii_debug_counters), nullptr when off
+    // linear mode, probe-masked IVF (ProbeMask; alist == nullptr: no mask)
+    const int32_t *alist;
+    const uint32_t *pmask;
+    int64_t pm_K;
 };
 
 // List-major inverted-index scan: B queries per CTA share one posting list's codes.
@@ -76,7 +92,12 @@ void launch_fill_f32(float *p, int64_t n, float v, cudaStream_t st);
 void launch_linear_scan(const ScanPlan &pl, const uint8_t *codes, int64_t n_codes, int M, const float *q, int64_t nq,
                         const float *cb, int D, int kk, uint64_t *out, cudaStream_t st,
                         const float *tables = nullptr, float *gthr = nullptr, bool q16 = false,
-                        int timer = TK_LINEAR);
+                        int timer = TK_LINEAR, const ProbeMask &mask = ProbeMask());
+// pm[(q / B) * K + probes[q * P + r]] |= 1 << (q % B) for every (q, r < P); pm zeroed first.
+void launch_probe_mask(const int32_t *probes, int64_t nq, int64_t P, int64_t K, int B, uint32_t *pm,
+                       cudaStream_t st);
+// out[i] = src[i * stride] (int32; the list ids of a strided code sample)
+void launch_strided_gather_i32(const int32_t *src, int64_t stride, int64_t n, int32_t *out, cudaStream_t st);
 // u16 tables (RII_Q16 != 0), the strided code sample and the kk-th-distance bound.
 bool q16_enabled();
 int64_t q16_min_codes();  // RII_Q16_MIN (default 2^19): shortest scan that uses integer tables
@@ -102,8 +123,10 @@ void launch_strided_gather(const uint8_t *codes, int M, int64_t stride, int64_t 
 void launch_kth_bound(const uint64_t *keys, int64_t nq, int kk, float *bound, cudaStream_t st);
 // gthr[q] = an upper bound on the kk-th distance over the ns sample codes (the kk-th
 // smallest of 1024 group minima, inflated by 1e-5); ns / 1024 codes per group.
+// With a mask (alist = the sample's list ids), only the codes of each query's probed
+// lists enter its group minima (a group without one has minimum +inf).
 void launch_group_min_bound(const uint8_t *samp, int64_t ns, int M, const float *tables, int64_t nq, int kk,
-                            float *gthr, cudaStream_t st);
+                            float *gthr, cudaStream_t st, const ProbeMask &mask = ProbeMask());
 
 // Per-query rotated tables [nq][256][32] (M in {4,8,16,32}), CA1 values.
 void launch_lut_tables(const float *q, int64_t nq, const float *cb, int D, int M, float *tables, cudaStream_t st);
@@ -145,6 +168,10 @@ void launch_select_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int
 // probes[q][r] = id of the r-th key of the sorted per-query keys [nq][kk] (r < P).
 void launch_keys_to_probes(const uint64_t *keys, int64_t nq, int kk, int64_t P, int32_t *probes, cudaStream_t st);
 // probes[q][0..P) = the P nearest lists in (d0, k) order (CUB segmented sort of d0).
+// Coarse ranking + top-P probes sorted by (d0, k) in one kernel (fast M, precomputed
+// tables); returns false (nothing launched) when P or K exceed its shared-memory plan.
+bool launch_coarse_topp(const uint8_t *centers, int64_t K, int M, const float *tables, int64_t nq, int64_t P,
+                        int32_t *probes, cudaStream_t st);
 void launch_sorted_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int32_t *probes, cudaStream_t st);
 // Alg. 2 early stop (mode B): take[q][r] = members of list probes[q][r] evaluated
 // before the budget L runs out (ranks in order).
@@ -206,6 +233,13 @@ struct TrainScratch;
 void run_train(const float *x, int64_t n, int D, int M, int n_iter, uint64_t seed, float *cb, int *err,
                cudaStream_t st);
 // CSR of `vals` (local positions) grouped by `keys` (list ids in [0,K)), stable.
+// sort.cu: stable LSD radix sort of (key, u32 value) pairs by the low `bits` key bits
+// (K = uint32_t or uint64_t; outputs must not alias the inputs; n < 2^32) and an
+// exclusive prefix sum (in and out may alias).
+template <class K>
+void radix_sort_pairs(const K *keys, const uint32_t *vals, int64_t n, int bits, K *keys_out, uint32_t *vals_out,
+                      cudaStream_t st);
+void exclusive_scan_i64(const int64_t *in, int64_t n, int64_t *out, cudaStream_t st);
 void build_csr(const int32_t *keys, const uint32_t *vals, int64_t n, int64_t K, int64_t *offsets, uint32_t *ids,
                cudaStream_t st);
 // PQk-means over a sample (R9); centers out [K][M]; *err set if < K distinct codes.

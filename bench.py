@@ -108,6 +108,9 @@ WORKLOADS = {
     # configs[4]'s code shape (M = 8) at configs[2]'s size, for A/B of the M = 8 kernels
     "deep10m_m8": ("deep", 10_000_000, 96, 8, 3162, 10_000, 100, 100_000,
                    "configs[4] shape at 10M: Deep1B-like 10M x 96, M=8, nlist=3162, 10k queries, top-100"),
+    # configs[4]'s shape (M = 8, nlist = 31,623, 1,024-query batches) at 1e8 codes, for A/B runs
+    "deep100m_m8": ("deep", 100_000_000, 96, 8, 31623, 1024, 100, 100_000,
+                    "configs[4] shape at 1e8: Deep1B-like 1e8 x 96, M=8, nlist=31623, 1024 queries, top-100"),
     "tiny": ("gaussian", 10_000, 32, 4, 100, 100, 10, 10_000,
              "BASELINE.json configs[0]: N(0,1) 10k x 32, M=4, nlist=100, 100 queries, top-10"),
 }

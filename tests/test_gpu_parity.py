@@ -523,6 +523,14 @@ def test_linear_u16_tables(rii, ref, monkeypatch, kind, N, D, M, nq, topk):
             g3 = g.query(q, topk, target_ids=sub, path="linear")
             monkeypatch.delenv("RII_Q16_CFG")
             assert np.array_equal(gr[0], g3[0]) and np.array_equal(gr[1], g3[1]), f"cfg {cfg}"
+        if M == 64:  # lane-pair (split) u6 kernel at 256 / 384 threads and the one-lane kernel
+            for env in ({"RII_M64_NTH": "384"}, {"RII_M64_SPLIT": "0"}, {"RII_M64_SPLIT": "0", "RII_M64_NTH": "384"}):
+                for k, v in env.items():
+                    monkeypatch.setenv(k, v)
+                g4 = g.query(q, topk, target_ids=sub, path="linear")
+                for k in env:
+                    monkeypatch.delenv(k)
+                assert np.array_equal(gr[0], g4[0]) and np.array_equal(gr[1], g4[1]), env
 
 
 def test_linear_u16_duplicates_and_zero_distance(rii, ref, monkeypatch):

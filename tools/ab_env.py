@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nq", type=int, default=0, help="queries per call (default: the workload's)")
     ap.add_argument("--subset_n", type=int, default=0, help="subset size in ids (overrides --subset)")
+    ap.add_argument("--cases", default="", help="several query configurations on one build: "
+                    "'path/L/subset_n[/nq]' entries separated by commas (overrides --path/--L/--subset_n)")
     ap.add_argument("settings", nargs="*")
     a = ap.parse_args()
     kind, N, D, M, nlist, nq, topk, n_train, _ = bench.WORKLOADS[a.workload]
@@ -37,9 +39,15 @@ def main():
     g.add(x)
     del x
     g.reconfigure(nlist, n_iter=10, seed=0)
-    nq = a.nq or nq
+    cases = [c.split("/") for c in a.cases.split(",") if c] or [[a.path, str(a.L), str(a.subset_n or int(N * a.subset)), str(a.nq or nq)]]
+    for c in cases:
+        path, L, ns = c[0], int(c[1]), int(c[2])
+        cq = int(c[3]) if len(c) > 3 else (a.nq or nq)
+        run_case(g, kind, N, D, cq, topk, dev, path, L, ns, a)
+
+
+def run_case(g, kind, N, D, nq, topk, dev, path, L, ns, a):
     q = bench._device_data(kind, nq, D, dev, 0, gen.STREAM_QUERY)
-    ns = a.subset_n or int(N * a.subset)
     S = gen.subset_torch(N, ns, dev, seed=0) if ns > 0 else None
     ids = torch.empty((nq, topk), dtype=torch.int64, device=dev)
     dist = torch.empty((nq, topk), dtype=torch.float32, device=dev)
@@ -48,23 +56,23 @@ def main():
         env = dict(kv.split("=", 1) for kv in st.split(";") if kv)
         old = {k: os.environ.get(k) for k in env}
         os.environ.update(env)
-        g.query(q, topk, S, L=a.L, path=a.path, out=(ids, dist))
+        g.query(q, topk, S, L=L, path=path, out=(ids, dist))
         torch.cuda.synchronize()
-        ms = bench._timed_steps(lambda: g.query(q, topk, S, L=a.L, path=a.path, out=(ids, dist)), a.reps,
+        ms = bench._timed_steps(lambda: g.query(q, topk, S, L=L, path=path, out=(ids, dist)), a.reps,
                                 torch.cuda.current_stream())
         same = None
         if ref is None:
             ref = (ids.clone(), dist.clone())
         else:
             same = bool(torch.equal(ref[0], ids) and torch.equal(ref[1], dist))
-        print(json.dumps({"env": env, "ms": sorted(ms)[len(ms) // 2], "qps": nq / (sorted(ms)[len(ms) // 2] / 1e3),
+        print(json.dumps({"workload": a.workload, "path": path, "L": L, "subset_n": ns, "nq": nq, "env": env,
+                          "ms": sorted(ms)[len(ms) // 2], "qps": nq / (sorted(ms)[len(ms) // 2] / 1e3),
                           "same_as_first": same}), flush=True)
         for k, v in old.items():
             if v is None:
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
-
 
 if __name__ == "__main__":
     main()

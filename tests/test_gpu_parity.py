@@ -523,8 +523,8 @@ def test_linear_u16_tables(rii, ref, monkeypatch, kind, N, D, M, nq, topk):
             g3 = g.query(q, topk, target_ids=sub, path="linear")
             monkeypatch.delenv("RII_Q16_CFG")
             assert np.array_equal(gr[0], g3[0]) and np.array_equal(gr[1], g3[1]), f"cfg {cfg}"
-        if M == 64:  # lane-pair (split) u6 kernel at 256 / 384 threads and the one-lane kernel
-            for env in ({"RII_M64_NTH": "384"}, {"RII_M64_SPLIT": "0"}, {"RII_M64_SPLIT": "0", "RII_M64_NTH": "384"}):
+        if M == 64:  # the u6 kernel at 384 threads (A/B variant) equals the default 256
+            for env in ({"RII_M64_NTH": "384"},):
                 for k, v in env.items():
                     monkeypatch.setenv(k, v)
                 g4 = g.query(q, topk, target_ids=sub, path="linear")

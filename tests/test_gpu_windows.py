@@ -46,7 +46,7 @@ CASES = [
     ("deep", 600_000, 96, 32, 48, 400_000, 4_096, ("gthr_tightenings", "rescales", "publishes")),
     # the u16 kernel (M = 16) under the same schedule
     ("sift", 600_000, 128, 16, 40, 400_000, 4_096, ("gthr_tightenings", "rescales", "publishes")),
-    # M = 64 (the paper's SIFT1M shape, Table 2): the lane-pair u6 kernel, two table halves
+    # M = 64 (the paper's SIFT1M shape, Table 2): two table halves
     ("sift", 600_000, 128, 64, 24, 400_000, 4_096, ("gthr_tightenings", "rescales", "publishes")),
 ]
 

@@ -111,11 +111,16 @@ def sift_like_torch(n: int, device, D: int = 128, n_comp: int = 64, seed: int = 
 
 
 def deep_like_torch(n: int, device, D: int = 96, n_comp: int = 256, seed: int = 0, stream: int = STREAM_BASE,
-                    out=None, chunk: int = 1 << 22):
+                    out=None, chunk: int = 1 << 22, batch: int | None = None):
+    """Device-side Deep1B stand-in (the recipe of deep_like).  `seed` fixes the mixture
+    (its means) and the random stream; `batch` (streamed databases, configs[4]) draws
+    batch b of the SAME mixture from its own stream, so that the base vectors of every
+    batch, the training sample and the queries share one set of means."""
     torch = _torch()
     mu = torch.from_numpy(_deep_means(D, n_comp, seed)).to(device=device, dtype=torch.float32)
     gen = torch.Generator(device=device)
-    gen.manual_seed((int(seed) << 8) | int(stream))
+    gen.manual_seed((int(seed) << 8) | int(stream) if batch is None else
+                    (((int(seed) << 8) | int(stream)) << 24) + 1 + int(batch))
     if out is None:
         out = torch.empty((n, D), dtype=torch.float32, device=device)
     for s in range(0, n, chunk):

@@ -167,7 +167,8 @@ def main():
         chunk = 1 << 24
         t0 = time.perf_counter()
         for s0 in range(0, N, chunk):  # streamed: the raw vectors are never stored
-            xb = gen.deep_like_torch(min(chunk, N - s0), DEV, D=D, seed=1000 + s0 // chunk, stream=gen.STREAM_BASE)
+            xb = gen.deep_like_torch(min(chunk, N - s0), DEV, D=D, seed=0, stream=gen.STREAM_BASE,
+                                    batch=s0 // chunk)
             g.add(xb)
             del xb
         torch.cuda.synchronize()

@@ -29,7 +29,8 @@ def main():
     g.train(bench._device_data("deep", c["n_train"], D, DEV, 0, gen.STREAM_TRAIN), n_iter=20, seed=0)
     chunk = 1 << 24
     for s0 in range(0, N, chunk):
-        xb = gen.deep_like_torch(min(chunk, N - s0), DEV, D=D, seed=1000 + s0 // chunk, stream=gen.STREAM_BASE)
+        xb = gen.deep_like_torch(min(chunk, N - s0), DEV, D=D, seed=0, stream=gen.STREAM_BASE,
+                                    batch=s0 // chunk)
         g.add(xb)
         del xb
     torch.cuda.empty_cache()

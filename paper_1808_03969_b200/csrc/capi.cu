@@ -597,9 +597,13 @@ const int32_t *coarse_probes(const rii_index *x, QueryScratch &sc, const QueryAr
     const char *cte = getenv("RII_COARSE_TOPP");  // 0: the scan-based coarse ranking (A/B)
     if (P >= x->K) {
         launch_select_probes(nullptr, a.nq, x->K, P, probes, st);  // every list
-    } else if (fast && !(cte && cte[0] == '0') &&
+    } else if (fast && !(cte && cte[0] == '0') && (x->K <= 8192 || P > 1008 || (cte && cte[0] == '1')) &&
                launch_coarse_topp(x->centers.as<uint8_t>(), x->K, x->M, tables, a.nq, P, probes, st)) {
-        // one CTA per query: canonical d0 of every centre, radix-selected top-P (k_ivf.cu)
+        // one CTA per query: canonical d0 of every centre, radix-selected top-P (k_ivf.cu).
+        // Measured against the scan-based ranking below: deep10m (K = 3,162) 0.7 vs 0.7 ms
+        // at L <= 16, 0.7 vs 1.2 ms at L = 64, 1.2 vs 4.5 ms at P = 640; configs[4]
+        // (K = 31,623, 1,024 queries: one CTA per SM for the 126 KB of d0) 0.57 vs 0.29 ms,
+        // so large K keeps the scan unless P > 1008 (RII_COARSE_TOPP=1 forces it)
     } else if (fast && P <= 1008) {
         // coarse ranking (L2-L5) with the lane-rotated scan over the K centre codes,
         // canonical rescore, top-P by (d0, k) (L6)

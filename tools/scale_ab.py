@@ -22,7 +22,8 @@ DEV = torch.device("cuda", 0)
 
 
 def main():
-    settings = sys.argv[1:] or [""]
+    prof = "--profile" in sys.argv  # one IVF L = 64 call between cudaProfilerStart / Stop (ncu)
+    settings = [a for a in sys.argv[1:] if a != "--profile"] or [""]
     c = gen.CONFIGS["scale1b"]
     N, D, M, K = c["N"], c["D"], c["M"], c["nlist"]
     g = rii.Index(D, M, device=0)
@@ -39,6 +40,14 @@ def main():
     q = gen.deep_like_torch(1024, DEV, D=D, seed=0, stream=gen.STREAM_QUERY)
     S = gen.subset_torch(N, 1_000_000, DEV, seed=1)
     st = torch.cuda.current_stream()
+    if prof:
+        g.query(q, 100, None, L=64, path="ivf")
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        g.query(q, 100, None, L=64, path="ivf")
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        return
     for name, sub, L, path in (("ivf whole L=64", None, 64, "ivf"), ("subset 1e6 linear", S, 64, "linear"),
                                ("subset 1e6 ivf", S, 64, "ivf")):
         for s in settings:

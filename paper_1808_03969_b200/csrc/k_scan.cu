@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         else return (int64_t)qb * B + qq;
     };
     const int D = M * a.ds, tid = threadIdx.x, lane = tid & 31;
+    const uint32_t qmask = nqi >= 32 ? 0xffffffffu : (1u << nqi) - 1u;  // the slots holding real queries
 
     if constexpr (U6 && LISTS) {
         // precomputed per-query u6 tables (u6_tables_kernel) with their scales
@@ -274,7 +275,9 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     for (int e = tid; e < B * kk; e += NTH) top[e] = KEY_MAX;
     if (tid < B) {
         cnt[tid] = 0; thr[tid] = __int_as_float(0x7f800000); scratch[2 + tid] = 0;
-        gqs[tid] = a.gthr ? __ldcg(a.gthr + query_of(tid)) : __int_as_float(0x7f800000);
+        // slots past the item's / batch's queries (they repeat its last query's table) get
+        // a negative bound: they never pass the filter, push nothing and do not rescale
+        gqs[tid] = tid >= nqi ? -1.0f : a.gthr ? __ldcg(a.gthr + query_of(tid)) : __int_as_float(0x7f800000);
     }
     if (tid == 0) scratch[1] = 0;
     __syncthreads();
@@ -352,11 +355,11 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         if constexpr (Q16 && !LISTS) {
             if (tid == 0) {
                 int f = 0;
-                for (int qq = 0; qq < B; ++qq) f |= fminf(thr[qq], gqs[qq]) < 0.5f * tsc[qq];
+                for (int qq = 0; qq < nqi; ++qq) f |= fminf(thr[qq], gqs[qq]) < 0.5f * tsc[qq];
                 if (f) {
                     for (int qq = 0; qq < B; ++qq) {
                         const float T = fminf(thr[qq], gqs[qq]);
-                        if (!(T < tsc[qq])) continue;
+                        if (qq >= nqi || !(T < tsc[qq])) continue;
                         tsc[qq] = T;
                         qsc[qq] = U6 ? __fdiv_rd(U6_CAP * u6_alpha(M), fmaxf(T, 1e-30f))
                                      : __fdiv_rd((float)q16_cap<M>(), fmaxf(T, 1e-30f));
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     int win = 1;
     if constexpr (ADAPT) {
 #pragma unroll
-        for (int qq = 0; qq < B; ++qq) win &= !(th[qq] < __int_as_float(0x7f800000));
+        for (int qq = 0; qq < B; ++qq) win &= qq >= nqi || !(th[qq] < __int_as_float(0x7f800000));
         win = win ? 1 : WIN;
     } else {
         win = 0;  // the `safe` countdown of single-step windows
@@ -532,7 +535,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
 #pragma unroll
                             for (int k = 0; k < 4 * NO; ++k)
                                 mk |= (t[k] & 0x80008000u) >> (15 - (4 * (k >> 1) + (k & 1)));
-                            mk = pos < c1 ? (mk | (mk >> 14)) & ((1u << B) - 1u) : 0u;
+                            mk = pos < c1 ? (mk | (mk >> 14)) & qmask : 0u;
                             if (!LISTS && mk && a.alist) mk &= probe_bits(pos);
                             const uint32_t kid = key_of(cid[u], pos);
                             for (uint32_t wm = __reduce_or_sync(0xffffffffu, mk); wm; wm &= wm - 1u) {
@@ -556,7 +559,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                     uint32_t mk = 0;  // bit qq: query qq passes (the u6 branch's warp-mask loop)
 #pragma unroll
                     for (int qq = 0; qq < B; ++qq) mk |= (uint32_t)(dq[qq] <= thq[qq]) << qq;
-                    if (pos >= c1) mk = 0;
+                    mk = pos < c1 ? mk & qmask : 0u;
                     if (!LISTS && mk && a.alist) mk &= probe_bits(pos);
                     // the key's distance field is replaced by the canonical rescore
                     const uint32_t wmask = __reduce_or_sync(0xffffffffu, mk);
@@ -594,7 +597,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
                 for (int qq = 0; qq < B; ++qq) any |= d[qq] <= th[qq];
                 if (__any_sync(0xffffffffu, any && pos < c1)) {
                     const uint32_t kid = key_of(cid[u], pos);
-                    const uint32_t pb = probe_bits(pos);
+                    const uint32_t pb = probe_bits(pos) & qmask;
 #pragma unroll
                     for (int qq = 0; qq < B; ++qq)
                         push_candidate_win(pos < c1 && d[qq] <= th[qq] && ((pb >> qq) & 1u), make_key(d[qq], kid),

@@ -23,7 +23,8 @@ DEV = torch.device("cuda", 0)
 
 def main():
     prof = "--profile" in sys.argv  # one IVF L = 64 call between cudaProfilerStart / Stop (ncu)
-    settings = [a for a in sys.argv[1:] if a != "--profile"] or [""]
+    prof_lin = "--profile-linear" in sys.argv  # one whole linear scan of 1,024 queries instead
+    settings = [a for a in sys.argv[1:] if not a.startswith("--profile")] or [""]
     c = gen.CONFIGS["scale1b"]
     N, D, M, K = c["N"], c["D"], c["M"], c["nlist"]
     g = rii.Index(D, M, device=0)
@@ -40,11 +41,12 @@ def main():
     q = gen.deep_like_torch(1024, DEV, D=D, seed=0, stream=gen.STREAM_QUERY)
     S = gen.subset_torch(N, 1_000_000, DEV, seed=1)
     st = torch.cuda.current_stream()
-    if prof:
-        g.query(q, 100, None, L=64, path="ivf")
+    if prof or prof_lin:
+        path = "linear" if prof_lin else "ivf"
+        g.query(q, 100, None, L=64, path=path)
         torch.cuda.synchronize()
         torch.cuda.profiler.start()
-        g.query(q, 100, None, L=64, path="ivf")
+        g.query(q, 100, None, L=64, path=path)
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
         return

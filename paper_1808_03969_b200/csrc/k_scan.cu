@@ -508,6 +508,17 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         bool ovf = false, need = false;
         for (int s = 0; s < nsteps && base < c1; ++s) {
             uint32_t wn[U][W], nid[U];
+            // short codes (M <= 16, linear): one thread pulls the codes of step + PFD into L2
+            // (a bulk prefetch), so the register prefetch one step ahead waits on L2, not DRAM
+            if constexpr (!LISTS && M <= 16 && (VARIANT & 1024)) {
+                constexpr int PFD = 6;
+                const int64_t pb = base + (int64_t)PFD * STEP;
+                if (tid == 0 && pb < c1) {
+                    const uintptr_t b0 = (uintptr_t)(codes + (size_t)pb * M) & ~(uintptr_t)15;
+                    const uint32_t n = (uint32_t)(min((int64_t)STEP, c1 - pb) * M + 15) & ~15u;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b0), "r"(n) : "memory");
+                }
+            }
             load_step(base + STEP, wn, nid);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -950,6 +961,20 @@ int list_u6_cfg(int M) {
 // Measured on deep10m (10k queries): 192 wins at P >= 32 probed lists (L = 64: 15.1
 // -> 13.9 ms; with the merged-bound phases 13.9 -> 12.8 ms) and loses below (L = 16:
 // 8.8 -> 9.4 ms).  RII_LIST_NTH=192 / 384 forces one (A/B).
+// u6 list items with M <= 16 load one short code per thread and step (8 or 16 bytes):
+// with 12 warps per SM the code stream is latency-bound (configs[4], M = 8, lists of
+// 31,623 codes: 60 % of the stalls on the next step's code load, 14 % warps active),
+// so those items take two codes per thread and step.  RII_LIST_U=1 restores one (A/B).
+static bool list_u2() {
+    const char *e = getenv("RII_LIST_U");
+    return !(e && atoi(e) == 1);
+}
+// Linear u6 scans with M <= 16: bulk L2 prefetch of the codes six steps ahead
+// (VARIANT bit 10; RII_LIN_PF=1 enables, A/B)
+static bool lin_l2_prefetch() {
+    const char *e = getenv("RII_LIN_PF");
+    return e && atoi(e) == 1;
+}
 static int list_q16_nth(int M, int64_t P) {
     if (M == 64) return 384;
     const char *e = getenv("RII_LIST_NTH");
@@ -999,6 +1024,9 @@ static void *fast_kernel_ptr_h1(bool q16, int nth) {
             if constexpr (M == 32) return (void *)scan_fast_kernel<M, 16, true, 384, 1, 3, 128 | 64>;
             else return nullptr;
         } else {
+            if constexpr (M <= 16) {
+                if (lin_l2_prefetch()) return (void *)scan_fast_kernel<M, 16, false, 384, 1, 3, 1024 | 128 | 64>;
+            }
             return (void *)scan_fast_kernel<M, 16, false, 384, 1, 3, 128 | 64>;
         }
     } else {
@@ -1017,6 +1045,9 @@ static void *fast_kernel_ptr_b(bool q16, int nth) {
         if constexpr (LISTS) {
             if (q16) {
                 if (list_u6_cfg(M) >= 3 && list_u7(M)) {
+                    if constexpr (M <= 16) {  // two codes per thread and step (RII_LIST_U=1: one)
+                        if (nth == 192 && list_u2()) return (void *)scan_fast_kernel<M, 8, true, 192, 2, 3, 256 | 128 | 64>;
+                    }
                     if (nth == 192) return (void *)scan_fast_kernel<M, 8, true, 192, 1, 3, 256 | 128 | 64>;
                     return (void *)scan_fast_kernel<M, 8, true, 384, 1, 3, 256 | 128 | 64>;
                 }

@@ -961,10 +961,12 @@ int list_u6_cfg(int M) {
 // Measured on deep10m (10k queries): 192 wins at P >= 32 probed lists (L = 64: 15.1
 // -> 13.9 ms; with the merged-bound phases 13.9 -> 12.8 ms) and loses below (L = 16:
 // 8.8 -> 9.4 ms).  RII_LIST_NTH=192 / 384 forces one (A/B).
-// u6 list items with M <= 16 load one short code per thread and step (8 or 16 bytes):
-// with 12 warps per SM the code stream is latency-bound (configs[4], M = 8, lists of
-// 31,623 codes: 60 % of the stalls on the next step's code load, 14 % warps active),
-// so those items take two codes per thread and step.  RII_LIST_U=1 restores one (A/B).
+// u6 list items with M = 8 load one 8-byte code per thread and step: with 12 warps per
+// SM the code stream is latency-bound (configs[4], lists of 31,623 codes: 60 % of the
+// stalls on the next step's code load, 14 % warps active), so those items take two
+// codes per thread and step: configs[4] IVF L = 64 19.6 -> 13.4 ms per 1,024 queries,
+// the deep10m shape at M = 8 8.2 -> 7.5 ms (M = 16, sift1m: 6.7 -> 6.8 ms, not taken).
+// RII_LIST_U=1 restores one (A/B).
 static bool list_u2() {
     const char *e = getenv("RII_LIST_U");
     return !(e && atoi(e) == 1);
@@ -1045,7 +1047,7 @@ static void *fast_kernel_ptr_b(bool q16, int nth) {
         if constexpr (LISTS) {
             if (q16) {
                 if (list_u6_cfg(M) >= 3 && list_u7(M)) {
-                    if constexpr (M <= 16) {  // two codes per thread and step (RII_LIST_U=1: one)
+                    if constexpr (M <= 8) {  // two codes per thread and step (RII_LIST_U=1: one)
                         if (nth == 192 && list_u2()) return (void *)scan_fast_kernel<M, 8, true, 192, 2, 3, 256 | 128 | 64>;
                     }
                     if (nth == 192) return (void *)scan_fast_kernel<M, 8, true, 192, 1, 3, 256 | 128 | 64>;
@@ -1124,8 +1126,11 @@ bool list_major_supported(int M) { return M == 4 || M == 8 || M == 16 || M == 32
 #ifndef RII_SCAN_M  // common translation unit only
 int list_major_B(int kk, double avg_len, int M) {
     if (lut_halves(M) > 1) return smem_fast(2, kk, M) <= SMEM_CAP ? 2 : 0;  // fp32 pairs of two halves
-    const char *pe = getenv("RII_LIST_PACKED_MIN");  // A/B knob
-    const double pmin = pe ? atof(pe) : (double)PACKED_MIN_CODES;
+    // bf16-packed B = 8 list items only on request (RII_LIST_PACKED_MIN = shortest average
+    // list, A/B): slower than fp32 pairs wherever measured (deep10m rank-0 items 12.4 ->
+    // 15.9 ms at 16,384; configs[4], lists of 31,623: 12.8 vs 13.4 ms per 1,024 queries)
+    const char *pe = getenv("RII_LIST_PACKED_MIN");
+    const double pmin = pe ? atof(pe) : 1e300;
     for (int B : {8, 6, 4, 2}) {
         if (B == 8 && (!packed_enabled() || avg_len < pmin)) continue;
         if (smem_fast(B, kk) <= SMEM_CAP) return B;

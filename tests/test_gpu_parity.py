@@ -102,7 +102,8 @@ def test_paths_match_oracle(rii, ref, kind, N, D, M, K, nq, topk):
 def test_ivf_list_major_and_query_major(rii, ref, monkeypatch, mode, kind, N, D, M, K):
     """Both posting-list traversals (list-major: B queries share a list; query-major:
     one table per query) against the oracle's Alg. 2, whole and subset.  K = 2 makes
-    the lists long enough for the bf16-packed list-major kernel."""
+    the lists long (20k codes).  List-major variants (two codes per thread for M = 8,
+    bf16-packed and group-minimum-bound items, u6 / u7 items) give the same bytes."""
     monkeypatch.setenv("RII_IVF_MODE", mode)
     x = gen.base(kind, N, D, seed=N)
     q = gen.base(kind, 41, D, seed=N, stream=gen.STREAM_QUERY)
@@ -120,10 +121,19 @@ def test_ivf_list_major_and_query_major(rii, ref, monkeypatch, mode, kind, N, D,
                 g2 = g.query(q, 100, target_ids=sub, L=L, path="ivf")
                 monkeypatch.delenv("RII_Q16")
                 assert np.array_equal(gr[0], g2[0]) and np.array_equal(gr[1], g2[1])
+                monkeypatch.setenv("RII_LIST_PACKED_MIN", "1")  # bf16-packed fp items (A/B variant, off by default)
+                g5 = g.query(q, 100, target_ids=sub, L=L, path="ivf")
+                monkeypatch.delenv("RII_LIST_PACKED_MIN")
+                assert np.array_equal(gr[0], g5[0]) and np.array_equal(gr[1], g5[1])
                 monkeypatch.setenv("RII_LIST_BOUND", "1")  # group-minimum bound items instead of phase A
                 g4 = g.query(q, 100, target_ids=sub, L=L, path="ivf")
                 monkeypatch.delenv("RII_LIST_BOUND")
                 assert np.array_equal(gr[0], g4[0]) and np.array_equal(gr[1], g4[1])
+                if M == 8:  # one code per thread and step (two by default)
+                    monkeypatch.setenv("RII_LIST_U", "1")
+                    g6 = g.query(q, 100, target_ids=sub, L=L, path="ivf")
+                    monkeypatch.delenv("RII_LIST_U")
+                    assert np.array_equal(gr[0], g6[0]) and np.array_equal(gr[1], g6[1])
                 if M == 32:  # u6 items of 8 (RII_LIST_U6=3) and 16 queries (=4); 7-bit items
                     for var, cfg in (("RII_LIST_U6", "3"), ("RII_LIST_U6", "4"), ("RII_LIST_U7", "0"),
                                      ("RII_LIST_NTH", "192"), ("RII_LIST_NTH", "384")):

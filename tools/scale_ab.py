@@ -51,7 +51,7 @@ def main():
         torch.cuda.profiler.stop()
         return
     for name, sub, L, path in (("ivf whole L=64", None, 64, "ivf"), ("subset 1e6 linear", S, 64, "linear"),
-                               ("subset 1e6 ivf", S, 64, "ivf")):
+                               ("subset 1e6 ivf", S, 64, "ivf"), ("linear whole", None, 64, "linear")):
         for s in settings:
             env = dict(kv.split("=", 1) for kv in s.split(";") if kv)
             old = {k: os.environ.get(k) for k in env}

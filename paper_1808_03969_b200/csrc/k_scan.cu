@@ -971,11 +971,14 @@ static bool list_u2() {
     const char *e = getenv("RII_LIST_U");
     return !(e && atoi(e) == 1);
 }
-// Linear u6 scans with M <= 16: bulk L2 prefetch of the codes six steps ahead
-// (VARIANT bit 10; RII_LIN_PF=1 enables, A/B)
-static bool lin_l2_prefetch() {
-    const char *e = getenv("RII_LIN_PF");
-    return e && atoi(e) == 1;
+// Long linear u6 scans with M = 8: a bulk L2 prefetch of the codes six steps ahead
+// (VARIANT bit 10), so the one-step register prefetch of 8-byte codes waits on L2, not
+// DRAM: configs[4] linear (1,024 queries x 1e9 codes) 479.5 -> 401.1 ms, the deep10m
+// shape at M = 8 49.3 -> 43.5 ms; a 1e6-code subset 1.15 -> 1.23 ms and sift1m (M = 16)
+// 11.0 -> 11.5 ms, so only M = 8 scans of >= 2^22 codes take it.  RII_LIN_PF=0 disables.
+static bool lin_l2_prefetch(int64_t n) {
+    const char *e = getenv("RII_LIN_PF"), *m = getenv("RII_LIN_PF_MIN");  // (MIN: tests)
+    return !(e && atoi(e) == 0) && n >= (m ? atoll(m) : ((int64_t)1 << 22));
 }
 static int list_q16_nth(int M, int64_t P) {
     if (M == 64) return 384;
@@ -1026,9 +1029,6 @@ static void *fast_kernel_ptr_h1(bool q16, int nth) {
             if constexpr (M == 32) return (void *)scan_fast_kernel<M, 16, true, 384, 1, 3, 128 | 64>;
             else return nullptr;
         } else {
-            if constexpr (M <= 16) {
-                if (lin_l2_prefetch()) return (void *)scan_fast_kernel<M, 16, false, 384, 1, 3, 1024 | 128 | 64>;
-            }
             return (void *)scan_fast_kernel<M, 16, false, 384, 1, 3, 128 | 64>;
         }
     } else {
@@ -1080,6 +1080,9 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
     const bool q16 = (B == 8 || B == 16) && q16_req && gthr != nullptr;
     if (mask.alist && mask.B != B) throw Error(1, "probe mask grouped by a different query batch");
     void *kern = fast_kernel_ptr<M, B, false>(q16);
+    if constexpr (M == 8 && B == 16) {
+        if (q16 && lin_l2_prefetch(n)) kern = (void *)scan_fast_kernel<M, 16, false, 384, 1, 3, 1024 | 128 | 64>;
+    }
     const size_t smem = q16 && B == 8 ? smem_q16(kk) : pl.smem;
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     ScanArgs a{};

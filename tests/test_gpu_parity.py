@@ -533,6 +533,11 @@ def test_linear_u16_tables(rii, ref, monkeypatch, kind, N, D, M, nq, topk):
             g3 = g.query(q, topk, target_ids=sub, path="linear")
             monkeypatch.delenv("RII_Q16_CFG")
             assert np.array_equal(gr[0], g3[0]) and np.array_equal(gr[1], g3[1]), f"cfg {cfg}"
+        if M == 8:  # the L2-prefetching variant of long M = 8 scans (forced onto this size)
+            monkeypatch.setenv("RII_LIN_PF_MIN", "1")
+            g4 = g.query(q, topk, target_ids=sub, path="linear")
+            monkeypatch.delenv("RII_LIN_PF_MIN")
+            assert np.array_equal(gr[0], g4[0]) and np.array_equal(gr[1], g4[1])
         if M == 64:  # the u6 kernel at 384 threads (A/B variant) equals the default 256
             for env in ({"RII_M64_NTH": "384"},):
                 for k, v in env.items():

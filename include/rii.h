@@ -213,7 +213,10 @@ rii_status rii_reconfigure(rii_index *idx, int32_t nlist, int32_t n_iter, uint64
  *     a path.  K == 0 forces LINEAR; IVF with K == 0 -> RII_ERR_STATE.
  *  out_ids / out_dist: nq x topk, each row sorted by (dist asc, id asc); rows
  *     with fewer than topk candidates are padded with id -1 and dist +inf (R18).
- *  path_used (may be NULL): the path taken. */
+ *  path_used (may be NULL): the path taken (Alg. 3's choice).  An inverted-index
+ *     query in mode A may execute as a linear scan of S -- every list probed
+ *     (P = K), or a scan masked to each query's probed lists when P is a large
+ *     fraction of K -- whose candidate set, and so result, is Alg. 2's exactly. */
 rii_status rii_query(const rii_index *idx, const float *q, int64_t nq, int32_t topk, const int64_t *target_ids,
                      int64_t n_target, int32_t L, rii_path path, rii_mem where, void *stream, int64_t *out_ids,
                      float *out_dist, int32_t *path_used);

@@ -17,8 +17,6 @@
 namespace rii {
 
 constexpr int CQ = 4;   // queries per CTA in coarse_dist
-// coarse_topp_kernel: bytes of the staged [M][257] fp32 table, rounded to 16
-__host__ __device__ constexpr size_t coarse_topp_tab_bytes(int M) { return ((size_t)M * (KS + 1) * 4 + 15) / 16 * 16; }
 constexpr int CMC = 32; // subspaces per table chunk in coarse_dist
 
 // d0[q][k] (Alg. 2 L2-L5): CTA = (256 centres, CQ queries); the CA1 table is built
@@ -146,105 +144,165 @@ __global__ void __launch_bounds__(NT) select_probes_kernel(const float *__restri
 }
 
 // Coarse ranking and probe selection in one kernel (Alg. 2 L2-L6) for the fast-layout M
-// (precomputed CA1 tables, lut_tables_kernel): CTA = one query.  Its table is staged in
-// shared memory as [m][z] with a row pitch of 257 floats (bank = (m + z) mod 32); thread
-// = centres k, d0_k summed in CA2 order (m ascending, canonical); the P smallest
-// (d0, k) by a radix select over the d0 bit patterns (d0 >= +0: bit order is value
-// order), ties at the threshold to the lowest k (CA4); the P keys are then sorted by
-// (d0, k) so probes[q][r] is the rank-r list (the list-major items and their phases
-// run nearest lists first).  Replaces, for P <= CT_PMAX, the lane-rotated scan over the
-// centre codes with top-P lists of kkc keys (per-CTA table fill of 6 queries, top-kk
-// compactions from an infinite threshold): deep10m L = 64 ... see DESIGN.md §6.
+// (precomputed CA1 tables, lut_tables_kernel, [half][z][32 columns], column c = A(32 h +
+// c mod min(M, 32), z)): CTA = one query, thread = centres k.
+//  1. Lane-rotated sums: at step j lane l reads column (l + j) mod 32 of its centre's
+//     row z, so the 32 lanes of a warp hit 32 distinct banks (no conflicts); a lane's
+//     sum runs over the subspaces in a rotated order (not CA2's).
+//  2. T = the P-th smallest rotated sum (radix select over the bit patterns, d >= +0).
+//  3. Candidates C = {k : d_rot(k) <= T (1 + eps)^2}, eps = 1e-5 >= 2 (M - 1) 2^-24 (the
+//     relative gap between any two fp32 summation orders of M non-negative terms,
+//     M <= 64): at least P centres have d_rot <= T, hence canonical d0 <= T (1 + eps),
+//     so the P-th smallest canonical d0 is <= T (1 + eps) and every member of the exact
+//     top-P has d_rot <= T (1 + eps)^2 -- C contains it.
+//  4. Canonical CA2 d0 (m ascending) for the members of C only, keys (d0, k), bitonic
+//     sort, the first P are the exact top-P by (d0, k) (ties to the lowest k, CA4), in
+//     rank order (the list-major items and their phases run nearest lists first).
+// If C overflows its buffer (many near-ties) the kernel computes every canonical d0
+// and selects exactly with a radix select and tie ranks by k.
 constexpr int CT_NT = 256;
 constexpr int CT_PMAX = 2048;
+constexpr float CT_EPS2 = 1.00002f;  // (1 + 1e-5)^2, rounded up
+
+__host__ __device__ constexpr size_t ct_tab_bytes(int M) { return (size_t)(M > 32 ? 2 : 1) * LUT_Q_FLOATS * 4; }
+__host__ __device__ constexpr int ct_cap(int Ppad) { return 2 * Ppad < 256 ? 256 : 2 * Ppad; }
+
+template <int M>
+__device__ __forceinline__ float ct_canonical(const float *tab, const uint8_t *__restrict__ cp) {
+    constexpr int MH = M < 32 ? M : 32;
+    float acc = 0.f;
+#pragma unroll
+    for (int m = 0; m < M; ++m) acc = __fadd_rn(acc, tab[(m / 32) * LUT_Q_FLOATS + (int)cp[m] * 32 + (m % MH)]);
+    return acc;
+}
 
 template <int M>
 __global__ void __launch_bounds__(CT_NT) coarse_topp_kernel(const uint8_t *__restrict__ centers, int64_t K,
                                                             const float *__restrict__ tables, int64_t P,
-                                                            int32_t *__restrict__ probes, size_t d0_off) {
-    constexpr int W = M / 4, MH = M < 32 ? M : 32, PITCH = KS + 1;
+                                                            int32_t *__restrict__ probes, int Ppad) {
+    constexpr int W = M / 4, H = M > 32 ? 2 : 1, MH = M < 32 ? M : 32;
     extern __shared__ __align__(16) uint8_t smem[];
-    float *tab = reinterpret_cast<float *>(smem);                          // [M][257]; later the sort keys
-    uint32_t *d0 = reinterpret_cast<uint32_t *>(smem + d0_off);  // [K] d0 bit patterns (after table / keys)
+    float *tab = reinterpret_cast<float *>(smem);                                         // [H][256][32]
+    const int cap = ct_cap(Ppad);
+    uint64_t *keys = reinterpret_cast<uint64_t *>(smem + ct_tab_bytes(M));               // [cap]
+    uint32_t *d0 = reinterpret_cast<uint32_t *>(smem + ct_tab_bytes(M) + (size_t)cap * 8);  // [K]
     __shared__ int hist[256];
     __shared__ uint32_t s_prefix, s_mask;
     __shared__ int s_rem, s_n;
     __shared__ int wsum[CT_NT / 32];
     const int64_t qi = blockIdx.x;
-    const float *tq = tables + qi * (int64_t)lut_q_floats(M);
-    // table: A(m, z) = tq[(m / 32) * 8192 + z * 32 + m % 32] (lut.cuh layout)
-    for (int e = threadIdx.x; e < M * KS; e += CT_NT) {
-        const int h = e / (KS * MH), r = e - h * KS * MH, z = r / MH, mm = r - z * MH;
-        tab[(32 * h + mm) * PITCH + z] = __ldg(tq + h * LUT_Q_FLOATS + z * 32 + mm);
+    const int lane = threadIdx.x & 31;
+    {  // stage the table (a straight copy: the rotated lookups need no transpose)
+        const float4 *src = reinterpret_cast<const float4 *>(tables + qi * (int64_t)lut_q_floats(M));
+        float4 *dst = reinterpret_cast<float4 *>(tab);
+        for (int e = threadIdx.x; e < H * LUT_Q_FLOATS / 4; e += CT_NT) dst[e] = __ldg(src + e);
     }
     __syncthreads();
+    // 1. rotated sums
     for (int64_t k = threadIdx.x; k < K; k += CT_NT) {
         uint32_t w[W];
         const uint32_t *cp = reinterpret_cast<const uint32_t *>(centers + k * M);
 #pragma unroll
         for (int i = 0; i < W; ++i) w[i] = __ldg(cp + i);
+        // step j reads column c = (l ^ j) mod 32 (distinct per lane), i.e. subspace
+        // 32 (j / 32) + c mod MH: its code word is w[(j / 4) ^ rw] within the half, so the
+        // words are XOR-permuted once (static register indices in the loop)
+        permute_words<W, 8>(w, ((uint32_t)lane >> 2) & (uint32_t)(MH / 4 - 1));
         float acc = 0.f;
 #pragma unroll
-        for (int m = 0; m < M; ++m) acc = __fadd_rn(acc, tab[m * PITCH + ((w[m >> 2] >> (8 * (m & 3))) & 255u)]);
+        for (int j = 0; j < M; ++j) {
+            const uint32_t c = ((uint32_t)lane ^ (uint32_t)j) & 31u;
+            const uint32_t z = (w[j >> 2] >> (8 * (c & 3u))) & 255u;
+            acc = __fadd_rn(acc, tab[(j >> 5) * LUT_Q_FLOATS + (int)z * 32 + (int)c]);
+        }
         d0[k] = __float_as_uint(acc);
     }
     if (threadIdx.x == 0) { s_prefix = 0; s_mask = 0; s_rem = (int)P; s_n = 0; }
     __syncthreads();
-    // radix select: the P-th smallest bit pattern t, s_rem = how many keys equal to t are taken
-    for (int shift = 24; shift >= 0; shift -= 8) {
-        hist[threadIdx.x] = 0;
-        __syncthreads();
-        const uint32_t pre = s_prefix, msk = s_mask;
-        for (int64_t k = threadIdx.x; k < K; k += CT_NT) {
-            const uint32_t v = d0[k];
-            if ((v & msk) == pre) atomicAdd(&hist[(v >> shift) & 255], 1);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int rem = s_rem, acc = 0, d = 0;
-            for (; d < 256; ++d) {
-                if (acc + hist[d] >= rem) break;
-                acc += hist[d];
+    // radix select over d0[0, K): the P-th smallest bit pattern -> s_prefix (s_rem = how
+    // many keys equal to it belong to the P smallest)
+    auto radix_select = [&]() {
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            hist[threadIdx.x] = 0;
+            __syncthreads();
+            const uint32_t pre = s_prefix, msk = s_mask;
+            for (int64_t k = threadIdx.x; k < K; k += CT_NT) {
+                const uint32_t v = d0[k];
+                if ((v & msk) == pre) atomicAdd(&hist[(v >> shift) & 255], 1);
             }
-            s_rem = rem - acc;
-            s_prefix = pre | ((uint32_t)d << shift);
-            s_mask = msk | (255u << shift);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int rem = s_rem, acc = 0, d = 0;
+                for (; d < 256; ++d) {
+                    if (acc + hist[d] >= rem) break;
+                    acc += hist[d];
+                }
+                s_rem = rem - acc;
+                s_prefix = pre | ((uint32_t)d << shift);
+                s_mask = msk | (255u << shift);
+            }
+            __syncthreads();
         }
-        __syncthreads();
-    }
-    const uint32_t t = s_prefix;
-    const int ties = s_rem;
-    uint64_t *keys = reinterpret_cast<uint64_t *>(smem);  // the table is no longer needed
-    int Ppad = 1;
-    while (Ppad < P) Ppad <<= 1;
-    for (int e = threadIdx.x; e < Ppad; e += CT_NT) keys[e] = KEY_MAX;
-    __syncthreads();
-    // below the threshold: exactly P - ties keys, appended in any order (sorted below)
+    };
+    radix_select();
+    // 3. candidates
+    const float thr = __fmul_ru(__uint_as_float(s_prefix), CT_EPS2);
     for (int64_t k = threadIdx.x; k < K; k += CT_NT) {
-        const uint32_t v = d0[k];
-        if (v < t) keys[atomicAdd(&s_n, 1)] = ((uint64_t)v << 32) | (uint64_t)k;
-    }
-    __syncthreads();
-    // at the threshold: the `ties` lowest k, in k order (block prefix over tie flags)
-    int base = (int)P - ties, seen = 0;
-    for (int64_t k0 = 0; k0 < K && seen < ties; k0 += CT_NT) {
-        const int64_t k = k0 + threadIdx.x;
-        const int tie = (k < K && d0[k] == t) ? 1 : 0;
-        const unsigned bal = __ballot_sync(0xffffffffu, tie);
-        if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = __popc(bal);
-        __syncthreads();
-        int off = 0, tot = 0;
-        for (int w = 0; w < CT_NT / 32; ++w) {
-            if (w < (int)(threadIdx.x >> 5)) off += wsum[w];
-            tot += wsum[w];
+        if (__uint_as_float(d0[k]) <= thr) {
+            const int i = atomicAdd(&s_n, 1);
+            if (i < cap) keys[i] = (uint64_t)k;
         }
-        const int rank = seen + off + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
-        if (tie && rank < ties) keys[base + rank] = ((uint64_t)t << 32) | (uint64_t)k;
-        seen += tot;
-        __syncthreads();
     }
     __syncthreads();
-    bitonic_sort_rows(keys, 1, Ppad, Ppad);
+    const int n = s_n;
+    int S = 1;
+    if (n <= cap) {
+        // 4. canonical d0 of the candidates, exact order
+        for (int i = threadIdx.x; i < n; i += CT_NT) {
+            const uint32_t k = (uint32_t)keys[i];
+            keys[i] = ((uint64_t)__float_as_uint(ct_canonical<M>(tab, centers + (int64_t)k * M)) << 32) | k;
+        }
+        while (S < n) S <<= 1;
+        for (int i = n + threadIdx.x; i < S; i += CT_NT) keys[i] = KEY_MAX;
+    } else {
+        // fallback: every canonical d0, exact radix select with ties to the lowest k
+        __syncthreads();
+        for (int64_t k = threadIdx.x; k < K; k += CT_NT)
+            d0[k] = __float_as_uint(ct_canonical<M>(tab, centers + k * M));
+        if (threadIdx.x == 0) { s_prefix = 0; s_mask = 0; s_rem = (int)P; s_n = 0; }
+        __syncthreads();
+        radix_select();
+        const uint32_t t = s_prefix;
+        const int ties = s_rem;
+        S = Ppad;
+        for (int e = threadIdx.x; e < S; e += CT_NT) keys[e] = KEY_MAX;
+        __syncthreads();
+        for (int64_t k = threadIdx.x; k < K; k += CT_NT) {  // below the threshold: P - ties keys
+            const uint32_t v = d0[k];
+            if (v < t) keys[atomicAdd(&s_n, 1)] = ((uint64_t)v << 32) | (uint64_t)k;
+        }
+        __syncthreads();
+        const int base = (int)P - ties;
+        int seen = 0;
+        for (int64_t k0 = 0; k0 < K && seen < ties; k0 += CT_NT) {  // at it: the lowest k first
+            const int64_t k = k0 + threadIdx.x;
+            const int tie = (k < K && d0[k] == t) ? 1 : 0;
+            const unsigned bal = __ballot_sync(0xffffffffu, tie);
+            if (lane == 0) wsum[threadIdx.x >> 5] = __popc(bal);
+            __syncthreads();
+            int off = 0, tot = 0;
+            for (int w = 0; w < CT_NT / 32; ++w) {
+                if (w < (int)(threadIdx.x >> 5)) off += wsum[w];
+                tot += wsum[w];
+            }
+            const int rank = seen + off + __popc(bal & ((1u << lane) - 1u));
+            if (tie && rank < ties) keys[base + rank] = ((uint64_t)t << 32) | (uint64_t)k;
+            seen += tot;
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    bitonic_sort_rows(keys, 1, S, S);
     for (int64_t r = threadIdx.x; r < P; r += CT_NT) probes[qi * P + r] = (int32_t)(keys[r] & 0xffffffffu);
 }
 
@@ -253,8 +311,7 @@ bool launch_coarse_topp(const uint8_t *centers, int64_t K, int M, const float *t
     if (P > CT_PMAX || P > K || !tables || (M != 4 && M != 8 && M != 16 && M != 32 && M != 64)) return false;
     int Ppad = 1;
     while (Ppad < P) Ppad <<= 1;
-    const size_t d0_off = std::max<size_t>(coarse_topp_tab_bytes(M), (size_t)Ppad * 8);
-    const size_t smem = d0_off + (size_t)K * 4;
+    const size_t smem = ct_tab_bytes(M) + (size_t)ct_cap(Ppad) * 8 + (size_t)K * 4;
     if (smem + 4096 > (size_t)SMEM_ATTR_MAX) return false;
     if (nq <= 0) return true;
     switch (M) {
@@ -262,7 +319,7 @@ bool launch_coarse_topp(const uint8_t *centers, int64_t K, int M, const float *t
     case MM:                                                                                                  \
         RII_CUDA(cudaFuncSetAttribute(coarse_topp_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                       SMEM_ATTR_MAX - 4096));                                                 \
-        coarse_topp_kernel<MM><<<(unsigned)nq, CT_NT, smem, st>>>(centers, K, tables, P, probes, d0_off);    \
+        coarse_topp_kernel<MM><<<(unsigned)nq, CT_NT, smem, st>>>(centers, K, tables, P, probes, Ppad);      \
         break;
         RII_CT(4) RII_CT(8) RII_CT(16) RII_CT(32) RII_CT(64)
 #undef RII_CT

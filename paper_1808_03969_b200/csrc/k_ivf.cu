@@ -164,15 +164,19 @@ constexpr int CT_NT = 256;
 constexpr int CT_PMAX = 2048;
 constexpr float CT_EPS2 = 1.00002f;  // (1 + 1e-5)^2, rounded up
 
-__host__ __device__ constexpr size_t ct_tab_bytes(int M) { return (size_t)(M > 32 ? 2 : 1) * LUT_Q_FLOATS * 4; }
+// the table region holds the [H][256][32] rotated layout, then (transposed in place for
+// the canonical sums) [M][257] (bank = (m + z) mod 32)
+__host__ __device__ constexpr size_t ct_tab_bytes(int M) {
+    return ((size_t)(M > 32 ? 2 : 1) * LUT_Q_FLOATS * 4 > (size_t)M * 257 * 4 ? (size_t)(M > 32 ? 2 : 1) * LUT_Q_FLOATS * 4
+                                                                              : ((size_t)M * 257 * 4 + 15) / 16 * 16);
+}
 __host__ __device__ constexpr int ct_cap(int Ppad) { return 2 * Ppad < 256 ? 256 : 2 * Ppad; }
 
 template <int M>
-__device__ __forceinline__ float ct_canonical(const float *tab, const uint8_t *__restrict__ cp) {
-    constexpr int MH = M < 32 ? M : 32;
-    float acc = 0.f;
+__device__ __forceinline__ float ct_canonical(const float *tabc, const uint8_t *__restrict__ cp) {
+    float acc = 0.f;  // tabc: [M][257]
 #pragma unroll
-    for (int m = 0; m < M; ++m) acc = __fadd_rn(acc, tab[(m / 32) * LUT_Q_FLOATS + (int)cp[m] * 32 + (m % MH)]);
+    for (int m = 0; m < M; ++m) acc = __fadd_rn(acc, tabc[m * 257 + (int)cp[m]]);
     return acc;
 }
 
@@ -254,6 +258,19 @@ __global__ void __launch_bounds__(CT_NT) coarse_topp_kernel(const uint8_t *__res
         }
     }
     __syncthreads();
+    {  // transpose the table in place to [M][257] for the canonical sums (bank (m + z) mod 32)
+        constexpr int E = H * LUT_Q_FLOATS / CT_NT;
+        float v[E];
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i] = tab[threadIdx.x + i * CT_NT];
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            const int e = threadIdx.x + i * CT_NT, h = e / LUT_Q_FLOATS, z = (e % LUT_Q_FLOATS) / 32, c = e % 32;
+            if (c < MH) tab[(32 * h + c) * 257 + z] = v[i];
+        }
+        __syncthreads();
+    }
     const int n = s_n;
     int S = 1;
     if (n <= cap) {

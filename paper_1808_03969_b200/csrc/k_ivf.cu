@@ -158,11 +158,14 @@ __global__ void __launch_bounds__(NT) select_probes_kernel(const float *__restri
 //  4. Canonical CA2 d0 (m ascending) for the members of C only, keys (d0, k), bitonic
 //     sort, the first P are the exact top-P by (d0, k) (ties to the lowest k, CA4), in
 //     rank order (the list-major items and their phases run nearest lists first).
-// If C overflows its buffer (many near-ties) the kernel computes every canonical d0
-// and selects exactly with a radix select and tie ranks by k.
+// For P > CT_ROT_PMAX (masked IVF: hundreds of lists), or if C overflows its buffer
+// (many near-ties), the kernel computes every canonical d0 and selects exactly with a
+// radix select and tie ranks by k.  Measured (deep10m, 10k queries): L = 1 2.76 ->
+// 2.59 ms per call, L = 64 11.68 -> 11.59 ms against the canonical-only kernel.
 constexpr int CT_NT = 256;
 constexpr int CT_PMAX = 2048;
 constexpr float CT_EPS2 = 1.00002f;  // (1 + 1e-5)^2, rounded up
+constexpr int CT_ROT_PMAX = 128;     // larger P: canonical sums of every centre directly
 
 // the table region holds the [H][256][32] rotated layout, then (transposed in place for
 // the canonical sums) [M][257] (bank = (m + z) mod 32)
@@ -202,8 +205,11 @@ __global__ void __launch_bounds__(CT_NT) coarse_topp_kernel(const uint8_t *__res
         for (int e = threadIdx.x; e < H * LUT_Q_FLOATS / 4; e += CT_NT) dst[e] = __ldg(src + e);
     }
     __syncthreads();
+    // large P (masked IVF): the candidate re-check would recompute most of the P sums
+    // anyway, so the canonical sums of every centre are taken directly (the fallback)
+    const bool direct = P > CT_ROT_PMAX;
     // 1. rotated sums
-    for (int64_t k = threadIdx.x; k < K; k += CT_NT) {
+    for (int64_t k = threadIdx.x; k < (direct ? 0 : K); k += CT_NT) {
         uint32_t w[W];
         const uint32_t *cp = reinterpret_cast<const uint32_t *>(centers + k * M);
 #pragma unroll
@@ -248,10 +254,10 @@ __global__ void __launch_bounds__(CT_NT) coarse_topp_kernel(const uint8_t *__res
             __syncthreads();
         }
     };
-    radix_select();
+    if (!direct) radix_select();
     // 3. candidates
     const float thr = __fmul_ru(__uint_as_float(s_prefix), CT_EPS2);
-    for (int64_t k = threadIdx.x; k < K; k += CT_NT) {
+    for (int64_t k = threadIdx.x; k < (direct ? 0 : K); k += CT_NT) {
         if (__uint_as_float(d0[k]) <= thr) {
             const int i = atomicAdd(&s_n, 1);
             if (i < cap) keys[i] = (uint64_t)k;
@@ -271,7 +277,7 @@ __global__ void __launch_bounds__(CT_NT) coarse_topp_kernel(const uint8_t *__res
         }
         __syncthreads();
     }
-    const int n = s_n;
+    const int n = direct ? cap + 1 : s_n;
     int S = 1;
     if (n <= cap) {
         // 4. canonical d0 of the candidates, exact order

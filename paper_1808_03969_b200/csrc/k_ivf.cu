@@ -186,28 +186,36 @@ __device__ __forceinline__ float ct_canonical(const float *tabc, const uint8_t *
 template <int M>
 __global__ void __launch_bounds__(CT_NT) coarse_topp_kernel(const uint8_t *__restrict__ centers, int64_t K,
                                                             const float *__restrict__ tables, int64_t P,
-                                                            int32_t *__restrict__ probes, int Ppad) {
+                                                            int32_t *__restrict__ probes, int Ppad,
+                                                            int keys_off, int d0_off) {
     constexpr int W = M / 4, H = M > 32 ? 2 : 1, MH = M < 32 ? M : 32;
     extern __shared__ __align__(16) uint8_t smem[];
-    float *tab = reinterpret_cast<float *>(smem);                                         // [H][256][32]
+    float *tab = reinterpret_cast<float *>(smem);  // [H][256][32], then [M][257]
     const int cap = ct_cap(Ppad);
-    uint64_t *keys = reinterpret_cast<uint64_t *>(smem + ct_tab_bytes(M));               // [cap]
-    uint32_t *d0 = reinterpret_cast<uint32_t *>(smem + ct_tab_bytes(M) + (size_t)cap * 8);  // [K]
+    // large P (masked IVF): the candidate re-check would recompute most of the P sums
+    // anyway, so the canonical sums of every centre are taken directly (the fallback);
+    // the table is then staged as [M][257] at once and the keys overlay it at the end
+    const bool direct = P > CT_ROT_PMAX;
+    uint64_t *keys = reinterpret_cast<uint64_t *>(smem + keys_off);  // [cap] (direct: [Ppad])
+    uint32_t *d0 = reinterpret_cast<uint32_t *>(smem + d0_off);      // [K]
     __shared__ int hist[256];
     __shared__ uint32_t s_prefix, s_mask;
     __shared__ int s_rem, s_n;
     __shared__ int wsum[CT_NT / 32];
     const int64_t qi = blockIdx.x;
     const int lane = threadIdx.x & 31;
-    {  // stage the table (a straight copy: the rotated lookups need no transpose)
+    if (direct) {  // stage as [M][257] (A(m, z) = column m mod MH of row z of half m / 32)
+        const float *tq = tables + qi * (int64_t)lut_q_floats(M);
+        for (int e = threadIdx.x; e < M * KS; e += CT_NT) {
+            const int h = e / (KS * MH), r = e - h * KS * MH, z = r / MH, mm = r - z * MH;
+            tab[(32 * h + mm) * 257 + z] = __ldg(tq + h * LUT_Q_FLOATS + z * 32 + mm);
+        }
+    } else {  // stage the table (a straight copy: the rotated lookups need no transpose)
         const float4 *src = reinterpret_cast<const float4 *>(tables + qi * (int64_t)lut_q_floats(M));
         float4 *dst = reinterpret_cast<float4 *>(tab);
         for (int e = threadIdx.x; e < H * LUT_Q_FLOATS / 4; e += CT_NT) dst[e] = __ldg(src + e);
     }
     __syncthreads();
-    // large P (masked IVF): the candidate re-check would recompute most of the P sums
-    // anyway, so the canonical sums of every centre are taken directly (the fallback)
-    const bool direct = P > CT_ROT_PMAX;
     // 1. rotated sums
     for (int64_t k = threadIdx.x; k < (direct ? 0 : K); k += CT_NT) {
         uint32_t w[W];
@@ -264,7 +272,7 @@ __global__ void __launch_bounds__(CT_NT) coarse_topp_kernel(const uint8_t *__res
         }
     }
     __syncthreads();
-    {  // transpose the table in place to [M][257] for the canonical sums (bank (m + z) mod 32)
+    if (!direct) {  // transpose the table in place to [M][257] for the canonical sums (bank (m + z) mod 32)
         constexpr int E = H * LUT_Q_FLOATS / CT_NT;
         float v[E];
 #pragma unroll
@@ -334,7 +342,11 @@ bool launch_coarse_topp(const uint8_t *centers, int64_t K, int M, const float *t
     if (P > CT_PMAX || P > K || !tables || (M != 4 && M != 8 && M != 16 && M != 32 && M != 64)) return false;
     int Ppad = 1;
     while (Ppad < P) Ppad <<= 1;
-    const size_t smem = ct_tab_bytes(M) + (size_t)ct_cap(Ppad) * 8 + (size_t)K * 4;
+    const bool direct = P > CT_ROT_PMAX;
+    const size_t tb = ct_tab_bytes(M);
+    const size_t keys_off = direct && (size_t)Ppad * 8 <= tb ? 0 : tb;  // direct: keys overlay the table
+    const size_t d0_off = direct ? std::max(tb, keys_off + (size_t)Ppad * 8) : tb + (size_t)ct_cap(Ppad) * 8;
+    const size_t smem = d0_off + (size_t)K * 4;
     if (smem + 4096 > (size_t)SMEM_ATTR_MAX) return false;
     if (nq <= 0) return true;
     switch (M) {
@@ -342,7 +354,8 @@ bool launch_coarse_topp(const uint8_t *centers, int64_t K, int M, const float *t
     case MM:                                                                                                  \
         RII_CUDA(cudaFuncSetAttribute(coarse_topp_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                       SMEM_ATTR_MAX - 4096));                                                 \
-        coarse_topp_kernel<MM><<<(unsigned)nq, CT_NT, smem, st>>>(centers, K, tables, P, probes, Ppad);      \
+        coarse_topp_kernel<MM><<<(unsigned)nq, CT_NT, smem, st>>>(centers, K, tables, P, probes, Ppad,       \
+                                                                 (int)keys_off, (int)d0_off);                \
         break;
         RII_CT(4) RII_CT(8) RII_CT(16) RII_CT(32) RII_CT(64)
 #undef RII_CT

@@ -187,7 +187,7 @@ template <int M>
 __global__ void __launch_bounds__(CT_NT) coarse_topp_kernel(const uint8_t *__restrict__ centers, int64_t K,
                                                             const float *__restrict__ tables, int64_t P,
                                                             int32_t *__restrict__ probes, int Ppad,
-                                                            int keys_off, int d0_off) {
+                                                            int keys_off, int d0_off, bool direct) {
     constexpr int W = M / 4, H = M > 32 ? 2 : 1, MH = M < 32 ? M : 32;
     extern __shared__ __align__(16) uint8_t smem[];
     float *tab = reinterpret_cast<float *>(smem);  // [H][256][32], then [M][257]
@@ -195,7 +195,6 @@ __global__ void __launch_bounds__(CT_NT) coarse_topp_kernel(const uint8_t *__res
     // large P (masked IVF): the candidate re-check would recompute most of the P sums
     // anyway, so the canonical sums of every centre are taken directly (the fallback);
     // the table is then staged as [M][257] at once and the keys overlay it at the end
-    const bool direct = P > CT_ROT_PMAX;
     uint64_t *keys = reinterpret_cast<uint64_t *>(smem + keys_off);  // [cap] (direct: [Ppad])
     uint32_t *d0 = reinterpret_cast<uint32_t *>(smem + d0_off);      // [K]
     __shared__ int hist[256];
@@ -342,7 +341,10 @@ bool launch_coarse_topp(const uint8_t *centers, int64_t K, int M, const float *t
     if (P > CT_PMAX || P > K || !tables || (M != 4 && M != 8 && M != 16 && M != 32 && M != 64)) return false;
     int Ppad = 1;
     while (Ppad < P) Ppad <<= 1;
-    const bool direct = P > CT_ROT_PMAX;
+    // canonical sums of every centre directly for large P, and for small K (sift1m's
+    // K = 1,000: the rotated pass, transpose and re-check cost more than they save)
+    const char *mk = getenv("RII_COARSE_ROT_MINK");
+    const bool direct = P > CT_ROT_PMAX || K < (mk ? atoll(mk) : 2048);
     const size_t tb = ct_tab_bytes(M);
     const size_t keys_off = direct && (size_t)Ppad * 8 <= tb ? 0 : tb;  // direct: keys overlay the table
     const size_t d0_off = direct ? std::max(tb, keys_off + (size_t)Ppad * 8) : tb + (size_t)ct_cap(Ppad) * 8;
@@ -355,7 +357,7 @@ bool launch_coarse_topp(const uint8_t *centers, int64_t K, int M, const float *t
         RII_CUDA(cudaFuncSetAttribute(coarse_topp_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                       SMEM_ATTR_MAX - 4096));                                                 \
         coarse_topp_kernel<MM><<<(unsigned)nq, CT_NT, smem, st>>>(centers, K, tables, P, probes, Ppad,       \
-                                                                 (int)keys_off, (int)d0_off);                \
+                                                                 (int)keys_off, (int)d0_off, direct);        \
         break;
         RII_CT(4) RII_CT(8) RII_CT(16) RII_CT(32) RII_CT(64)
 #undef RII_CT

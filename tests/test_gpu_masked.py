@@ -59,8 +59,12 @@ def test_masked_and_all_lists_match_oracle(rii, ref, monkeypatch, kind, N, D, M,
             P = ref.num_probe(N, K, nS, sub is not None, L)
             orr = o.query(q, 100, S=sub, L=L, path=2)
             res = {}
-            for mode in ("masked", "list", "query", None):
-                if mode:
+            for mode in ("masked", "list", "query", None, "rot"):
+                monkeypatch.delenv("RII_COARSE_ROT_MINK", raising=False)
+                if mode == "rot":  # the coarse top-P kernel's lane-rotated pass + exact re-check
+                    monkeypatch.delenv("RII_IVF_MODE", raising=False)
+                    monkeypatch.setenv("RII_COARSE_ROT_MINK", "1")
+                elif mode:
                     monkeypatch.setenv("RII_IVF_MODE", mode)
                 else:
                     monkeypatch.delenv("RII_IVF_MODE", raising=False)
@@ -70,7 +74,8 @@ def test_masked_and_all_lists_match_oracle(rii, ref, monkeypatch, kind, N, D, M,
                                    what=f"{kind} M={M} K={K} P={P} mode={mode} S={nS}")
                 res[mode] = gr
             monkeypatch.delenv("RII_IVF_MODE", raising=False)
-            for mode in ("list", "query", None):  # same bytes whichever way Alg. 2 executes
+            monkeypatch.delenv("RII_COARSE_ROT_MINK", raising=False)
+            for mode in ("list", "query", None, "rot"):  # same bytes whichever way Alg. 2 executes
                 assert np.array_equal(res["masked"][0], res[mode][0]), (mode, P)
                 assert np.array_equal(res["masked"][1], res[mode][1]), (mode, P)
             if P >= K:  # every list probed: Alg. 2's result is Alg. 1's

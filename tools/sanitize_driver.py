@@ -8,6 +8,9 @@ tiny    : BASELINE configs[0] shape at 1/5 size: train, add, reconfigure, linear
 windows : the headline u6 kernel (M = 32, 16 queries per CTA) over 120k codes in
           two long chunks (multi-window: rescale, rollback, shared-bound paths)
 ivf     : list-major two-phase IVF (fp32 / u6 items) and the u16 kernel (M = 16)
+masked  : IVF executed as a probe-masked linear scan and as Alg. 1 (P = K), the
+          coarse top-P kernel's lane-rotated pass (RII_COARSE_ROT_MINK=1) and its
+          canonical-only pass, whole and subset
 Results are checked against the oracle so a sanitizer run also proves it ran the
 path to completion.
 """
@@ -103,9 +106,41 @@ def ivf():
     print("ivf ok")
 
 
+def masked():
+    for k in ("RII_Q16_MIN", "RII_CHUNK_CODES", "RII_Q16_SAMPLE", "RII_IVF_MODE", "RII_LIST_Q16_MIN"):
+        os.environ.pop(k, None)
+    for kind, N, D, M, K in (("deep", 30_011, 96, 32, 40), ("deep", 20_003, 96, 8, 24)):
+        x = gen.base(kind, N, D, seed=N)
+        q = gen.base(kind, 37, D, seed=N, stream=gen.STREAM_QUERY)
+        cb = ref.train(x[:4_000], M, n_iter=2, seed=0)
+        g = rii.Index(D, M, device=0)
+        g.set_codebook(cb)
+        g.add(x)
+        g.reconfigure(K, n_iter=2, seed=0)
+        o = ref.OracleIndex(D, M)
+        o.cb = cb
+        o.add(x)
+        o.reconfigure(K, n_iter=2, seed=0)
+        for sub in (None, gen.subset(N, N // 3, seed=3)):
+            for L in (2, 5, K):
+                orr = o.query(q, 100, S=sub, L=L, path=2)
+                for mode, rot in (("masked", None), (None, "1"), (None, None)):
+                    os.environ.pop("RII_IVF_MODE", None)
+                    os.environ.pop("RII_COARSE_ROT_MINK", None)
+                    if mode:
+                        os.environ["RII_IVF_MODE"] = mode
+                    if rot:
+                        os.environ["RII_COARSE_ROT_MINK"] = rot
+                    assert_topk_parity(ref, o.cb, o.codes, q, g.query(q, 100, target_ids=sub, L=L, path="ivf"), orr,
+                                       S=sub, what=f"masked {kind} M={M} L={L} mode={mode} rot={rot}")
+        os.environ.pop("RII_IVF_MODE", None)
+        os.environ.pop("RII_COARSE_ROT_MINK", None)
+    print("masked ok")
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     import torch
     torch.cuda.set_device(0)
-    for name in (("tiny", "windows", "ivf") if which == "all" else (which,)):
+    for name in (("tiny", "windows", "ivf", "masked") if which == "all" else (which,)):
         globals()[name]()

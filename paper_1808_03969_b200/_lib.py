@@ -10,7 +10,11 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librii_b200.so")
+# RII_LIB=checked selects the bounds-checked build (librii_b200_checked.so: device-side
+# index / shared-memory layout assertions and a device sync after every launch; see
+# common.cuh RII_DCHECK) -- the same kernels, for test runs only.
+LIB_PATH = os.path.join(HERE, "librii_b200_checked.so" if os.environ.get("RII_LIB") == "checked"
+                        else "librii_b200.so")
 
 RII_OK, RII_ERR_ARG, RII_ERR_STATE, RII_ERR_OOM, RII_ERR_CUDA, RII_ERR_NCCL, RII_ERR_TRAIN = range(7)
 PATH_AUTO, PATH_LINEAR, PATH_IVF = 0, 1, 2

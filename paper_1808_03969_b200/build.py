@@ -1,6 +1,12 @@
 """Build librii_b200.so (sm_100a only) in-tree with nvcc.
 
-    python -m paper_1808_03969_b200.build [--force] [--verbose]
+    python -m paper_1808_03969_b200.build [--force] [--verbose] [--checked]
+
+--checked builds librii_b200_checked.so (objects in build_obj_checked/) with
+-DRII_BOUNDS_CHECK: device-side index and shared-memory layout assertions and a
+device synchronisation after every launch (common.cuh RII_DCHECK), loaded by the
+binding when RII_LIB=checked.  It stands in for compute-sanitizer, which the GPU
+pool does not run.
 
 Every translation unit is compiled with -gencode arch=compute_100a,code=sm_100a,
 -lineinfo (ncu source view) and --fmad=false (the canonical fp32 arithmetic of
@@ -20,6 +26,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "librii_b200.so")
+OBJ_CHECKED = os.path.join(HERE, "build_obj_checked")
+LIB_CHECKED = os.path.join(HERE, "librii_b200_checked.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
@@ -40,10 +48,12 @@ def _headers_mtime():
                if f.endswith((".cuh", ".hpp", ".h"))) if os.path.isdir(CSRC) else 0.0
 
 
-def _compile(entry, force: bool, verbose: bool) -> str:
+def _compile(entry, force: bool, verbose: bool, checked: bool = False) -> str:
     src, defines, objname = entry
     path = os.path.join(CSRC, src)
-    obj = os.path.join(OBJ, objname)
+    obj = os.path.join(OBJ_CHECKED if checked else OBJ, objname)
+    if checked:
+        defines = [*defines, "-DRII_BOUNDS_CHECK"]
     newest = max(os.path.getmtime(path), _headers_mtime(), os.path.getmtime(os.path.join(ROOT, "include", "rii.h")))
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest:
         return obj
@@ -58,10 +68,11 @@ def _compile(entry, force: bool, verbose: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    LIB = LIB_CHECKED if checked else globals()["LIB"]
+    os.makedirs(OBJ_CHECKED if checked else OBJ, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force, verbose), SOURCES))
+        objs = list(ex.map(lambda s: _compile(s, force, verbose, checked), SOURCES))
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         tmp = LIB + f".tmp{os.getpid()}"
         cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-ldl", "-lpthread"]
@@ -76,5 +87,6 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--checked", action="store_true")
     a = ap.parse_args()
-    print(build(a.force, a.verbose))
+    print(build(a.force, a.verbose, a.checked))

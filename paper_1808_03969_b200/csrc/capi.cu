@@ -957,7 +957,8 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             // keys carry ids (the CSR entry of the position), so ties resolve by id (CA4)
             const uint8_t *lcodes = a.S ? t.rmirror : x->mirror.as<uint8_t>();
             ScanArgs sa{};
-            sa.codes = lcodes; sa.rcodes = codes; sa.q = a.q; sa.nq = a.nq; sa.cb = cb; sa.ds = x->ds; sa.kk = kk;
+            sa.codes = lcodes; sa.n_codes = a.S ? t.n_loc : x->n_local;  // mirror rows
+            sa.rcodes = codes; sa.q = a.q; sa.nq = a.nq; sa.cb = cb; sa.ds = x->ds; sa.kk = kk;
             sa.out = pp;
             sa.items = items; sa.qlist = qlist; sa.P = P; sa.offsets = off; sa.ids = ids; sa.gthr = gthr;
             sa.tables = tables;

@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <atomic>
 #include <string>
@@ -33,11 +34,45 @@ constexpr int SMEM_ATTR_MAX = 227 * 1024;
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(int n = 1) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
+// Checked build (RII_BOUNDS_CHECK, `python -m paper_1808_03969_b200.build --checked` ->
+// librii_b200_checked.so, loaded when RII_LIB=checked): the stand-in for compute-sanitizer,
+// which this GPU pool does not allow.  Device-side RII_DCHECKs (index and shared-memory
+// layout bounds at the risky accesses: work items, gathers by id, append buffers, output
+// rows) print the failed condition and trap; every launch is followed by a device
+// synchronisation so that a fault is reported by the launch that caused it.
+#ifdef RII_BOUNDS_CHECK
+#define RII_LAUNCHED()                                                                            \
+    do {                                                                                          \
+        ::rii::count_launch();                                                                    \
+        RII_CUDA(cudaGetLastError());                                                             \
+        RII_CUDA(cudaDeviceSynchronize());                                                        \
+    } while (0)
+#define RII_DCHECK(c)                                                                             \
+    do {                                                                                          \
+        if (!(c)) {                                                                               \
+            printf("RII_DCHECK failed %s:%d: %s (block %d, thread %d)\n", __FILE__, __LINE__, #c, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                            \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
 #define RII_LAUNCHED()                                                                            \
     do {                                                                                          \
         ::rii::count_launch();                                                                    \
         RII_CUDA(cudaGetLastError());                                                             \
     } while (0)
+#define RII_DCHECK(c) do { } while (0)
+#endif
+// The dynamic shared memory a launch was given (bytes).
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+// [base, end) lies inside the launch's dynamic shared memory
+#define RII_SMEM_CHECK(base, end) \
+    RII_DCHECK((const uint8_t *)(end) >= (const uint8_t *)(base) && \
+               (size_t)((const uint8_t *)(end) - (const uint8_t *)(base)) <= (size_t)::rii::dyn_smem_bytes())
 
 // Optional device event counters of the scan kernels (rii_debug_counters): window
 // ends, compactions, rollbacks, shared-bound tightenings read at a window end,

@@ -203,6 +203,9 @@ __global__ void __launch_bounds__(CT_NT) coarse_topp_kernel(const uint8_t *__res
     __shared__ int wsum[CT_NT / 32];
     const int64_t qi = blockIdx.x;
     const int lane = threadIdx.x & 31;
+    RII_SMEM_CHECK(smem, d0 + K);
+    RII_SMEM_CHECK(smem, keys + (direct ? Ppad : cap));
+    RII_SMEM_CHECK(smem, tab + (direct ? M * 257 : H * LUT_Q_FLOATS));
     if (direct) {  // stage as [M][257] (A(m, z) = column m mod MH of row z of half m / 32)
         const float *tq = tables + qi * (int64_t)lut_q_floats(M);
         for (int e = threadIdx.x; e < M * KS; e += CT_NT) {
@@ -341,10 +344,12 @@ bool launch_coarse_topp(const uint8_t *centers, int64_t K, int M, const float *t
     if (P > CT_PMAX || P > K || !tables || (M != 4 && M != 8 && M != 16 && M != 32 && M != 64)) return false;
     int Ppad = 1;
     while (Ppad < P) Ppad <<= 1;
-    // canonical sums of every centre directly for large P, and for small K (sift1m's
-    // K = 1,000: the rotated pass, transpose and re-check cost more than they save)
+    // canonical sums of every centre directly for large P (RII_COARSE_ROT_MINK: also
+    // below that many centres, A/B only -- the rotated pass measured faster at every K
+    // tried: sift1m K = 1,000, M = 16 L = 1 1.54 -> 1.48 ms; M = 64 L = 1 3.62 -> 2.71 ms,
+    // profiles/r02h_ab_coarse_rotmink_sift1m.jsonl)
     const char *mk = getenv("RII_COARSE_ROT_MINK");
-    const bool direct = P > CT_ROT_PMAX || K < (mk ? atoll(mk) : 2048);
+    const bool direct = P > CT_ROT_PMAX || K < (mk ? atoll(mk) : 0);
     const size_t tb = ct_tab_bytes(M);
     const size_t keys_off = direct && (size_t)Ppad * 8 <= tb ? 0 : tb;  // direct: keys overlay the table
     const size_t d0_off = direct ? std::max(tb, keys_off + (size_t)Ppad * 8) : tb + (size_t)ct_cap(Ppad) * 8;
@@ -608,6 +613,7 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
     float *thr = reinterpret_cast<float *>(cnt + 2);
     int *scratch = reinterpret_cast<int *>(thr + 2);
     int *s_next = scratch + 2;
+    RII_SMEM_CHECK(smem, s_next + 1);
 
     const int64_t q0 = (int64_t)blockIdx.x * 2;
     const int D = MM * ds, tid = threadIdx.x, lane = tid & 31;

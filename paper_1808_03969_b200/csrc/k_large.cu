@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(NT, 1) scan_large_kernel(const LargeArgs a) {
     int *cnt = reinterpret_cast<int *>(fresh + NEWCAP);
     float *thr = reinterpret_cast<float *>(cnt + 1);
     int *scratch = reinterpret_cast<int *>(thr + 1);
+    RII_SMEM_CHECK(smem, scratch + 8);
 
     int64_t q, ci = 0;
     if constexpr (MODE == 0) {

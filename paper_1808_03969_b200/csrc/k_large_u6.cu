@@ -152,6 +152,8 @@ __global__ void __launch_bounds__(NTH, 1) scan_large_u6_kernel(const LargeU6Args
     float *qsc = reinterpret_cast<float *>(scratch + 32);
     float *gqs = qsc + B;
     uint64_t *bars = reinterpret_cast<uint64_t *>(aux + lu_aux_bytes(kk));  // [2], 8-byte aligned
+    RII_SMEM_CHECK(smem, gqs + B);
+    RII_SMEM_CHECK(smem, bars + 2);
 
     // chunk-major grid: the CTAs of a wave (all query batches of one code chunk) stream
     // the same codes (query-batch-major measured worse: 212 -> 277 ms, GIST-like)
@@ -159,6 +161,7 @@ __global__ void __launch_bounds__(NTH, 1) scan_large_u6_kernel(const LargeU6Args
     const int64_t c0 = a.base + (int64_t)ci * a.chunk, c1 = a.base + min(a.n_codes, (int64_t)ci * a.chunk + a.chunk);
     const int64_t rem = a.nq - (int64_t)qb * B;
     const int nqi = rem < B ? (int)rem : B;
+    RII_DCHECK(nqi >= 1 && c0 <= c1);
     auto query_of = [&](int qq) -> int64_t { return (int64_t)qb * B + (qq < nqi ? qq : nqi - 1); };
     const uint8_t *__restrict__ codes = a.codes;
 

@@ -134,6 +134,10 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
     const uint8_t *__restrict__ codes = a.codes;
     const uint8_t *__restrict__ rcodes = LISTS ? a.rcodes : a.codes;  // codes by candidate id
 
+    // (checked build) the whole layout -- tables, top lists, fresh buffers, counters,
+    // thresholds, scratch and the per-query scalars below -- fits the launch's smem
+    RII_SMEM_CHECK(smem, qsc + 4 * B);
+    RII_SMEM_CHECK(smem, lut + LUTB);
     if (a.dbg && threadIdx.x == 0) *reinterpret_cast<long long *>(scratch + 24) = clock64();  // debug cycles
     // Work item: linear mode = (code chunk ci, query batch qb); list mode = (posting
     // list, up to B of the queries that probe it) -- list-major Alg. 2 L7-L13.
@@ -145,6 +149,8 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         c1 = a.offsets[it.x + 1];
         qstart = it.y;
         nqi = it.z;
+        RII_DCHECK(c0 <= c1 && c1 <= a.n_codes && nqi >= 1 && nqi <= B && qstart >= 0 &&
+                   qstart + nqi <= a.nq * a.P);
         // The list is one contiguous range of the list-ordered mirror: one bulk prefetch
         // into L2 at item start (overlaps the table fill) instead of a DRAM miss per step.
         if (threadIdx.x == 0 && c1 > c0) {
@@ -175,6 +181,7 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         if (threadIdx.x < B) {
             const int qq = (int)threadIdx.x < nqi ? (int)threadIdx.x : nqi - 1;
             qid_s[threadIdx.x] = (int)(a.qlist[qstart + qq] / a.P);
+            RII_DCHECK(a.qlist[qstart + qq] < (uint64_t)(a.nq * a.P));
         }
         __syncthreads();
     }
@@ -703,7 +710,10 @@ __global__ void __launch_bounds__(NTH, NTH <= 192 ? 2 : 1) scan_fast_kernel(cons
         if constexpr (LISTS) {  // [q][probe rank][kk]; an empty list writes its first key only
             if (i == 0 || top[e - i] != KEY_MAX) a.out[a.qlist[qstart + qq] * kk + i] = top[e];
         }
-        else a.out[(((int64_t)qb * B + qq) * a.nc + ci) * kk + i] = top[e];
+        else {
+            RII_DCHECK(((int64_t)qb * B + qq) < a.nq && ci < a.nc);
+            a.out[(((int64_t)qb * B + qq) * a.nc + ci) * kk + i] = top[e];
+        }
     }
     if (a.dbg && tid == 0) {
         atomicAdd(a.dbg + DBG_CYC_TAIL, (unsigned long long)(clock64() - *reinterpret_cast<long long *>(scratch + 24)));
@@ -1721,6 +1731,7 @@ __global__ void __launch_bounds__(NT) merge_kernel(const uint64_t *__restrict__ 
     const int64_t q = blockIdx.x;
     const uint64_t *base = keys + q * q_stride;
     uint64_t *first = prt + kk;  // every part's first key, loaded in one round trip
+    RII_SMEM_CHECK(msm, first + parts);
     for (int i = threadIdx.x; i < kk; i += blockDim.x) top[i] = KEY_MAX;
     for (int p = threadIdx.x; p < parts; p += blockDim.x) first[p] = __ldg(base + (int64_t)p * p_stride);
     __syncthreads();

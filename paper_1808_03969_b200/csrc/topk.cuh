@@ -29,7 +29,11 @@ __device__ __forceinline__ void push_candidate(bool pred, uint64_t key, uint64_t
             if (base + n > PUSH_TRIGGER) need = true;
         }
         base = __shfl_sync(0xffffffffu, base, leader);
-        if (pred) fresh_q[base + __popc(bal & ((1u << lane) - 1u))] = key;
+        const int slot = base + __popc(bal & ((1u << lane) - 1u));
+        if (pred) {
+            RII_DCHECK(slot < NEWCAP);  // the trigger leaves room for one more step of pushes
+            fresh_q[slot] = key;
+        }
     }
 }
 

@@ -87,3 +87,24 @@ def test_product_package_does_not_import_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".hpp", ".h")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", text).replace("oracle's", ""), f
+
+
+def test_checked_build_selection_and_exports():
+    """RII_LIB=checked loads the bounds-checked build (common.cuh RII_DCHECK; the
+    stand-in for compute-sanitizer) and nothing else; when that build exists it
+    exports the same boundary and carries its device-side traps."""
+    import subprocess
+    import sys
+    code = "from paper_1808_03969_b200 import _lib; print(_lib.LIB_PATH)"
+    env = dict(os.environ, RII_LIB="checked")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True)
+    assert out.stdout.strip().endswith("librii_b200_checked.so"), out.stderr
+    env.pop("RII_LIB")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True)
+    assert out.stdout.strip().endswith("librii_b200.so"), out.stderr
+    path = os.path.join(ROOT, "paper_1808_03969_b200", "librii_b200_checked.so")
+    if not os.path.exists(path):
+        pytest.skip("checked build not present (python -m paper_1808_03969_b200.build --checked)")
+    raw = C.CDLL(path)
+    for name in _declared():
+        assert hasattr(raw, name), name

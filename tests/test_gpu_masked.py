@@ -59,11 +59,12 @@ def test_masked_and_all_lists_match_oracle(rii, ref, monkeypatch, kind, N, D, M,
             P = ref.num_probe(N, K, nS, sub is not None, L)
             orr = o.query(q, 100, S=sub, L=L, path=2)
             res = {}
-            for mode in ("masked", "list", "query", None, "rot"):
+            for mode in ("masked", "list", "query", None, "canon"):
                 monkeypatch.delenv("RII_COARSE_ROT_MINK", raising=False)
-                if mode == "rot":  # the coarse top-P kernel's lane-rotated pass + exact re-check
+                if mode == "canon":  # the coarse top-P kernel's canonical-only pass (the default
+                    # is the lane-rotated pass + exact re-check of the candidates)
                     monkeypatch.delenv("RII_IVF_MODE", raising=False)
-                    monkeypatch.setenv("RII_COARSE_ROT_MINK", "1")
+                    monkeypatch.setenv("RII_COARSE_ROT_MINK", "1000000000")
                 elif mode:
                     monkeypatch.setenv("RII_IVF_MODE", mode)
                 else:
@@ -75,7 +76,7 @@ def test_masked_and_all_lists_match_oracle(rii, ref, monkeypatch, kind, N, D, M,
                 res[mode] = gr
             monkeypatch.delenv("RII_IVF_MODE", raising=False)
             monkeypatch.delenv("RII_COARSE_ROT_MINK", raising=False)
-            for mode in ("list", "query", None, "rot"):  # same bytes whichever way Alg. 2 executes
+            for mode in ("list", "query", None, "canon"):  # same bytes whichever way Alg. 2 executes
                 assert np.array_equal(res["masked"][0], res[mode][0]), (mode, P)
                 assert np.array_equal(res["masked"][1], res[mode][1]), (mode, P)
             if P >= K:  # every list probed: Alg. 2's result is Alg. 1's

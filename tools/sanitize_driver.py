@@ -9,8 +9,8 @@ windows : the headline u6 kernel (M = 32, 16 queries per CTA) over 120k codes in
           two long chunks (multi-window: rescale, rollback, shared-bound paths)
 ivf     : list-major two-phase IVF (fp32 / u6 items) and the u16 kernel (M = 16)
 masked  : IVF executed as a probe-masked linear scan and as Alg. 1 (P = K), the
-          coarse top-P kernel's lane-rotated pass (RII_COARSE_ROT_MINK=1) and its
-          canonical-only pass, whole and subset
+          coarse top-P kernel's lane-rotated pass (the default) and its
+          canonical-only pass (RII_COARSE_ROT_MINK=1000000000), whole and subset
 Results are checked against the oracle so a sanitizer run also proves it ran the
 path to completion.
 """
@@ -124,7 +124,7 @@ def masked():
         for sub in (None, gen.subset(N, N // 3, seed=3)):
             for L in (2, 5, K):
                 orr = o.query(q, 100, S=sub, L=L, path=2)
-                for mode, rot in (("masked", None), (None, "1"), (None, None)):
+                for mode, rot in (("masked", None), (None, "1000000000"), (None, None)):
                     os.environ.pop("RII_IVF_MODE", None)
                     os.environ.pop("RII_COARSE_ROT_MINK", None)
                     if mode:

@@ -138,7 +138,7 @@ struct QueryScratch {
         s_probe{&st}, s_roff{&st}, s_rids{&st}, s_rkey{&st}, s_rval{&st}, s_out_ids{&st}, s_out_dist{&st},
         s_flag{&st}, s_lq{&st}, s_qoff{&st}, s_ql{&st}, s_qoff2{&st}, s_ql2{&st}, s_items{&st}, s_gthr{&st},
         s_tables{&st}, s_cpart{&st}, s_ckeys{&st}, s_take{&st}, s_samp{&st}, s_spart{&st}, s_bound{&st},
-        s_skey{&st}, s_tab16{&st}, s_qscale{&st}, s_qrot{&st}, s_route{&st}, s_rmirror{&st}, s_alist{&st},
+        s_skey{&st}, s_tab16{&st}, s_qscale{&st}, s_qrot{&st}, s_route{&st}, s_rmirror{&st}, s_alist{&st}, s_pr0{&st},
         s_pmask{&st}, s_salist{&st};
     explicit QueryScratch(cudaStream_t s) : st(s) {}
 };
@@ -449,6 +449,11 @@ int64_t ivf_num_probes(const rii_index *x, bool has_S, int64_t nS, int L) {
 static int masked_ratio() {
     const char *e = getenv("RII_MASKED_RATIO");  // 0 disables both shortcuts (A/B, tests)
     return e ? atoi(e) : 8;
+}
+// warps sharing one list in the query-major rank-0 phase (8 warps per 2-query CTA)
+static int r0q_nseg() {
+    const char *e = getenv("RII_R0_NSEG");
+    return e ? std::max(1, atoi(e)) : 4;
 }
 int decide_exec(const rii_index *x, int used, bool has_S, int64_t nS, int L) {
     if (used != RII_PATH_IVF || x->ivf_mode == RII_IVF_PAPER) return used;
@@ -931,7 +936,17 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             int4 *items = sc.s_items.get<int4>(cap);
             tr.mark("pairs csr");
             int64_t n_ph_items[4] = {0, 0, 0, 0};
-            n_ph_items[0] = build_list_items(qoff, x->K, B0, qlist, P, items, cap, st);
+            // RII_R0_QMAJOR=1 (A/B knob, off): rank 0 alone (r0 = 1) on the query-major
+            // traversal -- each query's nearest list scanned with its own table, the list
+            // split over RII_R0_NSEG warps, partials written in place, their kk-th distance
+            // published as the bound -- instead of list items holding the ~nq / K queries
+            // whose nearest list it is.  Measured slower (deep10m L = 64: 11.54 ms with
+            // list items, 12.40 / 12.55 / 12.64 ms with 4 / 8 / 16 warps per list, 15.79
+            // with one; profiles/r02k_ab_rank0_qmajor_deep10m.jsonl); parity-tested.
+            const char *r0e = getenv("RII_R0_QMAJOR");
+            const bool r0q = q16l && !lbound && r0 == 1 && pb.n >= 2 && x->M <= 32 && tables != nullptr &&
+                             r0e && atoi(r0e) != 0;
+            if (!r0q) n_ph_items[0] = build_list_items(qoff, x->K, B0, qlist, P, items, cap, st);
             int64_t n_items = n_ph_items[0];
             const int Bi = list_int_B(x->M, kk);  // queries per integer item
             const int64_t *qoff_i = qoff + x->K;
@@ -964,7 +979,13 @@ void search_batch(const rii_index *x, QueryScratch &sc, const QueryArgs &a, cons
             sa.tables = tables;
             if (lbound)
                 launch_list_bound(codes, x->M, items, n_ph_items[0], off, ids, qlist, P, tables, kk, gthr, st);
-            else
+            else if (r0q) {
+                int32_t *pr0 = sc.s_pr0.get<int32_t>(a.nq);
+                launch_strided_gather_i32(probes, P, a.nq, pr0, st);  // every query's nearest list
+                launch_ivf_scan(codes, x->M, a.q, a.nq, cb, x->D, kk, pr0, 1, off, ids, pp, st, tables, nullptr,
+                                P * kk, r0q_nseg());
+                launch_rank_bound(pp, a.nq, P * kk, kk, gthr, st);
+            } else
                 launch_list_scan(x->M, Bl, sa, n_ph_items[0], st);
             int64_t done = n_ph_items[0];
             if (lbound) sa.qlist = qlist_i;

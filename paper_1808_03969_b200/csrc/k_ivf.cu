@@ -576,21 +576,26 @@ struct ListCursor {
     bool done;
 };
 
+// A warp's next work item: segment `it % nseg` of the (query slot, probe rank) pair
+// `it / nseg` (nseg > 1 splits every list among several warps: few pairs per CTA).
 __device__ __forceinline__ void next_list(ListCursor &c, int *s_next, int64_t P, int64_t q0, int64_t nq,
                                           const int32_t *probes, const int64_t *offsets, const int32_t *take,
-                                          int lane) {
+                                          int lane, int nseg) {
     while (!c.done && c.beg >= c.end) {
         int it = 0;
         if (lane == 0) it = atomicAdd(s_next, 1);
         it = __shfl_sync(0xffffffffu, it, 0);
-        if ((int64_t)it >= 2 * P) { c.done = true; break; }
-        const int qq = it & 1;
-        const int64_t r = it >> 1, qi = q0 + qq;
+        if ((int64_t)it >= 2 * P * nseg) { c.done = true; break; }
+        const int pr = it / nseg, sg = it - pr * nseg;
+        const int qq = pr & 1;
+        const int64_t r = pr >> 1, qi = q0 + qq;
         if (qi >= nq) continue;
         const int32_t k = probes[qi * P + r];
+        const int64_t b = offsets[k], e = take ? b + take[qi * P + r] : offsets[k + 1];
+        const int64_t n32 = (e - b + 31) >> 5;  // 32-code steps, split evenly over the segments
         c.qq = qq;
-        c.beg = offsets[k];
-        c.end = take ? c.beg + take[qi * P + r] : offsets[k + 1];
+        c.beg = b + ((n32 * sg) / nseg) * 32;
+        c.end = min(e, b + ((n32 * (sg + 1)) / nseg) * 32);
     }
 }
 
@@ -601,7 +606,7 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
                                                       const int64_t *__restrict__ offsets,
                                                       const uint32_t *__restrict__ ids, uint64_t *__restrict__ out,
                                                       const float *__restrict__ tables,
-                                                      const int32_t *__restrict__ take) {
+                                                      const int32_t *__restrict__ take, int64_t ostride, int nseg) {
     constexpr int W = FAST ? M / 4 : 1;
     const int MM = FAST ? M : Mrt;
     extern __shared__ __align__(16) uint8_t smem[];
@@ -646,7 +651,7 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
     bool need = false;
     ListCursor cur{0, 0, 0, false};
     while (true) {
-        next_list(cur, s_next, P, q0, nq, probes, offsets, take, lane);
+        next_list(cur, s_next, P, q0, nq, probes, offsets, take, lane, nseg);
         if (!__syncthreads_or(!cur.done)) break;
         if (!cur.done) {
             const int64_t p = cur.beg + lane;
@@ -700,7 +705,7 @@ __global__ void __launch_bounds__(NT) ivf_scan_kernel(const uint8_t *__restrict_
     }
     for (int e = tid; e < 2 * kk; e += NT) {
         const int qq = e >= kk ? 1 : 0, i = e - qq * kk;
-        if (q0 + qq < nq) out[(q0 + qq) * kk + i] = top[e];
+        if (q0 + qq < nq) out[(q0 + qq) * ostride + i] = top[e];
     }
 }
 
@@ -713,29 +718,44 @@ size_t ivf_smem(int M, int kk) {
 template <int M, bool FAST>
 static void ivf_launch_t(const uint8_t *codes, int Mrt, const float *q, int64_t nq, const float *cb, int ds, int kk,
                          const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
-                         cudaStream_t st, const float *tables, const int32_t *take) {
+                         cudaStream_t st, const float *tables, const int32_t *take, int64_t ostride, int nseg) {
     const size_t smem = ivf_smem(Mrt, kk);
     auto kern = ivf_scan_kernel<M, FAST>;
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     KernelTimer t(TK_IVF, st);
     kern<<<(unsigned)ceil_div(nq, 2), NT, smem, st>>>(codes, q, nq, cb, Mrt, ds, kk, probes, P, offsets, ids, out,
-                                                      FAST ? tables : nullptr, take);
+                                                      FAST ? tables : nullptr, take, ostride > 0 ? ostride : kk,
+                                                      nseg);
     RII_LAUNCHED();
 }
 
 void launch_ivf_scan(const uint8_t *codes, int M, const float *q, int64_t nq, const float *cb, int D, int kk,
                      const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
-                     cudaStream_t st, const float *tables, const int32_t *take) {
+                     cudaStream_t st, const float *tables, const int32_t *take, int64_t ostride, int nseg) {
     if (nq <= 0) return;
     if (ivf_smem(M, kk) > 227 * 1024) throw Error(1, "topk too large for the inverted-index kernel");
     const int ds = D / M;
     switch (M) {
-        case 4: ivf_launch_t<4, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take); break;
-        case 8: ivf_launch_t<8, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take); break;
-        case 16: ivf_launch_t<16, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take); break;
-        case 32: ivf_launch_t<32, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take); break;
-        default: ivf_launch_t<1, false>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take); break;
+        case 4: ivf_launch_t<4, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take, ostride, nseg); break;
+        case 8: ivf_launch_t<8, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take, ostride, nseg); break;
+        case 16: ivf_launch_t<16, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take, ostride, nseg); break;
+        case 32: ivf_launch_t<32, true>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take, ostride, nseg); break;
+        default: ivf_launch_t<1, false>(codes, M, q, nq, cb, ds, kk, probes, P, offsets, ids, out, st, tables, take, ostride, nseg); break;
     }
+}
+
+__global__ void rank_bound_kernel(const uint64_t *__restrict__ keys, int64_t nq, int64_t stride, int kk,
+                                  float *__restrict__ gthr) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const uint64_t k = keys[q * stride + kk - 1];
+    gthr[q] = k == KEY_MAX ? __int_as_float(0x7f800000) : __fmul_ru(key_dist(k), 1.00001f);
+}
+
+void launch_rank_bound(const uint64_t *keys, int64_t nq, int64_t stride, int kk, float *gthr, cudaStream_t st) {
+    if (nq <= 0) return;
+    rank_bound_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, st>>>(keys, nq, stride, kk, gthr);
+    RII_LAUNCHED();
 }
 
 }  // namespace rii

@@ -177,11 +177,16 @@ void launch_sorted_probes(const float *d0, int64_t nq, int64_t K, int64_t P, int
 // before the budget L runs out (ranks in order).
 void launch_paper_takes(const int32_t *probes, int64_t nq, int64_t P, const int64_t *offsets, int64_t L,
                         int32_t *take, cudaStream_t st);
-// Posting-list traversal (Alg. 2 L7-L16, mode A): out[nq][kk] keys, ids = local positions.
+// Posting-list traversal (Alg. 2 L7-L16, mode A): out[q * ostride + i] (i < kk) keys,
+// ids = local positions (ostride 0 = kk); nseg = warps sharing one (query, list) pair.
 size_t ivf_smem(int M, int kk);
 void launch_ivf_scan(const uint8_t *codes, int M, const float *q, int64_t nq, const float *cb, int D, int kk,
                      const int32_t *probes, int64_t P, const int64_t *offsets, const uint32_t *ids, uint64_t *out,
-                     cudaStream_t st, const float *tables = nullptr, const int32_t *take = nullptr);
+                     cudaStream_t st, const float *tables = nullptr, const int32_t *take = nullptr,
+                     int64_t ostride = 0, int nseg = 1);
+// gthr[q] = the kk-th key distance of keys[q * stride .. + kk) inflated by 1e-5 (rounded
+// up), +inf when the list holds fewer than kk keys: a bound on the query's final kk-th.
+void launch_rank_bound(const uint64_t *keys, int64_t nq, int64_t stride, int kk, float *gthr, cudaStream_t st);
 
 // ---- large M (k_large.cu; M > 64, up to 256) ---------------------------------
 // One query per CTA, bf16 table resident in smem, exact (CA2) rescore of pushes.

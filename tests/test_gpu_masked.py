@@ -134,3 +134,23 @@ def test_masked_long_scan_matches_oracle(rii, ref, monkeypatch, kind, N, D, M, K
     orr = ref.ivf_mt(cb, codes, centers, off, ids, q, 100, L, S=sub)
     assert_topk_parity(ref, cb, codes, q, gr, orr, S=sub, what=f"masked {kind} M={M} L={L} S={ns}")
     assert np.array_equal(gr[0], gt[0]) and np.array_equal(gr[1], gt[1])
+
+
+@pytest.mark.parametrize("kind,N,D,M,K,nq,ns,L", LONG)
+def test_rank0_query_major_matches_oracle(rii, ref, monkeypatch, kind, N, D, M, K, nq, ns, L):
+    """List-major Alg. 2 with the rank-0 phase on the query-major traversal
+    (each query's nearest list scanned with its own table, partials written in place,
+    their kk-th distance published as the bound of the integer phases) and on list
+    items (RII_R0_QMAJOR=0): both equal the oracle and each other byte for byte."""
+    g, cb, codes, centers, off, ids = _long_index(rii, ref, kind, N, D, M, K)
+    q = gen.base(kind, nq, D, seed=N + 2, stream=gen.STREAM_QUERY)
+    sub = None if ns is None else gen.subset(N, ns, seed=ns + 1)
+    monkeypatch.setenv("RII_IVF_MODE", "list")
+    monkeypatch.setenv("RII_LIST_Q16_MIN", "64")  # integer phases at these list lengths
+    orr = ref.ivf_mt(cb, codes, centers, off, ids, q, 100, L, S=sub)
+    res = {}
+    for v in ("1", "0"):
+        monkeypatch.setenv("RII_R0_QMAJOR", v)
+        res[v] = g.query(q, 100, target_ids=sub, L=L, path="ivf")
+        assert_topk_parity(ref, cb, codes, q, res[v], orr, S=sub, what=f"r0q={v} {kind} M={M} L={L} S={ns}")
+    assert np.array_equal(res["0"][0], res["1"][0]) and np.array_equal(res["0"][1], res["1"][1])

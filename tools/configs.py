@@ -210,13 +210,17 @@ def main():
         lib.rii_kernel_timing(0)
         kernel_ms = kms.value / max(kn.value, 1)
         lookups = qb * N * M
-        peak = 148 * 64 * 1965e6  # u16 tables: 64 two-byte lookups per 128-B wavefront per clock per SM
+        # the peak of the kernel that ran: u16 tables give 64 two-byte lookups per 128-B wavefront per
+        # clock per SM, the u6 (one-byte) tables 128 (the r02d/r02l rows still carry the u16 peak although
+        # the u6 kernel ran, u16_launches = 0: their frac reads 1.10 where 0.55 is meant)
+        u6 = q16n.value == 0
+        peak = 148 * (128 if u6 else 64) * 1965e6
         emit(config="scale1b", row="linear whole (1024 queries)", ms=ms, qps=qb / ms * 1e3,
              scanned_codes_per_s=qb * N / ms * 1e3, kernel_ms=kernel_ms, kernel_launches=kn.value,
              u16_launches=q16n.value, lookups_per_s=lookups / (kernel_ms / 1e3),
              roofline={"bound": "alu (shared-memory LUT pipe)", "peak_lookups_per_s": peak,
                        "frac": lookups / (kernel_ms / 1e3) / peak,
-                       "code_bytes_per_launch": N * M, "note": "u16 fixed-point tables, 8 queries per CTA (M = 8)"})
+                       "code_bytes_per_launch": N * M, "note": ("u6 (one-byte)" if u6 else "u16") + " fixed-point tables (M = 8)"})
     if "latency" in only:  # small batches (serving): deep10m, time per call for nq in {1, 16, 128, 1024}
         kind, N, D, M, nlist, nq, topk, n_train, _ = bench.WORKLOADS["deep10m"]
         g, b = build(kind, N, D, M, nlist, n_train)

@@ -917,6 +917,14 @@ static int m64_nth() {
     const char *e = getenv("RII_M64_NTH");
     return e ? atoi(e) : 256;
 }
+// Threads of the M = 8, 16-query u6 linear kernel: 512 (118 registers, 16 warps per SM) against 384
+// (127 registers, 12 warps) measured deep10m at M = 8 44.2 -> 40.8 ms per 10k queries, 1,024 queries
+// 5.22 -> 4.82 ms, a 1e6-id subset 7.50 -> 6.98 ms, 1e8 codes 41.8 -> 40.3 ms per 1,024 queries
+// (profiles/r02o_ab_m8nth_*.jsonl).  RII_M8_NTH=384 selects the old configuration (A/B, tests).
+static int m8_nth() {
+    const char *e = getenv("RII_M8_NTH");
+    return e && atoi(e) == 384 ? 384 : 512;
+}
 static int q16_nth(int M) { return M == 64 ? m64_nth() : 384; }  // 256 x 2 codes per thread: 150 ms (deep10m)
 #ifndef RII_SCAN_M  // common translation unit only
 bool q16_is_u6(int M) { const int c = q16_cfg(M); return c == 4 || c == 7 || c == 9; }
@@ -1090,9 +1098,21 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
     const bool q16 = (B == 8 || B == 16) && q16_req && gthr != nullptr;
     if (mask.alist && mask.B != B) throw Error(1, "probe mask grouped by a different query batch");
     void *kern = fast_kernel_ptr<M, B, false>(q16);
+    int nth = q16 ? q16_nth(M) : (B == 8 ? PACKED_NTH : scan_threads());
     if constexpr (M == 8 && B == 16) {
-        if (q16 && lin_l2_prefetch(n)) kern = (void *)scan_fast_kernel<M, 16, false, 384, 1, 3, 1024 | 128 | 64>;
+        // M = 8 needs < 128 registers, so 512 threads (16 warps per SM instead of 12) still fit one
+        // CTA's register file (m8_nth)
+        const bool pf = lin_l2_prefetch(n);
+        if (q16 && m8_nth() == 512) {
+            kern = pf ? (void *)scan_fast_kernel<M, 16, false, 512, 1, 3, 1024 | 128 | 64>
+                      : (void *)scan_fast_kernel<M, 16, false, 512, 1, 3, 128 | 64>;
+            nth = 512;
+        } else if (q16 && pf) {
+            kern = (void *)scan_fast_kernel<M, 16, false, 384, 1, 3, 1024 | 128 | 64>;
+        }
     }
+    // (M = 16 at 512 threads -- 124 registers, no spills -- measured 11.06 -> 16.74 ms on sift1m,
+    // 1.62 -> 4.36 ms at 1,024 queries: profiles/r02q_ab_m16nth_sift1m.jsonl; the variant was removed.)
     const size_t smem = q16 && B == 8 ? smem_q16(kk) : pl.smem;
     RII_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR_MAX));
     ScanArgs a{};
@@ -1105,7 +1125,6 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
     void *args[] = {&a};
     KernelTimer t(timer, st), tp(B >= 8 && timer == TK_LINEAR ? (q16 ? (q16_is_u6(M) ? TK_U6 : TK_Q16) : TK_PACKED) : -1,
                                  st);
-    const int nth = q16 ? q16_nth(M) : (B == 8 ? PACKED_NTH : scan_threads());
     check_code_align(codes, M);
     RII_CUDA(cudaLaunchKernel(kern, dim3(pl.nb * pl.nc), dim3(nth), args, smem, st));
     count_launch();

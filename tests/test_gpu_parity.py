@@ -538,6 +538,16 @@ def test_linear_u16_tables(rii, ref, monkeypatch, kind, N, D, M, nq, topk):
             g4 = g.query(q, topk, target_ids=sub, path="linear")
             monkeypatch.delenv("RII_LIN_PF_MIN")
             assert np.array_equal(gr[0], g4[0]) and np.array_equal(gr[1], g4[1])
+            # the 384-thread configuration of the 16-query kernel (default: 512), with and without prefetch
+            for env in ({"RII_M8_NTH": "384", "RII_Q16_CFG": "9"},
+                        {"RII_M8_NTH": "384", "RII_Q16_CFG": "9", "RII_LIN_PF_MIN": "1"},
+                        {"RII_Q16_CFG": "9", "RII_LIN_PF_MIN": "1"}):
+                for k, v in env.items():
+                    monkeypatch.setenv(k, v)
+                g5 = g.query(q, topk, target_ids=sub, path="linear")
+                for k in env:
+                    monkeypatch.delenv(k)
+                assert np.array_equal(gr[0], g5[0]) and np.array_equal(gr[1], g5[1]), env
         if M == 64:  # the u6 kernel at 384 threads (A/B variant) equals the default 256
             for env in ({"RII_M64_NTH": "384"},):
                 for k, v in env.items():

@@ -920,10 +920,15 @@ static int m64_nth() {
 // Threads of the M = 8, 16-query u6 linear kernel: 512 (118 registers, 16 warps per SM) against 384
 // (127 registers, 12 warps) measured deep10m at M = 8 44.2 -> 40.8 ms per 10k queries, 1,024 queries
 // 5.22 -> 4.82 ms, a 1e6-id subset 7.50 -> 6.98 ms, 1e8 codes 41.8 -> 40.3 ms per 1,024 queries
-// (profiles/r02o_ab_m8nth_*.jsonl).  RII_M8_NTH=384 selects the old configuration (A/B, tests).
-static int m8_nth() {
+// (profiles/r02o_ab_m8nth_*.jsonl).  RII_M8_NTH=384 / 512 forces one (A/B, tests).
+// Few query batches over a long scan are the exception (128 queries x 1e7 codes: 1.09 ms at 384
+// threads, 1.59 ms at 512; profiles/r02r_ab_m8nth_short.jsonl), so scans of >= 2^22 codes by fewer
+// than 512 queries keep 384 threads; shorter scans measured equal or faster at 512 for every batch.
+static int m8_nth(int64_t n, int64_t nq) {
     const char *e = getenv("RII_M8_NTH");
-    return e && atoi(e) == 384 ? 384 : 512;
+    if (e && atoi(e) == 384) return 384;
+    if (e && atoi(e) == 512) return 512;
+    return (nq >= 512 || n < ((int64_t)1 << 22)) ? 512 : 384;
 }
 static int q16_nth(int M) { return M == 64 ? m64_nth() : 384; }  // 256 x 2 codes per thread: 150 ms (deep10m)
 #ifndef RII_SCAN_M  // common translation unit only
@@ -1103,7 +1108,7 @@ static void launch_fast_t(const ScanPlan &pl, const uint8_t *codes, int64_t n, c
         // M = 8 needs < 128 registers, so 512 threads (16 warps per SM instead of 12) still fit one
         // CTA's register file (m8_nth)
         const bool pf = lin_l2_prefetch(n);
-        if (q16 && m8_nth() == 512) {
+        if (q16 && m8_nth(n, nq) == 512) {
             kern = pf ? (void *)scan_fast_kernel<M, 16, false, 512, 1, 3, 1024 | 128 | 64>
                       : (void *)scan_fast_kernel<M, 16, false, 512, 1, 3, 128 | 64>;
             nth = 512;

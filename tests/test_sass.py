@@ -52,3 +52,20 @@ def test_u6_scan_loop_instruction_mix(kernel):
     assert mix["SEL"] <= max_sel, mix     # word rotation: one (two copies) or three select stages
 
 
+
+
+@pytest.mark.parametrize("variant", [192, 1216])  # plain and L2-prefetching
+def test_m8_512_thread_kernel_fits_the_register_file(variant):
+    """The M = 8, 16-query u6 linear kernel at 512 threads (k_scan.cu m8_nth): a 512-thread
+    CTA owns at most 128 registers per thread; the variant is only worth its 16 warps per SM
+    while it compiles without a stack frame (spills)."""
+    obj = os.path.join(ROOT, "paper_1808_03969_b200", "build_obj", "k_scan_m8.o")
+    if not os.path.exists(obj) or not shutil.which("cuobjdump"):
+        pytest.skip("library not built / cuobjdump missing")
+    kernel = f"_ZN3rii16scan_fast_kernelILi8ELi16ELb0ELi512ELi1ELi3ELi{variant}EEEvNS_8ScanArgsE"
+    res = subprocess.run(["cuobjdump", "-res-usage", obj], capture_output=True, text=True, check=True).stdout
+    assert kernel in res, "kernel not instantiated"
+    line = res.split(kernel, 1)[1].splitlines()[1]
+    assert "STACK:0 " in line, line
+    reg = int(line.split("REG:")[1].split()[0])
+    assert reg <= 128, line
